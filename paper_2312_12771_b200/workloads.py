@@ -1,0 +1,218 @@
+"""Seeded synthetic workloads for the five BASELINE.json configs.
+
+This module holds input generation only -- meshes, phase fields, material
+tables, boundary data -- and none of the method's arithmetic.  It is the one
+module shared by the oracle-side tests and the GPU path.
+
+Conventions:
+  * macro and RVE domains are [0,1]^d with uniform grids, nodes lexicographic
+    (x fastest), Q1 counter-clockwise / hex8 bottom-then-top local order;
+  * RVE b = e * 2^d + q (one RVE per macro Gauss point, Dirac basis P:246-292);
+  * phases are per RVE element, assigned by element centroid;
+  * config 3 draws u_s(i, j) = top 53 bits of splitmix64(seed ^ (s << 56) ^
+    (i << 24) ^ j) / 2^53, seed 12771.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+SEED = 12771
+_M64 = (1 << 64) - 1
+
+
+def splitmix64(x: np.ndarray) -> np.ndarray:
+    """Vectorised splitmix64 finaliser on uint64 (wrapping arithmetic)."""
+    z = (x.astype(np.uint64) + np.uint64(0x9E3779B97F4A7C15))
+    z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+    z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+    return z ^ (z >> np.uint64(31))
+
+
+def uniform(seed: int, s: int, i, j) -> np.ndarray:
+    """Counter-based U[0,1) draw u_s(i, j)."""
+    i = np.asarray(i, dtype=np.uint64)
+    j = np.asarray(j, dtype=np.uint64)
+    key = np.uint64(seed) ^ (np.uint64(s) << np.uint64(56)) ^ (i << np.uint64(24)) ^ j
+    with np.errstate(over="ignore"):
+        z = splitmix64(key)
+    return (z >> np.uint64(11)).astype(np.float64) / float(1 << 53)
+
+
+# --------------------------------------------------------------------------
+# structured meshes
+# --------------------------------------------------------------------------
+def local_offsets(dim: int) -> np.ndarray:
+    """Integer offsets of the local nodes (CCW in 2-D, bottom then top face in 3-D)."""
+    if dim == 1:
+        return np.array([[0], [1]])
+    quad = np.array([[0, 0], [1, 0], [1, 1], [0, 1]])
+    if dim == 2:
+        return quad
+    return np.array([[x, y, z] for z in (0, 1) for x, y in quad])
+
+
+def grid_mesh(dim: int, n: int, L: float = 1.0):
+    """Uniform grid of [0,L]^dim with n cells per direction -> (coords, conn)."""
+    idx = np.indices([n + 1] * dim).reshape(dim, -1)[::-1].T  # columns x, y, z; x fastest
+    coords = idx * (L / n)
+    off = local_offsets(dim)
+    cells = np.indices([n] * dim).reshape(dim, -1)[::-1].T  # columns: x, y, z with x fastest
+    strides = np.array([(n + 1) ** k for k in range(dim)])
+    conn = ((cells[:, None, :] + off[None, :, :]) * strides).sum(-1).astype(np.int32)
+    return np.ascontiguousarray(coords, dtype=np.float64), np.ascontiguousarray(conn)
+
+
+def centroids(dim: int, n: int) -> np.ndarray:
+    cells = np.indices([n] * dim).reshape(dim, -1)[::-1].T
+    return (cells + 0.5) / n
+
+
+def boundary_nodes(dim: int, n: int) -> np.ndarray:
+    idx = np.indices([n + 1] * dim).reshape(dim, -1)[::-1].T
+    return np.nonzero(((idx == 0) | (idx == n)).any(1))[0]
+
+
+def face_nodes(dim: int, n: int, axis: int, value: int) -> np.ndarray:
+    idx = np.indices([n + 1] * dim).reshape(dim, -1)[::-1].T
+    return np.nonzero(idx[:, axis] == value)[0]
+
+
+# --------------------------------------------------------------------------
+# workloads
+# --------------------------------------------------------------------------
+@dataclasses.dataclass
+class Workload:
+    name: str
+    dim: int
+    nel: int               # macro cells per direction
+    r: int                 # RVE cells per direction
+    kind: str              # "linear" (E, nu) or "nh" (alpha, kappa)
+    phase: np.ndarray      # [n_rve | 1][r^dim] uint8
+    mat: np.ndarray        # [n_rve | 1][n_phase][2] float64
+    dir_dof: np.ndarray    # int32 Dirichlet DOFs (node*dim + comp)
+    dir_val: np.ndarray    # float64 prescribed values (total load)
+    body: np.ndarray | None
+    n_steps: int = 1
+    description: str = ""
+
+    @property
+    def n_qp(self) -> int:
+        return 2 ** self.dim
+
+    @property
+    def n_rve(self) -> int:
+        return self.nel ** self.dim * self.n_qp
+
+    @property
+    def n_dof(self) -> int:
+        return (self.nel + 1) ** self.dim * self.dim
+
+    @property
+    def n_pad(self) -> int:
+        return self.dim * self.r ** self.dim
+
+    @property
+    def n_f(self) -> int:
+        return self.n_pad - self.dim
+
+    @property
+    def m(self) -> int:
+        if self.kind == "nh":
+            return self.dim * self.dim
+        return {1: 1, 2: 3, 3: 6}[self.dim]
+
+    def macro_mesh(self):
+        return grid_mesh(self.dim, self.nel)
+
+    def rve_mesh(self):
+        return grid_mesh(self.dim, self.r)
+
+    def flop_per_rve(self) -> float:
+        """Dense condensation flops counted on n_f: n^3/3 + 2 n^2 m + n m^2."""
+        n, m = self.n_f, self.m + (1 if self.kind == "nh" else 0)
+        return n ** 3 / 3.0 + 2.0 * n * n * m + n * m * m
+
+
+def _affine_dirichlet(dim, nel, strain11):
+    nodes = boundary_nodes(dim, nel)
+    coords, _ = grid_mesh(dim, nel)
+    dofs, vals = [], []
+    for n in nodes:
+        for c in range(dim):
+            dofs.append(n * dim + c)
+            vals.append(strain11 * coords[n, 0] if c == 0 else 0.0)
+    return np.array(dofs, np.int32), np.array(vals)
+
+
+def _clamped_left(dim, nel):
+    nodes = face_nodes(dim, nel, 0, 0)
+    dofs = np.array([n * dim + c for n in nodes for c in range(dim)], np.int32)
+    return dofs, np.zeros(len(dofs))
+
+
+def _inclusion_phase(dim, r, vf):
+    rad = math.sqrt(vf / math.pi) if dim == 2 else (3.0 * vf / (4.0 * math.pi)) ** (1.0 / 3.0)
+    c = centroids(dim, r)
+    return (np.linalg.norm(c - 0.5, axis=1) < rad).astype(np.uint8)[None, :]
+
+
+def config1(nel: int = 4, r: int = 8) -> Workload:
+    c = centroids(2, r)
+    phase = (c[:, 0] >= 0.5).astype(np.uint8)[None, :]
+    mat = np.array([[[1.0, 0.3], [10.0, 0.3]]])
+    d, v = _affine_dirichlet(2, nel, 1e-3)
+    return Workload("cfg1_laminate", 2, nel, r, "linear", phase, mat, d, v, None,
+                    description="2-D laminate, affine eps_xx = 1e-3 on the boundary")
+
+
+def config2(nel: int = 32, r: int = 16) -> Workload:
+    phase = _inclusion_phase(2, r, 0.3)
+    mat = np.array([[[1.0, 0.3], [10.0, 0.3]]])
+    d, v = _clamped_left(2, nel)
+    return Workload("cfg2_disc", 2, nel, r, "linear", phase, mat, d, v, np.array([0.0, -1.0]),
+                    description="2-D centred disc vf 0.3, E ratio 10, clamped left edge, body force (0,-1)")
+
+
+def config3(nel: int = 64, r: int = 32, seed: int = SEED) -> Workload:
+    n_rve = nel * nel * 4
+    nelr = r * r
+    b = np.arange(n_rve, dtype=np.uint64)[:, None]
+    e = np.arange(nelr, dtype=np.uint64)[None, :]
+    phase = (uniform(seed, 0, b, e) < 0.4).astype(np.uint8)
+    p = np.arange(2, dtype=np.uint64)[None, :]
+    E = 10.0 ** (2.0 * uniform(seed, 1, b, p))
+    nu = 0.2 + 0.2 * uniform(seed, 2, b, p)
+    mat = np.stack([E, nu], axis=-1)
+    d, v = _clamped_left(2, nel)
+    return Workload("cfg3_random", 2, nel, r, "linear", phase, mat, d, v, np.array([0.0, -1.0]),
+                    description="2-D Bernoulli(0.4) phases, E log-uniform [1,100], nu U[0.2,0.4] per phase per RVE")
+
+
+def config4(nel: int = 8, r: int = 8) -> Workload:
+    phase = _inclusion_phase(3, r, 0.2)
+    mat = np.array([[[1.0, 0.3], [20.0, 0.3]]])
+    d, v = _affine_dirichlet(3, nel, 1e-3)
+    return Workload("cfg4_sphere", 3, nel, r, "linear", phase, mat, d, v, None,
+                    description="3-D centred sphere vf 0.2, E ratio 20, affine uniaxial strain 1e-3")
+
+
+def config5(nel: int = 32, r: int = 16, n_steps: int = 10, stretch: float = 0.1) -> Workload:
+    phase = _inclusion_phase(2, r, 0.3)
+    mat = np.array([[[0.5, 2.0], [5.0, 20.0]]])  # (alpha, kappa): mu = 2 alpha, lambda = kappa
+    dl, vl = _clamped_left(2, nel)
+    right = face_nodes(2, nel, 0, nel)
+    dr = np.array([n * 2 for n in right], np.int32)
+    d = np.concatenate([dl, dr])
+    v = np.concatenate([vl, np.full(len(dr), stretch)])
+    return Workload("cfg5_neohooke", 2, nel, r, "nh", phase, mat, d, v, None, n_steps=n_steps,
+                    description="2-D finite-strain Neo-Hookean disc, right edge stretched to 1.1 in 10 steps")
+
+
+CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}
+
+
+def make(cfg: int, **kw) -> Workload:
+    return CONFIGS[cfg](**kw)

@@ -1,0 +1,423 @@
+"""Pins of the CPU oracle against what the paper and mechanics fix (CPU only).
+
+Each test names the passage or closed form it relies on.  None of them
+re-types the oracle's own formula: they use closed forms, invariants, finite
+differences, a textbook dense solve, and the brute-force monolithic system of
+tests/bruteforce.py.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2312_12771_b200 import workloads as W
+
+from . import bruteforce as bf
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _iso_voigt_closed(dim, E, nu):
+    lam = E * nu / ((1 + nu) * (1 - 2 * nu))
+    mu = E / (2 * (1 + nu))
+    full = bf.iso_tangent_full(dim, E, nu)
+    return lam, mu, full
+
+
+# ---------------------------------------------------------------- materials
+def test_linear_C_matches_fourth_order_isotropic_tensor():
+    """Voigt C (engineering shear) must reproduce sigma = lam tr(eps) I + 2 mu eps."""
+    rng = np.random.default_rng(0)
+    for dim in (2, 3):
+        E, nu = 3.7, 0.27
+        C = oracle.linear_C(dim, E, nu)
+        lam, mu, _ = _iso_voigt_closed(dim, E, nu)
+        eps = rng.standard_normal((dim, dim))
+        eps = 0.5 * (eps + eps.T)
+        sig = lam * np.trace(eps) * np.eye(dim) + 2 * mu * eps
+        if dim == 2:
+            ev = np.array([eps[0, 0], eps[1, 1], 2 * eps[0, 1]])
+            sv = np.array([sig[0, 0], sig[1, 1], sig[0, 1]])
+        else:
+            ev = np.array([eps[0, 0], eps[1, 1], eps[2, 2], 2 * eps[1, 2], 2 * eps[0, 2], 2 * eps[0, 1]])
+            sv = np.array([sig[0, 0], sig[1, 1], sig[2, 2], sig[1, 2], sig[0, 2], sig[0, 1]])
+        np.testing.assert_allclose(C @ ev, sv, rtol=1e-14, atol=1e-14)
+
+
+def test_nh_stress_free_reference_and_fd_consistency():
+    """P(I) = 0, Psi(I) = 0; P = dPsi/dF and A = dP/dF by central differences."""
+    for alpha, kappa in [(0.5, 2.0), (5.0, 20.0), (27.0, 60.0)]:
+        psi, P, A = oracle.nh_material(np.array([1.0, 0, 0, 1.0]), alpha, kappa)
+        assert abs(psi) < 1e-15 and np.abs(P).max() < 1e-13
+    rng = np.random.default_rng(1)
+    h = 1e-6
+    for _ in range(20):
+        F = np.array([1.0, 0, 0, 1.0]) + 0.2 * rng.standard_normal(4)
+        alpha, kappa = 0.5 + rng.random(), 2 + 10 * rng.random()
+        psi, P, A = oracle.nh_material(F, alpha, kappa)
+        for j in range(4):
+            dF = np.zeros(4)
+            dF[j] = h
+            pp, Pp, _ = oracle.nh_material(F + dF, alpha, kappa)
+            pm, Pm, _ = oracle.nh_material(F - dF, alpha, kappa)
+            assert abs((pp - pm) / (2 * h) - P[j]) < 1e-6 * max(1, abs(P[j]))
+            np.testing.assert_allclose((Pp - Pm) / (2 * h), A[:, j], rtol=1e-6, atol=1e-6)
+        np.testing.assert_allclose(A, A.T, atol=1e-13)
+        # independent numpy implementation of the same energy's derivatives
+        Pb, Ab, _ = bf.nh_response(F, alpha, kappa)
+        np.testing.assert_allclose(P, Pb, rtol=1e-13, atol=1e-13)
+        np.testing.assert_allclose(A, Ab, rtol=1e-13, atol=1e-13)
+
+
+def test_nh_linearisation_is_isotropic_mu_2alpha_lambda_kappa():
+    """A(I) = lam d_ij d_kl + mu (d_ik d_jl + d_il d_jk) with mu = 2 alpha, lam = kappa (R11)."""
+    alpha, kappa = 0.5, 2.0
+    _, _, A = oracle.nh_material(np.array([1.0, 0, 0, 1.0]), alpha, kappa)
+    mu, lam = 2 * alpha, kappa
+    d = np.eye(2)
+    ref = (lam * np.einsum("ij,kl->ijkl", d, d) + mu * (np.einsum("ik,jl->ijkl", d, d)
+                                                        + np.einsum("il,jk->ijkl", d, d))).reshape(4, 4)
+    np.testing.assert_allclose(A, ref, atol=1e-14)
+
+
+def test_nh_rejects_nonpositive_jacobian():
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.nh_material(np.array([1.0, 0, 0, -1.0]), 1.0, 1.0)
+    assert e.value.code == oracle.ORC_ERR_JACOBIAN
+
+
+# ---------------------------------------------------------------- skyline
+def test_skyline_cholesky_solve_matches_textbook_dense_solve():
+    rng = np.random.default_rng(2)
+    n = 40
+    A = np.zeros((n, n))
+    for i in range(n):  # random profile
+        lo = max(0, i - rng.integers(0, 12))
+        A[i, lo:i + 1] = rng.standard_normal(i + 1 - lo)
+    A = A @ A.T + n * np.eye(n)
+    b = rng.standard_normal(n)
+    x = oracle.dense_spd_solve(A, b)
+    np.testing.assert_allclose(x, np.linalg.solve(A, b), rtol=1e-12)
+
+
+# ---------------------------------------------------------------- RVE pins
+@pytest.mark.parametrize("dim,r", [(2, 3), (2, 4), (3, 2), (3, 3)])
+def test_homogeneous_rve_returns_C_exactly(dim, r):
+    """Check (b): for a homogeneous RVE, K_fe = 0 by periodicity (discrete int grad w = 0) so C_eff = C."""
+    C = oracle.linear_C(dim, 2.5, 0.31)
+    Ce, Wf = oracle.rve_condense_linear(dim, r, C, want_W=True)
+    np.testing.assert_allclose(Ce, C, rtol=1e-13, atol=1e-13)
+    assert np.abs(Wf).max() < 1e-13
+
+
+def test_laminate_closed_form_config1():
+    """Check (c): laminate normal to x -- Q1 is exact, C_eff equals the Backus closed form."""
+    g = json.load(open(os.path.join(GOLD, "laminate_cfg1.json")))
+    wl = W.config1()
+    Ce = oracle.condense_batch_linear(2, wl.r, wl.phase, wl.mat, 1)[0]
+    np.testing.assert_allclose(Ce, np.array(g["C_eff_voigt"]), rtol=0, atol=1e-14 * np.abs(Ce).max())
+    # the same values from the closed form itself, computed here from the phase constants
+    C0, C1 = oracle.linear_C(2, 1.0, 0.3), oracle.linear_C(2, 10.0, 0.3)
+    h = lambda f: 1.0 / (0.5 / f(C0) + 0.5 / f(C1))  # noqa: E731  harmonic mean
+    a = lambda f: 0.5 * f(C0) + 0.5 * f(C1)  # noqa: E731
+    c11 = h(lambda C: C[0, 0])
+    c12 = a(lambda C: C[0, 1] / C[0, 0]) * c11
+    c22 = a(lambda C: C[1, 1] - C[0, 1] ** 2 / C[0, 0]) + a(lambda C: C[0, 1] / C[0, 0]) ** 2 * c11
+    c33 = h(lambda C: C[2, 2])
+    np.testing.assert_allclose([Ce[0, 0], Ce[0, 1], Ce[1, 1], Ce[2, 2]], [c11, c12, c22, c33], rtol=1e-14)
+
+
+def _loewner_ge(A, B, tol):
+    return np.linalg.eigvalsh(0.5 * ((A - B) + (A - B).T)).min() >= -tol
+
+
+@pytest.mark.parametrize("dim,r,n", [(2, 6, 12), (3, 3, 4)])
+def test_bounds_symmetry_spd_random_rves(dim, r, n):
+    """Check (d): Reuss <= C_eff <= Voigt (Loewner), symmetric, SPD; Dirichlet (ii) >= periodic."""
+    rng = np.random.default_rng(3 + dim)
+    for t in range(n):
+        E = 10 ** (2 * rng.random(r ** dim))
+        nu = 0.2 + 0.2 * rng.random(r ** dim)
+        Cq = np.stack([oracle.linear_C(dim, E[e], nu[e]) for e in range(r ** dim)])
+        Cq4 = np.repeat(Cq[:, None], 2 ** dim, axis=1)
+        Ce = oracle.rve_condense_linear(dim, r, Cq4)
+        Cv = Cq.mean(0)
+        Cr = np.linalg.inv(np.linalg.inv(Cq).mean(0))
+        tol = 1e-12 * np.abs(Cv).max()
+        assert np.abs(Ce - Ce.T).max() <= 1e-13 * np.abs(Ce).max()
+        assert np.linalg.eigvalsh(Ce).min() > 0
+        assert _loewner_ge(Cv, Ce, tol), "Voigt bound"
+        assert _loewner_ge(Ce, Cr, tol), "Reuss bound"
+        Cd = oracle.rve_condense_linear(dim, r, Cq4, mode=1)
+        assert _loewner_ge(Cd, Ce, tol), "Dirichlet >= periodic"
+        Ct = oracle.rve_condense_linear(dim, r, Cq4, mode=2)
+        np.testing.assert_allclose(Ct, Cv, rtol=1e-13, atol=1e-15)  # Taylor (i) = Voigt
+
+
+def test_symmetry_classes_disc_and_sphere():
+    """Centred disc on a symmetric grid: C11 = C22, C13 = C23 = 0; sphere: cubic symmetry."""
+    wl = W.config2()
+    C = oracle.condense_batch_linear(2, wl.r, wl.phase, wl.mat, 1)[0]
+    assert abs(C[0, 0] - C[1, 1]) < 1e-12 * C[0, 0]
+    assert abs(C[0, 2]) < 1e-13 and abs(C[1, 2]) < 1e-13
+    wl = W.config4(r=4)
+    C = oracle.condense_batch_linear(3, wl.r, wl.phase, wl.mat, 1)[0]
+    s = 1e-12 * C[0, 0]
+    assert abs(C[0, 0] - C[1, 1]) < s and abs(C[0, 0] - C[2, 2]) < s
+    assert abs(C[0, 1] - C[0, 2]) < s and abs(C[0, 1] - C[1, 2]) < s
+    assert abs(C[3, 3] - C[4, 4]) < s and abs(C[3, 3] - C[5, 5]) < s
+    off = C.copy()
+    off[:3, :3] = 0
+    np.fill_diagonal(off, 0)
+    assert np.abs(off).max() < s
+
+
+def test_hill_mandel_energy_identity():
+    """eps^T C_eff eps = |Omega|^-1 int sigma : eps~ at the RVE solution (eq:hillA).
+
+    The right side is evaluated with the brute-force element routines on the oracle's
+    fluctuation field W; it is a second, independent quadrature of the same energy."""
+    dim, r = 2, 5
+    rng = np.random.default_rng(7)
+    E = 10 ** (2 * rng.random(r * r))
+    Cq = np.stack([oracle.linear_C(2, E[e], 0.3) for e in range(r * r)])
+    Ce, Wf = oracle.rve_condense_linear(2, r, np.repeat(Cq[:, None], 4, 1), want_W=True)
+    eps = rng.standard_normal(3)
+    w = eps @ Wf  # fluctuation in independent layout
+    dofmap, nf, indep = bf.periodic_dofs(2, r)
+    energy = 0.0
+    for e in range(r * r):
+        nodes, _ = bf._elem_nodes(2, r, e)
+        wl = np.array([w[indep[n] * 2 + c] for n in nodes for c in range(2)])
+        full = bf.iso_tangent_full(2, E[e], 0.3)
+        for xi in bf._qps(2):
+            g = bf._grads(2, 1.0 / r, xi)
+            H = bf._grad_op(2, g) @ wl + np.array([eps[0], eps[2] / 2, eps[2] / 2, eps[1]])
+            energy += (0.5 / r) ** 2 * H @ full @ H
+    assert abs(energy - eps @ Ce @ eps) < 1e-12 * abs(energy)
+
+
+# ---------------------------------------------------------------- brute force (e)
+def _brute_linear(dim, nel, r, E, nu, dir_dof, dir_val, body):
+    def tangent(b, e):
+        return bf.iso_tangent_full(dim, E[b, e], nu[b, e])
+    mono = bf.Monolithic(dim, nel, r, tangent, dir_dof, body)
+    u, wfree = mono.solve_linear(dir_val)
+    return mono, u, mono.to_indep_layout(wfree)
+
+
+@pytest.mark.parametrize("dim,nel,r", [(2, 2, 4), (3, 2, 2)])
+def test_condensation_equals_monolithic_bruteforce(dim, nel, r):
+    """Check (e): the full uncondensed [K D; E L] solve equals condense + macro + recover."""
+    rng = np.random.default_rng(11 + dim)
+    n_rve = nel ** dim * 2 ** dim
+    nelr = r ** dim
+    phase = (rng.random((n_rve, nelr)) < 0.4).astype(np.uint8)
+    mat = np.stack([10 ** (2 * rng.random((n_rve, 2))), 0.2 + 0.2 * rng.random((n_rve, 2))], -1)
+    E = np.take_along_axis(mat[..., 0], phase.astype(int), 1)
+    nu = np.take_along_axis(mat[..., 1], phase.astype(int), 1)
+    # clamp the x = 0 face, body force
+    nodes = W.face_nodes(dim, nel, 0, 0)
+    dir_dof = np.array([n * dim + c for n in nodes for c in range(dim)], np.int32)
+    dir_val = 1e-3 * rng.standard_normal(len(dir_dof))
+    body = np.array([0.3, -1.0, 0.2][:dim])
+    mono, u_bf, w_bf = _brute_linear(dim, nel, r, E, nu, dir_dof, dir_val, body)
+    C, Wf = oracle.condense_batch_linear(dim, r, phase, mat, n_rve, want_W=True)
+    u = oracle.macro_solve(dim, nel, C, dir_dof, dir_val, body=body)
+    eps = oracle.macro_kin(dim, nel, u)
+    w = oracle.recover_linear(Wf, eps)
+    np.testing.assert_allclose(u, u_bf, rtol=0, atol=1e-12 * np.abs(u_bf).max())
+    np.testing.assert_allclose(w, w_bf, rtol=0, atol=1e-12 * np.abs(w_bf).max())
+
+
+def test_nh_newton_step_equals_monolithic_bruteforce():
+    """Check (e), finite strain: one condensed Newton step (eq:solution2 + P:424-427) equals the
+    full monolithic Newton step on a tiny instance, at a non-trivial state (u, w)."""
+    rng = np.random.default_rng(5)
+    wl = W.config5(nel=2, r=4, n_steps=2)
+    wl.phase = (rng.random((1, 16)) < 0.5).astype(np.uint8)
+    u = 0.01 * rng.standard_normal(wl.n_dof)
+    u[wl.dir_dof] = 0.0
+    w = 0.01 * rng.standard_normal((wl.n_rve, 32))
+    w[:, :2] = 0.0  # corner class
+    x_dir = wl.dir_val / wl.n_steps
+    du, dw, info = oracle.newton_step_nh(wl, u, w, x_dir)
+
+    mat = wl.mat[0]
+
+    def material(b, e, F):
+        P, A, J = bf.nh_response(F, *mat[wl.phase[0, e]])
+        assert J > 0
+        return P, A
+
+    mono = bf.Monolithic(2, wl.nel, wl.r, None, wl.dir_dof, wl.body)
+    du_bf, dw_bf = mono.newton_step(u, mono.from_indep_layout(w), material, x_dir)
+    np.testing.assert_allclose(du, du_bf, rtol=0, atol=1e-11 * np.abs(du_bf).max())
+    np.testing.assert_allclose(dw, mono.to_indep_layout(dw_bf), rtol=0, atol=1e-11 * np.abs(dw_bf).max())
+
+
+def test_nh_reference_state_equals_linear_condensation():
+    """At F = I, w = 0 the NH condensation is the linear one with mu = 2 alpha, lambda = kappa."""
+    wl = W.config5(nel=1, r=8)
+    out = oracle.condense_batch_nh(wl.r, wl.phase, wl.mat, np.array([[1.0, 0, 0, 1.0]]))
+    mu = 2 * wl.mat[0, :, 0]
+    lam = wl.mat[0, :, 1]
+    E = mu * (3 * lam + 2 * mu) / (lam + mu)
+    nu = lam / (2 * (lam + mu))
+    # plane strain: the 2-D oracle C uses the 3-D (E, nu) -> lambda = E nu/((1+nu)(1-2nu)) which
+    # equals kappa only if we feed the plane-strain-consistent pair; convert exactly:
+    nu_ps = lam / (2 * (lam + mu))
+    E_ps = mu * 2 * (1 + nu_ps)
+    Cv = oracle.condense_batch_linear(2, wl.r, wl.phase, np.stack([E_ps, nu_ps], -1)[None], 1)[0]
+    A = out["A_eff"][0]
+    idx = [(0, 0), (1, 1), (0, 1)]  # (11), (22), (12) in the full-gradient layout 0,3,1
+    fg = [0, 3, 1]
+    for i in range(3):
+        for j in range(3):
+            np.testing.assert_allclose(A[fg[i], fg[j]], Cv[i, j], rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(A[1, 1], A[1, 2], rtol=1e-12)  # minor symmetry at F = I
+    np.testing.assert_allclose(out["P_eff"], 0.0, atol=1e-14)
+    del E, nu, idx
+
+
+def test_nh_tangent_is_derivative_of_equilibrated_stress():
+    """A_eff = d<P>/dF at micro equilibrium: FD of the re-equilibrated average stress (§8(c) pin)."""
+    wl = W.config5(nel=1, r=6)
+    F0 = np.array([1.05, 0.02, -0.01, 0.97])
+
+    def equilibrated(F):
+        w = np.zeros((1, 72))
+        for _ in range(20):
+            c = oracle.condense_batch_nh(wl.r, wl.phase, wl.mat, F[None], w)
+            if c["rf_norm"][0] < 1e-14:
+                break
+            w = w + c["Z"]
+        return c
+
+    c0 = equilibrated(F0)
+    h = 1e-6
+    for j in range(4):
+        dF = np.zeros(4)
+        dF[j] = h
+        Pp = equilibrated(F0 + dF)["P_avg"][0]
+        Pm = equilibrated(F0 - dF)["P_avg"][0]
+        np.testing.assert_allclose((Pp - Pm) / (2 * h), c0["A_eff"][0][:, j], rtol=1e-6, atol=1e-7)
+    # at equilibrium the condensed stress is the average stress (R_micro = 0)
+    np.testing.assert_allclose(c0["P_eff"][0], c0["P_avg"][0], atol=1e-13)
+
+
+# ---------------------------------------------------------------- macro pins
+def test_config1_affine_patch_stress_and_recovery():
+    """C_eff is the same at every qp and the BC is affine => u = eps X exactly; laminate recovery."""
+    g = json.load(open(os.path.join(GOLD, "laminate_cfg1.json")))
+    wl = W.config1()
+    out = oracle.solve_linear(wl)
+    coords, _ = wl.macro_mesh()
+    np.testing.assert_allclose(out["u"][0::2], 1e-3 * coords[:, 0], atol=1e-15)
+    np.testing.assert_allclose(out["u"][1::2], 0.0, atol=1e-15)
+    sig = out["C_eff"][0] @ out["eps"][0]
+    np.testing.assert_allclose(sig, g["macro_stress"], atol=1e-16)
+    w = oracle.recover_linear(out["W"], out["eps"][0])  # [N_pad]
+    r = wl.r
+    wx = w[0::2].reshape(r, r)  # [y][x]
+    wy = w[1::2]
+    assert np.abs(wy).max() < 1e-16
+    x = np.arange(r) / r
+    expect = np.where(x <= 0.5, g["w_x_slope_soft"] * x, g["w_x_slope_soft"] * 0.5 + g["w_x_slope_stiff"] * (x - 0.5))
+    np.testing.assert_allclose(wx, np.broadcast_to(expect, (r, r)), atol=1e-16)
+    assert abs(wx[0, r // 2] - g["w_x_at_half"]) < 1e-16
+
+
+def test_macro_solution_satisfies_equilibrium():
+    """R(u) = sum eta B^T C_eff B u - f vanishes on the free DOFs (residual built by a
+    different routine than the direct solve), and u^T K u = f^T u (energy identity)."""
+    wl = W.config2(nel=6, r=6)
+    out = oracle.solve_linear(wl)
+    S = np.einsum("bij,bj->bi", out["C_eff"], out["eps"])
+    R = oracle.macro_residual(2, wl.nel, S, wl.body)
+    free = np.ones(wl.n_dof, bool)
+    free[wl.dir_dof] = False
+    f = -oracle.macro_residual(2, wl.nel, None, wl.body)
+    assert np.abs(R[free]).max() < 1e-12 * np.abs(f).max()
+    u = out["u"]
+    internal = oracle.macro_residual(2, wl.nel, S, None)
+    assert abs(u @ internal - f @ u) < 1e-12 * abs(f @ u)
+
+
+# ---------------------------------------------------------------- 1-D benchmark (a)
+def _bench1d(k):
+    g = json.load(open(os.path.join(GOLD, "bench1d.json")))
+    n = 2 ** k
+    L = g["macro_domain"][1]
+    # micro: RVE (0,1) with n P1 elements; lambda at the 2 Gauss points; tangent 2 lambda (R14)
+    xg = np.array([-1 / math.sqrt(3), 1 / math.sqrt(3)])
+    xc = (np.arange(n)[:, None] + 0.5 + 0.5 * xg[None, :]) / n
+    lam = 20.0 / np.cos(2 * math.pi * xc / 3 - math.pi / 3)
+    Cq = (2 * lam)[:, :, None, None]
+    Ch, Wf = oracle.rve_condense_linear(1, n, Cq, want_W=True)
+    # macro: P1, 2 Gauss points, Dirichlet phi(0) = 0, phi(1000), body load B = 1
+    D = np.full((n * 2, 1, 1), Ch[0, 0])
+    phi = oracle.macro_solve(1, n, D, [0, n], [g["phi_0"], g["phi_1000"]], body=np.array([g["body_load"]]), Lm=L)
+    F = oracle.macro_kin(1, n, phi, Lm=L)[:, 0]
+    return g, n, L, Ch[0, 0], Wf[0], phi, F, lam
+
+
+def test_bench1d_discrete_closed_forms():
+    """Check (a): C^h = 2/sum(h_e / lam_e) (chain of springs); nodal phi exact for P1 (R14)."""
+    for k in (3, 5):
+        g, n, L, Ch, Wf, phi, F, lam = _bench1d(k)
+        lam_bar = lam.mean(1)
+        assert abs(Ch - 2.0 / np.sum((1.0 / n) / lam_bar)) < 1e-12 * Ch
+        X = np.linspace(0, L, n + 1)
+        a = (g["phi_1000"] + L ** 2 / (2 * Ch)) / L
+        np.testing.assert_allclose(phi, -X ** 2 / (2 * Ch) + a * X, rtol=1e-12, atol=1e-9)
+    _, _, _, Ch, *_ = _bench1d(9)
+    assert abs(Ch - 80 * math.pi / (3 * math.sqrt(3))) < 1e-3  # O(h^2) to the harmonic mean
+
+
+def _l2_errors(k):
+    g, n, L, Ch, Wf, phi, F, lam = _bench1d(k)
+    c2, c1 = g["phi_a_c2"], g["phi_a_c1"]
+    # err_phi with 5-point Gauss per macro element
+    xs, ws = np.polynomial.legendre.leggauss(5)
+    h = L / n
+    num = den = 0.0
+    for e in range(n):
+        X = e * h + (xs + 1) * h / 2
+        ph = phi[e] + (phi[e + 1] - phi[e]) * (xs + 1) / 2
+        pa = c2 * X ** 2 + c1 * X
+        num += np.sum(ws * h / 2 * (ph - pa) ** 2)
+        den += np.sum(ws * h / 2 * pa ** 2)
+    err_phi = math.sqrt(num / den)
+    # err_w with the macro Gauss rule (reading R15) and 5-point Gauss per micro element
+    Wn = np.concatenate([Wf, Wf[:1]])  # node n == node 0 (corner class)
+    hm = 1.0 / n
+    xq = np.array([-1 / math.sqrt(3), 1 / math.sqrt(3)])
+    num = den = 0.0
+    for e in range(n):
+        for q in range(2):
+            Xk = e * h + (xq[q] + 1) * h / 2
+            Fa = 2 * c2 * Xk + c1
+            Fk = F[2 * e + q]
+            for c in range(n):
+                xt = c * hm + (xs + 1) * hm / 2
+                wh = Fk * (Wn[c] + (Wn[c + 1] - Wn[c]) * (xs + 1) / 2)
+                wa = Fa * (np.sin(2 * math.pi * xt / 3 - math.pi / 3) / math.sqrt(3) - xt + 0.5)
+                num += h / 2 * np.sum(ws * hm / 2 * (wh - wa) ** 2)
+                den += h / 2 * np.sum(ws * hm / 2 * wa ** 2)
+    return err_phi, math.sqrt(num / den)
+
+
+def test_bench1d_convergence_orders():
+    """Check (a): fitted orders over k = 4..7, [delta,1]: err_phi > 2, err_w = 1."""
+    g = json.load(open(os.path.join(GOLD, "bench1d.json")))["orders_delta1"]
+    ks = [4, 5, 6, 7]
+    e = np.array([_l2_errors(k) for k in ks])
+    hs = np.array([1000.0 / 2 ** k for k in ks])
+    p_phi = np.polyfit(np.log(hs), np.log(e[:, 0]), 1)[0]
+    p_w = np.polyfit(np.log(hs), np.log(e[:, 1]), 1)[0]
+    assert p_phi >= g["err_phi_min"], p_phi
+    assert abs(p_w - g["err_w"]) <= g["err_w_tol"], p_w
