@@ -1,0 +1,364 @@
+#!/usr/bin/env python
+"""bench.py -- batched RVE condensation + macro solve on B200 (arXiv 2312.12771 hot path).
+
+A step is one pass of the whole hot path over one synthetic batch (SURVEY.md
+§8(a)): hom_condense (K1 assembly + K2-K4 fused Cholesky / influence solves /
+Schur epilogue, all RVEs), hom_macro_solve (K5 assembly + K6/K7 PCG) and
+hom_recover_fluctuations (K8).  For config 5 a step is one monolithic Newton
+iteration (kinematics, condensation, residual norms, macro solve, update).
+
+Default workload: BASELINE.json configs[1] (config 2: 32x32 macro Q1, 4096 RVEs
+of 16x16 Q1 with a centred disc).  Prints ONE JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+Multi-GPU (torchrun): every rank solves its own independent replica of the
+workload (weak scaling, no data-path collective -- DESIGN.md §7); the timed
+region is bracketed by barriers and the max over ranks is reported.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 37.15  # measured DMMA peak, tools/fp64_peaks.cu -> MEASURED_FP64.json / profiles/r01_fp64_peaks.txt
+METRIC = "condensed RVE tangents/sec"
+
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def fp64_peak():
+    m = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
+    if "fp64_tflops" in m:
+        return float(m["fp64_tflops"]), "MEASURED_PEAKS.json fp64_tflops"
+    f = load_json(os.path.join(ROOT, "MEASURED_FP64.json")) or {}
+    if "fp64_dmma_tflops_microbench" in f:
+        return float(f["fp64_dmma_tflops_microbench"]), "MEASURED_FP64.json (DMMA microbenchmark, this pool's B200)"
+    return FP64_PEAK_TFLOPS, "measured DMMA microbenchmark (profiles/r01_fp64_peaks.txt)"
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle baseline
+def oracle_step_time(wl, target_s: float = 10.0):
+    """Time the CPU oracle (as it stands) on a bounded sample of the workload and scale to one step.
+
+    The oracle condenses `n` RVEs (phase rows replicated per RVE so nothing is deduplicated),
+    then the direct macro solve runs once at full size.  Returns (seconds per full step, detail)."""
+    import numpy as np
+
+    import oracle
+    nthreads = oracle.default_threads()
+    per = 1 if wl.phase.shape[0] == 1 else None
+
+    def sample(n):
+        ids = np.arange(n) % wl.n_rve
+        ph = np.repeat(wl.phase, n, 0) if per else wl.phase[ids]
+        mt = np.repeat(wl.mat, n, 0) if wl.mat.shape[0] == 1 else wl.mat[ids]
+        t0 = time.perf_counter()
+        if wl.kind == "linear":
+            C = oracle.condense_batch_linear(wl.dim, wl.r, ph, mt, n, want_W=True, nthreads=nthreads)[0]
+        else:
+            F = np.tile([1.0, 0.0, 0.0, 1.0], (n, 1))
+            C = oracle.condense_batch_nh(wl.r, ph, mt, F, nthreads=nthreads)["A_eff"]
+        return time.perf_counter() - t0, C
+
+    n = max(nthreads, 8)
+    t, _ = sample(n)
+    while t < 0.25 * target_s and n < wl.n_rve:
+        n = min(wl.n_rve, max(n * 2, int(n * 0.3 * target_s / max(t, 1e-3))))
+        t, C = sample(n)
+    t_rve = t / n
+    # macro direct solve at full size with representative tangents
+    Cm = np.broadcast_to(C[:1], (wl.n_rve,) + C.shape[1:]).copy()
+    t0 = time.perf_counter()
+    if wl.kind == "linear":
+        u = oracle.macro_solve(wl.dim, wl.nel, Cm, wl.dir_dof, wl.dir_val, body=wl.body)
+        oracle.macro_kin(wl.dim, wl.nel, u)
+    else:
+        oracle.macro_solve(2, wl.nel, Cm, wl.dir_dof, np.zeros(len(wl.dir_dof)), S=np.zeros((wl.n_rve, 4)),
+                           body=wl.body, kind=1)
+    t_macro = time.perf_counter() - t0
+    step = t_rve * wl.n_rve + t_macro
+    detail = {"cores": nthreads, "sample": f"{n} of {wl.n_rve} RVEs condensed (skyline Cholesky, unit-strain route, "
+                                             f"{t:.1f} s) + 1 full-size direct macro solve ({t_macro:.2f} s); "
+                                             f"scaled to a full step", "t_rve_s": t_rve, "t_macro_s": t_macro}
+    return step, detail
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ----------------------------------------------------------------------------- main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    from paper_2312_12771_b200 import workloads as W
+    wl = W.make(args.config)
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    config = {"workload": f"{wl.name}: {wl.description}", "config_index": args.config,
+              "n_rve": wl.n_rve, "rve_dofs": wl.n_pad, "n_f": wl.n_f, "macro_dof": wl.n_dof,
+              "flop_per_rve": wl.flop_per_rve(), "parallelism": f"replicas{world}" if world > 1 else "single",
+              "l2": "no flush: each step writes and re-reads the dense K_ff pool "
+                    f"({wl.n_rve * (wl.n_pad // 64 + (wl.n_pad % 64 > 0)) * (wl.n_pad // 64 + 1) // 2 * 32768 / 1e9:.1f} GB) "
+                    "which is far larger than the 126 MB L2"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        steps = []
+        detail = None
+        for i in range(args.warmup + args.steps):
+            st, detail = oracle_step_time(wl, target_s=2.0)
+            if i >= args.warmup:
+                steps.append(st)
+        t = statistics.median(steps)
+        val = wl.n_rve / t
+        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tangents/s", "n_gpus": 0,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+                "cpu_baseline": {"value": val, "unit": "tangents/s", "cores": detail["cores"], "kind": "oracle",
+                                 "sample": detail["sample"], "cpu": cpu_model()},
+                "e2e": {"value": val, "unit": "tangents/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line))
+        return
+
+    import numpy as np
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    from paper_2312_12771_b200.hom import Homogenizer
+
+    h = Homogenizer.from_workload(wl)
+    dev = torch.cuda.current_device()
+    B, m = h.n_rve, h.m
+    C = h.empty(B, m, m)
+    u = h.empty(h.n_dof)
+    w = h.empty(B, h.n_pad)
+    P_eff = h.empty(B, m) if h.finite else None
+    P_avg = h.empty(B, m) if h.finite else None
+    F = h.empty(B, m) if h.finite else None
+    du = h.empty(h.n_dof) if h.finite else None
+    cg_iters = []
+
+    if h.finite:  # a mid-load state: one converged load step first, then time Newton iterations
+        u0, _ = h.newton(1, tol=1e-9)
+        u.copy_(u0)
+
+    def step():
+        if h.finite:
+            h.macro_kinematics(u, F)
+            h.condense(F, C, P_eff, P_avg)
+            h.macro_residual_norm(P_avg)
+            h.micro_residual_max()
+            _, info = h.macro_solve(C, P_eff, scale=0.0, x=du)
+            h.newton_update(u, du)
+        else:
+            h.condense(None, C)
+            _, info = h.macro_solve(C, None, 1.0, u)
+            h.recover(u, w)
+        cg_iters.append(info.iterations)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    stream = torch.cuda.current_stream()
+    sampler = ClockSampler(dev)
+    sampler.start()
+    time.sleep(0.2)
+    h.profile(True)
+    n0 = h.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    launches = h.launch_count() - n0
+    ms = e0.elapsed_time(e1)
+    prof = h.profile_read()
+    h.profile(False)
+    clocks = sampler.stop()
+    if world > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = world * B * args.steps / (ms * 1e-3)
+
+    # ---------------- end to end: host inputs (pinned) -> C-ABI -> host results, every step
+    ph_host = torch.from_numpy(np.ascontiguousarray(wl.phase if wl.phase.shape[0] > 1 else wl.phase[0])).pin_memory()
+    mt_host = torch.from_numpy(np.ascontiguousarray(wl.mat if wl.mat.shape[0] > 1 else wl.mat[0])).pin_memory()
+    C_host = torch.empty((B, m, m), dtype=torch.float64).pin_memory()
+    u_host = torch.empty(h.n_dof, dtype=torch.float64).pin_memory()
+    w_host = torch.empty((B, h.n_pad), dtype=torch.float64).pin_memory()
+
+    def step_e2e():
+        h.set_phases(ph_host, mt_host)
+        step()
+        C_host.copy_(C, non_blocking=True)
+        u_host.copy_(u, non_blocking=True)
+        if not h.finite:
+            w_host.copy_(w, non_blocking=True)
+
+    for _ in range(args.warmup):
+        step_e2e()
+    torch.cuda.synchronize()
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step_e2e()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_e2e = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    h2d = ph_host.numel() * ph_host.element_size() + mt_host.numel() * mt_host.element_size()
+    d2h = C_host.numel() * 8 + u_host.numel() * 8 + (0 if h.finite else w_host.numel() * 8)
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    cond_ms, cond_n = prof["condense"]
+    flop_launch = wl.flop_per_rve() * min(h.sizes.rve_chunk, B)
+    n_cond = max(cond_n, 1)
+    achieved = flop_launch * n_cond / (cond_ms * 1e-3) / 1e12 if cond_ms > 0 else None
+    peak, peak_src = fp64_peak()
+    step_ms_total = sum(v[0] for v in prof.values())
+    breakdown = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
+                     "share": (v[0] / step_ms_total if step_ms_total else None)} for k, v in prof.items()}
+    asm_ms = prof["rve_assemble"][0] / max(prof["rve_assemble"][1], 1)
+    kff_bytes = B * (wl.n_pad // 64 + (wl.n_pad % 64 > 0)) * ((wl.n_pad // 64 + (wl.n_pad % 64 > 0)) + 1) // 2 * 32768
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "tangents/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
+        "roofline": {"bound": "tensor", "kernel": "k_condense (K2-K4 fused FP64 DMMA Cholesky + solves + Schur)",
+                     "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "peak_source": peak_src,
+                     "algorithmic": f"{wl.flop_per_rve():.4g} flop/RVE (n_f^3/3 + 2 n_f^2 m + n_f m^2, n_f={wl.n_f}) x "
+                                    f"{min(h.sizes.rve_chunk, B)} RVEs per launch"},
+        "fp64_tflops_condense": achieved,
+        "macro_solve_ms": (prof["macro_assemble"][0] + prof["cg"][0]) / args.steps,
+        "cg_iterations": statistics.median(cg_iters) if cg_iters else None,
+        "assembly": {"kernel": "k_rve_assemble (K1)", "ms_per_launch": asm_ms,
+                     "GBps": kff_bytes * min(h.sizes.rve_chunk, B) / B / (asm_ms * 1e-3) / 1e9 if asm_ms > 0 else None,
+                     "bytes": "dense tiled lower K_ff written per launch"},
+        "breakdown": breakdown,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "e2e": {"value": world * B * args.steps / (ms_e2e * 1e-3), "unit": "tangents/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "what": "hom_set_phases from pinned host + condense + macro solve + recovery + D2H of C_eff, u, w"},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        st, detail = oracle_step_time(wl)
+        line["cpu_baseline"] = {"value": wl.n_rve / st, "unit": "tangents/s", "cores": detail["cores"],
+                                "kind": "oracle", "sample": detail["sample"], "cpu": cpu_model()}
+    print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,226 @@
+/*
+ * hom.h -- C-ABI of libhom.so, the B200 (sm_100a) hot path of the monolithic
+ * FE^2 homogenization of Hesch, Schmidt & Schuss, arXiv 2312.12771.
+ *
+ * The path: a batch of independent RVE problems, one per macro
+ * Gauss point (Dirac macro basis), whose fluctuation DOFs
+ * are removed by static condensation -- the paper's null-space reduction
+ * P = [I, -D L^-1]^T -- followed by the condensed macro solve
+ * [K - D L^-1 E] dq = -[R_macro - D L^-1 R_micro] (eq:solution2)
+ * and the fluctuation update dw = -L^-1 [R_micro + E dq].
+ *
+ * Conventions used by every call:
+ *  - All floating point is IEEE binary64 (FP64).
+ *  - Host pointers (setup inputs) are copied during hom_setup; the caller may
+ *    free them when it returns.  Device pointers (d_*) are caller-owned,
+ *    contiguous, 8-byte aligned, on the context's device; the library never
+ *    frees them.  The context owns all scratch (K_ff chunk pool, influence
+ *    store X, CSR matrix, CG vectors, fluctuation state).
+ *  - Every call enqueues on `stream` (a cudaStream_t, NULL = legacy default)
+ *    and returns after enqueue, except where a call is documented to
+ *    synchronise (error flags, solver info).
+ *  - B = number of RVEs = n_macro_elems * 2^dim, RVE b = e * 2^dim + q,
+ *    Gauss points 2 per direction at +-1/sqrt(3), qp order x fastest.
+ *  - m = 3 (2-D Voigt [e11, e22, g12]), 6 (3-D Voigt [e11, e22, e33, g23,
+ *    g13, g12], engineering shear), 4 (2-D finite strain, F row-major
+ *    [F11, F12, F21, F22]).
+ *  - RVE fluctuation layout [B][N_pad]: N_pad = dim * n_indep, entry
+ *    dim*p + c for periodic independent node p (nodes of the RVE mesh with no
+ *    coordinate on an upper face, numbered in RVE-node order) and component
+ *    c; the corner class (independent node of the lowest corner) is fixed
+ *     and its entries are 0.
+ *  - Return value: HOM_OK or a hom_status code; details via hom_last_error.
+ *    No call aborts or throws.  One context per host thread.
+ */
+#ifndef HOM_H
+#define HOM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hom_ctx hom_ctx; /* opaque */
+
+typedef enum {
+  HOM_OK = 0,
+  HOM_ERR_INVALID_ARG = 1,     /* bad sizes, NULL where required, unsupported element */
+  HOM_ERR_MESH = 2,            /* unmatched periodic faces, det J <= 0, no lower corner */
+  HOM_ERR_NOT_SPD = 3,         /* Cholesky pivot <= 0 in an RVE (hom_error_info.rve, .row) */
+  HOM_ERR_JACOBIAN = 4,        /* micro J <= 0 at a quadrature point (finite strain) */
+  HOM_ERR_CG_NOT_CONVERGED = 5,/* macro CG hit max_iter before rtol */
+  HOM_ERR_CG_BREAKDOWN = 6,    /* p^T K p <= 0 in the macro CG */
+  HOM_ERR_CUDA = 7,            /* a CUDA runtime error (hom_error_info.cuda_error) */
+  HOM_ERR_OOM = 8              /* device allocation failed */
+} hom_status;
+
+/* Macro mesh.  Q1 (4 nodes, counter-clockwise) in 2-D,
+ * hex8 (bottom face CCW, then top face) in 3-D.  Dirichlet DOFs are
+ * dof = node*dim + comp with prescribed values (Gamma^phi); body_force
+ * is a constant body load per unit reference volume (eq:weakMech). */
+typedef struct {
+  int32_t dim;              /* 2 or 3 */
+  int32_t n_nodes;
+  int32_t n_elems;
+  int32_t nodes_per_elem;   /* 4 (2-D) or 8 (3-D) */
+  const double* coords;     /* host [n_nodes][dim] */
+  const int32_t* conn;      /* host [n_elems][nodes_per_elem] */
+  int32_t n_dirichlet;
+  const int32_t* dirichlet_dof;   /* host [n_dirichlet] */
+  const double* dirichlet_value;  /* host [n_dirichlet] (total prescribed value) */
+  const double* body_force;       /* host [dim] or NULL */
+} hom_macro_mesh;
+
+/* RVE mesh: an axis-aligned box meshed with Q1/hex8 elements whose opposite
+ * faces carry matching nodes; the periodic pairing (eq:Con (iii)) is
+ * found in hom_setup by coordinate matching. */
+typedef struct {
+  int32_t dim;
+  int32_t n_nodes;
+  int32_t n_elems;
+  int32_t nodes_per_elem;
+  const double* coords;     /* host [n_nodes][dim] */
+  const int32_t* conn;      /* host [n_elems][nodes_per_elem] */
+} hom_rve_mesh;
+
+/* Phase id per RVE element; per_rve = 1: [B][n_rve_elems], 0: [n_rve_elems] shared. */
+typedef struct {
+  int32_t per_rve;
+  const uint8_t* phase;     /* host */
+} hom_phase_field;
+
+/* Materials per phase.  kind 0: linear isotropic (E, nu), plane strain in 2-D.
+ * kind 1: the paper's Cook energy with beta = 0 (R11),
+ *   Psi = alpha (F:F - 2) + kappa/2 (J - 1)^2 - 2 alpha ln J, params (alpha, kappa), 2-D only. */
+typedef struct {
+  int32_t kind;
+  int32_t n_phases;
+  int32_t per_rve;          /* 1: [B][n_phases][2], 0: [n_phases][2] */
+  const double* params;     /* host */
+} hom_materials;
+
+typedef struct {
+  int32_t finite_strain;    /* must equal (materials.kind == 1) */
+  double cg_rtol;           /* relative residual ||r||/||b|| (default 1e-13 if <= 0) */
+  int32_t cg_max_iter;      /* default 20000 if <= 0 */
+  int32_t rve_chunk;        /* RVEs condensed per pass; <= 0: automatic (memory budget) */
+  int32_t check_info;       /* 1: hom_condense synchronises once to report NOT_SPD / JACOBIAN */
+  double mem_budget_gb;     /* K_ff pool budget for automatic chunking; <= 0: 48 GB */
+} hom_options;
+
+typedef struct {
+  int32_t n_rve;            /* B */
+  int32_t m;                /* tangent size */
+  int32_t n_pad;            /* fluctuation entries per RVE */
+  int32_t n_tiles;          /* 64x64 tiles per K_ff dimension */
+  int32_t n_macro_dof;
+  int32_t n_macro_free;
+  int32_t macro_nnz;        /* scalar CSR entries of the macro stiffness */
+  int32_t rve_chunk;
+  double rve_volume;        /* |Omega| */
+} hom_sizes;
+
+typedef struct {
+  int32_t iterations;
+  double rel_residual;      /* ||r|| / ||b|| at exit */
+  double rhs_norm;          /* ||b|| */
+} hom_solve_info;
+
+typedef struct {
+  int32_t code;
+  int32_t rve;              /* offending RVE or -1 */
+  int32_t row;              /* Cholesky row (NOT_SPD) or micro qp (JACOBIAN), or -1 */
+  int32_t cuda_error;
+  char message[256];
+} hom_error_info;
+
+/* Build a context: validates the meshes, finds the periodic pairing and the
+ * fixed corner, precomputes shape-gradient tables and the macro CSR pattern,
+ * copies phases and materials to the device and allocates all scratch.
+ * Synchronises `stream` before returning. */
+int hom_setup(hom_ctx** out, const hom_macro_mesh* macro, const hom_rve_mesh* rve,
+              const hom_phase_field* phases, const hom_materials* materials,
+              const hom_options* options, void* stream);
+
+int hom_get_sizes(const hom_ctx* ctx, hom_sizes* out);
+
+/* Macro kinematics at every macro qp: d_u [n_macro_dof] -> d_kin [B][m]:
+ * Voigt strain eps = B u (small strain) or F = I + grad u (finite strain). */
+int hom_macro_kinematics(hom_ctx* ctx, const double* d_u, double* d_kin, void* stream);
+
+/* Condense every RVE (eq:solution1/2): assemble K_ff, K_fe (, r_f) (eq:discreteSys_D/L,
+ * P:348-358), factor K_ff = G G^T, Y = G^-1 [K_fe | r_f], X = G^-T Y (stored in the
+ * context for recovery) and
+ *   d_C_eff [B][m][m] = <C> - Y^T Y / |Omega|     (row-major),
+ *   d_P_eff [B][m]    = <P> - K_Ff K_ff^-1 r_f / |Omega|   (finite strain; NULL otherwise),
+ *   d_P_avg [B][m]    = <P>                                 (finite strain; nullable).
+ * Small strain: d_kin is ignored (may be NULL).  Finite strain: d_kin = F per RVE [B][4];
+ * the current fluctuation state (hom_set_fluctuations / hom_recover_fluctuations) is used.
+ * With options.check_info the call synchronises once and returns HOM_ERR_NOT_SPD or
+ * HOM_ERR_JACOBIAN for the first failing RVE. */
+int hom_condense(hom_ctx* ctx, const double* d_kin, double* d_C_eff, double* d_P_eff,
+                 double* d_P_avg, void* stream);
+
+/* Solve the condensed macro system by Jacobi-preconditioned CG on the free DOFs:
+ *   K_FF x_F = -R_F - K_FD x_D,   K = sum_qp eta B^T D_b B,  R = sum_qp eta B^T S_b - f_body,
+ * with x_D = dirichlet_scale * dirichlet_value.  d_D = C_eff/A_eff [B][m][m]; d_S [B][m] or NULL.
+ * Linear: d_S = NULL, scale = 1 -> x = u.  Newton: d_S = P_eff, scale = increment -> x = du.
+ * d_x [n_macro_dof] is written in full (x_D included).  If `info` is non-NULL the call
+ * synchronises and fills it; CG failure is returned as a status either way (synchronising). */
+int hom_macro_solve(hom_ctx* ctx, const double* d_D, const double* d_S, double dirichlet_scale,
+                    double* d_x, hom_solve_info* info, void* stream);
+
+/* ||R_F||_2 with R = sum_qp eta B^T S_b - f_body (macro residual, eq:linSys); synchronises. */
+int hom_macro_residual_norm(hom_ctx* ctx, const double* d_S, double* norm, void* stream);
+
+/* Fluctuation recovery (eq:reduction P:388-390 / P:424-427).
+ * Small strain: d_w [B][N_pad] = -X_b eps_b(d_x)           (d_x = u).
+ * Finite strain: w += -(X_b dF_b(d_x) + K_ff^-1 r_f,b)       (d_x = du), internal state;
+ *                copied to d_w if non-NULL. */
+int hom_recover_fluctuations(hom_ctx* ctx, const double* d_x, double* d_w, void* stream);
+
+/* Finite-strain Newton update of both scales: u += du and
+ * w += -(X_b dF_b(du) + K_ff^-1 r_f,b), using the factorisation of the last
+ * hom_condense.  d_u, d_du [n_macro_dof]. */
+int hom_newton_update(hom_ctx* ctx, double* d_u, const double* d_du, void* stream);
+
+/* Finite-strain fluctuation state [B][N_pad] (checkpoint / parity-per-state). */
+int hom_set_fluctuations(hom_ctx* ctx, const double* d_w, void* stream);
+int hom_get_fluctuations(hom_ctx* ctx, double* d_w, void* stream);
+
+/* max_b ||r_f,b||_2 of the last finite-strain hom_condense (R_micro); synchronises. */
+int hom_micro_residual_max(hom_ctx* ctx, double* out, void* stream);
+
+/* Replace the phase field and/or material table (same shapes and per_rve flags as at
+ * setup) from HOST memory (pinned recommended) with asynchronous copies on `stream`;
+ * either pointer may be NULL to keep the current data.  This is the per-step input
+ * of an end-to-end run. */
+int hom_set_phases(hom_ctx* ctx, const uint8_t* h_phase, const double* h_params, void* stream);
+
+/* Kernel launches enqueued by this context since creation (for launch accounting). */
+int64_t hom_launch_count(const hom_ctx* ctx);
+
+/* Per-kernel-class device time, measured with CUDA events recorded around each launch
+ * on the launching stream while profiling is enabled. */
+enum {
+  HOM_PROF_RVE_ASSEMBLE = 0, /* K1 (and the finite-strain material pass) */
+  HOM_PROF_CONDENSE = 1,     /* K2-K4 fused Cholesky / solves / Schur */
+  HOM_PROF_MACRO_ASSEMBLE = 2,/* K5 + right-hand side */
+  HOM_PROF_CG = 3,           /* K6/K7 */
+  HOM_PROF_RECOVER = 4,      /* K8 + kinematics */
+  HOM_PROF_OTHER = 5,
+  HOM_PROF_N = 6
+};
+int hom_profile_enable(hom_ctx* ctx, int enable);
+/* Synchronises on the last recorded event, writes the accumulated milliseconds and
+ * launch counts per class (arrays of HOM_PROF_N), and resets the accumulators. */
+int hom_profile_read(hom_ctx* ctx, double* ms, int64_t* launches);
+
+int hom_last_error(const hom_ctx* ctx, hom_error_info* out);
+void hom_destroy(hom_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HOM_H */

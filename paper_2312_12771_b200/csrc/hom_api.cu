@@ -1,0 +1,675 @@
+// hom_api.cu -- the C-ABI of libhom.so (include/hom.h): context setup (a0),
+// and the four calls of the hot path (hom_condense, hom_macro_solve,
+// hom_recover_fluctuations, hom_macro_kinematics).  Host code here only
+// validates, builds index tables once, allocates, and enqueues kernels; every
+// step of the method runs on the GPU.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <vector>
+
+#include "hom_internal.cuh"
+
+using hom::CgState;
+using hom::MacroDev;
+using hom::RveDev;
+
+struct hom_ctx {
+  int device = 0;
+  hom_options opt{};
+  hom_error_info err{};
+  int64_t launches = 0;
+  int dim = 0, B = 0, m = 0, finite = 0, chunk = 0, macro_free = 0;
+  RveDev R{};
+  MacroDev M{};
+  std::vector<void*> allocs;
+  // chunk-local scratch
+  double *Kt = nullptr, *Y = nullptr, *Cavg = nullptr, *Pavg = nullptr, *Aq = nullptr, *Pq = nullptr;
+  // whole-batch state
+  double *X = nullptr, *rfn = nullptr, *w = nullptr, *kin = nullptr;
+  int *info = nullptr, *jflag = nullptr, *first_fail = nullptr;
+  // macro
+  double *val = nullptr, *diag = nullptr, *rhs = nullptr, *cgwork = nullptr, *Rfree = nullptr, *scal = nullptr;
+  CgState* cgst = nullptr;
+  size_t phase_bytes = 0, mat_bytes = 0;
+  // event profiling (hom_profile_enable / hom_profile_read)
+  struct ProfRec {
+    int cls;
+    cudaEvent_t a, b;
+  };
+  bool prof_on = false;
+  std::vector<ProfRec> prof;
+  std::vector<cudaEvent_t> pool, all_events;
+};
+
+namespace {
+
+cudaEvent_t prof_event(hom_ctx* c) {
+  if (!c->pool.empty()) {
+    cudaEvent_t e = c->pool.back();
+    c->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  c->all_events.push_back(e);
+  return e;
+}
+
+constexpr int JFLAG_NONE = 0x7f7f7f7f;  // jflag bytes memset to 0x7f: no failing qp
+
+int set_err(hom_ctx* c, int code, const char* msg, int rve = -1, int row = -1, int cuda = 0) {
+  if (c) {
+    c->err.code = code;
+    c->err.rve = rve;
+    c->err.row = row;
+    c->err.cuda_error = cuda;
+    snprintf(c->err.message, sizeof(c->err.message), "%s", msg);
+  }
+  return code;
+}
+
+int check_cuda(hom_ctx* c, cudaError_t e, const char* where) {
+  if (e == cudaSuccess) return HOM_OK;
+  char buf[256];
+  snprintf(buf, sizeof(buf), "%s: %s", where, cudaGetErrorString(e));
+  return set_err(c, e == cudaErrorMemoryAllocation ? HOM_ERR_OOM : HOM_ERR_CUDA, buf, -1, -1, (int)e);
+}
+
+template <typename T>
+T* dalloc(hom_ctx* c, size_t n, int* rc) {
+  if (*rc) return nullptr;
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T));
+  if (e != cudaSuccess) {
+    *rc = check_cuda(c, e, "cudaMalloc");
+    return nullptr;
+  }
+  c->allocs.push_back(p);
+  return static_cast<T*>(p);
+}
+
+template <typename T>
+T* upload(hom_ctx* c, const std::vector<T>& v, cudaStream_t s, int* rc) {
+  T* p = dalloc<T>(c, v.size(), rc);
+  if (*rc) return nullptr;
+  if (!v.empty()) {
+    cudaError_t e = cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s);
+    if (e != cudaSuccess) *rc = check_cuda(c, e, "cudaMemcpyAsync");
+  }
+  return p;
+}
+
+// Reference element: multilinear Lagrange on [-1,1]^d, local order CCW (2-D) /
+// bottom face then top face (3-D); 2-point Gauss per direction, x fastest.
+double ref_sign(int dim, int a, int k) {
+  int a2 = a & 3;
+  if (k == 0) return (a2 == 1 || a2 == 2) ? 1.0 : -1.0;
+  if (k == 1) return (a2 >= 2) ? 1.0 : -1.0;
+  (void)dim;
+  return a >= 4 ? 1.0 : -1.0;
+}
+
+// grads [nq][nen][dim], wdet [nq], shp [nq][nen] of one element; returns false if det J <= 0.
+bool element_tables(int dim, const double* x /*[nen][dim]*/, double* grad, double* wdet, double* shp) {
+  const int nen = 1 << dim, nq = 1 << dim;
+  const double gp = 1.0 / std::sqrt(3.0);
+  for (int q = 0; q < nq; ++q) {
+    double xi[3];
+    for (int k = 0; k < dim; ++k) xi[k] = ((q >> k) & 1) ? gp : -gp;
+    double dN[8][3], N[8];
+    for (int a = 0; a < nen; ++a) {
+      double f[3];
+      for (int k = 0; k < dim; ++k) f[k] = 0.5 * (1.0 + ref_sign(dim, a, k) * xi[k]);
+      N[a] = 1.0;
+      for (int k = 0; k < dim; ++k) N[a] *= f[k];
+      for (int k = 0; k < dim; ++k) {
+        double d = 0.5 * ref_sign(dim, a, k);
+        for (int l = 0; l < dim; ++l)
+          if (l != k) d *= f[l];
+        dN[a][k] = d;
+      }
+    }
+    double J[3][3] = {};
+    for (int a = 0; a < nen; ++a)
+      for (int i = 0; i < dim; ++i)
+        for (int j = 0; j < dim; ++j) J[i][j] += x[a * dim + i] * dN[a][j];
+    double det, Ji[3][3];
+    if (dim == 2) {
+      det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
+      Ji[0][0] = J[1][1] / det; Ji[0][1] = -J[0][1] / det;
+      Ji[1][0] = -J[1][0] / det; Ji[1][1] = J[0][0] / det;
+    } else {
+      double c00 = J[1][1] * J[2][2] - J[1][2] * J[2][1];
+      double c01 = J[1][2] * J[2][0] - J[1][0] * J[2][2];
+      double c02 = J[1][0] * J[2][1] - J[1][1] * J[2][0];
+      det = J[0][0] * c00 + J[0][1] * c01 + J[0][2] * c02;
+      Ji[0][0] = c00 / det;
+      Ji[1][0] = c01 / det;
+      Ji[2][0] = c02 / det;
+      Ji[0][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) / det;
+      Ji[1][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) / det;
+      Ji[2][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) / det;
+      Ji[0][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) / det;
+      Ji[1][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) / det;
+      Ji[2][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) / det;
+    }
+    if (!(det > 0.0)) return false;
+    wdet[q] = det;  // Gauss weights are 1
+    for (int a = 0; a < nen; ++a) {
+      if (shp) shp[q * nen + a] = N[a];
+      for (int i = 0; i < dim; ++i) {
+        double s = 0.0;
+        for (int j = 0; j < dim; ++j) s += dN[a][j] * Ji[j][i];
+        grad[(q * nen + a) * dim + i] = s;
+      }
+    }
+  }
+  return true;
+}
+
+// Shared-element triples between node pairs of a mesh with element->node map `en`.
+struct PairTables {
+  std::vector<int> inc_ptr, inc;          // node -> (e<<4 | a)
+  std::vector<int> nbr_ptr, nbr, owner;   // node -> sorted neighbours
+  std::vector<int> sh_ptr, sh;            // neighbour entry -> (e<<8 | a<<4 | b)
+};
+
+PairTables build_pairs(int n_nodes, int ne, int nen, const std::vector<int>& en) {
+  PairTables T;
+  std::vector<std::vector<int>> inc(n_nodes);
+  for (int e = 0; e < ne; ++e)
+    for (int a = 0; a < nen; ++a) inc[en[e * nen + a]].push_back((e << 4) | a);
+  T.inc_ptr.assign(n_nodes + 1, 0);
+  for (int p = 0; p < n_nodes; ++p) {
+    T.inc_ptr[p + 1] = T.inc_ptr[p] + (int)inc[p].size();
+    T.inc.insert(T.inc.end(), inc[p].begin(), inc[p].end());
+  }
+  T.nbr_ptr.assign(n_nodes + 1, 0);
+  T.sh_ptr.push_back(0);
+  for (int p = 0; p < n_nodes; ++p) {
+    std::map<int, std::vector<int>> nb;  // sorted by neighbour
+    for (int code : inc[p]) {
+      int e = code >> 4, a = code & 15;
+      for (int b = 0; b < nen; ++b) nb[en[e * nen + b]].push_back((e << 8) | (a << 4) | b);
+    }
+    for (auto& kv : nb) {
+      T.nbr.push_back(kv.first);
+      T.owner.push_back(p);
+      T.sh.insert(T.sh.end(), kv.second.begin(), kv.second.end());
+      T.sh_ptr.push_back((int)T.sh.size());
+    }
+    T.nbr_ptr[p + 1] = (int)T.nbr.size();
+  }
+  return T;
+}
+
+}  // namespace
+
+extern "C" {
+
+int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve, const hom_phase_field* ph,
+              const hom_materials* mat, const hom_options* options, void* stream) {
+  if (!out) return HOM_ERR_INVALID_ARG;
+  *out = nullptr;
+  hom_ctx* c = new hom_ctx();
+  cudaStream_t s = (cudaStream_t)stream;
+  int rc = HOM_OK;
+  auto fail = [&](int code, const char* msg) {
+    set_err(c, code, msg);
+    return code;
+  };
+  if (!mac || !rve || !ph || !mat || !options || !mac->coords || !mac->conn || !rve->coords || !rve->conn ||
+      !ph->phase || !mat->params) {
+    rc = fail(HOM_ERR_INVALID_ARG, "NULL argument");
+    *out = c;
+    return rc;
+  }
+  c->opt = *options;
+  if (c->opt.cg_rtol <= 0) c->opt.cg_rtol = 1e-13;
+  if (c->opt.cg_max_iter <= 0) c->opt.cg_max_iter = 20000;
+  if (c->opt.mem_budget_gb <= 0) c->opt.mem_budget_gb = 48.0;
+  cudaGetDevice(&c->device);
+  const int dim = mac->dim;
+  *out = c;
+  if ((dim != 2 && dim != 3) || rve->dim != dim || mac->nodes_per_elem != (1 << dim) ||
+      rve->nodes_per_elem != (1 << dim) || mac->n_elems <= 0 || rve->n_elems <= 0 || mat->n_phases <= 0 ||
+      (mat->kind != 0 && mat->kind != 1) || (mat->kind == 1 && dim != 2) ||
+      (options->finite_strain != 0) != (mat->kind == 1))
+    return fail(HOM_ERR_INVALID_ARG, "unsupported dimension / element / material combination");
+  const int nen = 1 << dim, nq = 1 << dim;
+  c->dim = dim;
+  c->finite = mat->kind == 1;
+  c->m = c->finite ? 4 : (dim == 2 ? 3 : 6);
+  c->B = mac->n_elems * nq;
+
+  // ------------------------------------------------------------ macro mesh
+  MacroDev& M = c->M;
+  M.dim = dim; M.nen = nen; M.nq = nq; M.ne = mac->n_elems; M.n_nodes = mac->n_nodes;
+  M.ndof = mac->n_nodes * dim; M.m = c->m; M.finite = c->finite;
+  std::vector<int> mconn(mac->conn, mac->conn + (size_t)M.ne * nen);
+  for (int v : mconn)
+    if (v < 0 || v >= M.n_nodes) return fail(HOM_ERR_MESH, "macro connectivity out of range");
+  std::vector<double> mgrad((size_t)M.ne * nq * nen * dim), mw((size_t)M.ne * nq), shp((size_t)nq * nen);
+  for (int e = 0; e < M.ne; ++e) {
+    double x[8 * 3];
+    for (int a = 0; a < nen; ++a)
+      for (int k = 0; k < dim; ++k) x[a * dim + k] = mac->coords[(size_t)mconn[e * nen + a] * dim + k];
+    if (!element_tables(dim, x, &mgrad[(size_t)e * nq * nen * dim], &mw[(size_t)e * nq], e == 0 ? shp.data() : nullptr))
+      return fail(HOM_ERR_MESH, "macro element with det J <= 0");
+  }
+  PairTables MP = build_pairs(M.n_nodes, M.ne, nen, mconn);
+  // scalar CSR over all DOFs, node-block structure
+  std::vector<int> rowptr(M.ndof + 1, 0), col, nzblk;
+  std::vector<uint8_t> nzcc;
+  for (int n = 0; n < M.n_nodes; ++n)
+    for (int ci = 0; ci < dim; ++ci) {
+      int row = n * dim + ci;
+      for (int k = MP.nbr_ptr[n]; k < MP.nbr_ptr[n + 1]; ++k)
+        for (int cj = 0; cj < dim; ++cj) {
+          int cl = MP.nbr[k] * dim + cj;
+          col.push_back(cl);
+          nzblk.push_back(k);
+          nzcc.push_back((uint8_t)(ci * 4 + cj + (cl == row ? 16 : 0)));
+        }
+      rowptr[row + 1] = (int)col.size();
+    }
+  M.nnz = (int)col.size();
+  std::vector<uint8_t> dmask(M.ndof, 0);
+  std::vector<double> dval(M.ndof, 0.0), fbody(M.ndof, 0.0);
+  if (mac->n_dirichlet > 0 && (!mac->dirichlet_dof || !mac->dirichlet_value))
+    return fail(HOM_ERR_INVALID_ARG, "Dirichlet arrays missing");
+  for (int i = 0; i < mac->n_dirichlet; ++i) {
+    int d = mac->dirichlet_dof[i];
+    if (d < 0 || d >= M.ndof) return fail(HOM_ERR_INVALID_ARG, "Dirichlet DOF out of range");
+    dmask[d] = 1;
+    dval[d] = mac->dirichlet_value[i];
+  }
+  c->macro_free = 0;
+  for (int i = 0; i < M.ndof; ++i) c->macro_free += !dmask[i];
+  if (mac->body_force) {  // consistent body load f_A = sum eta N^A b (a0 setup, eq:linSys)
+    for (int e = 0; e < M.ne; ++e)
+      for (int q = 0; q < nq; ++q)
+        for (int a = 0; a < nen; ++a)
+          for (int k = 0; k < dim; ++k)
+            fbody[(size_t)mconn[e * nen + a] * dim + k] += mw[(size_t)e * nq + q] * shp[q * nen + a] * mac->body_force[k];
+  }
+
+  // ------------------------------------------------------------ RVE mesh, periodic pairing
+  RveDev& R = c->R;
+  R.dim = dim; R.nen = nen; R.nq = nq; R.ne = rve->n_elems;
+  R.m = c->m; R.finite = c->finite; R.ncol = c->m + (c->finite ? 1 : 0);
+  const int rn = rve->n_nodes;
+  double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+  for (int n = 0; n < rn; ++n)
+    for (int k = 0; k < dim; ++k) {
+      lo[k] = std::min(lo[k], rve->coords[(size_t)n * dim + k]);
+      hi[k] = std::max(hi[k], rve->coords[(size_t)n * dim + k]);
+    }
+  double Lmax = 0.0;
+  for (int k = 0; k < dim; ++k) Lmax = std::max(Lmax, hi[k] - lo[k]);
+  if (!(Lmax > 0.0)) return fail(HOM_ERR_MESH, "degenerate RVE box");
+  const double tol = 1e-9 * Lmax;
+  auto key_of = [&](int n, bool fold, int* lower_cnt) {
+    std::vector<long long> key(dim);
+    int lc = 0;
+    for (int k = 0; k < dim; ++k) {
+      double x = rve->coords[(size_t)n * dim + k] - lo[k];
+      if (fold && std::fabs(x - (hi[k] - lo[k])) < tol) x = 0.0;
+      if (std::fabs(x) < tol) { x = 0.0; lc++; }
+      key[k] = std::llround(x / (1e-7 * Lmax));
+    }
+    if (lower_cnt) *lower_cnt = lc;
+    return key;
+  };
+  auto on_upper = [&](int n) {
+    for (int k = 0; k < dim; ++k)
+      if (std::fabs(rve->coords[(size_t)n * dim + k] - hi[k]) < tol) return true;
+    return false;
+  };
+  std::map<std::vector<long long>, int> indep_of;
+  std::vector<int> indep(rn, -1), members, expect;
+  for (int n = 0; n < rn; ++n) {
+    if (on_upper(n)) continue;
+    int lc = 0;
+    auto key = key_of(n, false, &lc);
+    if (indep_of.count(key)) return fail(HOM_ERR_MESH, "duplicate RVE node");
+    int id = (int)indep_of.size();
+    indep_of[key] = id;
+    indep[n] = id;
+    members.push_back(1);
+    expect.push_back(1 << lc);
+  }
+  for (int n = 0; n < rn; ++n) {
+    if (!on_upper(n)) continue;
+    auto key = key_of(n, true, nullptr);
+    auto it = indep_of.find(key);
+    if (it == indep_of.end()) return fail(HOM_ERR_MESH, "unmatched periodic RVE node");
+    indep[n] = it->second;
+    members[it->second]++;
+  }
+  for (size_t p = 0; p < members.size(); ++p)
+    if (members[p] != expect[p]) return fail(HOM_ERR_MESH, "periodic faces do not match");
+  R.n_indep = (int)indep_of.size();
+  {
+    std::vector<long long> zero(dim, 0);
+    auto it = indep_of.find(zero);
+    if (it == indep_of.end()) return fail(HOM_ERR_MESH, "RVE has no node at its lower corner");
+    R.corner = it->second;
+  }
+  R.npad = dim * R.n_indep;
+  R.nt = (R.npad + hom::TILE - 1) / hom::TILE;
+  R.NT = R.nt * hom::TILE;
+  std::vector<int> rconn(rve->conn, rve->conn + (size_t)R.ne * nen), eind((size_t)R.ne * nen);
+  for (size_t i = 0; i < rconn.size(); ++i) {
+    if (rconn[i] < 0 || rconn[i] >= rn) return fail(HOM_ERR_MESH, "RVE connectivity out of range");
+    eind[i] = indep[rconn[i]];
+  }
+  if (R.ne >= (1 << 23)) return fail(HOM_ERR_INVALID_ARG, "RVE too large");
+  std::vector<double> rgrad((size_t)R.ne * nq * nen * dim), rw((size_t)R.ne * nq);
+  double vol = 0.0;
+  for (int e = 0; e < R.ne; ++e) {
+    double x[8 * 3];
+    for (int a = 0; a < nen; ++a)
+      for (int k = 0; k < dim; ++k) x[a * dim + k] = rve->coords[(size_t)rconn[e * nen + a] * dim + k];
+    if (!element_tables(dim, x, &rgrad[(size_t)e * nq * nen * dim], &rw[(size_t)e * nq], nullptr))
+      return fail(HOM_ERR_MESH, "RVE element with det J <= 0");
+    for (int q = 0; q < nq; ++q) vol += rw[(size_t)e * nq + q];
+  }
+  R.vol = vol;
+  PairTables RP = build_pairs(R.n_indep, R.ne, nen, eind);
+  R.phase_per_rve = ph->per_rve ? 1 : 0;
+  R.mat_per_rve = mat->per_rve ? 1 : 0;
+  R.n_phase = mat->n_phases;
+  size_t nph_entries = (size_t)(R.phase_per_rve ? c->B : 1) * R.ne;
+  std::vector<uint8_t> phase(ph->phase, ph->phase + nph_entries);
+  for (uint8_t v : phase)
+    if (v >= mat->n_phases) return fail(HOM_ERR_INVALID_ARG, "phase id >= n_phases");
+  std::vector<double> params(mat->params, mat->params + (size_t)(R.mat_per_rve ? c->B : 1) * R.n_phase * 2);
+
+  // ------------------------------------------------------------ chunking + allocation
+  const size_t tiles = (size_t)R.nt * (R.nt + 1) / 2;
+  const size_t per_rve = tiles * hom::TILE_ELEMS * 8 + (size_t)R.NT * hom::RHSW * 8 + 64 * 8 * 2 +
+                         (c->finite ? (size_t)R.ne * nq * 20 * 8 : 0);
+  int chunk = c->opt.rve_chunk > 0 ? c->opt.rve_chunk
+                                   : (int)std::min<double>(c->B, std::floor(c->opt.mem_budget_gb * 1e9 / per_rve));
+  chunk = std::max(1, std::min(chunk, c->B));
+  c->chunk = chunk;
+
+  R.elem_indep = upload(c, eind, s, &rc);
+  R.grad = upload(c, rgrad, s, &rc);
+  R.wdet = upload(c, rw, s, &rc);
+  R.inc_ptr = upload(c, RP.inc_ptr, s, &rc);
+  R.inc = upload(c, RP.inc, s, &rc);
+  R.nbr_ptr = upload(c, RP.nbr_ptr, s, &rc);
+  R.nbr = upload(c, RP.nbr, s, &rc);
+  R.nbr_owner = upload(c, RP.owner, s, &rc);
+  R.sh_ptr = upload(c, RP.sh_ptr, s, &rc);
+  R.sh = upload(c, RP.sh, s, &rc);
+  R.phase = upload(c, phase, s, &rc);
+  R.mat = upload(c, params, s, &rc);
+  c->phase_bytes = phase.size();
+  c->mat_bytes = params.size() * sizeof(double);
+  M.conn = upload(c, mconn, s, &rc);
+  M.grad = upload(c, mgrad, s, &rc);
+  M.shp = upload(c, shp, s, &rc);
+  M.wdet = upload(c, mw, s, &rc);
+  M.rowptr = upload(c, rowptr, s, &rc);
+  M.col = upload(c, col, s, &rc);
+  M.nz_blk = upload(c, nzblk, s, &rc);
+  M.nz_cc = upload(c, nzcc, s, &rc);
+  M.blk_ptr = upload(c, MP.sh_ptr, s, &rc);
+  M.blk_sh = upload(c, MP.sh, s, &rc);
+  M.ninc_ptr = upload(c, MP.inc_ptr, s, &rc);
+  M.ninc = upload(c, MP.inc, s, &rc);
+  M.dmask = upload(c, dmask, s, &rc);
+  M.dval = upload(c, dval, s, &rc);
+  M.fbody = upload(c, fbody, s, &rc);
+
+  c->Kt = dalloc<double>(c, tiles * hom::TILE_ELEMS * chunk, &rc);
+  c->Y = dalloc<double>(c, (size_t)R.NT * hom::RHSW * chunk, &rc);
+  c->Cavg = dalloc<double>(c, (size_t)64 * chunk, &rc);
+  c->Pavg = dalloc<double>(c, (size_t)8 * chunk, &rc);
+  if (c->finite) {
+    c->Aq = dalloc<double>(c, (size_t)chunk * R.ne * nq * 16, &rc);
+    c->Pq = dalloc<double>(c, (size_t)chunk * R.ne * nq * 4, &rc);
+    c->w = dalloc<double>(c, (size_t)c->B * R.npad, &rc);
+  }
+  c->X = dalloc<double>(c, (size_t)c->B * R.NT * hom::RHSW, &rc);
+  c->rfn = dalloc<double>(c, c->B, &rc);
+  c->kin = dalloc<double>(c, (size_t)c->B * c->m, &rc);
+  c->info = dalloc<int>(c, c->B, &rc);
+  c->jflag = dalloc<int>(c, c->B, &rc);
+  c->first_fail = dalloc<int>(c, 2, &rc);
+  c->val = dalloc<double>(c, M.nnz, &rc);
+  c->diag = dalloc<double>(c, M.ndof, &rc);
+  c->rhs = dalloc<double>(c, M.ndof, &rc);
+  c->Rfree = dalloc<double>(c, M.ndof, &rc);
+  c->cgwork = dalloc<double>(c, (size_t)4 * M.ndof, &rc);
+  c->scal = dalloc<double>(c, 4, &rc);
+  c->cgst = dalloc<CgState>(c, 1, &rc);
+  if (rc) return rc;
+  if (c->finite) cudaMemsetAsync(c->w, 0, sizeof(double) * (size_t)c->B * R.npad, s);
+  cudaMemsetAsync(c->rfn, 0, sizeof(double) * c->B, s);
+  rc = check_cuda(c, cudaStreamSynchronize(s), "hom_setup");
+  return rc;
+}
+
+int hom_get_sizes(const hom_ctx* c, hom_sizes* o) {
+  if (!c || !o) return HOM_ERR_INVALID_ARG;
+  o->n_rve = c->B;
+  o->m = c->m;
+  o->n_pad = c->R.npad;
+  o->n_tiles = c->R.nt;
+  o->n_macro_dof = c->M.ndof;
+  o->n_macro_free = c->macro_free;
+  o->macro_nnz = c->M.nnz;
+  o->rve_chunk = c->chunk;
+  o->rve_volume = c->R.vol;
+  return HOM_OK;
+}
+
+// Every kernel launch goes through run(): it counts the launch and, while profiling
+// is enabled, brackets it with CUDA events on the launching stream.
+extern "C++" template <typename F>
+void run(hom_ctx* c, int cls, cudaStream_t s, F&& f) {
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (c->prof_on) {
+    a = prof_event(c);
+    cudaEventRecord(a, s);
+  }
+  f();
+  c->launches++;
+  if (c->prof_on) {
+    b = prof_event(c);
+    cudaEventRecord(b, s);
+    c->prof.push_back({cls, a, b});
+  }
+}
+
+int hom_macro_kinematics(hom_ctx* c, const double* d_u, double* d_kin, void* stream) {
+  if (!c || !d_u || !d_kin) return set_err(c, HOM_ERR_INVALID_ARG, "hom_macro_kinematics: NULL");
+  run(c, HOM_PROF_RECOVER, (cudaStream_t)stream,
+      [&] { hom::launch_macro_kin(c->M, d_u, d_kin, 1, (cudaStream_t)stream); });
+  return check_cuda(c, cudaGetLastError(), "hom_macro_kinematics");
+}
+
+int hom_condense(hom_ctx* c, const double* d_kin, double* d_C_eff, double* d_P_eff, double* d_P_avg,
+                 void* stream) {
+  if (!c || !d_C_eff) return set_err(c, HOM_ERR_INVALID_ARG, "hom_condense: NULL");
+  if (c->finite && !d_kin) return set_err(c, HOM_ERR_INVALID_ARG, "hom_condense: finite strain needs F");
+  cudaStream_t s = (cudaStream_t)stream;
+  const RveDev& R = c->R;
+  cudaMemsetAsync(c->info, 0, sizeof(int) * c->B, s);
+  if (c->finite) cudaMemsetAsync(c->jflag, 0x7f, sizeof(int) * c->B, s);  // = JFLAG_NONE
+  for (int b0 = 0; b0 < c->B; b0 += c->chunk) {
+    int nb = std::min(c->chunk, c->B - b0);
+    if (c->finite)
+      run(c, HOM_PROF_RVE_ASSEMBLE, s,
+          [&] { hom::launch_rve_material_nh(R, b0, nb, d_kin, c->w, c->Aq, c->Pq, c->jflag, s); });
+    run(c, HOM_PROF_RVE_ASSEMBLE, s,
+        [&] { hom::launch_rve_assemble(R, b0, nb, c->Kt, c->Y, c->Cavg, c->Pavg, c->rfn, c->Aq, c->Pq, s); });
+    run(c, HOM_PROF_CONDENSE, s, [&] {
+      hom::launch_condense(R, b0, nb, c->Kt, c->Y, c->Cavg, c->Pavg, d_C_eff, d_P_eff, d_P_avg, c->X, c->info, s);
+    });
+  }
+  int rc = check_cuda(c, cudaGetLastError(), "hom_condense");
+  if (rc || !c->opt.check_info) return rc;
+  int h[2] = {INT_MAX, INT_MAX};
+  cudaMemcpyAsync(c->first_fail, h, sizeof(h), cudaMemcpyHostToDevice, s);
+  run(c, HOM_PROF_OTHER, s, [&] { hom::launch_first_fail(c->info, c->B, 0, c->first_fail, s); });
+  if (c->finite)
+    run(c, HOM_PROF_OTHER, s, [&] { hom::launch_first_fail(c->jflag, c->B, JFLAG_NONE, c->first_fail + 1, s); });
+  cudaMemcpyAsync(h, c->first_fail, sizeof(h), cudaMemcpyDeviceToHost, s);
+  rc = check_cuda(c, cudaStreamSynchronize(s), "hom_condense sync");
+  if (rc) return rc;
+  if (h[1] != INT_MAX) {
+    int q = -1;
+    cudaMemcpy(&q, c->jflag + h[1], sizeof(int), cudaMemcpyDeviceToHost);
+    return set_err(c, HOM_ERR_JACOBIAN, "micro Jacobian J <= 0", h[1], q);
+  }
+  if (h[0] != INT_MAX) {
+    int row = -1;
+    cudaMemcpy(&row, c->info + h[0], sizeof(int), cudaMemcpyDeviceToHost);
+    return set_err(c, HOM_ERR_NOT_SPD, "K_ff not positive definite", h[0], row - 1);
+  }
+  return HOM_OK;
+}
+
+int hom_macro_solve(hom_ctx* c, const double* d_D, const double* d_S, double scale, double* d_x,
+                    hom_solve_info* info, void* stream) {
+  if (!c || !d_D || !d_x) return set_err(c, HOM_ERR_INVALID_ARG, "hom_macro_solve: NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  run(c, HOM_PROF_MACRO_ASSEMBLE, s, [&] { hom::launch_macro_assemble(c->M, d_D, c->val, c->diag, s); });
+  run(c, HOM_PROF_MACRO_ASSEMBLE, s, [&] { hom::launch_macro_rhs(c->M, c->val, d_S, scale, c->rhs, nullptr, s); });
+  run(c, HOM_PROF_CG, s, [&] {
+    hom::launch_macro_cg(c->M, c->val, c->diag, c->rhs, scale, c->opt.cg_rtol, c->opt.cg_max_iter, d_x,
+                         c->cgwork, c->cgst, s);
+  });
+  int rc = check_cuda(c, cudaGetLastError(), "hom_macro_solve");
+  if (rc) return rc;
+  CgState st{};
+  cudaMemcpyAsync(&st, c->cgst, sizeof(st), cudaMemcpyDeviceToHost, s);
+  rc = check_cuda(c, cudaStreamSynchronize(s), "hom_macro_solve sync");
+  if (rc) return rc;
+  if (info) {
+    info->iterations = st.iterations;
+    info->rel_residual = st.rel_residual;
+    info->rhs_norm = st.rhs_norm;
+  }
+  if (st.status == 5) return set_err(c, HOM_ERR_CG_NOT_CONVERGED, "macro CG did not converge");
+  if (st.status == 6) return set_err(c, HOM_ERR_CG_BREAKDOWN, "macro CG breakdown (p^T K p <= 0)");
+  return HOM_OK;
+}
+
+int hom_macro_residual_norm(hom_ctx* c, const double* d_S, double* norm, void* stream) {
+  if (!c || !norm) return set_err(c, HOM_ERR_INVALID_ARG, "hom_macro_residual_norm: NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  run(c, HOM_PROF_MACRO_ASSEMBLE, s, [&] { hom::launch_macro_rhs(c->M, nullptr, d_S, 0.0, nullptr, c->Rfree, s); });
+  run(c, HOM_PROF_OTHER, s, [&] { hom::launch_norm(c->Rfree, c->M.ndof, c->scal, s); });
+  cudaMemcpyAsync(norm, c->scal, sizeof(double), cudaMemcpyDeviceToHost, s);
+  return check_cuda(c, cudaStreamSynchronize(s), "hom_macro_residual_norm");
+}
+
+int hom_recover_fluctuations(hom_ctx* c, const double* d_x, double* d_w, void* stream) {
+  if (!c || !d_x) return set_err(c, HOM_ERR_INVALID_ARG, "hom_recover_fluctuations: NULL");
+  if (!c->finite && !d_w) return set_err(c, HOM_ERR_INVALID_ARG, "hom_recover_fluctuations: d_w NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  run(c, HOM_PROF_RECOVER, s, [&] { hom::launch_macro_kin(c->M, d_x, c->kin, 0, s); });
+  if (c->finite) {
+    run(c, HOM_PROF_RECOVER, s, [&] { hom::launch_recover(c->R, c->B, c->X, c->kin, c->w, 1, s); });
+    if (d_w) cudaMemcpyAsync(d_w, c->w, sizeof(double) * (size_t)c->B * c->R.npad, cudaMemcpyDeviceToDevice, s);
+  } else {
+    run(c, HOM_PROF_RECOVER, s, [&] { hom::launch_recover(c->R, c->B, c->X, c->kin, d_w, 0, s); });
+  }
+  return check_cuda(c, cudaGetLastError(), "hom_recover_fluctuations");
+}
+
+int hom_newton_update(hom_ctx* c, double* d_u, const double* d_du, void* stream) {
+  if (!c || !d_u || !d_du || !c->finite) return set_err(c, HOM_ERR_INVALID_ARG, "hom_newton_update");
+  cudaStream_t s = (cudaStream_t)stream;
+  run(c, HOM_PROF_RECOVER, s, [&] { hom::launch_macro_kin(c->M, d_du, c->kin, 0, s); });
+  run(c, HOM_PROF_RECOVER, s, [&] { hom::launch_recover(c->R, c->B, c->X, c->kin, c->w, 1, s); });
+  run(c, HOM_PROF_OTHER, s, [&] { hom::launch_axpy(d_u, d_du, 1.0, c->M.ndof, s); });
+  return check_cuda(c, cudaGetLastError(), "hom_newton_update");
+}
+
+int hom_set_fluctuations(hom_ctx* c, const double* d_w, void* stream) {
+  if (!c || !d_w || !c->finite) return set_err(c, HOM_ERR_INVALID_ARG, "hom_set_fluctuations");
+  cudaMemcpyAsync(c->w, d_w, sizeof(double) * (size_t)c->B * c->R.npad, cudaMemcpyDeviceToDevice,
+                  (cudaStream_t)stream);
+  return check_cuda(c, cudaGetLastError(), "hom_set_fluctuations");
+}
+
+int hom_get_fluctuations(hom_ctx* c, double* d_w, void* stream) {
+  if (!c || !d_w || !c->finite) return set_err(c, HOM_ERR_INVALID_ARG, "hom_get_fluctuations");
+  cudaMemcpyAsync(d_w, c->w, sizeof(double) * (size_t)c->B * c->R.npad, cudaMemcpyDeviceToDevice,
+                  (cudaStream_t)stream);
+  return check_cuda(c, cudaGetLastError(), "hom_get_fluctuations");
+}
+
+int hom_micro_residual_max(hom_ctx* c, double* out, void* stream) {
+  if (!c || !out) return set_err(c, HOM_ERR_INVALID_ARG, "hom_micro_residual_max: NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  run(c, HOM_PROF_OTHER, s, [&] { hom::launch_max_reduce(c->rfn, c->B, c->scal + 1, s); });
+  cudaMemcpyAsync(out, c->scal + 1, sizeof(double), cudaMemcpyDeviceToHost, s);
+  return check_cuda(c, cudaStreamSynchronize(s), "hom_micro_residual_max");
+}
+
+int hom_set_phases(hom_ctx* c, const uint8_t* h_phase, const double* h_params, void* stream) {
+  if (!c) return HOM_ERR_INVALID_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (h_phase)
+    cudaMemcpyAsync(const_cast<uint8_t*>(c->R.phase), h_phase, c->phase_bytes, cudaMemcpyHostToDevice, s);
+  if (h_params)
+    cudaMemcpyAsync(const_cast<double*>(c->R.mat), h_params, c->mat_bytes, cudaMemcpyHostToDevice, s);
+  return check_cuda(c, cudaGetLastError(), "hom_set_phases");
+}
+
+int hom_profile_enable(hom_ctx* c, int enable) {
+  if (!c) return HOM_ERR_INVALID_ARG;
+  c->prof_on = enable != 0;
+  return HOM_OK;
+}
+
+int hom_profile_read(hom_ctx* c, double* ms, int64_t* launches) {
+  if (!c || !ms) return HOM_ERR_INVALID_ARG;
+  for (int i = 0; i < HOM_PROF_N; ++i) {
+    ms[i] = 0.0;
+    if (launches) launches[i] = 0;
+  }
+  if (!c->prof.empty()) {
+    int rc = check_cuda(c, cudaEventSynchronize(c->prof.back().b), "hom_profile_read");
+    if (rc) return rc;
+  }
+  for (auto& r : c->prof) {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, r.a, r.b);
+    ms[r.cls] += t;
+    if (launches) launches[r.cls]++;
+    c->pool.push_back(r.a);
+    c->pool.push_back(r.b);
+  }
+  c->prof.clear();
+  return HOM_OK;
+}
+
+int64_t hom_launch_count(const hom_ctx* c) { return c ? c->launches : 0; }
+
+int hom_last_error(const hom_ctx* c, hom_error_info* out) {
+  if (!c || !out) return HOM_ERR_INVALID_ARG;
+  *out = c->err;
+  return HOM_OK;
+}
+
+void hom_destroy(hom_ctx* c) {
+  if (!c) return;
+  for (void* p : c->allocs) cudaFree(p);
+  for (cudaEvent_t e : c->all_events) cudaEventDestroy(e);
+  delete c;
+}
+
+}  // extern "C"

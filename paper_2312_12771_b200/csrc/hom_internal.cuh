@@ -1,0 +1,92 @@
+// hom_internal.cuh -- device-side data structures and kernel entry points of libhom.so.
+// Product path only; shares nothing with oracle/ (DESIGN.md §2).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/hom.h"
+
+namespace hom {
+
+constexpr int TILE = 64;          // K_ff tile edge (rows and columns)
+constexpr int TILE_ELEMS = TILE * TILE;
+constexpr int KC = 32;            // k-chunk staged per pipeline stage
+constexpr int RHSW = 8;           // right-hand-side columns kept per RVE (m <= 6, +1 for r_f)
+constexpr int NTHR = 256;         // threads per CTA of the RVE kernels
+
+// Geometry + topology of the (shared) RVE mesh and the per-RVE phase/material tables.
+struct RveDev {
+  int dim, nen, nq, ne;           // spatial dim, nodes/elem, qps/elem, elements
+  int n_indep, npad, nt, NT;      // independent nodes, dim*n_indep, tiles, nt*64
+  int corner;                     // fixed independent node (corner class)
+  int m, ncol, finite;            // tangent size, RHS columns used, finite strain flag
+  double vol;                     // |Omega|
+  const int* elem_indep;          // [ne][nen]
+  const double* grad;             // [ne][nq][nen][dim]  dN/dx at the qps
+  const double* wdet;             // [ne][nq]            Gauss weight * det J
+  const int* inc_ptr;             // [n_indep+1] incidences (e<<4 | a) of each independent node
+  const int* inc;
+  const int* nbr_ptr;             // [n_indep+1] neighbour list of each independent node
+  const int* nbr;                 // neighbour independent node
+  const int* nbr_owner;           // owner node of each neighbour entry
+  const int* sh_ptr;              // [n_nbr+1] shared (e<<8 | a<<4 | b) triples per neighbour entry
+  const int* sh;
+  const uint8_t* phase;           // [B|1][ne]
+  int phase_per_rve;
+  const double* mat;              // [B|1][n_phase][2]
+  int mat_per_rve, n_phase;
+};
+
+struct MacroDev {
+  int dim, nen, nq, ne, n_nodes, ndof, m, finite, nnz;
+  const int* conn;                // [ne][nen]
+  const double* grad;             // [ne][nq][nen][dim]
+  const double* shp;              // [nq][nen]
+  const double* wdet;             // [ne][nq]
+  const int* rowptr;              // [ndof+1] scalar CSR
+  const int* col;                 // [nnz]
+  const int* nz_blk;              // [nnz] node-pair block of each entry
+  const uint8_t* nz_cc;           // [nnz] ci*4 + cj
+  const int* blk_ptr;             // [n_blk+1] shared (E<<8 | a<<4 | b) per node-pair block
+  const int* blk_sh;
+  const int* ninc_ptr;            // [n_nodes+1] incidences (E<<4 | a)
+  const int* ninc;
+  const uint8_t* dmask;           // [ndof] 1 = Dirichlet
+  const double* dval;             // [ndof] prescribed value (0 where free)
+  const double* fbody;            // [ndof] consistent body load
+};
+
+struct CgState {
+  int iterations;
+  int status;                     // 0 ok, 5 not converged, 6 breakdown
+  double rel_residual;
+  double rhs_norm;
+};
+
+// ---- kernels (launch wrappers; all enqueue on `s`) ----
+void launch_rve_material_nh(const RveDev& R, int b0, int nb, const double* F, const double* w,
+                            double* Aq, double* Pq, int* jflag, cudaStream_t s);
+void launch_rve_assemble(const RveDev& R, int b0, int nb, double* Kt, double* Y, double* Cavg,
+                         double* Pavg, double* rfn, const double* Aq, const double* Pq,
+                         cudaStream_t s);
+void launch_condense(const RveDev& R, int b0, int nb, double* Kt, double* Y, const double* Cavg,
+                     const double* Pavg, double* Ceff, double* Peff, double* PavgOut, double* X,
+                     int* info, cudaStream_t s);
+void launch_first_fail(const int* flags, int n, int sentinel, int* out, cudaStream_t s);
+void launch_max_reduce(const double* v, int n, double* out, cudaStream_t s);
+
+void launch_macro_kin(const MacroDev& M, const double* u, double* kin, int add_identity,
+                      cudaStream_t s);
+void launch_macro_assemble(const MacroDev& M, const double* D, double* val, double* diag,
+                           cudaStream_t s);
+void launch_macro_rhs(const MacroDev& M, const double* val, const double* S, double scale,
+                      double* rhs, double* Rfree, cudaStream_t s);
+void launch_macro_cg(const MacroDev& M, const double* val, const double* diag, const double* rhs,
+                     double scale, double rtol, int max_iter, double* x, double* work,
+                     CgState* st, cudaStream_t s);
+void launch_norm(const double* v, int n, double* out, cudaStream_t s);
+void launch_axpy(double* y, const double* x, double a, int n, cudaStream_t s);
+void launch_recover(const RveDev& R, int B, const double* X, const double* kin, double* w,
+                    int accumulate, cudaStream_t s);
+
+}  // namespace hom

@@ -1,0 +1,321 @@
+// macro.cu -- K5-K8: macro kinematics, condensed macro stiffness into CSR,
+// right-hand side with Dirichlet lifting, Jacobi-PCG, fluctuation recovery.
+//
+// PAPER.md eq:linSys / eq:linSys2 with the condensed tangent of
+// eq:solution1/2: K_M = sum_qp eta B_q^T D_b B_q and
+// R = sum_qp eta B_q^T S_b - f_body.  Recovery follows eq:reduction
+// and the dw update.  All reductions run in a fixed order so the
+// results are bitwise reproducible.
+#include "hom_internal.cuh"
+
+namespace hom {
+
+// Voigt strain-displacement entry B_a[k][c] from the gradient g of N_a.
+template <int DIM>
+__device__ __forceinline__ double voigtB(const double* g, int k, int c) {
+  if (DIM == 2) {
+    if (k == 0) return c == 0 ? g[0] : 0.0;
+    if (k == 1) return c == 1 ? g[1] : 0.0;
+    return c == 0 ? g[1] : g[0];  // g12
+  } else {
+    switch (k) {
+      case 0: return c == 0 ? g[0] : 0.0;
+      case 1: return c == 1 ? g[1] : 0.0;
+      case 2: return c == 2 ? g[2] : 0.0;
+      case 3: return c == 1 ? g[2] : (c == 2 ? g[1] : 0.0);  // g23
+      case 4: return c == 0 ? g[2] : (c == 2 ? g[0] : 0.0);  // g13
+      default: return c == 0 ? g[1] : (c == 1 ? g[0] : 0.0); // g12
+    }
+  }
+}
+
+// ---------------------------------------------------------------- kinematics
+template <int DIM>
+__global__ void k_macro_kin(MacroDev M, const double* __restrict__ u, double* __restrict__ kin,
+                            int add_identity) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= M.ne * M.nq) return;
+  int e = t / M.nq, q = t % M.nq;
+  double out[9];
+  for (int k = 0; k < M.m; ++k) out[k] = 0.0;
+  for (int a = 0; a < M.nen; ++a) {
+    int n = M.conn[e * M.nen + a];
+    const double* g = M.grad + ((long)t * M.nen + a) * DIM;
+    for (int c = 0; c < DIM; ++c) {
+      double uc = u[n * DIM + c];
+      if (M.finite) {
+        for (int J = 0; J < DIM; ++J) out[c * DIM + J] += uc * g[J];
+      } else {
+        for (int k = 0; k < M.m; ++k) out[k] += voigtB<DIM>(g, k, c) * uc;
+      }
+    }
+  }
+  if (M.finite && add_identity)
+    for (int i = 0; i < DIM; ++i) out[i * DIM + i] += 1.0;
+  for (int k = 0; k < M.m; ++k) kin[(long)t * M.m + k] = out[k];
+}
+
+void launch_macro_kin(const MacroDev& M, const double* u, double* kin, int add_identity, cudaStream_t s) {
+  int n = M.ne * M.nq;
+  if (M.dim == 2) k_macro_kin<2><<<(n + 127) / 128, 128, 0, s>>>(M, u, kin, add_identity);
+  else k_macro_kin<3><<<(n + 127) / 128, 128, 0, s>>>(M, u, kin, add_identity);
+}
+
+// ---------------------------------------------------------------- K5 assembly
+template <int DIM>
+__global__ void k_macro_assemble(MacroDev M, const double* __restrict__ D, double* __restrict__ val,
+                                 double* __restrict__ diag) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= M.nnz) return;
+  int blk = M.nz_blk[k];
+  int ci = (M.nz_cc[k] >> 2) & 3, cj = M.nz_cc[k] & 3;
+  const int m = M.m;
+  double v = 0.0;
+  for (int s = M.blk_ptr[blk]; s < M.blk_ptr[blk + 1]; ++s) {
+    int code = M.blk_sh[s];
+    int E = code >> 8, a = (code >> 4) & 15, b = code & 15;
+    for (int q = 0; q < M.nq; ++q) {
+      int t = E * M.nq + q;
+      const double* ga = M.grad + ((long)t * M.nen + a) * DIM;
+      const double* gb = M.grad + ((long)t * M.nen + b) * DIM;
+      const double* Dq = D + (long)t * m * m;
+      double w = M.wdet[t], s2 = 0.0;
+      if (M.finite) {
+        for (int J = 0; J < DIM; ++J)
+          for (int L = 0; L < DIM; ++L) s2 += ga[J] * Dq[(ci * DIM + J) * m + cj * DIM + L] * gb[L];
+      } else {
+        for (int kk = 0; kk < m; ++kk) {
+          double bak = voigtB<DIM>(ga, kk, ci);
+          if (bak == 0.0) continue;
+          double t2 = 0.0;
+          for (int l = 0; l < m; ++l) t2 += Dq[kk * m + l] * voigtB<DIM>(gb, l, cj);
+          s2 += bak * t2;
+        }
+      }
+      v += w * s2;
+    }
+  }
+  val[k] = v;
+  if (M.nz_cc[k] & 16) diag[M.col[k]] = v;  // bit 4: col == row (set by hom_setup)
+}
+
+void launch_macro_assemble(const MacroDev& M, const double* D, double* val, double* diag, cudaStream_t s) {
+  if (M.dim == 2) k_macro_assemble<2><<<(M.nnz + 255) / 256, 256, 0, s>>>(M, D, val, diag);
+  else k_macro_assemble<3><<<(M.nnz + 255) / 256, 256, 0, s>>>(M, D, val, diag);
+}
+
+// ---------------------------------------------------------------- RHS
+// rhs_i = -R_i - sum_j K_ij x_D,j (free rows), 0 on Dirichlet rows;  Rfree_i = R_i (free) or 0.
+template <int DIM>
+__global__ void k_macro_rhs(MacroDev M, const double* __restrict__ val, const double* __restrict__ S,
+                            double scale, double* __restrict__ rhs, double* __restrict__ Rfree) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= M.ndof) return;
+  if (M.dmask[i]) {
+    if (rhs) rhs[i] = 0.0;
+    if (Rfree) Rfree[i] = 0.0;
+    return;
+  }
+  int n = i / DIM, c = i % DIM;
+  double R = -M.fbody[i];
+  if (S) {
+    for (int s = M.ninc_ptr[n]; s < M.ninc_ptr[n + 1]; ++s) {
+      int E = M.ninc[s] >> 4, a = M.ninc[s] & 15;
+      for (int q = 0; q < M.nq; ++q) {
+        int t = E * M.nq + q;
+        const double* g = M.grad + ((long)t * M.nen + a) * DIM;
+        const double* Sq = S + (long)t * M.m;
+        double v = 0.0;
+        if (M.finite) {
+          for (int J = 0; J < DIM; ++J) v += g[J] * Sq[c * DIM + J];
+        } else {
+          for (int k = 0; k < M.m; ++k) v += voigtB<DIM>(g, k, c) * Sq[k];
+        }
+        R += M.wdet[t] * v;
+      }
+    }
+  }
+  if (Rfree) Rfree[i] = R;
+  if (rhs) {
+    double lift = 0.0;
+    if (val) {
+      for (int k = M.rowptr[i]; k < M.rowptr[i + 1]; ++k) {
+        int j = M.col[k];
+        if (M.dmask[j]) lift += val[k] * (scale * M.dval[j]);
+      }
+    }
+    rhs[i] = -R - lift;
+  }
+}
+
+void launch_macro_rhs(const MacroDev& M, const double* val, const double* S, double scale, double* rhs,
+                      double* Rfree, cudaStream_t s) {
+  if (M.dim == 2) k_macro_rhs<2><<<(M.ndof + 255) / 256, 256, 0, s>>>(M, val, S, scale, rhs, Rfree);
+  else k_macro_rhs<3><<<(M.ndof + 255) / 256, 256, 0, s>>>(M, val, S, scale, rhs, Rfree);
+}
+
+// ---------------------------------------------------------------- reductions
+constexpr int CG_THR = 1024;
+
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  if (warp == 0) {
+    double x = (lane < (int)(blockDim.x >> 5)) ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
+    if (lane == 0) red[32] = x;
+  }
+  __syncthreads();
+  double r = red[32];
+  __syncthreads();
+  return r;
+}
+
+__device__ __forceinline__ void block_sum2(double& a, double& b, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+  }
+  if (lane == 0) { red[warp] = a; red[40 + warp] = b; }
+  __syncthreads();
+  if (warp == 0) {
+    int nw = blockDim.x >> 5;
+    double x = lane < nw ? red[lane] : 0.0, y = lane < nw ? red[40 + lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      x += __shfl_down_sync(0xffffffffu, x, o);
+      y += __shfl_down_sync(0xffffffffu, y, o);
+    }
+    if (lane == 0) { red[32] = x; red[33] = y; }
+  }
+  __syncthreads();
+  a = red[32];
+  b = red[33];
+  __syncthreads();
+}
+
+__global__ void k_norm(const double* __restrict__ v, int n, double* out) {
+  __shared__ double red[80];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += v[i] * v[i];
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) *out = sqrt(s);
+}
+void launch_norm(const double* v, int n, double* out, cudaStream_t s) { k_norm<<<1, CG_THR, 0, s>>>(v, n, out); }
+
+// ---------------------------------------------------------------- K6/K7: PCG
+// One persistent CTA: SpMV, dots and axpys of every iteration in one launch,
+// no host round trip per iteration (K6/K7).
+__global__ void __launch_bounds__(CG_THR) k_macro_cg(MacroDev M, const double* __restrict__ val,
+                                                     const double* __restrict__ diag,
+                                                     const double* __restrict__ b, double scale,
+                                                     double rtol, int max_iter, double* __restrict__ xout,
+                                                     double* __restrict__ work, CgState* st) {
+  __shared__ double red[80];
+  const int n = M.ndof, tid = threadIdx.x;
+  double* x = work;
+  double* r = work + n;
+  double* p = work + 2 * (long)n;
+  double* q = work + 3 * (long)n;
+  double rz = 0.0, bb = 0.0;
+  for (int i = tid; i < n; i += CG_THR) {
+    double bi = M.dmask[i] ? 0.0 : b[i];
+    double zi = M.dmask[i] ? 0.0 : bi / diag[i];
+    x[i] = 0.0;
+    r[i] = bi;
+    p[i] = zi;
+    rz += bi * zi;
+    bb += bi * bi;
+  }
+  block_sum2(rz, bb, red);
+  const double bnorm = sqrt(bb);
+  int it = 0, status = 0;
+  double rr = bb;
+  if (bnorm > 0.0) {
+    for (it = 1; it <= max_iter; ++it) {
+      double pq = 0.0;
+      for (int i = tid; i < n; i += CG_THR) {
+        double s = 0.0;
+        if (!M.dmask[i]) {
+          for (int k = M.rowptr[i]; k < M.rowptr[i + 1]; ++k) s += val[k] * p[M.col[k]];
+        }
+        q[i] = s;
+        pq += p[i] * s;
+      }
+      pq = block_sum(pq, red);
+      if (!(pq > 0.0)) { status = 6; break; }
+      const double alpha = rz / pq;
+      double rzn = 0.0;
+      rr = 0.0;
+      for (int i = tid; i < n; i += CG_THR) {
+        x[i] += alpha * p[i];
+        double ri = r[i] - alpha * q[i];
+        r[i] = ri;
+        double zi = M.dmask[i] ? 0.0 : ri / diag[i];
+        rr += ri * ri;
+        rzn += ri * zi;
+      }
+      block_sum2(rr, rzn, red);
+      if (sqrt(rr) <= rtol * bnorm) break;
+      const double beta = rzn / rz;
+      rz = rzn;
+      for (int i = tid; i < n; i += CG_THR) {
+        double zi = M.dmask[i] ? 0.0 : r[i] / diag[i];
+        p[i] = zi + beta * p[i];
+      }
+      __syncthreads();
+    }
+    if (status == 0 && it > max_iter) { status = 5; it = max_iter; }
+  }
+  for (int i = tid; i < n; i += CG_THR) xout[i] = M.dmask[i] ? scale * M.dval[i] : x[i];
+  if (tid == 0) {
+    st->iterations = it;
+    st->status = status;
+    st->rel_residual = bnorm > 0.0 ? sqrt(rr) / bnorm : 0.0;
+    st->rhs_norm = bnorm;
+  }
+}
+
+void launch_macro_cg(const MacroDev& M, const double* val, const double* diag, const double* rhs,
+                     double scale, double rtol, int max_iter, double* x, double* work, CgState* st,
+                     cudaStream_t s) {
+  k_macro_cg<<<1, CG_THR, 0, s>>>(M, val, diag, rhs, scale, rtol, max_iter, x, work, st);
+}
+
+__global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, double a, int n) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) y[i] += a * x[i];
+}
+void launch_axpy(double* y, const double* x, double a, int n, cudaStream_t s) {
+  k_axpy<<<(n + 255) / 256, 256, 0, s>>>(y, x, a, n);
+}
+
+// ---------------------------------------------------------------- K8 recovery
+// accumulate = 0: w = -X[:, :m] kin            (small strain, kin = eps)
+// accumulate = 1: w += -(X[:, m] + X[:, :m] kin) (finite strain, kin = grad du)
+__global__ void k_recover(RveDev R, int B, const double* __restrict__ X, const double* __restrict__ kin,
+                          double* __restrict__ w, int accumulate) {
+  long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long)B * R.npad) return;
+  int b = (int)(t / R.npad), i = (int)(t % R.npad);
+  const double* xr = X + ((long)b * R.NT + i) * RHSW;
+  const double* kb = kin + (long)b * R.m;
+  double v = 0.0;
+  for (int k = 0; k < R.m; ++k) v += xr[k] * kb[k];
+  if (accumulate) w[t] -= xr[R.m] + v;
+  else w[t] = -v;
+}
+
+void launch_recover(const RveDev& R, int B, const double* X, const double* kin, double* w, int accumulate,
+                    cudaStream_t s) {
+  long n = (long)B * R.npad;
+  k_recover<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(R, B, X, kin, w, accumulate);
+}
+
+}  // namespace hom

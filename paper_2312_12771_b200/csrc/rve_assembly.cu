@@ -1,0 +1,333 @@
+// rve_assembly.cu -- K1: batched RVE assembly of K_ff, K_fe (, r_f), <C> (, <P>).
+//
+// PAPER.md eq:discreteSys_D and eq:discreteSys_L: for RVE b the
+// micro-micro block is K_ff = sum_e sum_qp eta~ B_f^T C B_f and the coupling is
+// K_fe = sum eta~ B_f^T C (un-normalised, R2); the periodic
+// constraint (eq:Con (iii); nodal coupling P:604-612) is applied on the
+// fly through the element -> independent-node map, and the corner class is an
+// identity pad.  Output is the dense lower K_ff in 64x64 tiles, tile (I,J),
+// I >= J, at index I(I+1)/2 + J, each tile row-major; K_fe (and r_f) go to the
+// right-hand-side block Y [NT][8].
+//
+// One CTA per RVE: the tile is zero-filled and scattered in shared memory, then
+// streamed to HBM with coalesced 16-byte stores -- the kernel is HBM-write bound
+// (K1).
+#include "hom_internal.cuh"
+
+namespace hom {
+
+// sigma(e_k)[c][J] for the unit Voigt strain k of an isotropic material.
+template <int DIM>
+__device__ __forceinline__ double unit_stress(int k, int c, int J, double lam, double mu) {
+  constexpr int NN = DIM;  // normal components first
+  double s = 0.0;
+  if (k < NN) {
+    if (c == J) s += lam;
+    if (c == k && J == k) s += 2.0 * mu;
+  } else {
+    int i, j;
+    if (DIM == 2) { i = 0; j = 1; }
+    else if (k == 3) { i = 1; j = 2; }
+    else if (k == 4) { i = 0; j = 2; }
+    else { i = 0; j = 1; }
+    if ((c == i && J == j) || (c == j && J == i)) s += mu;  // 2 mu * (1/2)
+  }
+  return s;
+}
+
+// ---------------------------------------------------------------------------
+// K1a (finite strain): per (RVE, element, qp) deformation gradient, stress and
+// tangent of the Cook energy with beta = 0.  F~ = F + grad w
+// (eq:microGrad).
+// ---------------------------------------------------------------------------
+__global__ void k_rve_material_nh(RveDev R, int b0, int nb, const double* __restrict__ Fbar,
+                                  const double* __restrict__ w, double* __restrict__ Aq,
+                                  double* __restrict__ Pq, int* __restrict__ jflag) {
+  const int per = R.ne * R.nq;
+  long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= (long)nb * per) return;
+  int bl = (int)(gid / per), eq = (int)(gid % per);
+  int e = eq / R.nq, q = eq % R.nq;
+  int b = b0 + bl;
+  const double* Fb = Fbar + (long)b * 4;
+  double F[4] = {Fb[0], Fb[1], Fb[2], Fb[3]};
+  const double* wb = w + (long)b * R.npad;
+  for (int a = 0; a < R.nen; ++a) {
+    int p = R.elem_indep[e * R.nen + a];
+    const double* g = R.grad + ((long)(e * R.nq + q) * R.nen + a) * 2;
+    double w0 = wb[2 * p], w1 = wb[2 * p + 1];
+    F[0] += w0 * g[0]; F[1] += w0 * g[1];
+    F[2] += w1 * g[0]; F[3] += w1 * g[1];
+  }
+  int ph = R.phase[(R.phase_per_rve ? (long)b * R.ne : 0) + e];
+  const double* mp = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * 2 : 0) + 2 * ph;
+  double alpha = mp[0], kappa = mp[1];
+  double J = F[0] * F[3] - F[1] * F[2];
+  double* A = Aq + gid * 16;
+  double* P = Pq + gid * 4;
+  if (!(J > 0.0)) {
+    atomicMin(&jflag[b], eq);  // first failing qp of this RVE (jflag init INT_MAX)
+    for (int i = 0; i < 16; ++i) A[i] = 0.0;
+    for (int i = 0; i < 4; ++i) P[i] = 0.0;
+    return;
+  }
+  double H[4] = {F[3], -F[2], -F[1], F[0]};  // cof F (2-D specialisation of 1/2 F xx F)
+  double dPsidJ = kappa * (J - 1.0) - 2.0 * alpha / J;
+  double d2 = kappa + 2.0 * alpha / (J * J);
+  for (int i = 0; i < 4; ++i) P[i] = 2.0 * alpha * F[i] + dPsidJ * H[i];
+  // dH/dF is the constant anti-diagonal [0 0 0 1; 0 0 -1 0; 0 -1 0 0; 1 0 0 0]
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j) {
+      double v = d2 * H[i] * H[j];
+      if (i == j) v += 2.0 * alpha;
+      if (i + j == 3) v += ((i == 0 || i == 3) ? 1.0 : -1.0) * dPsidJ;
+      A[i * 4 + j] = v;
+    }
+}
+
+void launch_rve_material_nh(const RveDev& R, int b0, int nb, const double* F, const double* w,
+                            double* Aq, double* Pq, int* jflag, cudaStream_t s) {
+  long n = (long)nb * R.ne * R.nq;
+  int thr = 256;
+  k_rve_material_nh<<<(unsigned)((n + thr - 1) / thr), thr, 0, s>>>(R, b0, nb, F, w, Aq, Pq, jflag);
+}
+
+// ---------------------------------------------------------------------------
+// K1: assembly.  ISO = isotropic closed form K_ab^{ij} = lam g_a^i g_b^j +
+// mu g_a^j g_b^i + mu d_ij (g_a . g_b) (small strain); otherwise the tangent
+// is read per qp from Aq (finite strain, full-gradient form).
+// ---------------------------------------------------------------------------
+template <int DIM, bool ISO>
+__global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double* __restrict__ Kt,
+                                                       double* __restrict__ Y, double* __restrict__ Cavg,
+                                                       double* __restrict__ Pavg, double* __restrict__ rfn,
+                                                       const double* __restrict__ Aq,
+                                                       const double* __restrict__ Pq) {
+  extern __shared__ __align__(16) double smem[];
+  double* tile = smem;                 // [64*64]
+  double* red = smem + TILE_ELEMS;     // [NTHR] reduction scratch
+  double* s_lam = red + NTHR;          // [ne] (ISO)
+  double* s_mu = s_lam + R.ne;         // [ne] (ISO)
+  const int tid = threadIdx.x;
+  const int bl = blockIdx.x;
+  const int b = b0 + bl;
+  const int nen = R.nen, nq = R.nq, ne = R.ne;
+  const long tq0 = (long)bl * ne * nq;  // offset of this RVE in Aq/Pq (chunk-local)
+
+  if (ISO) {
+    const uint8_t* ph = R.phase + (R.phase_per_rve ? (long)b * ne : 0);
+    const double* mt = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * 2 : 0);
+    for (int e = tid; e < ne; e += NTHR) {
+      int p = ph[e];
+      double E = mt[2 * p], nu = mt[2 * p + 1];
+      s_lam[e] = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+      s_mu[e] = E / (2.0 * (1.0 + nu));
+    }
+  }
+  __syncthreads();
+
+  // ---- volume averages <C> (and <P>) ----
+  {
+    constexpr int NV = ISO ? 2 : 20;
+    double acc[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+    for (int eq = tid; eq < ne * nq; eq += NTHR) {
+      double wq = R.wdet[eq];
+      if (ISO) {
+        int e = eq / nq;
+        acc[0] += wq * s_lam[e];
+        acc[1] += wq * s_mu[e];
+      } else {
+        const double* A = Aq + (tq0 + eq) * 16;
+        const double* P = Pq + (tq0 + eq) * 4;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) acc[i] += wq * A[i];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) acc[16 + i] += wq * P[i];
+      }
+    }
+    for (int v = 0; v < NV; ++v) {
+      red[tid] = acc[v];
+      __syncthreads();
+      for (int s = NTHR / 2; s > 0; s >>= 1) {
+        if (tid < s) red[tid] += red[tid + s];
+        __syncthreads();
+      }
+      acc[v] = red[0] / R.vol;  // every thread keeps the total
+      __syncthreads();
+    }
+    if (tid == 0) {
+      double* C = Cavg + (long)bl * 64;
+      if (ISO) {
+        const int m = R.m;
+        for (int i = 0; i < m * m; ++i) C[i] = 0.0;
+        for (int i = 0; i < DIM; ++i)
+          for (int j = 0; j < DIM; ++j) C[i * m + j] = acc[0] + (i == j ? 2.0 * acc[1] : 0.0);
+        for (int i = DIM; i < m; ++i) C[i * m + i] = acc[1];
+      } else {
+        for (int i = 0; i < 16; ++i) C[i] = acc[i];
+        for (int i = 0; i < 4; ++i) Pavg[(long)bl * 8 + i] = acc[16 + i];
+      }
+    }
+  }
+
+  // ---- right-hand sides: K_fe (cols 0..m-1) and r_f (col m, finite strain) ----
+  {
+    double rr = 0.0;
+    double* Yb = Y + (long)bl * R.NT * RHSW;
+    for (int i = tid; i < R.NT; i += NTHR) {
+      double out[RHSW];
+#pragma unroll
+      for (int k = 0; k < RHSW; ++k) out[k] = 0.0;
+      int p = i / DIM, c = i % DIM;
+      if (i < R.npad && p != R.corner) {
+        for (int s = R.inc_ptr[p]; s < R.inc_ptr[p + 1]; ++s) {
+          int e = R.inc[s] >> 4, a = R.inc[s] & 15;
+          for (int q = 0; q < nq; ++q) {
+            const double* g = R.grad + ((long)(e * nq + q) * nen + a) * DIM;
+            double wq = R.wdet[e * nq + q];
+            if (ISO) {
+              double lam = s_lam[e], mu = s_mu[e];
+              for (int k = 0; k < R.m; ++k) {
+                double v = 0.0;
+#pragma unroll
+                for (int J = 0; J < DIM; ++J) v += g[J] * unit_stress<DIM>(k, c, J, lam, mu);
+                out[k] += wq * v;
+              }
+            } else {
+              const double* A = Aq + (tq0 + e * nq + q) * 16;
+              const double* P = Pq + (tq0 + e * nq + q) * 4;
+              for (int k = 0; k < 4; ++k) {
+                double v = 0.0;
+#pragma unroll
+                for (int J = 0; J < DIM; ++J) v += g[J] * A[(c * DIM + J) * 4 + k];
+                out[k] += wq * v;
+              }
+              double v = 0.0;
+#pragma unroll
+              for (int J = 0; J < DIM; ++J) v += g[J] * P[c * DIM + J];
+              out[4] += wq * v;
+            }
+          }
+        }
+        if (!ISO) rr += out[4] * out[4];
+      }
+      double2* dst = reinterpret_cast<double2*>(Yb + (long)i * RHSW);
+#pragma unroll
+      for (int k = 0; k < RHSW / 2; ++k) dst[k] = make_double2(out[2 * k], out[2 * k + 1]);
+    }
+    if (!ISO) {  // ||r_f|| over the free DOFs (R_micro)
+      red[tid] = rr;
+      __syncthreads();
+      for (int s = NTHR / 2; s > 0; s >>= 1) {
+        if (tid < s) red[tid] += red[tid + s];
+        __syncthreads();
+      }
+      if (tid == 0) rfn[b] = sqrt(red[0]);
+      __syncthreads();
+    }
+  }
+
+  // ---- K_ff tiles ----
+  const int nt = R.nt;
+  double* Kb = Kt + (long)bl * (nt * (nt + 1) / 2) * TILE_ELEMS;
+  for (int I = 0; I < nt; ++I) {
+    const int r0 = I * TILE;
+    int p_lo = r0 / DIM, p_hi = min((r0 + TILE - 1) / DIM, R.n_indep - 1);
+    const int k_lo = p_lo < R.n_indep ? R.nbr_ptr[p_lo] : 0;
+    const int k_hi = p_lo < R.n_indep ? R.nbr_ptr[p_hi + 1] : 0;
+    for (int J = 0; J <= I; ++J) {
+      const int c0 = J * TILE;
+      double2* t2 = reinterpret_cast<double2*>(tile);
+      for (int i = tid; i < TILE_ELEMS / 2; i += NTHR) t2[i] = make_double2(0.0, 0.0);
+      __syncthreads();
+      for (int k = k_lo + tid; k < k_hi; k += NTHR) {
+        int p = R.nbr_owner[k], q = R.nbr[k];
+        if (p == R.corner || q == R.corner) continue;
+        int pr = p * DIM, qc = q * DIM;
+        if (qc + DIM <= c0 || qc >= c0 + TILE) continue;
+        double blk[DIM][DIM];
+#pragma unroll
+        for (int i = 0; i < DIM; ++i)
+#pragma unroll
+          for (int j = 0; j < DIM; ++j) blk[i][j] = 0.0;
+        for (int s = R.sh_ptr[k]; s < R.sh_ptr[k + 1]; ++s) {
+          int code = R.sh[s];
+          int e = code >> 8, a = (code >> 4) & 15, bb = code & 15;
+          for (int qq = 0; qq < nq; ++qq) {
+            const double* ga = R.grad + ((long)(e * nq + qq) * nen + a) * DIM;
+            const double* gb = R.grad + ((long)(e * nq + qq) * nen + bb) * DIM;
+            double wq = R.wdet[e * nq + qq];
+            if (ISO) {
+              double lam = s_lam[e] * wq, mu = s_mu[e] * wq;
+              double dot = 0.0;
+#pragma unroll
+              for (int t = 0; t < DIM; ++t) dot += ga[t] * gb[t];
+#pragma unroll
+              for (int i = 0; i < DIM; ++i)
+#pragma unroll
+                for (int j = 0; j < DIM; ++j)
+                  blk[i][j] += lam * ga[i] * gb[j] + mu * ga[j] * gb[i] + (i == j ? mu * dot : 0.0);
+            } else {
+              const double* A = Aq + (tq0 + e * nq + qq) * 16;
+#pragma unroll
+              for (int i = 0; i < DIM; ++i)
+#pragma unroll
+                for (int j = 0; j < DIM; ++j) {
+                  double v = 0.0;
+#pragma unroll
+                  for (int Jd = 0; Jd < DIM; ++Jd)
+#pragma unroll
+                    for (int Ld = 0; Ld < DIM; ++Ld) v += ga[Jd] * A[(i * DIM + Jd) * 4 + j * DIM + Ld] * gb[Ld];
+                  blk[i][j] += wq * v;
+                }
+            }
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < DIM; ++i) {
+          int rr = pr + i - r0;
+          if (rr < 0 || rr >= TILE) continue;
+#pragma unroll
+          for (int j = 0; j < DIM; ++j) {
+            int cc = qc + j - c0;
+            if (cc < 0 || cc >= TILE) continue;
+            tile[rr * TILE + cc] = blk[i][j];
+          }
+        }
+      }
+      if (I == J) {  // identity pads: corner class and DOFs beyond N_pad
+        for (int i = tid; i < TILE; i += NTHR) {
+          int g = r0 + i;
+          if (g >= R.npad || g / DIM == R.corner) tile[i * TILE + i] = 1.0;
+        }
+      }
+      __syncthreads();
+      double2* dst = reinterpret_cast<double2*>(Kb + (long)(I * (I + 1) / 2 + J) * TILE_ELEMS);
+      for (int i = tid; i < TILE_ELEMS / 2; i += NTHR) dst[i] = t2[i];
+      __syncthreads();
+    }
+  }
+}
+
+void launch_rve_assemble(const RveDev& R, int b0, int nb, double* Kt, double* Y, double* Cavg,
+                         double* Pavg, double* rfn, const double* Aq, const double* Pq,
+                         cudaStream_t s) {
+  size_t sm = (size_t)(TILE_ELEMS + NTHR + 2 * R.ne) * sizeof(double);
+  if (R.finite) {
+    auto k = k_rve_assemble<2, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, rfn, Aq, Pq);
+  } else if (R.dim == 2) {
+    auto k = k_rve_assemble<2, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, rfn, Aq, Pq);
+  } else {
+    auto k = k_rve_assemble<3, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, rfn, Aq, Pq);
+  }
+}
+
+}  // namespace hom

@@ -1,0 +1,212 @@
+"""GPU parity of the libhom.so path (through the C-ABI) against the CPU oracle.
+
+Tolerances are BASELINE.json north_star's: relative Frobenius error <= 1e-10 on
+C_eff and <= 1e-8 on macro displacements (FP64).  Fluctuations are held to the
+same 1e-8 as the displacements they are recovered from.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2312_12771_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+TOL_C = 1e-10
+TOL_U = 1e-8
+
+
+def rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def gpu_linear(wl, **kw):
+    from paper_2312_12771_b200.hom import Homogenizer
+    h = Homogenizer.from_workload(wl, **kw)
+    C, u, w, info = h.solve_linear()
+    out = {"C": C.cpu().numpy(), "u": u.cpu().numpy(), "w": w.cpu().numpy(), "info": info, "h": h}
+    return out
+
+
+def check_linear_against_oracle(wl, **kw):
+    g = gpu_linear(wl, **kw)
+    o = oracle.solve_linear(wl)
+    assert rel(g["C"], o["C_eff"]) <= TOL_C, rel(g["C"], o["C_eff"])
+    assert rel(g["u"], o["u"]) <= TOL_U, rel(g["u"], o["u"])
+    w_o = oracle.recover_linear(o["W"], o["eps"])
+    assert rel(g["w"], w_o) <= TOL_U, rel(g["w"], w_o)
+    assert g["info"].rel_residual <= 1e-13
+    return g, o
+
+
+# ------------------------------------------------------------------ configs 1, 2, 4 (full size)
+def test_config1_full_matches_oracle_and_closed_form(torch_cuda):
+    g, o = check_linear_against_oracle(W.config1())
+    C = g["C"][0]
+    np.testing.assert_allclose([C[0, 0], C[0, 1], C[1, 1], C[2, 2]],
+                               [2.447552447552447, 1.048951048951049, 6.493506493506493, 0.699300699300699],
+                               rtol=1e-12)
+
+
+def test_config2_full_matches_oracle(torch_cuda):
+    check_linear_against_oracle(W.config2())
+
+
+def test_config4_full_matches_oracle(torch_cuda):
+    check_linear_against_oracle(W.config4())
+
+
+@pytest.mark.parametrize("r", [3, 5, 12, 20])
+def test_ragged_rve_sizes(torch_cuda, r):
+    """N_pad not a multiple of the 64-wide tile (ragged tail, identity pads)."""
+    wl = W.config3(nel=2, r=r, seed=7 + r)
+    check_linear_against_oracle(wl)
+
+
+def test_ragged_3d(torch_cuda):
+    wl = W.config4(nel=2, r=5)
+    wl.phase = (np.arange(125) % 3 == 0).astype(np.uint8)[None]
+    check_linear_against_oracle(wl)
+
+
+# ------------------------------------------------------------------ config 3
+def test_config3_reduced_macro_full_rve(torch_cuda):
+    """Config 3's 32x32 RVEs with per-RVE random phases and moduli (every RVE different)."""
+    check_linear_against_oracle(W.config3(nel=4))
+
+
+def test_config3_full_size_sampled(torch_cuda):
+    """Full config 3 (16384 RVEs, launch configuration of the bench's chunked path): C_eff of
+    sampled RVEs against the oracle, and the macro solution checked by the oracle's residual."""
+    wl = W.config3()
+    g = gpu_linear(wl)
+    rng = np.random.default_rng(0)
+    ids = np.sort(rng.choice(wl.n_rve, 24, replace=False))
+    ids = np.unique(np.concatenate([ids, [0, wl.n_rve - 1]]))
+    o = oracle.solve_linear(wl, rve_ids=ids)
+    assert rel(g["C"][ids], o["C_eff_subset"]) <= TOL_C
+    # macro equilibrium with the GPU tangents (property valid at any size)
+    eps = oracle.macro_kin(2, wl.nel, g["u"])
+    S = np.einsum("bij,bj->bi", g["C"], eps)
+    R = oracle.macro_residual(2, wl.nel, S, wl.body)
+    free = np.ones(wl.n_dof, bool)
+    free[wl.dir_dof] = False
+    f = -oracle.macro_residual(2, wl.nel, None, wl.body)
+    assert np.linalg.norm(R[free]) <= 1e-10 * np.linalg.norm(f[free])
+    # the oracle's direct macro solve with the GPU tangents: the CG solution to 1e-8
+    u_direct = oracle.macro_solve(2, wl.nel, g["C"], wl.dir_dof, wl.dir_val, body=wl.body)
+    assert rel(g["u"], u_direct) <= TOL_U
+    w_o = oracle.recover_linear(o["W_subset"], eps[ids])
+    assert rel(g["w"][ids], w_o) <= TOL_U
+
+
+def test_chunking_is_bitwise_invariant(torch_cuda):
+    wl = W.config3(nel=2, r=12)
+    a = gpu_linear(wl)
+    b = gpu_linear(wl, rve_chunk=5)
+    assert np.array_equal(a["C"], b["C"]) and np.array_equal(a["u"], b["u"]) and np.array_equal(a["w"], b["w"])
+
+
+def test_determinism_bitwise(torch_cuda):
+    wl = W.config2(nel=8)
+    g = gpu_linear(wl)
+    h = g["h"]
+    for _ in range(2):
+        C, u, w, _ = h.solve_linear()
+        assert np.array_equal(C.cpu().numpy(), g["C"])
+        assert np.array_equal(u.cpu().numpy(), g["u"])
+        assert np.array_equal(w.cpu().numpy(), g["w"])
+
+
+# ------------------------------------------------------------------ config 5 (finite strain)
+def test_config5_condense_per_state(torch_cuda):
+    """Reading R13: feed a non-trivial oracle state (u, w) to hom_condense; A_eff and P_eff <= 1e-10."""
+    import torch
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = W.config5(nel=4, n_steps=2)
+    steps = oracle.newton_nh(wl, steps=1)
+    u, w = steps[-1]["u"], steps[-1]["w"]
+    # perturb to a non-equilibrium state so r_f != 0
+    rng = np.random.default_rng(1)
+    w = w + 1e-3 * rng.standard_normal(w.shape)
+    w[:, :2] = 0.0
+    G = oracle.macro_kin(2, wl.nel, u, kind=1)
+    Fb = G + np.array([1.0, 0, 0, 1.0])
+    c = oracle.condense_batch_nh(wl.r, wl.phase, wl.mat, Fb, w)
+    h = Homogenizer.from_workload(wl)
+    h.set_fluctuations(torch.tensor(w, device="cuda"))
+    F = h.macro_kinematics(torch.tensor(u, device="cuda"))
+    assert rel(F.cpu().numpy(), Fb) <= 1e-14
+    A, Pe, Pa = h.condense(F)
+    assert rel(A.cpu().numpy(), c["A_eff"]) <= TOL_C
+    assert rel(Pe.cpu().numpy(), c["P_eff"]) <= TOL_C
+    assert rel(Pa.cpu().numpy(), c["P_avg"]) <= TOL_C
+    assert abs(h.micro_residual_max() - c["rf_norm"].max()) <= 1e-10 * c["rf_norm"].max()
+    # one Newton update of both scales
+    du_o, dw_o, _ = oracle.newton_step_nh(wl, u, w, np.zeros(len(wl.dir_dof)))
+    du, _ = h.macro_solve(A, Pe, scale=0.0)
+    assert rel(du.cpu().numpy(), du_o) <= TOL_U
+    ut = torch.tensor(u, device="cuda")
+    h.newton_update(ut, du)
+    assert rel(h.get_fluctuations().cpu().numpy(), w + dw_o) <= TOL_U
+    assert rel(ut.cpu().numpy(), u + du_o) <= TOL_U
+
+
+def test_config5_newton_load_steps(torch_cuda):
+    """Full load-stepping Newton (reduced macro): u per converged step <= 1e-8 vs the oracle,
+    and quadratic decay of the macro residual (S:414 reading)."""
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = W.config5(nel=4, n_steps=4)
+    o = oracle.newton_nh(wl, tol=1e-11)
+    assert all(s["converged"] for s in o)
+    h = Homogenizer.from_workload(wl)
+    u, hist = h.newton(wl.n_steps, tol=1e-11)
+    assert rel(u.cpu().numpy(), o[-1]["u"]) <= TOL_U
+    for hs in hist:
+        r = [x[0] for x in hs]
+        for i in range(1, len(r) - 1):
+            if r[i] < 1e-2 * r[0] and r[i + 1] > 1e-13:
+                assert np.log(r[i + 1]) / np.log(r[i]) >= 1.7 or r[i + 1] < 1e-12
+
+
+# ------------------------------------------------------------------ failure reporting
+def test_not_spd_reports_rve(torch_cuda):
+    from paper_2312_12771_b200.hom import Homogenizer, HomError
+    wl = W.config3(nel=2, r=6, seed=3)
+    wl.mat = wl.mat.copy()
+    wl.mat[5, :, 0] = -1.0  # negative stiffness in RVE 5 -> K_ff indefinite
+    with pytest.raises(HomError) as e:
+        Homogenizer.from_workload(wl).condense()
+    assert e.value.code == 3 and e.value.rve == 5
+
+
+def test_jacobian_reports_rve(torch_cuda):
+    import torch
+    from paper_2312_12771_b200.hom import Homogenizer, HomError
+    wl = W.config5(nel=2)
+    h = Homogenizer.from_workload(wl)
+    F = torch.tensor(np.tile([1.0, 0, 0, 1.0], (wl.n_rve, 1)), device="cuda")
+    F[7] = torch.tensor([1.0, 0.0, 0.0, -0.5])
+    with pytest.raises(HomError) as e:
+        h.condense(F)
+    assert e.value.code == 4 and e.value.rve == 7
+
+
+def test_cg_not_converged_status(torch_cuda):
+    from paper_2312_12771_b200.hom import Homogenizer, HomError
+    h = Homogenizer.from_workload(W.config2(nel=8), cg_max_iter=3)
+    C = h.condense()
+    with pytest.raises(HomError) as e:
+        h.macro_solve(C)
+    assert e.value.code == 5
