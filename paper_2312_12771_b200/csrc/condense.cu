@@ -88,6 +88,171 @@ __device__ __forceinline__ void mma_chunk(double (&acc)[4][2][2], const double* 
   }
 }
 
+// ------------------------------------------------------------------ diagonal tile
+// One warp: Cholesky of the 16x16 block at (k0,k0) of the swizzled 64x64 tile sT
+// (lower part, in registers, shuffles only) and its inverse into the same block of sX.
+// Returns the first failing local pivot (16 = none); warp-uniform.
+__device__ __forceinline__ int chol_inv16(double* sT, double* sX, int k0, int lane) {
+  const unsigned FULL = 0xffffffffu;
+  const int r = lane & 15;
+  double a[16];
+#pragma unroll
+  for (int c = 0; c < 16; ++c) a[c] = (c <= r) ? sT[sw64(k0 + r, k0 + c)] : 0.0;
+  int fail = 16;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    double dkk = __shfl_sync(FULL, a[k], k);
+    if (!(dkk > 0.0) && fail == 16) fail = k;
+    double piv = sqrt(dkk), ip = 1.0 / piv;
+    a[k] = (r == k) ? piv : a[k] * ip;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if (j > k) {  // compile-time after unrolling: a[] stays in registers
+        double ljk = __shfl_sync(FULL, a[k], j);
+        if (r >= j) a[j] = fma(-a[k], ljk, a[j]);
+      }
+    }
+  }
+  if (lane < 16) {
+#pragma unroll
+    for (int c = 0; c < 16; ++c)
+      if (c <= r) sT[sw64(k0 + r, k0 + c)] = a[c];
+  }
+  __syncwarp();
+  // X = L^-1: lane c builds column c by forward substitution (L rows read as smem broadcasts)
+  const int c = lane & 15;
+  double x[16];
+#pragma unroll
+  for (int rr = 0; rr < 16; ++rr) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k < rr) s = fma(sT[sw64(k0 + rr, k0 + k)], x[k], s);
+    x[rr] = (rr >= c) ? (((rr == c) ? 1.0 : 0.0) - s) / sT[sw64(k0 + rr, k0 + rr)] : 0.0;
+  }
+  if (lane < 16) {
+#pragma unroll
+    for (int rr = 0; rr < 16; ++rr) sX[sw64(k0 + rr, k0 + c)] = x[rr];
+  }
+  return fail;
+}
+
+// 8x8 output tile: acc += A[r0.., k0..k0+nk) * B[c0.., k0..)^T   (both [row][k], sw64)
+__device__ __forceinline__ void tile8_abt(double (&acc)[2], const double* A, int r0, const double* B, int c0,
+                                          int k0, int nk, int lane, double sign) {
+  const int lr = lane >> 2, lc = lane & 3;
+  for (int k = k0; k < k0 + nk; k += 4)
+    dmma(acc[0], acc[1], sign * A[sw64(r0 + lr, k + lc)], B[sw64(c0 + lr, k + lc)]);
+}
+// 8x8 output tile: acc += A[r0.., k..) * B[k.., c0..)   (A [row][k], B [k][col], sw64)
+__device__ __forceinline__ void tile8_ab(double (&acc)[2], const double* A, int r0, const double* B, int c0,
+                                         int k0, int nk, int lane, double sign) {
+  const int lr = lane >> 2, lc = lane & 3;
+  for (int k = k0; k < k0 + nk; k += 4)
+    dmma(acc[0], acc[1], sign * A[sw64(r0 + lr, k + lc)], B[sw64(k + lc, c0 + lr)]);
+}
+
+// Blocked (16-wide) Cholesky of the 64x64 tile in sT followed by the blocked
+// triangular inverse; on return sT holds G_JJ^-1 (exact zeros above the
+// diagonal).  sX is 64x64 + 768 doubles of scratch.  All block updates run on
+// DMMA; about 18 CTA barriers instead of one per column.
+__device__ __forceinline__ bool factor_invert_diag(double* sT, double* sX, int* sFail, int J, int tid) {
+  const int lane = tid & 31, warp = tid >> 5;
+  const int lr = lane >> 2, lc = lane & 3;
+  for (int i = tid; i < TILE_ELEMS; i += NTHR) sX[i] = 0.0;
+  __syncthreads();
+  for (int kb = 0; kb < 4; ++kb) {
+    const int k0 = 16 * kb;
+    if (warp == 0) {
+      int f = chol_inv16(sT, sX, k0, lane);
+      if (f < 16 && lane == 0 && sFail[0] == 0) sFail[0] = J * TILE + k0 + f + 1;
+    }
+    __syncthreads();
+    if (sFail[0]) return false;
+    if (kb == 3) break;
+    const int rb0 = k0 + 16, nrb = (TILE - rb0) / 8;  // row blocks below the panel
+    // panel: L_ik = A_ik * Linv_kk^T, rows rb0..63, cols k0..k0+15 (nrb x 2 tiles)
+    double pan[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    const int nt_pan = nrb * 2;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      int t = warp + 8 * u;
+      if (t < nt_pan) tile8_abt(pan[u], sT, rb0 + 8 * (t >> 1), sX, k0 + 8 * (t & 1), k0, 16, lane, 1.0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      int t = warp + 8 * u;
+      if (t < nt_pan) {
+        int r = rb0 + 8 * (t >> 1) + lr, cc = k0 + 8 * (t & 1) + 2 * lc;
+        sT[sw64(r, cc)] = pan[u][0];
+        sT[sw64(r, cc + 1)] = pan[u][1];
+      }
+    }
+    __syncthreads();
+    // trailing: A_ij -= L_ik L_jk^T for lower 8x8 tiles of rows/cols rb0..63
+    const int ntr = nrb * (nrb + 1) / 2;
+    for (int t = warp; t < ntr; t += 8) {
+      int ti = 0;
+      while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+      int tj = t - ti * (ti + 1) / 2;
+      int r = rb0 + 8 * ti, cb = rb0 + 8 * tj;
+      double acc[2] = {sT[sw64(r + lr, cb + 2 * lc)], sT[sw64(r + lr, cb + 2 * lc + 1)]};
+      tile8_abt(acc, sT, r, sT, cb, k0, 16, lane, -1.0);
+      sT[sw64(r + lr, cb + 2 * lc)] = acc[0];
+      sT[sw64(r + lr, cb + 2 * lc + 1)] = acc[1];
+    }
+    __syncthreads();
+  }
+  // off-diagonal blocks of the inverse: X_ik = -X_ii sum_{j=k}^{i-1} L_ij X_jk
+  double* sTmp = sX + TILE_ELEMS;  // 3 blocks of 16x16, plain row-major
+  for (int i = 1; i < 4; ++i) {
+    const int ntile = 4 * i;  // blocks k = 0..i-1, 2x2 tiles each
+    double tv[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      int t = warp + 8 * u;
+      if (t < ntile) {
+        int k = t >> 2, q = t & 3;
+        tile8_ab(tv[u], sT, 16 * i + 8 * (q >> 1), sX, 16 * k + 8 * (q & 1), 16 * k, 16 * (i - k), lane, 1.0);
+        int rr = 8 * (q >> 1) + lr, cc = 8 * (q & 1) + 2 * lc;
+        sTmp[k * 256 + rr * 16 + cc] = tv[u][0];
+        sTmp[k * 256 + rr * 16 + cc + 1] = tv[u][1];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      int t = warp + 8 * u;
+      if (t < ntile) {
+        int k = t >> 2, q = t & 3;
+        int r0 = 8 * (q >> 1), c0 = 8 * (q & 1);
+        double acc[2] = {0.0, 0.0};
+#pragma unroll
+        for (int kk = 0; kk < 16; kk += 4)
+          dmma(acc[0], acc[1], -sX[sw64(16 * i + r0 + lr, 16 * i + kk + lc)], sTmp[k * 256 + (kk + lc) * 16 + c0 + lr]);
+        tv[u][0] = acc[0];
+        tv[u][1] = acc[1];
+      }
+    }
+    // X_ik written after all warps read X_ii / sTmp (X_ii is a different block: no hazard)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      int t = warp + 8 * u;
+      if (t < ntile) {
+        int k = t >> 2, q = t & 3;
+        int r = 16 * i + 8 * (q >> 1) + lr, cc = 16 * k + 8 * (q & 1) + 2 * lc;
+        sX[sw64(r, cc)] = tv[u][0];
+        sX[sw64(r, cc + 1)] = tv[u][1];
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = tid; i < TILE_ELEMS; i += NTHR) sT[i] = sX[i];
+  __syncthreads();
+  return true;
+}
+
 // Smem budget (doubles): sT 4096 | stage[2] x (A 2048 + B 2048 + Yc 256) | sY 512 | sY2 512 | misc
 constexpr int STAGE_DBL = 2 * 64 * KC + KC * RHSW;
 constexpr int SMEM_DBL = TILE_ELEMS + 2 * STAGE_DBL + 2 * 64 * RHSW + 64;
@@ -172,44 +337,8 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
       sY[swy(r, cc + 1)] = y.y - yacc[1];
     }
     __syncthreads();
-    // ---------- unblocked Cholesky of the 64x64 diagonal tile ----------
-    for (int k = 0; k < TILE; ++k) {
-      double d = sT[sw64(k, k)];
-      if (!(d > 0.0)) {  // not SPD (or NaN): first failing row
-        if (tid == 0 && sFail[0] == 0) sFail[0] = J * TILE + k + 1;
-      }
-      double piv = sqrt(d), inv = 1.0 / piv;
-      __syncthreads();
-      if (tid == 0) sT[sw64(k, k)] = piv;
-      if (tid > k && tid < TILE) sT[sw64(tid, k)] *= inv;
-      __syncthreads();
-      {
-        int i = k + 1 + (tid >> 2);
-        if (i < TILE) {
-          double lik = sT[sw64(i, k)];
-          for (int j = k + 1 + (tid & 3); j <= i; j += 4) sT[sw64(i, j)] -= lik * sT[sw64(j, k)];
-        }
-      }
-      __syncthreads();
-    }
-    if (sFail[0]) break;
-    // ---------- invert G_JJ (lower) into the stage area, then copy back ----------
-    {
-      double* sInv = sStage;  // 64x64 swizzled
-      const int j = tid >> 2, sub = tid & 3;  // column j, 4 lanes per column
-      for (int i = 0; i < TILE; ++i) {
-        double part = 0.0;
-        for (int k = j + sub; k < i; k += 4) part += sT[sw64(i, k)] * sInv[sw64(k, j)];
-        part += __shfl_xor_sync(0xffffffffu, part, 1);  // 4-lane group = one column
-        part += __shfl_xor_sync(0xffffffffu, part, 2);
-        double v = (i >= j) ? ((i == j ? 1.0 : 0.0) - part) / sT[sw64(i, i)] : 0.0;
-        if (sub == 0) sInv[sw64(i, j)] = v;  // zero above the diagonal
-        __syncwarp();
-      }
-      __syncthreads();
-      for (int idx = tid; idx < TILE_ELEMS; idx += NTHR) sT[idx] = sInv[idx];
-      __syncthreads();
-    }
+    // ---------- blocked Cholesky + inverse of the 64x64 diagonal tile ----------
+    if (!factor_invert_diag(sT, sStage, sFail, J, tid)) break;
     // ---------- Y_J = G_JJ^-1 (Kfe_J - sum) ; S += Y_J^T Y_J ----------
     {
       double y[2] = {0.0, 0.0};

@@ -35,6 +35,7 @@ struct hom_ctx {
   double *val = nullptr, *diag = nullptr, *rhs = nullptr, *cgwork = nullptr, *Rfree = nullptr, *scal = nullptr;
   CgState* cgst = nullptr;
   size_t phase_bytes = 0, mat_bytes = 0;
+  int max_slice_nnz = 0;  // largest CSR slice of a 8-CTA cluster partition (CG smem sizing)
   // event profiling (hom_profile_enable / hom_profile_read)
   struct ProfRec {
     int cls;
@@ -278,6 +279,11 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
       rowptr[row + 1] = (int)col.size();
     }
   M.nnz = (int)col.size();
+  for (int G : {8, 16})
+    for (int g = 0; g < G; ++g) {
+      int a = (int)((long)M.ndof * g / G), b = (int)((long)M.ndof * (g + 1) / G);
+      c->max_slice_nnz = std::max(c->max_slice_nnz, rowptr[b] - rowptr[a]);
+    }
   std::vector<uint8_t> dmask(M.ndof, 0);
   std::vector<double> dval(M.ndof, 0.0), fbody(M.ndof, 0.0);
   if (mac->n_dirichlet > 0 && (!mac->dirichlet_dof || !mac->dirichlet_value))
@@ -546,8 +552,10 @@ int hom_macro_solve(hom_ctx* c, const double* d_D, const double* d_S, double sca
   run(c, HOM_PROF_MACRO_ASSEMBLE, s, [&] { hom::launch_macro_assemble(c->M, d_D, c->val, c->diag, s); });
   run(c, HOM_PROF_MACRO_ASSEMBLE, s, [&] { hom::launch_macro_rhs(c->M, c->val, d_S, scale, c->rhs, nullptr, s); });
   run(c, HOM_PROF_CG, s, [&] {
-    hom::launch_macro_cg(c->M, c->val, c->diag, c->rhs, scale, c->opt.cg_rtol, c->opt.cg_max_iter, d_x,
-                         c->cgwork, c->cgst, s);
+    if (!hom::launch_macro_cg_cluster(c->M, c->max_slice_nnz, c->val, c->diag, c->rhs, scale, c->opt.cg_rtol,
+                                      c->opt.cg_max_iter, d_x, c->cgwork, c->cgst, s))
+      hom::launch_macro_cg(c->M, c->val, c->diag, c->rhs, scale, c->opt.cg_rtol, c->opt.cg_max_iter, d_x,
+                           c->cgwork, c->cgst, s);
   });
   int rc = check_cuda(c, cudaGetLastError(), "hom_macro_solve");
   if (rc) return rc;

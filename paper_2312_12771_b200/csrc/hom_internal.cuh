@@ -84,6 +84,9 @@ void launch_macro_rhs(const MacroDev& M, const double* val, const double* S, dou
 void launch_macro_cg(const MacroDev& M, const double* val, const double* diag, const double* rhs,
                      double scale, double rtol, int max_iter, double* x, double* work,
                      CgState* st, cudaStream_t s);
+bool launch_macro_cg_cluster(const MacroDev& M, int max_slice_nnz, const double* val, const double* diag,
+                             const double* rhs, double scale, double rtol, int max_iter, double* x, double* p,
+                             CgState* st, cudaStream_t s);
 void launch_norm(const double* v, int n, double* out, cudaStream_t s);
 void launch_axpy(double* y, const double* x, double a, int n, cudaStream_t s);
 void launch_recover(const RveDev& R, int B, const double* X, const double* kin, double* w,

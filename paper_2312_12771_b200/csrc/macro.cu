@@ -6,7 +6,11 @@
 // R = sum_qp eta B_q^T S_b - f_body.  Recovery follows eq:reduction
 // and the dw update.  All reductions run in a fixed order so the
 // results are bitwise reproducible.
+#include <cooperative_groups.h>
+
 #include "hom_internal.cuh"
+
+namespace cgx = cooperative_groups;
 
 namespace hom {
 
@@ -294,6 +298,179 @@ __global__ void k_axpy(double* __restrict__ y, const double* __restrict__ x, dou
 }
 void launch_axpy(double* y, const double* x, double a, int n, cudaStream_t s) {
   k_axpy<<<(n + 255) / 256, 256, 0, s>>>(y, x, a, n);
+}
+
+// ---------------------------------------------------------------- K6/K7: cluster PCG
+// One thread-block cluster (16 CTAs where the device allows it, else 8) runs the
+// whole Jacobi-PCG in a single launch: CTA g owns a contiguous slice of rows and
+// keeps that slice of the CSR matrix and of x, r, 1/diag, q, p in shared memory;
+// p is published in global memory (L2) for the SpMV gathers of the other CTAs;
+// dot products are reduced through DSMEM in a fixed order (bitwise deterministic,
+// identical in every CTA), and cluster barriers (barrier.cluster, which also
+// invalidates L1) separate the phases -- three per iteration, no host round trip.
+constexpr int CGC_THR = 512;
+constexpr int CGC_MAXG = 16;
+
+__device__ __forceinline__ void cl_reduce2(cgx::cluster_group& cl, double* slots, double& a, double& b,
+                                           double* wred) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+  }
+  if (lane == 0) { wred[warp] = a; wred[32 + warp] = b; }
+  __syncthreads();
+  const int G = cl.num_blocks();
+  if (threadIdx.x < G) {  // thread t publishes this CTA's partials into CTA t's slots
+    double sa = 0.0, sb = 0.0;
+    for (int w = 0; w < CGC_THR / 32; ++w) { sa += wred[w]; sb += wred[32 + w]; }
+    double* remote = cl.map_shared_rank(slots, (int)threadIdx.x);
+    remote[cl.block_rank()] = sa;
+    remote[CGC_MAXG + cl.block_rank()] = sb;
+  }
+  cl.sync();
+  a = 0.0;
+  b = 0.0;
+  for (int k = 0; k < G; ++k) { a += slots[k]; b += slots[CGC_MAXG + k]; }
+}
+
+__global__ void __launch_bounds__(CGC_THR) k_macro_cg_cluster(MacroDev M, const double* __restrict__ val,
+                                                              const double* __restrict__ diag,
+                                                              const double* __restrict__ b, double scale,
+                                                              double rtol, int max_iter, double* __restrict__ xout,
+                                                              double* __restrict__ pg, CgState* st,
+                                                              int csr_in_smem) {
+  cgx::cluster_group cl = cgx::this_cluster();
+  const int G = cl.num_blocks(), g = cl.block_rank();
+  const int n = M.ndof, tid = threadIdx.x;
+  const int r0 = (int)((long)n * g / G), r1 = (int)((long)n * (g + 1) / G), nr = r1 - r0;
+  extern __shared__ __align__(16) double sm[];
+  double* slots = sm;                      // [2 buffers][2*CGC_MAXG]
+  double* wred = sm + 4 * CGC_MAXG;        // [64]
+  double* sx = wred + 64;
+  double* sr = sx + nr;
+  double* sdi = sr + nr;
+  double* sq = sdi + nr;
+  double* sp = sq + nr;
+  double* sval = sp + nr;
+  const int nz0 = M.rowptr[r0], nnz = M.rowptr[r1] - nz0;
+  int* scol = reinterpret_cast<int*>(sval + (csr_in_smem ? nnz : 0));
+  int* srow = scol + (csr_in_smem ? nnz : 0);
+  if (csr_in_smem) {
+    for (int k = tid; k < nnz; k += CGC_THR) { sval[k] = val[nz0 + k]; scol[k] = M.col[nz0 + k]; }
+    for (int i = tid; i <= nr; i += CGC_THR) srow[i] = M.rowptr[r0 + i] - nz0;
+  }
+  double rz = 0.0, bb = 0.0;
+  for (int i = tid; i < nr; i += CGC_THR) {
+    int gi = r0 + i;
+    bool d = M.dmask[gi];
+    double bi = d ? 0.0 : b[gi];
+    double di = d ? 0.0 : 1.0 / diag[gi];
+    double zi = bi * di;
+    sx[i] = 0.0; sr[i] = bi; sdi[i] = di; sp[i] = zi;
+    pg[gi] = zi;
+    rz += bi * zi;
+    bb += bi * bi;
+  }
+  cl_reduce2(cl, slots + 2 * CGC_MAXG, rz, bb, wred);  // also publishes p
+  const double bnorm = sqrt(bb);
+  int it = 0, status = 0;
+  double rr = bb;
+  if (bnorm > 0.0) {
+    for (it = 1; it <= max_iter; ++it) {
+      double pq = 0.0, dummy = 0.0;
+      for (int i = tid; i < nr; i += CGC_THR) {
+        double s = 0.0;
+        if (sdi[i] != 0.0) {
+          if (csr_in_smem) {
+            for (int k = srow[i]; k < srow[i + 1]; ++k) s += sval[k] * pg[scol[k]];
+          } else {
+            for (int k = M.rowptr[r0 + i]; k < M.rowptr[r0 + i + 1]; ++k) s += val[k] * pg[M.col[k]];
+          }
+        }
+        sq[i] = s;
+        pq += sp[i] * s;
+      }
+      cl_reduce2(cl, slots, pq, dummy, wred);
+      if (!(pq > 0.0)) { status = 6; break; }
+      const double alpha = rz / pq;
+      double rzn = 0.0;
+      rr = 0.0;
+      for (int i = tid; i < nr; i += CGC_THR) {
+        sx[i] += alpha * sp[i];
+        double ri = sr[i] - alpha * sq[i];
+        sr[i] = ri;
+        rr += ri * ri;
+        rzn += ri * ri * sdi[i];
+      }
+      cl_reduce2(cl, slots + 2 * CGC_MAXG, rr, rzn, wred);
+      if (sqrt(rr) <= rtol * bnorm) break;
+      const double beta = rzn / rz;
+      rz = rzn;
+      for (int i = tid; i < nr; i += CGC_THR) {
+        double pi = sr[i] * sdi[i] + beta * sp[i];
+        sp[i] = pi;
+        pg[r0 + i] = pi;
+      }
+      cl.sync();  // p visible cluster-wide (release/acquire; L1 invalidated)
+    }
+    if (status == 0 && it > max_iter) { status = 5; it = max_iter; }
+  }
+  for (int i = tid; i < nr; i += CGC_THR) {
+    int gi = r0 + i;
+    xout[gi] = M.dmask[gi] ? scale * M.dval[gi] : sx[i];
+  }
+  if (g == 0 && tid == 0) {
+    st->iterations = it;
+    st->status = status;
+    st->rel_residual = bnorm > 0.0 ? sqrt(rr) / bnorm : 0.0;
+    st->rhs_norm = bnorm;
+  }
+  cl.sync();  // no CTA exits while others may still read its shared memory
+}
+
+// Returns false if no cluster configuration fits (caller falls back to one CTA).
+bool launch_macro_cg_cluster(const MacroDev& M, int max_slice_nnz, const double* val, const double* diag,
+                             const double* rhs, double scale, double rtol, int max_iter, double* x, double* p,
+                             CgState* st, cudaStream_t s) {
+  static int cached_G = -1;
+  for (int G : {16, 8}) {
+    if (cached_G > 0 && G != cached_G) continue;
+    int max_rows = (M.ndof + G - 1) / G + 1;
+    size_t base = (size_t)(4 * CGC_MAXG + 64 + 5 * max_rows) * 8;
+    size_t with_csr = base + (size_t)max_slice_nnz * 12 + (size_t)(max_rows + 1) * 4 + 64;
+    int csr = with_csr <= 200 * 1024;
+    size_t sm = csr ? with_csr : base;
+    if (sm > 200 * 1024) continue;
+    cudaFuncSetAttribute(k_macro_cg_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (G > 8) cudaFuncSetAttribute(k_macro_cg_cluster, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G, 1, 1);
+    cfg.blockDim = dim3(CGC_THR, 1, 1);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, k_macro_cg_cluster, &cfg) != cudaSuccess || ncl < 1) {
+      cudaGetLastError();
+      continue;
+    }
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_macro_cg_cluster, M, val, diag, rhs, scale, rtol, max_iter, x, p,
+                                       st, csr);
+    if (e == cudaSuccess) {
+      cached_G = G;
+      return true;
+    }
+    cudaGetLastError();
+  }
+  return false;
 }
 
 // ---------------------------------------------------------------- K8 recovery
