@@ -95,16 +95,17 @@ __device__ __forceinline__ void mma_chunk(double (&acc)[4][2][2], const double* 
 __device__ __forceinline__ int chol_inv16(double* sT, double* sX, int k0, int lane) {
   const unsigned FULL = 0xffffffffu;
   const int r = lane & 15;
-  double a[16];
+  double a[16], ip[16];
 #pragma unroll
   for (int c = 0; c < 16; ++c) a[c] = (c <= r) ? sT[sw64(k0 + r, k0 + c)] : 0.0;
   int fail = 16;
+  // Pivot chain: one rsqrt per pivot (no sqrt, no division); every lane keeps 1/L_kk.
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
     double dkk = __shfl_sync(FULL, a[k], k);
     if (!(dkk > 0.0) && fail == 16) fail = k;
-    double piv = sqrt(dkk), ip = 1.0 / piv;
-    a[k] = (r == k) ? piv : a[k] * ip;
+    ip[k] = rsqrt(dkk);
+    a[k] = (r == k) ? dkk * ip[k] : a[k] * ip[k];
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       if (j > k) {  // compile-time after unrolling: a[] stays in registers
@@ -119,16 +120,19 @@ __device__ __forceinline__ int chol_inv16(double* sT, double* sX, int k0, int la
       if (c <= r) sT[sw64(k0 + r, k0 + c)] = a[c];
   }
   __syncwarp();
-  // X = L^-1: lane c builds column c by forward substitution (L rows read as smem broadcasts)
+  // X = L^-1: lane c builds column c by forward substitution (L rows read as smem
+  // broadcasts), two partial sums to halve the dependent FMA chain.
   const int c = lane & 15;
   double x[16];
 #pragma unroll
   for (int rr = 0; rr < 16; ++rr) {
-    double s = 0.0;
+    double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-    for (int k = 0; k < 16; ++k)
-      if (k < rr) s = fma(sT[sw64(k0 + rr, k0 + k)], x[k], s);
-    x[rr] = (rr >= c) ? (((rr == c) ? 1.0 : 0.0) - s) / sT[sw64(k0 + rr, k0 + rr)] : 0.0;
+    for (int k = 0; k < 16; k += 2) {
+      if (k < rr) s0 = fma(sT[sw64(k0 + rr, k0 + k)], x[k], s0);
+      if (k + 1 < rr) s1 = fma(sT[sw64(k0 + rr, k0 + k + 1)], x[k + 1], s1);
+    }
+    x[rr] = (rr >= c) ? (((rr == c) ? 1.0 : 0.0) - (s0 + s1)) * ip[rr] : 0.0;
   }
   if (lane < 16) {
 #pragma unroll

@@ -387,6 +387,65 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   }
   R.vol = vol;
   PairTables RP = build_pairs(R.n_indep, R.ne, nen, eind);
+  // geometry-only element matrices of the isotropic closed form (K1 small strain)
+  const int ND = nen * dim, m = c->m;
+  std::vector<double> Klam, Kmu, Flam, Fmu, evol(R.ne, 0.0);
+  if (!c->finite) {
+    Klam.assign((size_t)R.ne * ND * ND, 0.0);
+    Kmu.assign((size_t)R.ne * ND * ND, 0.0);
+    Flam.assign((size_t)R.ne * ND * m, 0.0);
+    Fmu.assign((size_t)R.ne * ND * m, 0.0);
+  }
+  static const int shear2[1][2] = {{0, 1}};
+  static const int shear3[3][2] = {{1, 2}, {0, 2}, {0, 1}};
+  for (int e = 0; e < R.ne; ++e)
+    for (int q = 0; q < nq; ++q) {
+      const double w = rw[(size_t)e * nq + q];
+      evol[e] += w;
+      if (c->finite) continue;
+      const double* G = &rgrad[((size_t)e * nq + q) * nen * dim];
+      for (int a = 0; a < nen; ++a)
+        for (int i = 0; i < dim; ++i) {
+          const double* ga = G + a * dim;
+          for (int bb = 0; bb < nen; ++bb) {
+            const double* gb = G + bb * dim;
+            double dot = 0.0;
+            for (int t = 0; t < dim; ++t) dot += ga[t] * gb[t];
+            for (int j = 0; j < dim; ++j) {
+              size_t idx = (size_t)e * ND * ND + (size_t)(a * dim + i) * ND + bb * dim + j;
+              Klam[idx] += w * ga[i] * gb[j];
+              Kmu[idx] += w * (ga[j] * gb[i] + (i == j ? dot : 0.0));
+            }
+          }
+          for (int k = 0; k < m; ++k) {
+            size_t idx = ((size_t)e * ND + a * dim + i) * m + k;
+            if (k < dim) {
+              Flam[idx] += w * ga[i];
+              Fmu[idx] += (i == k) ? w * 2.0 * ga[k] : 0.0;
+            } else {
+              const int* pr = dim == 2 ? shear2[k - 2] : shear3[k - 3];
+              if (i == pr[0]) Fmu[idx] += w * ga[pr[1]];
+              if (i == pr[1]) Fmu[idx] += w * ga[pr[0]];
+            }
+          }
+        }
+    }
+  // structural nonzero pattern of the lower 64x64 tiles (same for every RVE)
+  const int nt_ = (dim * R.n_indep + hom::TILE - 1) / hom::TILE;
+  std::vector<uint8_t> tile_nz((size_t)nt_ * nt_, 0);
+  for (int t = 0; t < nt_; ++t) tile_nz[(size_t)t * nt_ + t] = 1;
+  for (int pp = 0; pp < R.n_indep; ++pp) {
+    if (pp == R.corner) continue;
+    for (int k = RP.nbr_ptr[pp]; k < RP.nbr_ptr[pp + 1]; ++k) {
+      int qq = RP.nbr[k];
+      if (qq == R.corner) continue;
+      for (int ci = 0; ci < dim; ++ci)
+        for (int cj = 0; cj < dim; ++cj) {
+          int I = (pp * dim + ci) / hom::TILE, J = (qq * dim + cj) / hom::TILE;
+          if (I >= J) tile_nz[(size_t)I * nt_ + J] = 1;
+        }
+    }
+  }
   R.phase_per_rve = ph->per_rve ? 1 : 0;
   R.mat_per_rve = mat->per_rve ? 1 : 0;
   R.n_phase = mat->n_phases;
@@ -415,6 +474,12 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   R.nbr_owner = upload(c, RP.owner, s, &rc);
   R.sh_ptr = upload(c, RP.sh_ptr, s, &rc);
   R.sh = upload(c, RP.sh, s, &rc);
+  R.Klam = upload(c, Klam, s, &rc);
+  R.Kmu = upload(c, Kmu, s, &rc);
+  R.Flam = upload(c, Flam, s, &rc);
+  R.Fmu = upload(c, Fmu, s, &rc);
+  R.evol = upload(c, evol, s, &rc);
+  R.tile_nz = upload(c, tile_nz, s, &rc);
   R.phase = upload(c, phase, s, &rc);
   R.mat = upload(c, params, s, &rc);
   c->phase_bytes = phase.size();

@@ -35,6 +35,14 @@ struct RveDev {
   int phase_per_rve;
   const double* mat;              // [B|1][n_phase][2]
   int mat_per_rve, n_phase;
+  // geometry-only element matrices of the isotropic closed form (small strain):
+  // K_e = lam_e * Klam_e + mu_e * Kmu_e, K_fe rows = lam_e * Flam_e + mu_e * Fmu_e
+  const double* Klam;             // [ne][nen*dim][nen*dim]
+  const double* Kmu;
+  const double* Flam;             // [ne][nen*dim][m]
+  const double* Fmu;
+  const double* evol;             // [ne] element volume
+  const uint8_t* tile_nz;         // [nt*nt] 1 if lower tile (I,J) of K_ff has a structural nonzero
 };
 
 struct MacroDev {

@@ -93,27 +93,48 @@ void launch_rve_material_nh(const RveDev& R, int b0, int nb, const double* F, co
 }
 
 // ---------------------------------------------------------------------------
-// K1: assembly.  ISO = isotropic closed form K_ab^{ij} = lam g_a^i g_b^j +
-// mu g_a^j g_b^i + mu d_ij (g_a . g_b) (small strain); otherwise the tangent
-// is read per qp from Aq (finite strain, full-gradient form).
+// K1: assembly.  ISO (small strain): element blocks from geometry-only tables,
+// K_e = lam_e Klam_e + mu_e Kmu_e (isotropic closed form K_ab^{ij} = lam g_a^i g_b^j
+// + mu g_a^j g_b^i + mu d_ij g_a.g_b integrated at setup).  Finite strain: the
+// tangent is read per qp from Aq (full-gradient form).
+//
+// Tiles: structurally-zero tiles (per-mesh bitmap) are written from a zero
+// buffer with TMA bulk stores; nonzero tiles are zero-filled + scattered in one
+// of two shared-memory buffers and streamed out with cp.async.bulk while the
+// next tile is being built (double buffering).
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(ssrc);
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(s), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+constexpr int ZBUF = 1024;  // doubles of the zero buffer (8 KB): 4 bulk stores per zero tile
+
 template <int DIM, bool ISO>
 __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double* __restrict__ Kt,
                                                        double* __restrict__ Y, double* __restrict__ Cavg,
                                                        double* __restrict__ Pavg, double* __restrict__ rfn,
                                                        const double* __restrict__ Aq,
                                                        const double* __restrict__ Pq) {
-  extern __shared__ __align__(16) double smem[];
-  double* tile = smem;                 // [64*64]
-  double* red = smem + TILE_ELEMS;     // [NTHR] reduction scratch
-  double* s_lam = red + NTHR;          // [ne] (ISO)
-  double* s_mu = s_lam + R.ne;         // [ne] (ISO)
+  extern __shared__ __align__(128) double smem[];
+  double* tbuf = smem;                       // 2 x [64*64]
+  double* zbuf = smem + 2 * TILE_ELEMS;      // [ZBUF] zeros
+  double* red = zbuf + ZBUF;                 // [NTHR] reduction scratch
+  double* s_lam = red + NTHR;                // [ne] (ISO)
+  double* s_mu = s_lam + R.ne;               // [ne] (ISO)
   const int tid = threadIdx.x;
   const int bl = blockIdx.x;
   const int b = b0 + bl;
   const int nen = R.nen, nq = R.nq, ne = R.ne;
+  constexpr int ND = ISO ? (DIM == 2 ? 8 : 24) : 8;  // nen*dim
   const long tq0 = (long)bl * ne * nq;  // offset of this RVE in Aq/Pq (chunk-local)
 
+  for (int i = tid; i < ZBUF; i += NTHR) zbuf[i] = 0.0;
   if (ISO) {
     const uint8_t* ph = R.phase + (R.phase_per_rve ? (long)b * ne : 0);
     const double* mt = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * 2 : 0);
@@ -132,13 +153,15 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
     double acc[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) acc[i] = 0.0;
-    for (int eq = tid; eq < ne * nq; eq += NTHR) {
-      double wq = R.wdet[eq];
-      if (ISO) {
-        int e = eq / nq;
-        acc[0] += wq * s_lam[e];
-        acc[1] += wq * s_mu[e];
-      } else {
+    if (ISO) {
+      for (int e = tid; e < ne; e += NTHR) {
+        double v = R.evol[e];
+        acc[0] += v * s_lam[e];
+        acc[1] += v * s_mu[e];
+      }
+    } else {
+      for (int eq = tid; eq < ne * nq; eq += NTHR) {
+        double wq = R.wdet[eq];
         const double* A = Aq + (tq0 + eq) * 16;
         const double* P = Pq + (tq0 + eq) * 4;
 #pragma unroll
@@ -147,29 +170,37 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
         for (int i = 0; i < 4; ++i) acc[16 + i] += wq * P[i];
       }
     }
+    // one pass: warp shuffles, then NV partial rows in smem
+    const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
     for (int v = 0; v < NV; ++v) {
-      red[tid] = acc[v];
-      __syncthreads();
-      for (int s = NTHR / 2; s > 0; s >>= 1) {
-        if (tid < s) red[tid] += red[tid + s];
-        __syncthreads();
-      }
-      acc[v] = red[0] / R.vol;  // every thread keeps the total
-      __syncthreads();
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc[v] += __shfl_down_sync(0xffffffffu, acc[v], o);
     }
+    if (lane == 0)
+#pragma unroll
+      for (int v = 0; v < NV; ++v) red[v * 8 + warp] = acc[v];
+    __syncthreads();
     if (tid == 0) {
+      double tot[NV];
+      for (int v = 0; v < NV; ++v) {
+        tot[v] = 0.0;
+        for (int w = 0; w < NTHR / 32; ++w) tot[v] += red[v * 8 + w];
+        tot[v] /= R.vol;
+      }
       double* C = Cavg + (long)bl * 64;
       if (ISO) {
         const int m = R.m;
         for (int i = 0; i < m * m; ++i) C[i] = 0.0;
         for (int i = 0; i < DIM; ++i)
-          for (int j = 0; j < DIM; ++j) C[i * m + j] = acc[0] + (i == j ? 2.0 * acc[1] : 0.0);
-        for (int i = DIM; i < m; ++i) C[i * m + i] = acc[1];
+          for (int j = 0; j < DIM; ++j) C[i * m + j] = tot[0] + (i == j ? 2.0 * tot[1] : 0.0);
+        for (int i = DIM; i < m; ++i) C[i * m + i] = tot[1];
       } else {
-        for (int i = 0; i < 16; ++i) C[i] = acc[i];
-        for (int i = 0; i < 4; ++i) Pavg[(long)bl * 8 + i] = acc[16 + i];
+        for (int i = 0; i < 16; ++i) C[i] = tot[i];
+        for (int i = 0; i < 4; ++i) Pavg[(long)bl * 8 + i] = tot[16 + i];
       }
     }
+    __syncthreads();
   }
 
   // ---- right-hand sides: K_fe (cols 0..m-1) and r_f (col m, finite strain) ----
@@ -184,18 +215,17 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
       if (i < R.npad && p != R.corner) {
         for (int s = R.inc_ptr[p]; s < R.inc_ptr[p + 1]; ++s) {
           int e = R.inc[s] >> 4, a = R.inc[s] & 15;
-          for (int q = 0; q < nq; ++q) {
-            const double* g = R.grad + ((long)(e * nq + q) * nen + a) * DIM;
-            double wq = R.wdet[e * nq + q];
-            if (ISO) {
-              double lam = s_lam[e], mu = s_mu[e];
-              for (int k = 0; k < R.m; ++k) {
-                double v = 0.0;
+          if (ISO) {
+            const double lam = s_lam[e], mu = s_mu[e];
+            const double* fl = R.Flam + ((long)e * ND + a * DIM + c) * R.m;
+            const double* fm = R.Fmu + ((long)e * ND + a * DIM + c) * R.m;
 #pragma unroll
-                for (int J = 0; J < DIM; ++J) v += g[J] * unit_stress<DIM>(k, c, J, lam, mu);
-                out[k] += wq * v;
-              }
-            } else {
+            for (int k = 0; k < RHSW; ++k)
+              if (k < R.m) out[k] += lam * fl[k] + mu * fm[k];
+          } else {
+            for (int q = 0; q < nq; ++q) {
+              const double* g = R.grad + ((long)(e * nq + q) * nen + a) * DIM;
+              double wq = R.wdet[e * nq + q];
               const double* A = Aq + (tq0 + e * nq + q) * 16;
               const double* P = Pq + (tq0 + e * nq + q) * 4;
               for (int k = 0; k < 4; ++k) {
@@ -232,12 +262,27 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   // ---- K_ff tiles ----
   const int nt = R.nt;
   double* Kb = Kt + (long)bl * (nt * (nt + 1) / 2) * TILE_ELEMS;
+  if (tid == 0) fence_proxy_async();  // zbuf visible to the async proxy
+  int nzt = 0;                        // nonzero tiles built so far (buffer parity)
   for (int I = 0; I < nt; ++I) {
     const int r0 = I * TILE;
     int p_lo = r0 / DIM, p_hi = min((r0 + TILE - 1) / DIM, R.n_indep - 1);
     const int k_lo = p_lo < R.n_indep ? R.nbr_ptr[p_lo] : 0;
     const int k_hi = p_lo < R.n_indep ? R.nbr_ptr[p_hi + 1] : 0;
     for (int J = 0; J <= I; ++J) {
+      double* gt = Kb + (long)(I * (I + 1) / 2 + J) * TILE_ELEMS;
+      if (!R.tile_nz[I * nt + J]) {
+        if (tid == 0) {
+#pragma unroll
+          for (int z = 0; z < TILE_ELEMS / ZBUF; ++z) bulk_store(gt + z * ZBUF, zbuf, ZBUF * 8);
+          bulk_commit();
+        }
+        continue;
+      }
+      double* tile = tbuf + (nzt & 1) * TILE_ELEMS;
+      ++nzt;
+      if (tid == 0) bulk_wait_read1();  // the buffer's previous bulk store has finished reading
+      __syncthreads();
       const int c0 = J * TILE;
       double2* t2 = reinterpret_cast<double2*>(tile);
       for (int i = tid; i < TILE_ELEMS / 2; i += NTHR) t2[i] = make_double2(0.0, 0.0);
@@ -255,21 +300,19 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
         for (int s = R.sh_ptr[k]; s < R.sh_ptr[k + 1]; ++s) {
           int code = R.sh[s];
           int e = code >> 8, a = (code >> 4) & 15, bb = code & 15;
-          for (int qq = 0; qq < nq; ++qq) {
-            const double* ga = R.grad + ((long)(e * nq + qq) * nen + a) * DIM;
-            const double* gb = R.grad + ((long)(e * nq + qq) * nen + bb) * DIM;
-            double wq = R.wdet[e * nq + qq];
-            if (ISO) {
-              double lam = s_lam[e] * wq, mu = s_mu[e] * wq;
-              double dot = 0.0;
+          if (ISO) {
+            const double lam = s_lam[e], mu = s_mu[e];
+            const double* kl = R.Klam + (long)e * ND * ND + (a * DIM) * ND + bb * DIM;
+            const double* km = R.Kmu + (long)e * ND * ND + (a * DIM) * ND + bb * DIM;
 #pragma unroll
-              for (int t = 0; t < DIM; ++t) dot += ga[t] * gb[t];
+            for (int i = 0; i < DIM; ++i)
 #pragma unroll
-              for (int i = 0; i < DIM; ++i)
-#pragma unroll
-                for (int j = 0; j < DIM; ++j)
-                  blk[i][j] += lam * ga[i] * gb[j] + mu * ga[j] * gb[i] + (i == j ? mu * dot : 0.0);
-            } else {
+              for (int j = 0; j < DIM; ++j) blk[i][j] += lam * kl[i * ND + j] + mu * km[i * ND + j];
+          } else {
+            for (int qq = 0; qq < nq; ++qq) {
+              const double* ga = R.grad + ((long)(e * nq + qq) * nen + a) * DIM;
+              const double* gb = R.grad + ((long)(e * nq + qq) * nen + bb) * DIM;
+              double wq = R.wdet[e * nq + qq];
               const double* A = Aq + (tq0 + e * nq + qq) * 16;
 #pragma unroll
               for (int i = 0; i < DIM; ++i)
@@ -304,17 +347,20 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
         }
       }
       __syncthreads();
-      double2* dst = reinterpret_cast<double2*>(Kb + (long)(I * (I + 1) / 2 + J) * TILE_ELEMS);
-      for (int i = tid; i < TILE_ELEMS / 2; i += NTHR) dst[i] = t2[i];
-      __syncthreads();
+      if (tid == 0) {
+        fence_proxy_async();
+        bulk_store(gt, tile, TILE_ELEMS * 8);
+        bulk_commit();
+      }
     }
   }
+  if (tid == 0) bulk_wait_all();
 }
 
 void launch_rve_assemble(const RveDev& R, int b0, int nb, double* Kt, double* Y, double* Cavg,
                          double* Pavg, double* rfn, const double* Aq, const double* Pq,
                          cudaStream_t s) {
-  size_t sm = (size_t)(TILE_ELEMS + NTHR + 2 * R.ne) * sizeof(double);
+  size_t sm = (size_t)(2 * TILE_ELEMS + ZBUF + NTHR + 2 * R.ne) * sizeof(double);
   if (R.finite) {
     auto k = k_rve_assemble<2, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
