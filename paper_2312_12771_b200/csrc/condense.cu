@@ -24,6 +24,10 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
+// -x by flipping the sign bit (integer op, keeps the FP64 pipe free for DMMA)
+__device__ __forceinline__ double neg(double x) {
+  return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ULL);
+}
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -33,7 +37,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-// swizzled word index inside a [rows][32] k-chunk and a [64][64] tile
+// swizzled word index inside a [rows][KC] k-chunk and a [rows][64] tile (row-chunk)
 __device__ __forceinline__ int sw32(int r, int k) { return r * KC + (k ^ ((r & 3) << 2)); }
 __device__ __forceinline__ int sw64(int r, int c) { return r * TILE + (c ^ ((r & 3) << 2)); }
 // [rows][8] right-hand-side block
@@ -43,61 +47,67 @@ __device__ __forceinline__ const double* tile_ptr(const double* Kb, int I, int J
   return Kb + (long)(I * (I + 1) / 2 + J) * TILE_ELEMS;
 }
 
-// Stage a [64][32] k-chunk of a row-major 64x64 global tile into swizzled smem.
+// ------------------------------------------------------------------ CTA shape
+// One CTA per RVE, 4 warps; each warp owns a 32x32 quadrant of a 64x64 output tile
+// (16 independent DMMA accumulators, 8 fragment loads per 16 DMMAs).  ~72 KB of
+// shared memory and <= 168 registers give 3 co-resident CTAs per SM: while one CTA
+// is in the latency-bound pivot chain of its diagonal tile (one warp, 64 dependent
+// rsqrt steps), the other two keep the FP64 tensor pipe busy
+// (profiles/r01/ncu_v6_cfg2.md: 30% of samples were warps waiting on that chain).
+constexpr int NTC = 128;          // threads per CTA
+constexpr int CPT = TILE / KC;    // k-chunks per tile
+
+// Phase timestamps for tools/condense_timing.cu only (HOM_TIMING build).
+#ifdef HOM_TIMING
+__device__ long long g_tm[64][40][8];
+__device__ __forceinline__ long long clk_ordered() {
+  long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+  return t;
+}
+#define TMARK(slot)                                                                   \
+  do {                                                                                \
+    if (blockIdx.x < 64 && J < 40 && threadIdx.x == 0) g_tm[blockIdx.x][J][slot] = clk_ordered(); \
+  } while (0)
+#else
+#define TMARK(slot) do {} while (0)
+#endif
+
+// Stage the [64][KC] k-chunk kc (columns kc*KC..) of a row-major 64x64 global tile into swizzled smem.
 __device__ __forceinline__ void stage_chunk(double* dst, const double* src_tile, int kc, int tid) {
+  constexpr int PPR = KC / 2;  // 16-byte pieces per row
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int idx = tid + NTHR * i;  // 0..1023 16-byte pieces
-    int r = idx >> 4, c2 = idx & 15;
+  for (int i = 0; i < 64 * PPR / NTC; ++i) {
+    int idx = tid + NTC * i;
+    int r = idx / PPR, c2 = idx % PPR;
     cp_async16(dst + sw32(r, 2 * c2), src_tile + r * TILE + kc * KC + 2 * c2);
   }
 }
-// Stage a full 64x64 tile into swizzled smem.
-__device__ __forceinline__ void stage_tile(double* dst, const double* src_tile, int tid) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    int idx = tid + NTHR * i;  // 0..2047
+// Stage rows [r0, r0+n) of a row-major 64x64 global tile into swizzled [n][64] smem (sw64, local rows).
+__device__ __forceinline__ void stage_rows(double* dst, const double* src_tile, int r0, int n, int tid) {
+  for (int idx = tid; idx < n * 32; idx += NTC) {
     int r = idx >> 5, c2 = idx & 31;
-    cp_async16(dst + sw64(r, 2 * c2), src_tile + r * TILE + 2 * c2);
+    cp_async16(dst + sw64(r, 2 * c2), src_tile + (r0 + r) * TILE + 2 * c2);
   }
 }
-// Stage rows [r0, r0+n) of an [NT][8] RHS block into swizzled [n][8] smem (n <= 64).
+// Stage rows [0, n) of an [.][8] RHS block into swizzled [n][8] smem.
 __device__ __forceinline__ void stage_rhs(double* dst, const double* src, int n, int tid) {
-  int pieces = n * (RHSW / 2);
-  for (int idx = tid; idx < pieces; idx += NTHR) {
+  for (int idx = tid; idx < n * (RHSW / 2); idx += NTC) {
     int k = idx >> 2, c2 = idx & 3;
     cp_async16(dst + swy(k, 2 * c2), src + k * RHSW + 2 * c2);
   }
 }
 
-// acc[4][2][2] += A(64x32 chunk) * B(64x32 chunk)^T for warp tile rows R0.., cols C0..
-__device__ __forceinline__ void mma_chunk(double (&acc)[4][2][2], const double* sA, const double* sB,
-                                          int R0, int C0, int lane) {
-  const int lr = lane >> 2, lc = lane & 3;
-#pragma unroll
-  for (int k0 = 0; k0 < KC; k0 += 4) {
-    double a[4], b[2];
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi) a[mi] = sA[sw32(R0 + 8 * mi + lr, k0 + lc)];
-#pragma unroll
-    for (int ni = 0; ni < 2; ++ni) b[ni] = sB[sw32(C0 + 8 * ni + lr, k0 + lc)];
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 2; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
-  }
-}
-
 // ------------------------------------------------------------------ diagonal tile
-// One warp: Cholesky of the 16x16 block at (k0,k0) of the swizzled 64x64 tile sT
-// (lower part, in registers, shuffles only) and its inverse into the same block of sX.
-// Returns the first failing local pivot (16 = none); warp-uniform.
-__device__ __forceinline__ int chol_inv16(double* sT, double* sX, int k0, int lane) {
+// Cholesky of the 16x16 block at (k0,k0) of sD (lower part; lanes hold rows,
+// shuffles only), then its inverse written over the block (zeros above the
+// diagonal).  Returns the first failing local pivot (16 = none); warp-uniform.
+__device__ __forceinline__ int chol16_inv_inplace(double* sD, int k0, int lane) {
   const unsigned FULL = 0xffffffffu;
   const int r = lane & 15;
   double a[16], ip[16];
 #pragma unroll
-  for (int c = 0; c < 16; ++c) a[c] = (c <= r) ? sT[sw64(k0 + r, k0 + c)] : 0.0;
+  for (int c = 0; c < 16; ++c) a[c] = (c <= r) ? sD[sw64(k0 + r, k0 + c)] : 0.0;
   int fail = 16;
   // Pivot chain: one rsqrt per pivot (no sqrt, no division); every lane keeps 1/L_kk.
 #pragma unroll
@@ -117,7 +127,7 @@ __device__ __forceinline__ int chol_inv16(double* sT, double* sX, int k0, int la
   if (lane < 16) {
 #pragma unroll
     for (int c = 0; c < 16; ++c)
-      if (c <= r) sT[sw64(k0 + r, k0 + c)] = a[c];
+      if (c <= r) sD[sw64(k0 + r, k0 + c)] = a[c];
   }
   __syncwarp();
   // X = L^-1: lane c builds column c by forward substitution (L rows read as smem
@@ -129,155 +139,190 @@ __device__ __forceinline__ int chol_inv16(double* sT, double* sX, int k0, int la
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll
     for (int k = 0; k < 16; k += 2) {
-      if (k < rr) s0 = fma(sT[sw64(k0 + rr, k0 + k)], x[k], s0);
-      if (k + 1 < rr) s1 = fma(sT[sw64(k0 + rr, k0 + k + 1)], x[k + 1], s1);
+      if (k < rr) s0 = fma(sD[sw64(k0 + rr, k0 + k)], x[k], s0);
+      if (k + 1 < rr) s1 = fma(sD[sw64(k0 + rr, k0 + k + 1)], x[k + 1], s1);
     }
     x[rr] = (rr >= c) ? (((rr == c) ? 1.0 : 0.0) - (s0 + s1)) * ip[rr] : 0.0;
   }
+  __syncwarp();
   if (lane < 16) {
 #pragma unroll
-    for (int rr = 0; rr < 16; ++rr) sX[sw64(k0 + rr, k0 + c)] = x[rr];
+    for (int rr = 0; rr < 16; ++rr) sD[sw64(k0 + rr, k0 + c)] = x[rr];
   }
+  __syncwarp();
   return fail;
 }
 
-// 8x8 output tile: acc += A[r0.., k0..k0+nk) * B[c0.., k0..)^T   (both [row][k], sw64)
-__device__ __forceinline__ void tile8_abt(double (&acc)[2], const double* A, int r0, const double* B, int c0,
-                                          int k0, int nk, int lane, double sign) {
-  const int lr = lane >> 2, lc = lane & 3;
-  for (int k = k0; k < k0 + nk; k += 4)
-    dmma(acc[0], acc[1], sign * A[sw64(r0 + lr, k + lc)], B[sw64(c0 + lr, k + lc)]);
-}
-// 8x8 output tile: acc += A[r0.., k..) * B[k.., c0..)   (A [row][k], B [k][col], sw64)
-__device__ __forceinline__ void tile8_ab(double (&acc)[2], const double* A, int r0, const double* B, int c0,
-                                         int k0, int nk, int lane, double sign) {
-  const int lr = lane >> 2, lc = lane & 3;
-  for (int k = k0; k < k0 + nk; k += 4)
-    dmma(acc[0], acc[1], sign * A[sw64(r0 + lr, k + lc)], B[sw64(k + lc, c0 + lr)]);
-}
 
-// Blocked (16-wide) Cholesky of the 64x64 tile in sT followed by the blocked
-// triangular inverse; on return sT holds G_JJ^-1 (exact zeros above the
-// diagonal).  sX is 64x64 + 768 doubles of scratch.  All block updates run on
-// DMMA; about 18 CTA barriers instead of one per column.
-__device__ __forceinline__ bool factor_invert_diag(double* sT, double* sX, int* sFail, int J, int tid) {
+// Blocked (16-wide) Cholesky of the SPD 64x64 tile in sD followed by the blocked
+// triangular inverse, in place, by the 4 warps of the CTA: the 16x16 pivot blocks on
+// warp 0 (registers + shuffles), panels, trailing updates and the off-diagonal
+// inverse blocks on DMMA over all warps.  On return sD = G_JJ^-1 (lower, exact zeros
+// above the diagonal: the caller zeroes the strict upper part).  sScr: 3 x 16x20.
+// Returns false (sFail set to the 1-based failing row of the RVE) on a non-positive pivot.
+__device__ __forceinline__ bool factor_invert_diag(double* sD, double* sScr, int* sFail, int J, int tid) {
   const int lane = tid & 31, warp = tid >> 5;
   const int lr = lane >> 2, lc = lane & 3;
-  for (int i = tid; i < TILE_ELEMS; i += NTHR) sX[i] = 0.0;
-  __syncthreads();
+#pragma unroll 1
   for (int kb = 0; kb < 4; ++kb) {
     const int k0 = 16 * kb;
     if (warp == 0) {
-      int f = chol_inv16(sT, sX, k0, lane);
-      if (f < 16 && lane == 0 && sFail[0] == 0) sFail[0] = J * TILE + k0 + f + 1;
+      const int f = chol16_inv_inplace(sD, k0, lane);  // block (kb,kb) := L_kk^-1
+      if (f < 16 && lane == 0) sFail[0] = J * TILE + k0 + f + 1;
     }
     __syncthreads();
     if (sFail[0]) return false;
     if (kb == 3) break;
-    const int rb0 = k0 + 16, nrb = (TILE - rb0) / 8;  // row blocks below the panel
-    // panel: L_ik = A_ik * Linv_kk^T, rows rb0..63, cols k0..k0+15 (nrb x 2 tiles)
-    double pan[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    const int nt_pan = nrb * 2;
+    const int rb0 = k0 + 16, nrt = (TILE - rb0) / 8;
+    // panel: L_ik = A_ik X_kk^T (X_kk lower: col tile 0 needs k < 8 only); row tiles over warps
+    double p[2][4];
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-      int t = warp + 8 * u;
-      if (t < nt_pan) tile8_abt(pan[u], sT, rb0 + 8 * (t >> 1), sX, k0 + 8 * (t & 1), k0, 16, lane, 1.0);
-    }
-    __syncthreads();
+      const int ti = warp + 4 * u;
+      if (ti < nrt) {
+        const int r = rb0 + 8 * ti + lr;
+        p[u][0] = p[u][1] = p[u][2] = p[u][3] = 0.0;
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      int t = warp + 8 * u;
-      if (t < nt_pan) {
-        int r = rb0 + 8 * (t >> 1) + lr, cc = k0 + 8 * (t & 1) + 2 * lc;
-        sT[sw64(r, cc)] = pan[u][0];
-        sT[sw64(r, cc + 1)] = pan[u][1];
+        for (int kk = 0; kk < 16; kk += 4) {
+          const double a = sD[sw64(r, k0 + kk + lc)];
+          if (kk < 8) dmma(p[u][0], p[u][1], a, sD[sw64(k0 + lr, k0 + kk + lc)]);
+          dmma(p[u][2], p[u][3], a, sD[sw64(k0 + 8 + lr, k0 + kk + lc)]);
+        }
       }
     }
     __syncthreads();
-    // trailing: A_ij -= L_ik L_jk^T for lower 8x8 tiles of rows/cols rb0..63
-    const int ntr = nrb * (nrb + 1) / 2;
-    for (int t = warp; t < ntr; t += 8) {
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int ti = warp + 4 * u;
+      if (ti < nrt) {
+        const int r = rb0 + 8 * ti + lr;
+        sD[sw64(r, k0 + 2 * lc)] = p[u][0];
+        sD[sw64(r, k0 + 2 * lc + 1)] = p[u][1];
+        sD[sw64(r, k0 + 8 + 2 * lc)] = p[u][2];
+        sD[sw64(r, k0 + 8 + 2 * lc + 1)] = p[u][3];
+      }
+    }
+    __syncthreads();
+    // trailing: A_ij -= L_ik L_jk^T on the lower 8x8 tiles of rows/cols rb0..63 (reads the
+    // panel columns, writes disjoint columns: no hazard between warps)
+    const int ntr = nrt * (nrt + 1) / 2;
+    for (int t = warp; t < ntr; t += 4) {
       int ti = 0;
       while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-      int tj = t - ti * (ti + 1) / 2;
-      int r = rb0 + 8 * ti, cb = rb0 + 8 * tj;
-      double acc[2] = {sT[sw64(r + lr, cb + 2 * lc)], sT[sw64(r + lr, cb + 2 * lc + 1)]};
-      tile8_abt(acc, sT, r, sT, cb, k0, 16, lane, -1.0);
-      sT[sw64(r + lr, cb + 2 * lc)] = acc[0];
-      sT[sw64(r + lr, cb + 2 * lc + 1)] = acc[1];
+      const int tj = t - ti * (ti + 1) / 2;
+      const int r = rb0 + 8 * ti, cb = rb0 + 8 * tj;
+      double acc0 = sD[sw64(r + lr, cb + 2 * lc)], acc1 = sD[sw64(r + lr, cb + 2 * lc + 1)];
+#pragma unroll
+      for (int kk = 0; kk < 16; kk += 4)
+        dmma(acc0, acc1, neg(sD[sw64(r + lr, k0 + kk + lc)]), sD[sw64(cb + lr, k0 + kk + lc)]);
+      sD[sw64(r + lr, cb + 2 * lc)] = acc0;
+      sD[sw64(r + lr, cb + 2 * lc + 1)] = acc1;
     }
     __syncthreads();
   }
-  // off-diagonal blocks of the inverse: X_ik = -X_ii sum_{j=k}^{i-1} L_ij X_jk
-  double* sTmp = sX + TILE_ELEMS;  // 3 blocks of 16x16, plain row-major
+  // off-diagonal blocks of the inverse, in place, block rows i ascending:
+  //   T_k = sum_{j=k}^{i-1} L_ij X_jk (all k < i in parallel; X_jk of rows j < i are final),
+  //   X_ik = -X_ii T_k written over L_ik after every T_k is formed.
+#pragma unroll 1
   for (int i = 1; i < 4; ++i) {
-    const int ntile = 4 * i;  // blocks k = 0..i-1, 2x2 tiles each
-    double tv[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    const int ntile = 4 * i;  // (k, tr, tc)
+    for (int t = warp; t < ntile; t += 4) {
+      const int k = t >> 2, tr = (t >> 1) & 1, tc = t & 1;
+      double t0 = 0.0, t1 = 0.0;
+      for (int j = k; j < i; ++j) {
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      int t = warp + 8 * u;
-      if (t < ntile) {
-        int k = t >> 2, q = t & 3;
-        tile8_ab(tv[u], sT, 16 * i + 8 * (q >> 1), sX, 16 * k + 8 * (q & 1), 16 * k, 16 * (i - k), lane, 1.0);
-        int rr = 8 * (q >> 1) + lr, cc = 8 * (q & 1) + 2 * lc;
-        sTmp[k * 256 + rr * 16 + cc] = tv[u][0];
-        sTmp[k * 256 + rr * 16 + cc + 1] = tv[u][1];
+        for (int kk = 0; kk < 16; kk += 4) {
+          if (j == k && tc == 1 && kk < 8) continue;  // X_kk[kk][8+n] = 0 for kk < 8
+          dmma(t0, t1, sD[sw64(16 * i + 8 * tr + lr, 16 * j + kk + lc)],
+               sD[sw64(16 * j + kk + lc, 16 * k + 8 * tc + lr)]);
+        }
       }
+      double* W = sScr + k * 320;
+      W[(8 * tr + lr) * 20 + 8 * tc + 2 * lc] = t0;
+      W[(8 * tr + lr) * 20 + 8 * tc + 2 * lc + 1] = t1;
     }
     __syncthreads();
+    for (int t = warp; t < ntile; t += 4) {
+      const int k = t >> 2, tr = (t >> 1) & 1, tc = t & 1;
+      const double* W = sScr + k * 320;
+      double o0 = 0.0, o1 = 0.0;
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      int t = warp + 8 * u;
-      if (t < ntile) {
-        int k = t >> 2, q = t & 3;
-        int r0 = 8 * (q >> 1), c0 = 8 * (q & 1);
-        double acc[2] = {0.0, 0.0};
-#pragma unroll
-        for (int kk = 0; kk < 16; kk += 4)
-          dmma(acc[0], acc[1], -sX[sw64(16 * i + r0 + lr, 16 * i + kk + lc)], sTmp[k * 256 + (kk + lc) * 16 + c0 + lr]);
-        tv[u][0] = acc[0];
-        tv[u][1] = acc[1];
+      for (int kk = 0; kk < 16; kk += 4) {
+        if (tr == 0 && kk >= 8) continue;  // X_ii lower
+        dmma(o0, o1, neg(sD[sw64(16 * i + 8 * tr + lr, 16 * i + kk + lc)]), W[(kk + lc) * 20 + 8 * tc + lr]);
       }
-    }
-    // X_ik written after all warps read X_ii / sTmp (X_ii is a different block: no hazard)
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      int t = warp + 8 * u;
-      if (t < ntile) {
-        int k = t >> 2, q = t & 3;
-        int r = 16 * i + 8 * (q >> 1) + lr, cc = 16 * k + 8 * (q & 1) + 2 * lc;
-        sX[sw64(r, cc)] = tv[u][0];
-        sX[sw64(r, cc + 1)] = tv[u][1];
-      }
+      const int r = 16 * i + 8 * tr + lr, cc = 16 * k + 8 * tc + 2 * lc;
+      sD[sw64(r, cc)] = o0;  // only X_ii and sScr are read in this phase: in-place write is safe
+      sD[sw64(r, cc + 1)] = o1;
     }
     __syncthreads();
   }
-  for (int i = tid; i < TILE_ELEMS; i += NTHR) sT[i] = sX[i];
-  __syncthreads();
   return true;
 }
 
-// Smem budget (doubles): sT 4096 | stage[2] x (A 2048 + B 2048 + Yc 256) | sY 512 | sY2 512 | misc
+// ------------------------------------------------------------------ MMA helpers
+// acc[4][4][2] += (-A(64xKC chunk)) * B(64xKC chunk)^T for the warp quadrant (R0, C0): acc starts
+// as the original tile, so the result is A_IJ - sum_K G_IK G_JK^T.  DIAG: skip the 8x8 blocks
+// strictly above the diagonal (the upper half is never used; frees the pipe for the other CTAs).
+template <bool DIAG>
+__device__ __forceinline__ void mma_chunk(double (&acc)[4][4][2], const double* sA, const double* sB,
+                                          int R0, int C0, int lane) {
+  if (DIAG && C0 > R0 + 24) return;  // quadrant entirely above the diagonal
+  const int lr = lane >> 2, lc = lane & 3;
+#pragma unroll
+  for (int k0 = 0; k0 < KC; k0 += 4) {
+    double a[4], b[4];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi) a[mi] = neg(sA[sw32(R0 + 8 * mi + lr, k0 + lc)]);
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) b[ni] = sB[sw32(C0 + 8 * ni + lr, k0 + lc)];
+#pragma unroll
+    for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+      for (int ni = 0; ni < 4; ++ni)
+        if (!DIAG || C0 + 8 * ni <= R0 + 8 * mi) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
+  }
+}
+
+// acc := this thread's accumulator-layout fragment of the quadrant of a row-major 64x64 global tile
+__device__ __forceinline__ void load_frag(double (&acc)[4][4][2], const double* T, int R0, int C0, int lane) {
+  const int lr = lane >> 2, lc = lane & 3;
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int ni = 0; ni < 4; ++ni) {
+      double2 v = __ldcg(reinterpret_cast<const double2*>(T + (R0 + 8 * mi + lr) * TILE + C0 + 8 * ni + 2 * lc));
+      acc[mi][ni][0] = v.x;
+      acc[mi][ni][1] = v.y;
+    }
+}
+
+// Smem (doubles): sT 64x64 | stage[2] x (A 64xKC + B 64xKC + Yc KCx8) | sY 64x8 | misc.
+// The stage area doubles as: factor scratch (3 x 16x20), Y_J (64x8), the full S_IJ tile of
+// the TRSM (64x64) and the backward row chunks -- never at the same time.
 constexpr int STAGE_DBL = 2 * 64 * KC + KC * RHSW;
-constexpr int SMEM_DBL = TILE_ELEMS + 2 * STAGE_DBL + 2 * 64 * RHSW + 64;
+constexpr int SMEM_DBL = TILE_ELEMS + 2 * STAGE_DBL + 64 * RHSW + 64;
+static_assert(SMEM_DBL * 8 <= 73 * 1024, "three CTAs per SM");
+static_assert(TILE_ELEMS <= 2 * STAGE_DBL, "S tile fits in the stage area");
+static_assert(16 * TILE + 16 * RHSW <= STAGE_DBL, "backward row chunk fits in a stage");
 
 // ------------------------------------------------------------------ kernel
-__global__ void __launch_bounds__(NTHR, 2)
+__global__ void __launch_bounds__(NTC, 3)
 k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
            const double* __restrict__ Cavg, const double* __restrict__ Pavg,
            double* __restrict__ Ceff, double* __restrict__ Peff, double* __restrict__ PavgOut,
            double* __restrict__ X, int* __restrict__ info) {
   extern __shared__ __align__(128) double smem[];
-  double* sT = smem;                              // 64x64 swizzled: diag work / G_JJ^-1
-  double* sStage = smem + TILE_ELEMS;             // 2 stages (also reused as a 64x64 tile)
-  double* sY = sStage + 2 * STAGE_DBL;            // 64x8 swizzled
-  double* sY2 = sY + 64 * RHSW;                   // 64x8 swizzled
-  double* sMisc = sY2 + 64 * RHSW;                // flags
-  int* sFail = reinterpret_cast<int*>(sMisc);
+  double* sT = smem;                        // 64x64 swizzled: S_JJ -> G_JJ^-1
+  double* sStage = sT + TILE_ELEMS;         // 2 stages | S tile | factor scratch | Y_J
+  double* sY = sStage + 2 * STAGE_DBL;      // 64x8 swizzled: Kfe_J - sum_K G_JK Y_K
+  int* sFail = reinterpret_cast<int*>(sY + 64 * RHSW);
+  double* sY2 = sStage;                     // Y_J (after the factorisation, before the off-diagonal tiles)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int lr = lane >> 2, lc = lane & 3;
-  const int R0 = (warp >> 2) * 32, C0 = (warp & 3) * 16;
+  const int R0 = (warp >> 1) * 32, C0 = (warp & 1) * 32;  // accumulation quadrant
+  const int cLo = warp, cHi = 7 - warp;                    // TRSM column-block pair (balanced)
   const int bl = blockIdx.x, b = b0 + bl;
   const int nt = R.nt, NT = R.NT;
   double* Kb = Kt + (long)bl * (nt * (nt + 1) / 2) * TILE_ELEMS;
@@ -289,80 +334,79 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
 
   // ======================= forward: factor + Y ==============================
   for (int J = 0; J < nt; ++J) {
-    // ---------- diagonal tile: acc = sum_K G_JK G_JK^T, yacc = sum_K G_JK Y_K ----------
-    double acc[4][2][2] = {};
-    double yacc[2] = {0.0, 0.0};
-    const int nk = J * 2;  // (K, kc) chunks
-    if (nk > 0) {
-      stage_chunk(sStage, tile_ptr(Kb, J, 0), 0, tid);
-      stage_rhs(sStage + 2 * 64 * KC, Yb, KC, tid);
-      cp_async_commit();
-    }
-    for (int c = 0; c < nk; ++c) {
-      if (c + 1 < nk) {
-        double* st = sStage + ((c + 1) & 1) * STAGE_DBL;
-        int K = (c + 1) >> 1, kc = (c + 1) & 1;
-        stage_chunk(st, tile_ptr(Kb, J, K), kc, tid);
-        stage_rhs(st + 2 * 64 * KC, Yb + (long)(K * TILE + kc * KC) * RHSW, KC, tid);
+    TMARK(0);
+    const int nk = J * CPT;  // (K, kc) chunks
+    // ---------- S_JJ = A_JJ - sum_K G_JK G_JK^T ; yacc = sum_K G_JK Y_K ----------
+    {
+      double acc[4][4][2];
+      double yacc[2][2] = {};
+      load_frag(acc, tile_ptr(Kb, J, J), R0, C0, lane);
+      if (nk > 0) {
+        stage_chunk(sStage, tile_ptr(Kb, J, 0), 0, tid);
+        stage_rhs(sStage + 2 * 64 * KC, Yb, KC, tid);
         cp_async_commit();
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
       }
-      __syncthreads();
-      const double* st = sStage + (c & 1) * STAGE_DBL;
-      mma_chunk(acc, st, st, R0, C0, lane);
-      {  // yacc (rows 8*warp.., 8 RHS columns) += G_JK chunk * Y_K chunk
-        const double* sYc = st + 2 * 64 * KC;
+      for (int c = 0; c < nk; ++c) {
+        if (c + 1 < nk) {
+          double* st = sStage + ((c + 1) & 1) * STAGE_DBL;
+          const int K = (c + 1) / CPT, kc = (c + 1) % CPT;
+          stage_chunk(st, tile_ptr(Kb, J, K), kc, tid);
+          stage_rhs(st + 2 * 64 * KC, Yb + (long)(K * TILE + kc * KC) * RHSW, KC, tid);
+          cp_async_commit();
+          cp_async_wait<1>();
+        } else {
+          cp_async_wait<0>();
+        }
+        __syncthreads();
+        const double* st = sStage + (c & 1) * STAGE_DBL;
+        mma_chunk<true>(acc, st, st, R0, C0, lane);
+        const double* sYc = st + 2 * 64 * KC;  // yacc rows 16*warp.. (2 blocks) x 8 RHS columns
 #pragma unroll
         for (int k0 = 0; k0 < KC; k0 += 4) {
-          double a = st[sw32(8 * warp + lr, k0 + lc)];
-          double bb = sYc[swy(k0 + lc, lr)];
-          dmma(yacc[0], yacc[1], a, bb);
+          const double bb = sYc[swy(k0 + lc, lr)];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) dmma(yacc[u][0], yacc[u][1], st[sw32(16 * warp + 8 * u + lr, k0 + lc)], bb);
         }
+        __syncthreads();
       }
-      __syncthreads();
-    }
-    // sT = A_JJ - acc ; sY = Kfe_J - yacc
-    {
-      const double* Ajj = tile_ptr(Kb, J, J);
+      // sT = lower(S_JJ), exact zeros above the diagonal
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) {
-          int r = R0 + 8 * mi + lr, cc = C0 + 8 * ni + 2 * lc;
-          double2 a = *reinterpret_cast<const double2*>(Ajj + r * TILE + cc);
-          sT[sw64(r, cc)] = a.x - acc[mi][ni][0];
-          sT[sw64(r, cc + 1)] = a.y - acc[mi][ni][1];
+        for (int ni = 0; ni < 4; ++ni) {
+          const int r = R0 + 8 * mi + lr, cc = C0 + 8 * ni + 2 * lc;
+          sT[sw64(r, cc)] = (cc <= r) ? acc[mi][ni][0] : 0.0;
+          sT[sw64(r, cc + 1)] = (cc + 1 <= r) ? acc[mi][ni][1] : 0.0;
         }
-      int r = 8 * warp + lr, cc = 2 * lc;
-      double2 y = *reinterpret_cast<const double2*>(Yb + (long)(J * TILE + r) * RHSW + cc);
-      sY[swy(r, cc)] = y.x - yacc[0];
-      sY[swy(r, cc + 1)] = y.y - yacc[1];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int r = 16 * warp + 8 * u + lr, cc = 2 * lc;
+        const double2 y = __ldcg(reinterpret_cast<const double2*>(Yb + (long)(J * TILE + r) * RHSW + cc));
+        sY[swy(r, cc)] = y.x - yacc[u][0];
+        sY[swy(r, cc + 1)] = y.y - yacc[u][1];
+      }
     }
     __syncthreads();
-    // ---------- blocked Cholesky + inverse of the 64x64 diagonal tile ----------
+    TMARK(1);
+    // ---------- blocked Cholesky + inverse of the diagonal tile ----------
     if (!factor_invert_diag(sT, sStage, sFail, J, tid)) break;
-    // ---------- Y_J = G_JJ^-1 (Kfe_J - sum) ; S += Y_J^T Y_J ----------
+    TMARK(2);
+    // ---------- Y_J = G_JJ^-1 (Kfe_J - sum) ; S += Y_J^T Y_J ; store G_JJ^-1 ----------
     {
-      double y[2] = {0.0, 0.0};
-      const int r = 8 * warp;
 #pragma unroll
-      for (int k0 = 0; k0 < TILE; k0 += 4) {
-        double a = sT[sw64(r + lr, k0 + lc)];
-        double bb = sY[swy(k0 + lc, lr)];
-        dmma(y[0], y[1], a, bb);
+      for (int u = 0; u < 2; ++u) {
+        const int r = 16 * warp + 8 * u;
+        double y0 = 0.0, y1 = 0.0;
+        for (int k0 = 0; k0 < r + 8; k0 += 4)  // G_JJ^-1 lower
+          dmma(y0, y1, sT[sw64(r + lr, k0 + lc)], sY[swy(k0 + lc, lr)]);
+        const int rr = r + lr, cc = 2 * lc;
+        sY2[swy(rr, cc)] = y0;
+        sY2[swy(rr, cc + 1)] = y1;
+        *reinterpret_cast<double2*>(Yb + (long)(J * TILE + rr) * RHSW + cc) = make_double2(y0, y1);
       }
-      int rr = r + lr, cc = 2 * lc;
-      sY2[swy(rr, cc)] = y[0];
-      sY2[swy(rr, cc + 1)] = y[1];
-      *reinterpret_cast<double2*>(Yb + (long)(J * TILE + rr) * RHSW + cc) = make_double2(y[0], y[1]);
-    }
-    // store G_JJ^-1 as tile (J,J)
-    {
       double* Gjj = Kb + (long)(J * (J + 1) / 2 + J) * TILE_ELEMS;
-      for (int idx = tid; idx < TILE_ELEMS / 2; idx += NTHR) {
-        int r = idx >> 5, cc = 2 * (idx & 31);
+      for (int idx = tid; idx < TILE_ELEMS / 2; idx += NTC) {
+        const int r = idx >> 5, cc = 2 * (idx & 31);
         *reinterpret_cast<double2*>(Gjj + r * TILE + cc) = make_double2(sT[sw64(r, cc)], sT[sw64(r, cc + 1)]);
       }
     }
@@ -370,12 +414,16 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
     if (tid < 64) {
       const int i = tid >> 3, j = tid & 7;
       double s = 0.0;
-      for (int r = 0; r < TILE; ++r) s += sY2[swy(r, i)] * sY2[swy(r, j)];
+      for (int r = 0; r < TILE; ++r) s = fma(sY2[swy(r, i)], sY2[swy(r, j)], s);
       Sacc += s;
     }
-    // ---------- off-diagonal tiles of column J ----------
+    __syncthreads();  // sY2 (stage area) free again
+    TMARK(3);
+    // ---------- off-diagonal tiles of column J: S_IJ, then G_IJ = S_IJ G_JJ^-T ----------
     for (int I = J + 1; I < nt; ++I) {
-      double a2[4][2][2] = {};
+      double acc[4][4][2];
+      const double* Aij = tile_ptr(Kb, I, J);
+      load_frag(acc, Aij, R0, C0, lane);
       if (nk > 0) {
         stage_chunk(sStage, tile_ptr(Kb, I, 0), 0, tid);
         stage_chunk(sStage + 64 * KC, tile_ptr(Kb, J, 0), 0, tid);
@@ -384,7 +432,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
       for (int c = 0; c < nk; ++c) {
         if (c + 1 < nk) {
           double* st = sStage + ((c + 1) & 1) * STAGE_DBL;
-          int K = (c + 1) >> 1, kc = (c + 1) & 1;
+          const int K = (c + 1) / CPT, kc = (c + 1) % CPT;
           stage_chunk(st, tile_ptr(Kb, I, K), kc, tid);
           stage_chunk(st + 64 * KC, tile_ptr(Kb, J, K), kc, tid);
           cp_async_commit();
@@ -394,46 +442,48 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
         }
         __syncthreads();
         const double* st = sStage + (c & 1) * STAGE_DBL;
-        mma_chunk(a2, st, st + 64 * KC, R0, C0, lane);
+        mma_chunk<false>(acc, st, st + 64 * KC, R0, C0, lane);
         __syncthreads();
       }
-      // S = A_IJ - acc into the stage area (64x64 swizzled)
+      // S_IJ into the stage area (full 64x64, sw64)
       double* sS = sStage;
-      const double* Aij = tile_ptr(Kb, I, J);
 #pragma unroll
       for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) {
-          int r = R0 + 8 * mi + lr, cc = C0 + 8 * ni + 2 * lc;
-          double2 a = *reinterpret_cast<const double2*>(Aij + r * TILE + cc);
-          sS[sw64(r, cc)] = a.x - a2[mi][ni][0];
-          sS[sw64(r, cc + 1)] = a.y - a2[mi][ni][1];
+        for (int ni = 0; ni < 4; ++ni) {
+          const int r = R0 + 8 * mi + lr, cc = C0 + 8 * ni + 2 * lc;
+          sS[sw64(r, cc)] = acc[mi][ni][0];
+          sS[sw64(r, cc + 1)] = acc[mi][ni][1];
         }
       __syncthreads();
-      // G_IJ = S * G_JJ^-T
-      double g[4][2][2] = {};
-#pragma unroll 4
-      for (int k0 = 0; k0 < TILE; k0 += 4) {
-        double a[4], bb[2];
+      // G_IJ = S_IJ (G_JJ^-1)^T: warp owns column blocks cLo, cHi (all rows); G_JJ^-1 lower, so
+      // column block c needs k < 8(c+1): 72 k-steps per warp for every warp.
+      double g[8][2][2] = {};
+      int k0 = 0;
+      for (; k0 < 8 * (cLo + 1); k0 += 4) {
+        const double bl0 = sT[sw64(8 * cLo + lr, k0 + lc)], bh0 = sT[sw64(8 * cHi + lr, k0 + lc)];
 #pragma unroll
-        for (int mi = 0; mi < 4; ++mi) a[mi] = sS[sw64(R0 + 8 * mi + lr, k0 + lc)];
+        for (int mi = 0; mi < 8; ++mi) {
+          const double a = sS[sw64(8 * mi + lr, k0 + lc)];
+          dmma(g[mi][0][0], g[mi][0][1], a, bl0);
+          dmma(g[mi][1][0], g[mi][1][1], a, bh0);
+        }
+      }
+      for (; k0 < 8 * (cHi + 1); k0 += 4) {
+        const double bh0 = sT[sw64(8 * cHi + lr, k0 + lc)];
 #pragma unroll
-        for (int ni = 0; ni < 2; ++ni) bb[ni] = sT[sw64(C0 + 8 * ni + lr, k0 + lc)];
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 2; ++ni) dmma(g[mi][ni][0], g[mi][ni][1], a[mi], bb[ni]);
+        for (int mi = 0; mi < 8; ++mi) dmma(g[mi][1][0], g[mi][1][1], sS[sw64(8 * mi + lr, k0 + lc)], bh0);
       }
       double* Gij = Kb + (long)(I * (I + 1) / 2 + J) * TILE_ELEMS;
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 2; ++ni) {
-          int r = R0 + 8 * mi + lr, cc = C0 + 8 * ni + 2 * lc;
-          *reinterpret_cast<double2*>(Gij + r * TILE + cc) = make_double2(g[mi][ni][0], g[mi][ni][1]);
-        }
+      for (int mi = 0; mi < 8; ++mi) {
+        const int r = 8 * mi + lr;
+        *reinterpret_cast<double2*>(Gij + r * TILE + 8 * cLo + 2 * lc) = make_double2(g[mi][0][0], g[mi][0][1]);
+        *reinterpret_cast<double2*>(Gij + r * TILE + 8 * cHi + 2 * lc) = make_double2(g[mi][1][0], g[mi][1][1]);
+      }
       __syncthreads();
     }
+    TMARK(4);
   }
 
   if (sFail[0]) {  // report and poison the outputs of this RVE
@@ -453,11 +503,11 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
     const int m = R.m;
     const double* Ca = Cavg + (long)bl * 64;
     if (tid < m * m) {
-      int i = tid / m, j = tid % m;
+      const int i = tid / m, j = tid % m;
       Ceff[(long)b * m * m + tid] = Ca[i * m + j] - sSum[i * 8 + j] / R.vol;
     }
     if (R.finite && tid < m) {
-      double pa = Pavg[(long)bl * 8 + tid];
+      const double pa = Pavg[(long)bl * 8 + tid];
       if (Peff) Peff[(long)b * m + tid] = pa - sSum[tid * 8 + m] / R.vol;
       if (PavgOut) PavgOut[(long)b * m + tid] = pa;
     }
@@ -465,75 +515,71 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
   }
 
   // ======================= backward: X = G^-T Y ===============================
+  // xacc[j][n] = sum_{I>J} sum_k G_IJ[k][j] X_I[k][n], streamed in 16-row chunks of G_IJ;
+  // warp owns rows j = 16*warp .. +15 (2 blocks).
+  constexpr int RC = 16, RPT = TILE / RC;
   for (int J = nt - 1; J >= 0; --J) {
-    double xacc[2] = {0.0, 0.0};
-    const int ni_cnt = nt - 1 - J;
-    // double-buffered: buffer = [64x64 tile | 64x8 X_I]
-    constexpr int BUF = TILE_ELEMS + 64 * RHSW;
-    double* buf0 = sStage;  // 2*BUF = 9216 <= 2*STAGE_DBL (8704)? see static_assert below
-    if (ni_cnt > 0) {
-      stage_tile(buf0, tile_ptr(Kb, J + 1, J), tid);
-      stage_rhs(buf0 + TILE_ELEMS, Xb + (long)(J + 1) * TILE * RHSW, TILE, tid);
+    double xacc[2][2] = {};
+    const int n = (nt - 1 - J) * RPT;
+    if (n > 0) {
+      stage_rows(sStage, tile_ptr(Kb, J + 1, J), 0, RC, tid);
+      stage_rhs(sStage + RC * TILE, Xb + (long)(J + 1) * TILE * RHSW, RC, tid);
       cp_async_commit();
     }
-    for (int c = 0; c < ni_cnt; ++c) {
-      const int I = J + 1 + c;
-      if (c + 1 < ni_cnt) {
-        double* nb = buf0 + ((c + 1) & 1) * BUF;
-        stage_tile(nb, tile_ptr(Kb, I + 1, J), tid);
-        stage_rhs(nb + TILE_ELEMS, Xb + (long)(I + 1) * TILE * RHSW, TILE, tid);
+    for (int q = 0; q < n; ++q) {
+      if (q + 1 < n) {
+        double* nb = sStage + ((q + 1) & 1) * STAGE_DBL;
+        const int I = J + 1 + (q + 1) / RPT, r0 = ((q + 1) % RPT) * RC;
+        stage_rows(nb, tile_ptr(Kb, I, J), r0, RC, tid);
+        stage_rhs(nb + RC * TILE, Xb + (long)(I * TILE + r0) * RHSW, RC, tid);
         cp_async_commit();
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
       __syncthreads();
-      const double* tl = buf0 + (c & 1) * BUF;
-      const double* xi = tl + TILE_ELEMS;
-      // xacc[j][n] += sum_k G_IJ[k][j] * X_I[k][n],  rows j = 8*warp..
+      const double* tl = sStage + (q & 1) * STAGE_DBL;
+      const double* xi = tl + RC * TILE;
 #pragma unroll
-      for (int k0 = 0; k0 < TILE; k0 += 4) {
-        double a = tl[sw64(k0 + lc, 8 * warp + lr)];
-        double bb = xi[swy(k0 + lc, lr)];
-        dmma(xacc[0], xacc[1], a, bb);
+      for (int k0 = 0; k0 < RC; k0 += 4) {
+        const double bb = xi[swy(k0 + lc, lr)];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          dmma(xacc[u][0], xacc[u][1], tl[sw64(k0 + lc, 16 * warp + 8 * u + lr)], bb);
       }
       __syncthreads();
     }
     // r = Y_J - xacc ; X_J = G_JJ^-T r
-    stage_tile(sT, tile_ptr(Kb, J, J), tid);
+    stage_rows(sT, tile_ptr(Kb, J, J), 0, TILE, tid);
     cp_async_commit();
-    {
-      int r = 8 * warp + lr, cc = 2 * lc;
-      double2 y = *reinterpret_cast<const double2*>(Yb + (long)(J * TILE + r) * RHSW + cc);
-      sY[swy(r, cc)] = y.x - xacc[0];
-      sY[swy(r, cc + 1)] = y.y - xacc[1];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int r = 16 * warp + 8 * u + lr, cc = 2 * lc;
+      const double2 y = __ldcg(reinterpret_cast<const double2*>(Yb + (long)(J * TILE + r) * RHSW + cc));
+      sY[swy(r, cc)] = y.x - xacc[u][0];
+      sY[swy(r, cc + 1)] = y.y - xacc[u][1];
     }
     cp_async_wait<0>();
     __syncthreads();
-    {
-      double x[2] = {0.0, 0.0};
 #pragma unroll
-      for (int k0 = 0; k0 < TILE; k0 += 4) {
-        double a = sT[sw64(k0 + lc, 8 * warp + lr)];  // (G_JJ^-1)^T
-        double bb = sY[swy(k0 + lc, lr)];
-        dmma(x[0], x[1], a, bb);
-      }
-      int rr = 8 * warp + lr, cc = 2 * lc;
-      *reinterpret_cast<double2*>(Xb + (long)(J * TILE + rr) * RHSW + cc) = make_double2(x[0], x[1]);
+    for (int u = 0; u < 2; ++u) {
+      const int r = 16 * warp + 8 * u;
+      double x0 = 0.0, x1 = 0.0;
+      for (int k0 = r; k0 < TILE; k0 += 4)  // (G_JJ^-1)^T upper: row j needs k >= j
+        dmma(x0, x1, sT[sw64(k0 + lc, r + lr)], sY[swy(k0 + lc, lr)]);
+      const int rr = r + lr, cc = 2 * lc;
+      *reinterpret_cast<double2*>(Xb + (long)(J * TILE + rr) * RHSW + cc) = make_double2(x0, x1);
     }
     __syncthreads();
   }
 }
-
-static_assert(2 * (TILE_ELEMS + 64 * RHSW) <= 2 * STAGE_DBL + 2 * 64 * RHSW,
-              "backward double buffer must fit in the stage area + sY/sY2");
 
 void launch_condense(const RveDev& R, int b0, int nb, double* Kt, double* Y, const double* Cavg,
                      const double* Pavg, double* Ceff, double* Peff, double* PavgOut, double* X,
                      int* info, cudaStream_t s) {
   size_t sm = (size_t)SMEM_DBL * sizeof(double);
   cudaFuncSetAttribute(k_condense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_condense<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, Ceff, Peff, PavgOut, X, info);
+  k_condense<<<nb, NTC, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, Ceff, Peff, PavgOut, X, info);
 }
 
 // ------------------------------------------------------------------ small reductions

@@ -10,7 +10,7 @@ namespace hom {
 
 constexpr int TILE = 64;          // K_ff tile edge (rows and columns)
 constexpr int TILE_ELEMS = TILE * TILE;
-constexpr int KC = 32;            // k-chunk staged per pipeline stage
+constexpr int KC = 16;            // k-chunk staged per pipeline stage (condense.cu)
 constexpr int RHSW = 8;           // right-hand-side columns kept per RVE (m <= 6, +1 for r_f)
 constexpr int NTHR = 256;         // threads per CTA of the RVE kernels
 
