@@ -107,6 +107,11 @@ typedef struct {
   int32_t rve_chunk;        /* RVEs condensed per pass; <= 0: automatic (memory budget) */
   int32_t check_info;       /* 1: hom_condense synchronises once to report NOT_SPD / JACOBIAN */
   double mem_budget_gb;     /* K_ff pool budget for automatic chunking; <= 0: 48 GB */
+  int32_t tile_sparse;      /* 0: dense blocked factorisation of every lower 64x64 tile of K_ff
+                               (BASELINE north_star).  1: tile-sparse -- only the tiles of the
+                               symbolic tile-level fill of K_ff's structural pattern are stored
+                               and factored; identical arithmetic on those tiles,
+                               the skipped products are exact zeros. */
 } hom_options;
 
 typedef struct {
@@ -121,6 +126,18 @@ typedef struct {
   double rve_volume;        /* |Omega| */
 } hom_sizes;
 
+/* Work per RVE of the condensation, from the tile structure (hom_get_work).  Tile counts
+ * are per RVE; a "product" is one 64x64x64 tile GEMM. */
+typedef struct {
+  int32_t a_tiles;          /* structurally nonzero lower tiles of K_ff (assembled by K1) */
+  int32_t g_tiles;          /* lower tiles processed / stored for G (all lower tiles if dense) */
+  int32_t diag_tiles;       /* diagonal tiles (factor + inverse each) */
+  int32_t syrk_tiles;       /* diagonal-update products G_JK G_JK^T */
+  int32_t gemm_tiles;       /* off-diagonal update products G_IK G_JK^T */
+  int32_t trsm_tiles;       /* off-diagonal tiles G_IJ = S_IJ G_JJ^-T */
+  double flop_dense;        /* algorithmic dense count n^3/3 + 2 n^2 m + n m^2 (n = n_f) */
+  double flop_executed;     /* DMMA flops k_condense executes for this tile structure */
+} hom_work;
 typedef struct {
   int32_t iterations;
   double rel_residual;      /* ||r|| / ||b|| at exit */
@@ -144,6 +161,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* macro, const hom_rve_mesh* rv
               const hom_options* options, void* stream);
 
 int hom_get_sizes(const hom_ctx* ctx, hom_sizes* out);
+int hom_get_work(const hom_ctx* ctx, hom_work* out);
 
 /* Macro kinematics at every macro qp: d_u [n_macro_dof] -> d_kin [B][m]:
  * Voigt strain eps = B u (small strain) or F = I + grad u (finite strain). */

@@ -43,8 +43,17 @@ __device__ __forceinline__ int sw64(int r, int c) { return r * TILE + (c ^ ((r &
 // [rows][8] right-hand-side block
 __device__ __forceinline__ int swy(int k, int n) { return k * RHSW + (n ^ (((k >> 1) & 1) << 2)); }
 
-__device__ __forceinline__ const double* tile_ptr(const double* Kb, int I, int J) {
-  return Kb + (long)(I * (I + 1) / 2 + J) * TILE_ELEMS;
+// lower tile (I,J) of this RVE's pool (slot map RveDev::tslot; every lower tile in the dense path)
+__device__ __forceinline__ double* tile_ptr(double* Kb, const RveDev& R, int I, int J) {
+  return Kb + (long)__ldg(R.tslot + I * R.nt + J) * TILE_ELEMS;
+}
+// G(I,K) and G(J,K) both structurally nonzero (always true in the dense path)
+__device__ __forceinline__ bool pair_nz(const RveDev& R, int I, int J, int K) {
+  return __ldg(R.g_nz + I * R.nt + K) && __ldg(R.g_nz + J * R.nt + K);
+}
+__device__ __forceinline__ int next_pair(const RveDev& R, int I, int J, int K) {
+  while (K < J && !pair_nz(R, I, J, K)) ++K;
+  return K;
 }
 
 // ------------------------------------------------------------------ CTA shape
@@ -325,7 +334,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
   const int cLo = warp, cHi = 7 - warp;                    // TRSM column-block pair (balanced)
   const int bl = blockIdx.x, b = b0 + bl;
   const int nt = R.nt, NT = R.NT;
-  double* Kb = Kt + (long)bl * (nt * (nt + 1) / 2) * TILE_ELEMS;
+  double* Kb = Kt + (long)bl * R.nslot * TILE_ELEMS;
   double* Yb = Y + (long)bl * NT * RHSW;
   double* Xb = X + (long)b * NT * RHSW;
 
@@ -335,30 +344,32 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
   // ======================= forward: factor + Y ==============================
   for (int J = 0; J < nt; ++J) {
     TMARK(0);
-    const int nk = J * CPT;  // (K, kc) chunks
     // ---------- S_JJ = A_JJ - sum_K G_JK G_JK^T ; yacc = sum_K G_JK Y_K ----------
+    // k-chunks (K, kc) run over the K < J with G_JK != 0, two-stage cp.async pipeline
     {
       double acc[4][4][2];
       double yacc[2][2] = {};
-      load_frag(acc, tile_ptr(Kb, J, J), R0, C0, lane);
-      if (nk > 0) {
-        stage_chunk(sStage, tile_ptr(Kb, J, 0), 0, tid);
-        stage_rhs(sStage + 2 * 64 * KC, Yb, KC, tid);
+      load_frag(acc, tile_ptr(Kb, R, J, J), R0, C0, lane);
+      int K = next_pair(R, J, J, 0), kc = 0, par = 0;
+      if (K < J) {
+        stage_chunk(sStage, tile_ptr(Kb, R, J, K), 0, tid);
+        stage_rhs(sStage + 2 * 64 * KC, Yb + (long)(K * TILE) * RHSW, KC, tid);
         cp_async_commit();
       }
-      for (int c = 0; c < nk; ++c) {
-        if (c + 1 < nk) {
-          double* st = sStage + ((c + 1) & 1) * STAGE_DBL;
-          const int K = (c + 1) / CPT, kc = (c + 1) % CPT;
-          stage_chunk(st, tile_ptr(Kb, J, K), kc, tid);
-          stage_rhs(st + 2 * 64 * KC, Yb + (long)(K * TILE + kc * KC) * RHSW, KC, tid);
+      while (K < J) {
+        int K2 = K, kc2 = kc + 1;
+        if (kc2 == CPT) { kc2 = 0; K2 = next_pair(R, J, J, K + 1); }
+        if (K2 < J) {
+          double* st = sStage + (par ^ 1) * STAGE_DBL;
+          stage_chunk(st, tile_ptr(Kb, R, J, K2), kc2, tid);
+          stage_rhs(st + 2 * 64 * KC, Yb + (long)(K2 * TILE + kc2 * KC) * RHSW, KC, tid);
           cp_async_commit();
           cp_async_wait<1>();
         } else {
           cp_async_wait<0>();
         }
         __syncthreads();
-        const double* st = sStage + (c & 1) * STAGE_DBL;
+        const double* st = sStage + par * STAGE_DBL;
         mma_chunk<true>(acc, st, st, R0, C0, lane);
         const double* sYc = st + 2 * 64 * KC;  // yacc rows 16*warp.. (2 blocks) x 8 RHS columns
 #pragma unroll
@@ -368,6 +379,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
           for (int u = 0; u < 2; ++u) dmma(yacc[u][0], yacc[u][1], st[sw32(16 * warp + 8 * u + lr, k0 + lc)], bb);
         }
         __syncthreads();
+        K = K2; kc = kc2; par ^= 1;
       }
       // sT = lower(S_JJ), exact zeros above the diagonal
 #pragma unroll
@@ -404,7 +416,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
         sY2[swy(rr, cc + 1)] = y1;
         *reinterpret_cast<double2*>(Yb + (long)(J * TILE + rr) * RHSW + cc) = make_double2(y0, y1);
       }
-      double* Gjj = Kb + (long)(J * (J + 1) / 2 + J) * TILE_ELEMS;
+      double* Gjj = tile_ptr(Kb, R, J, J);
       for (int idx = tid; idx < TILE_ELEMS / 2; idx += NTC) {
         const int r = idx >> 5, cc = 2 * (idx & 31);
         *reinterpret_cast<double2*>(Gjj + r * TILE + cc) = make_double2(sT[sw64(r, cc)], sT[sw64(r, cc + 1)]);
@@ -421,29 +433,40 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
     TMARK(3);
     // ---------- off-diagonal tiles of column J: S_IJ, then G_IJ = S_IJ G_JJ^-T ----------
     for (int I = J + 1; I < nt; ++I) {
+      if (!__ldg(R.g_nz + I * nt + J)) continue;  // structurally zero tile of G (tile-sparse path)
       double acc[4][4][2];
-      const double* Aij = tile_ptr(Kb, I, J);
-      load_frag(acc, Aij, R0, C0, lane);
-      if (nk > 0) {
-        stage_chunk(sStage, tile_ptr(Kb, I, 0), 0, tid);
-        stage_chunk(sStage + 64 * KC, tile_ptr(Kb, J, 0), 0, tid);
+      double* Aij = tile_ptr(Kb, R, I, J);
+      if (__ldg(R.tile_nz + I * nt + J)) {
+        load_frag(acc, Aij, R0, C0, lane);
+      } else {  // fill tile: A_IJ = 0 (never written by K1)
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+      }
+      int K = next_pair(R, I, J, 0), kc = 0, par = 0;
+      if (K < J) {
+        stage_chunk(sStage, tile_ptr(Kb, R, I, K), 0, tid);
+        stage_chunk(sStage + 64 * KC, tile_ptr(Kb, R, J, K), 0, tid);
         cp_async_commit();
       }
-      for (int c = 0; c < nk; ++c) {
-        if (c + 1 < nk) {
-          double* st = sStage + ((c + 1) & 1) * STAGE_DBL;
-          const int K = (c + 1) / CPT, kc = (c + 1) % CPT;
-          stage_chunk(st, tile_ptr(Kb, I, K), kc, tid);
-          stage_chunk(st + 64 * KC, tile_ptr(Kb, J, K), kc, tid);
+      while (K < J) {
+        int K2 = K, kc2 = kc + 1;
+        if (kc2 == CPT) { kc2 = 0; K2 = next_pair(R, I, J, K + 1); }
+        if (K2 < J) {
+          double* st = sStage + (par ^ 1) * STAGE_DBL;
+          stage_chunk(st, tile_ptr(Kb, R, I, K2), kc2, tid);
+          stage_chunk(st + 64 * KC, tile_ptr(Kb, R, J, K2), kc2, tid);
           cp_async_commit();
           cp_async_wait<1>();
         } else {
           cp_async_wait<0>();
         }
         __syncthreads();
-        const double* st = sStage + (c & 1) * STAGE_DBL;
+        const double* st = sStage + par * STAGE_DBL;
         mma_chunk<false>(acc, st, st + 64 * KC, R0, C0, lane);
         __syncthreads();
+        K = K2; kc = kc2; par ^= 1;
       }
       // S_IJ into the stage area (full 64x64, sw64)
       double* sS = sStage;
@@ -474,7 +497,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
 #pragma unroll
         for (int mi = 0; mi < 8; ++mi) dmma(g[mi][1][0], g[mi][1][1], sS[sw64(8 * mi + lr, k0 + lc)], bh0);
       }
-      double* Gij = Kb + (long)(I * (I + 1) / 2 + J) * TILE_ELEMS;
+      double* Gij = Aij;
 #pragma unroll
       for (int mi = 0; mi < 8; ++mi) {
         const int r = 8 * mi + lr;
@@ -518,27 +541,32 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
   // xacc[j][n] = sum_{I>J} sum_k G_IJ[k][j] X_I[k][n], streamed in 16-row chunks of G_IJ;
   // warp owns rows j = 16*warp .. +15 (2 blocks).
   constexpr int RC = 16, RPT = TILE / RC;
+  auto next_row = [&](int J, int I) {  // next I with G_IJ structurally nonzero
+    while (I < nt && !__ldg(R.g_nz + I * nt + J)) ++I;
+    return I;
+  };
   for (int J = nt - 1; J >= 0; --J) {
     double xacc[2][2] = {};
-    const int n = (nt - 1 - J) * RPT;
-    if (n > 0) {
-      stage_rows(sStage, tile_ptr(Kb, J + 1, J), 0, RC, tid);
-      stage_rhs(sStage + RC * TILE, Xb + (long)(J + 1) * TILE * RHSW, RC, tid);
+    int I = next_row(J, J + 1), rq = 0, par = 0;
+    if (I < nt) {
+      stage_rows(sStage, tile_ptr(Kb, R, I, J), 0, RC, tid);
+      stage_rhs(sStage + RC * TILE, Xb + (long)I * TILE * RHSW, RC, tid);
       cp_async_commit();
     }
-    for (int q = 0; q < n; ++q) {
-      if (q + 1 < n) {
-        double* nb = sStage + ((q + 1) & 1) * STAGE_DBL;
-        const int I = J + 1 + (q + 1) / RPT, r0 = ((q + 1) % RPT) * RC;
-        stage_rows(nb, tile_ptr(Kb, I, J), r0, RC, tid);
-        stage_rhs(nb + RC * TILE, Xb + (long)(I * TILE + r0) * RHSW, RC, tid);
+    while (I < nt) {
+      int I2 = I, rq2 = rq + 1;
+      if (rq2 == RPT) { rq2 = 0; I2 = next_row(J, I + 1); }
+      if (I2 < nt) {
+        double* nb = sStage + (par ^ 1) * STAGE_DBL;
+        stage_rows(nb, tile_ptr(Kb, R, I2, J), rq2 * RC, RC, tid);
+        stage_rhs(nb + RC * TILE, Xb + (long)(I2 * TILE + rq2 * RC) * RHSW, RC, tid);
         cp_async_commit();
         cp_async_wait<1>();
       } else {
         cp_async_wait<0>();
       }
       __syncthreads();
-      const double* tl = sStage + (q & 1) * STAGE_DBL;
+      const double* tl = sStage + par * STAGE_DBL;
       const double* xi = tl + RC * TILE;
 #pragma unroll
       for (int k0 = 0; k0 < RC; k0 += 4) {
@@ -548,9 +576,10 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
           dmma(xacc[u][0], xacc[u][1], tl[sw64(k0 + lc, 16 * warp + 8 * u + lr)], bb);
       }
       __syncthreads();
+      I = I2; rq = rq2; par ^= 1;
     }
     // r = Y_J - xacc ; X_J = G_JJ^-T r
-    stage_rows(sT, tile_ptr(Kb, J, J), 0, TILE, tid);
+    stage_rows(sT, tile_ptr(Kb, R, J, J), 0, TILE, tid);
     cp_async_commit();
 #pragma unroll
     for (int u = 0; u < 2; ++u) {

@@ -36,6 +36,7 @@ struct hom_ctx {
   CgState* cgst = nullptr;
   size_t phase_bytes = 0, mat_bytes = 0;
   int max_slice_nnz = 0;  // largest CSR slice of a 8-CTA cluster partition (CG smem sizing)
+  hom_work work{};
   // event profiling (hom_profile_enable / hom_profile_read)
   struct ProfRec {
     int cls;
@@ -446,6 +447,44 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
         }
     }
   }
+  // tiles the factorisation processes: all lower tiles (dense) or the symbolic tile-level
+  // fill of tile_nz, G(I,J) != 0 iff A(I,J) != 0 or G(I,K) G(J,K) != 0 for some K < J (tile-sparse)
+  std::vector<uint8_t> g_nz((size_t)nt_ * nt_, 0);
+  for (int I = 0; I < nt_; ++I)
+    for (int J = 0; J <= I; ++J) {
+      uint8_t v = c->opt.tile_sparse ? tile_nz[(size_t)I * nt_ + J] : 1;
+      for (int K = 0; K < J && !v; ++K) v = g_nz[(size_t)I * nt_ + K] && g_nz[(size_t)J * nt_ + K];
+      g_nz[(size_t)I * nt_ + J] = v;
+    }
+  std::vector<int> tslot((size_t)nt_ * nt_, -1);
+  int nslot = 0;
+  for (int I = 0; I < nt_; ++I)
+    for (int J = 0; J <= I; ++J)
+      if (g_nz[(size_t)I * nt_ + J]) tslot[(size_t)I * nt_ + J] = nslot++;
+  R.nslot = nslot;
+  {  // work per RVE in 64^3 tile products (hom_get_work)
+    auto& W = c->work;
+    W = hom_work{};
+    for (int J = 0; J < nt_; ++J) {
+      for (int K = 0; K < J; ++K) W.syrk_tiles += g_nz[(size_t)J * nt_ + K];
+      for (int I = J + 1; I < nt_; ++I) {
+        if (!g_nz[(size_t)I * nt_ + J]) continue;
+        W.trsm_tiles += 1;
+        for (int K = 0; K < J; ++K) W.gemm_tiles += g_nz[(size_t)I * nt_ + K] && g_nz[(size_t)J * nt_ + K];
+      }
+    }
+    for (size_t t = 0; t < tile_nz.size(); ++t) W.a_tiles += tile_nz[t];
+    W.g_tiles = nslot;
+    W.diag_tiles = nt_;
+    const double n = dim * R.n_indep - dim, mm = c->m + (c->finite ? 1 : 0);
+    W.flop_dense = n * n * n / 3.0 + 2.0 * n * n * mm + n * mm * mm;
+    // executed DMMA flops of k_condense (64^3 units: product 2*64^3; the diagonal SYRK skips
+    // the strictly-upper 8x8 blocks, 36/64; TRSM with the triangular G_JJ^-1, 36/64; the
+    // right-hand sides are 8 wide; diagonal factor + inverse ~420 m8n8k4 ops per tile)
+    const double T3 = 2.0 * 64 * 64 * 64, rhs = 2.0 * 64 * 64 * 8;
+    W.flop_executed = W.gemm_tiles * T3 + W.syrk_tiles * (T3 * 36.0 / 64.0 + rhs) +
+                      W.trsm_tiles * (T3 * 36.0 / 64.0 + rhs) + nt_ * (420.0 * 512 + 2 * rhs);
+  }
   R.phase_per_rve = ph->per_rve ? 1 : 0;
   R.mat_per_rve = mat->per_rve ? 1 : 0;
   R.n_phase = mat->n_phases;
@@ -456,7 +495,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   std::vector<double> params(mat->params, mat->params + (size_t)(R.mat_per_rve ? c->B : 1) * R.n_phase * 2);
 
   // ------------------------------------------------------------ chunking + allocation
-  const size_t tiles = (size_t)R.nt * (R.nt + 1) / 2;
+  const size_t tiles = (size_t)R.nslot;
   const size_t per_rve = tiles * hom::TILE_ELEMS * 8 + (size_t)R.NT * hom::RHSW * 8 + 64 * 8 * 2 +
                          (c->finite ? (size_t)R.ne * nq * 20 * 8 : 0);
   int chunk = c->opt.rve_chunk > 0 ? c->opt.rve_chunk
@@ -480,6 +519,8 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   R.Fmu = upload(c, Fmu, s, &rc);
   R.evol = upload(c, evol, s, &rc);
   R.tile_nz = upload(c, tile_nz, s, &rc);
+  R.g_nz = upload(c, g_nz, s, &rc);
+  R.tslot = upload(c, tslot, s, &rc);
   R.phase = upload(c, phase, s, &rc);
   R.mat = upload(c, params, s, &rc);
   c->phase_bytes = phase.size();
@@ -527,6 +568,12 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   cudaMemsetAsync(c->rfn, 0, sizeof(double) * c->B, s);
   rc = check_cuda(c, cudaStreamSynchronize(s), "hom_setup");
   return rc;
+}
+
+int hom_get_work(const hom_ctx* c, hom_work* o) {
+  if (!c || !o) return HOM_ERR_INVALID_ARG;
+  *o = c->work;
+  return HOM_OK;
 }
 
 int hom_get_sizes(const hom_ctx* c, hom_sizes* o) {

@@ -43,6 +43,12 @@ struct RveDev {
   const double* Fmu;
   const double* evol;             // [ne] element volume
   const uint8_t* tile_nz;         // [nt*nt] 1 if lower tile (I,J) of K_ff has a structural nonzero
+  // Tile structure of the factor: g_nz[I*nt+J] = 1 if lower tile (I,J) of G is
+  // processed -- every lower tile (dense path) or the symbolic tile fill of tile_nz
+  // (tile-sparse path); tslot[I*nt+J] = its slot in the per-RVE pool (-1: not stored).
+  const uint8_t* g_nz;
+  const int* tslot;
+  int nslot;                      // pool slots (64x64 tiles) per RVE
 };
 
 struct MacroDev {

@@ -5,13 +5,14 @@
 // K_fe = sum eta~ B_f^T C (un-normalised, R2); the periodic
 // constraint (eq:Con (iii); nodal coupling P:604-612) is applied on the
 // fly through the element -> independent-node map, and the corner class is an
-// identity pad.  Output is the dense lower K_ff in 64x64 tiles, tile (I,J),
-// I >= J, at index I(I+1)/2 + J, each tile row-major; K_fe (and r_f) go to the
-// right-hand-side block Y [NT][8].
+// identity pad.  Output is K_ff in 64x64 tiles: the structurally nonzero lower
+// tiles (I,J) (RveDev::tile_nz), each row-major at its pool slot RveDev::tslot;
+// structurally zero tiles are never written (k_condense starts their
+// accumulators at zero).  K_fe (and r_f) go to the right-hand-side block Y [NT][8].
 //
 // One CTA per RVE: the tile is zero-filled and scattered in shared memory, then
-// streamed to HBM with coalesced 16-byte stores -- the kernel is HBM-write bound
-// (K1).
+// streamed to HBM with TMA bulk stores (double-buffered) -- the kernel is
+// HBM-write bound (K1).
 #include "hom_internal.cuh"
 
 namespace hom {
@@ -113,7 +114,6 @@ __device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
-constexpr int ZBUF = 1024;  // doubles of the zero buffer (8 KB): 4 bulk stores per zero tile
 
 template <int DIM, bool ISO>
 __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double* __restrict__ Kt,
@@ -123,8 +123,7 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
                                                        const double* __restrict__ Pq) {
   extern __shared__ __align__(128) double smem[];
   double* tbuf = smem;                       // 2 x [64*64]
-  double* zbuf = smem + 2 * TILE_ELEMS;      // [ZBUF] zeros
-  double* red = zbuf + ZBUF;                 // [NTHR] reduction scratch
+  double* red = smem + 2 * TILE_ELEMS;       // [NTHR] reduction scratch
   double* s_lam = red + NTHR;                // [ne] (ISO)
   double* s_mu = s_lam + R.ne;               // [ne] (ISO)
   const int tid = threadIdx.x;
@@ -134,7 +133,6 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   constexpr int ND = ISO ? (DIM == 2 ? 8 : 24) : 8;  // nen*dim
   const long tq0 = (long)bl * ne * nq;  // offset of this RVE in Aq/Pq (chunk-local)
 
-  for (int i = tid; i < ZBUF; i += NTHR) zbuf[i] = 0.0;
   if (ISO) {
     const uint8_t* ph = R.phase + (R.phase_per_rve ? (long)b * ne : 0);
     const double* mt = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * 2 : 0);
@@ -261,8 +259,7 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
 
   // ---- K_ff tiles ----
   const int nt = R.nt;
-  double* Kb = Kt + (long)bl * (nt * (nt + 1) / 2) * TILE_ELEMS;
-  if (tid == 0) fence_proxy_async();  // zbuf visible to the async proxy
+  double* Kb = Kt + (long)bl * R.nslot * TILE_ELEMS;
   int nzt = 0;                        // nonzero tiles built so far (buffer parity)
   for (int I = 0; I < nt; ++I) {
     const int r0 = I * TILE;
@@ -270,15 +267,10 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
     const int k_lo = p_lo < R.n_indep ? R.nbr_ptr[p_lo] : 0;
     const int k_hi = p_lo < R.n_indep ? R.nbr_ptr[p_hi + 1] : 0;
     for (int J = 0; J <= I; ++J) {
-      double* gt = Kb + (long)(I * (I + 1) / 2 + J) * TILE_ELEMS;
-      if (!R.tile_nz[I * nt + J]) {
-        if (tid == 0) {
-#pragma unroll
-          for (int z = 0; z < TILE_ELEMS / ZBUF; ++z) bulk_store(gt + z * ZBUF, zbuf, ZBUF * 8);
-          bulk_commit();
-        }
-        continue;
-      }
+      // structurally zero tiles are not written: k_condense never reads them (it starts their
+      // accumulators at zero), so K1's HBM traffic is the nonzero tiles only
+      if (!R.tile_nz[I * nt + J]) continue;
+      double* gt = Kb + (long)R.tslot[I * nt + J] * TILE_ELEMS;
       double* tile = tbuf + (nzt & 1) * TILE_ELEMS;
       ++nzt;
       if (tid == 0) bulk_wait_read1();  // the buffer's previous bulk store has finished reading
@@ -360,7 +352,7 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
 void launch_rve_assemble(const RveDev& R, int b0, int nb, double* Kt, double* Y, double* Cavg,
                          double* Pavg, double* rfn, const double* Aq, const double* Pq,
                          cudaStream_t s) {
-  size_t sm = (size_t)(2 * TILE_ELEMS + ZBUF + NTHR + 2 * R.ne) * sizeof(double);
+  size_t sm = (size_t)(2 * TILE_ELEMS + NTHR + 2 * R.ne) * sizeof(double);
   if (R.finite) {
     auto k = k_rve_assemble<2, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

@@ -23,7 +23,7 @@ STATUS = {0: "HOM_OK", 1: "HOM_ERR_INVALID_ARG", 2: "HOM_ERR_MESH", 3: "HOM_ERR_
           7: "HOM_ERR_CUDA", 8: "HOM_ERR_OOM"}
 
 # every symbol include/hom.h declares (checked by tests/test_abi.py)
-EXPORTS = ["hom_setup", "hom_get_sizes", "hom_macro_kinematics", "hom_condense", "hom_macro_solve",
+EXPORTS = ["hom_setup", "hom_get_sizes", "hom_get_work", "hom_macro_kinematics", "hom_condense", "hom_macro_solve",
            "hom_macro_residual_norm", "hom_recover_fluctuations", "hom_newton_update", "hom_set_fluctuations",
            "hom_get_fluctuations", "hom_micro_residual_max", "hom_set_phases", "hom_launch_count",
            "hom_profile_enable", "hom_profile_read", "hom_last_error", "hom_destroy"]
@@ -53,13 +53,20 @@ class Materials(ctypes.Structure):
 
 class Options(ctypes.Structure):
     _fields_ = [("finite_strain", ctypes.c_int32), ("cg_rtol", ctypes.c_double), ("cg_max_iter", ctypes.c_int32),
-                ("rve_chunk", ctypes.c_int32), ("check_info", ctypes.c_int32), ("mem_budget_gb", ctypes.c_double)]
+                ("rve_chunk", ctypes.c_int32), ("check_info", ctypes.c_int32), ("mem_budget_gb", ctypes.c_double),
+                ("tile_sparse", ctypes.c_int32)]
 
 
 class Sizes(ctypes.Structure):
     _fields_ = [("n_rve", ctypes.c_int32), ("m", ctypes.c_int32), ("n_pad", ctypes.c_int32),
                 ("n_tiles", ctypes.c_int32), ("n_macro_dof", ctypes.c_int32), ("n_macro_free", ctypes.c_int32),
                 ("macro_nnz", ctypes.c_int32), ("rve_chunk", ctypes.c_int32), ("rve_volume", ctypes.c_double)]
+
+
+class Work(ctypes.Structure):
+    _fields_ = [("a_tiles", ctypes.c_int32), ("g_tiles", ctypes.c_int32), ("diag_tiles", ctypes.c_int32),
+                ("syrk_tiles", ctypes.c_int32), ("gemm_tiles", ctypes.c_int32), ("trsm_tiles", ctypes.c_int32),
+                ("flop_dense", ctypes.c_double), ("flop_executed", ctypes.c_double)]
 
 
 class SolveInfo(ctypes.Structure):
@@ -98,6 +105,7 @@ def lib(build_if_missing: bool = True):
         L.hom_setup.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.POINTER(MacroMesh), ctypes.POINTER(RveMesh),
                                 ctypes.POINTER(PhaseField), ctypes.POINTER(Materials), ctypes.POINTER(Options), P]
         L.hom_get_sizes.argtypes = [P, ctypes.POINTER(Sizes)]
+        L.hom_get_work.argtypes = [P, ctypes.POINTER(Work)]
         L.hom_macro_kinematics.argtypes = [P, P, P, P]
         L.hom_condense.argtypes = [P, P, P, P, P, P]
         L.hom_macro_solve.argtypes = [P, P, P, D, P, ctypes.POINTER(SolveInfo), P]
@@ -134,7 +142,7 @@ class Homogenizer:
 
     def __init__(self, macro_coords, macro_conn, dirichlet_dof, dirichlet_value, body_force,
                  rve_coords, rve_conn, phase, materials, kind="linear", cg_rtol=1e-13, cg_max_iter=20000,
-                 rve_chunk=0, check_info=True, mem_budget_gb=0.0):
+                 rve_chunk=0, check_info=True, mem_budget_gb=0.0, tile_sparse=False):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("Homogenizer needs a CUDA device (no CPU fallback)")
@@ -167,7 +175,8 @@ class Homogenizer:
         self.rve = RveMesh(dim, rc_.shape[0], rconn.shape[0], rconn.shape[1], _np_ptr(rc_), _np_ptr(rconn))
         self.phase = PhaseField(per_rve_phase, _np_ptr(ph))
         self.mat = Materials(1 if kind == "nh" else 0, n_phase, per_rve_mat, _np_ptr(mt))
-        self.opt = Options(1 if kind == "nh" else 0, cg_rtol, cg_max_iter, rve_chunk, int(check_info), mem_budget_gb)
+        self.opt = Options(1 if kind == "nh" else 0, cg_rtol, cg_max_iter, rve_chunk, int(check_info), mem_budget_gb,
+                           int(tile_sparse))
         self.finite = kind == "nh"
         h = ctypes.c_void_p()
         rc = L.hom_setup(ctypes.byref(h), ctypes.byref(self.macro), ctypes.byref(self.rve),
@@ -181,6 +190,9 @@ class Homogenizer:
         s = Sizes()
         L.hom_get_sizes(h, ctypes.byref(s))
         self.sizes = s
+        w = Work()
+        L.hom_get_work(h, ctypes.byref(w))
+        self.work = w
         self.n_rve, self.m, self.n_pad = s.n_rve, s.m, s.n_pad
         self.n_dof = s.n_macro_dof
         self.dim = dim
