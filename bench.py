@@ -351,7 +351,8 @@ def main():
         "macro_solve_ms": (prof["macro_assemble"][0] + prof["cg"][0]) / args.steps,
         "cg_iterations": statistics.median(cg_iters) if cg_iters else None,
         "assembly": {"kernel": "k_rve_assemble (K1)", "ms_per_launch": asm_ms,
-                     "GBps": asm_bytes_rve * per_launch / (asm_ms * 1e-3) / 1e9 if asm_ms > 0 else None,
+                     "GBps": asm_bytes_rve * B * args.steps / (prof["rve_assemble"][0] * 1e-3) / 1e9
+                     if prof["rve_assemble"][0] > 0 else None,
                      "bytes": f"{asm_bytes_rve} B/RVE: {work.a_tiles} structurally nonzero 64x64 K_ff tiles + K_fe + <C>"},
         "breakdown": breakdown,
         "gpu_launches": launches,

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <map>
+#include <string>
 #include <vector>
 
 #include "hom_internal.cuh"
@@ -513,8 +514,39 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   R.nbr_owner = upload(c, RP.owner, s, &rc);
   R.sh_ptr = upload(c, RP.sh_ptr, s, &rc);
   R.sh = upload(c, RP.sh, s, &rc);
-  R.Klam = upload(c, Klam, s, &rc);
-  R.Kmu = upload(c, Kmu, s, &rc);
+  {  // element types: (Klam, Kmu) geometry blocks equal to 1e-13 relative share one table (a uniform
+     // grid has one; the representative differs from the others only by coordinate rounding)
+    std::vector<int> etype(R.ne, 0);
+    std::vector<double> KlamT, KmuT;
+    if (!c->finite) {
+      const size_t blk = (size_t)ND * ND;
+      for (int e = 0; e < R.ne; ++e) {
+        double scale = 0.0;
+        for (size_t i = 0; i < blk; ++i) scale = std::max(scale, std::fabs(Kmu[e * blk + i]));
+        const double tol = 1e-13 * scale;
+        int found = -1;
+        for (int t = 0; t < (int)(KlamT.size() / blk) && found < 0; ++t) {
+          bool same = true;
+          for (size_t i = 0; i < blk && same; ++i)
+            same = std::fabs(Klam[e * blk + i] - KlamT[t * blk + i]) <= tol &&
+                   std::fabs(Kmu[e * blk + i] - KmuT[t * blk + i]) <= tol;
+          if (same) found = t;
+        }
+        if (found < 0) {
+          found = (int)(KlamT.size() / blk);
+          KlamT.insert(KlamT.end(), Klam.begin() + e * blk, Klam.begin() + (e + 1) * blk);
+          KmuT.insert(KmuT.end(), Kmu.begin() + e * blk, Kmu.begin() + (e + 1) * blk);
+        }
+        etype[e] = found;
+      }
+    }
+    R.ntype = c->finite ? 0 : (int)(KlamT.size() / ((size_t)ND * ND));
+    if ((size_t)R.ntype * ND * ND * 2 * sizeof(double) > 96 * 1024)
+      return fail(HOM_ERR_INVALID_ARG, "too many distinct RVE element geometries for the K1 shared-memory tables");
+    R.etype = upload(c, etype, s, &rc);
+    R.Klam = upload(c, KlamT, s, &rc);
+    R.Kmu = upload(c, KmuT, s, &rc);
+  }
   R.Flam = upload(c, Flam, s, &rc);
   R.Fmu = upload(c, Fmu, s, &rc);
   R.evol = upload(c, evol, s, &rc);

@@ -37,8 +37,10 @@ struct RveDev {
   int mat_per_rve, n_phase;
   // geometry-only element matrices of the isotropic closed form (small strain):
   // K_e = lam_e * Klam_e + mu_e * Kmu_e, K_fe rows = lam_e * Flam_e + mu_e * Fmu_e
-  const double* Klam;             // [ne][nen*dim][nen*dim]
+  const double* Klam;             // [ntype][nen*dim][nen*dim] (element type = identical geometry)
   const double* Kmu;
+  const int* etype;               // [ne] element -> type
+  int ntype;
   const double* Flam;             // [ne][nen*dim][m]
   const double* Fmu;
   const double* evol;             // [ne] element volume

@@ -10,9 +10,9 @@
 // structurally zero tiles are never written (k_condense starts their
 // accumulators at zero).  K_fe (and r_f) go to the right-hand-side block Y [NT][8].
 //
-// One CTA per RVE: the tile is zero-filled and scattered in shared memory, then
-// streamed to HBM with TMA bulk stores (double-buffered) -- the kernel is
-// HBM-write bound (K1).
+// One CTA per RVE; each warp gathers one node row-block of a tile at a time
+// and streams it out with coalesced 16-byte stores -- the kernel is HBM-write
+// bound (K1).
 #include "hom_internal.cuh"
 
 namespace hom {
@@ -99,20 +99,9 @@ void launch_rve_material_nh(const RveDev& R, int b0, int nb, const double* F, co
 // + mu g_a^j g_b^i + mu d_ij g_a.g_b integrated at setup).  Finite strain: the
 // tangent is read per qp from Aq (full-gradient form).
 //
-// Tiles: structurally-zero tiles (per-mesh bitmap) are written from a zero
-// buffer with TMA bulk stores; nonzero tiles are zero-filled + scattered in one
-// of two shared-memory buffers and streamed out with cp.async.bulk while the
-// next tile is being built (double buffering).
+// Tiles: only the structurally nonzero tiles (per-mesh bitmap) are written,
+// row by row with coalesced 16-byte stores (see the tile writer below).
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void bulk_store(void* gdst, const void* ssrc, unsigned bytes) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(ssrc);
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(gdst), "r"(s), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 
 template <int DIM, bool ISO>
@@ -122,10 +111,13 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
                                                        const double* __restrict__ Aq,
                                                        const double* __restrict__ Pq) {
   extern __shared__ __align__(128) double smem[];
-  double* tbuf = smem;                       // 2 x [64*64]
-  double* red = smem + 2 * TILE_ELEMS;       // [NTHR] reduction scratch
+  double* s_row = smem;                      // [8 warps][DIM][64] tile-row buffers
+  double* red = s_row + (NTHR / 32) * DIM * TILE;  // [NTHR] reduction scratch
   double* s_lam = red + NTHR;                // [ne] (ISO)
   double* s_mu = s_lam + R.ne;               // [ne] (ISO)
+  double* s_Kl = s_mu + R.ne;                // [ntype][ND][ND] (ISO)
+  double* s_Km = s_Kl + (ISO ? R.ntype * (DIM == 2 ? 64 : 576) : 0);
+  int* s_et = reinterpret_cast<int*>(s_Km + (ISO ? R.ntype * (DIM == 2 ? 64 : 576) : 0));  // [ne]
   const int tid = threadIdx.x;
   const int bl = blockIdx.x;
   const int b = b0 + bl;
@@ -134,6 +126,11 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   const long tq0 = (long)bl * ne * nq;  // offset of this RVE in Aq/Pq (chunk-local)
 
   if (ISO) {
+    for (int i = tid; i < R.ntype * ND * ND; i += NTHR) {
+      s_Kl[i] = R.Klam[i];
+      s_Km[i] = R.Kmu[i];
+    }
+    for (int e = tid; e < ne; e += NTHR) s_et[e] = R.etype[e];
     const uint8_t* ph = R.phase + (R.phase_per_rve ? (long)b * ne : 0);
     const double* mt = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * 2 : 0);
     for (int e = tid; e < ne; e += NTHR) {
@@ -257,102 +254,104 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
     }
   }
 
-  // ---- K_ff tiles ----
+  // ---- K_ff tiles: node-row gather, coalesced direct stores ----
+  // A warp owns one RVE node p at a time: lane j < deg(p) forms the DIM x DIM block K_pq of
+  // neighbour q = nbr(p, j) (sum over the shared elements, periodic map applied through the
+  // independent-node numbering) into the warp's [DIM][64] row buffer, then every lane stores
+  // its two columns of the DIM rows (512 B per row per warp, 16 B per lane).  Structurally
+  // zero tiles are never touched (k_condense starts their accumulators at zero).
   const int nt = R.nt;
   double* Kb = Kt + (long)bl * R.nslot * TILE_ELEMS;
-  int nzt = 0;                        // nonzero tiles built so far (buffer parity)
+  const int lane = tid & 31, warp = tid >> 5;
+  double* rowbuf = s_row + warp * DIM * TILE;
   for (int I = 0; I < nt; ++I) {
     const int r0 = I * TILE;
-    int p_lo = r0 / DIM, p_hi = min((r0 + TILE - 1) / DIM, R.n_indep - 1);
-    const int k_lo = p_lo < R.n_indep ? R.nbr_ptr[p_lo] : 0;
-    const int k_hi = p_lo < R.n_indep ? R.nbr_ptr[p_hi + 1] : 0;
+    const int p_lo = r0 / DIM, p_hi = min((r0 + TILE - 1) / DIM, R.NT / DIM);  // nodes touching rows r0..r0+63
     for (int J = 0; J <= I; ++J) {
-      // structurally zero tiles are not written: k_condense never reads them (it starts their
-      // accumulators at zero), so K1's HBM traffic is the nonzero tiles only
       if (!R.tile_nz[I * nt + J]) continue;
       double* gt = Kb + (long)R.tslot[I * nt + J] * TILE_ELEMS;
-      double* tile = tbuf + (nzt & 1) * TILE_ELEMS;
-      ++nzt;
-      if (tid == 0) bulk_wait_read1();  // the buffer's previous bulk store has finished reading
-      __syncthreads();
       const int c0 = J * TILE;
-      double2* t2 = reinterpret_cast<double2*>(tile);
-      for (int i = tid; i < TILE_ELEMS / 2; i += NTHR) t2[i] = make_double2(0.0, 0.0);
-      __syncthreads();
-      for (int k = k_lo + tid; k < k_hi; k += NTHR) {
-        int p = R.nbr_owner[k], q = R.nbr[k];
-        if (p == R.corner || q == R.corner) continue;
-        int pr = p * DIM, qc = q * DIM;
-        if (qc + DIM <= c0 || qc >= c0 + TILE) continue;
-        double blk[DIM][DIM];
+      for (int p = p_lo + warp; p <= p_hi; p += NTHR / 32) {
 #pragma unroll
-        for (int i = 0; i < DIM; ++i)
-#pragma unroll
-          for (int j = 0; j < DIM; ++j) blk[i][j] = 0.0;
-        for (int s = R.sh_ptr[k]; s < R.sh_ptr[k + 1]; ++s) {
-          int code = R.sh[s];
-          int e = code >> 8, a = (code >> 4) & 15, bb = code & 15;
-          if (ISO) {
-            const double lam = s_lam[e], mu = s_mu[e];
-            const double* kl = R.Klam + (long)e * ND * ND + (a * DIM) * ND + bb * DIM;
-            const double* km = R.Kmu + (long)e * ND * ND + (a * DIM) * ND + bb * DIM;
+        for (int ci = 0; ci < DIM; ++ci) *reinterpret_cast<double2*>(rowbuf + ci * TILE + 2 * lane) = make_double2(0.0, 0.0);
+        __syncwarp();
+        const bool pad = p >= R.n_indep || p == R.corner;  // identity rows (corner class, tail)
+        if (!pad) {
+          const int k0 = R.nbr_ptr[p], deg = R.nbr_ptr[p + 1] - k0;
+          for (int j = lane; j < deg; j += 32) {
+            const int k = k0 + j, q = R.nbr[k];
+            const int cq = q * DIM - c0;  // first column of q in this tile
+            if (q == R.corner || cq + DIM <= 0 || cq >= TILE) continue;
+            double blk[DIM][DIM];
 #pragma unroll
             for (int i = 0; i < DIM; ++i)
 #pragma unroll
-              for (int j = 0; j < DIM; ++j) blk[i][j] += lam * kl[i * ND + j] + mu * km[i * ND + j];
-          } else {
-            for (int qq = 0; qq < nq; ++qq) {
-              const double* ga = R.grad + ((long)(e * nq + qq) * nen + a) * DIM;
-              const double* gb = R.grad + ((long)(e * nq + qq) * nen + bb) * DIM;
-              double wq = R.wdet[e * nq + qq];
-              const double* A = Aq + (tq0 + e * nq + qq) * 16;
+              for (int jj = 0; jj < DIM; ++jj) blk[i][jj] = 0.0;
+            for (int sh = R.sh_ptr[k]; sh < R.sh_ptr[k + 1]; ++sh) {
+              const int code = R.sh[sh];
+              const int e = code >> 8, a = (code >> 4) & 15, bb = code & 15;
+              if (ISO) {
+                const double lam = s_lam[e], mu = s_mu[e];
+                const int t = s_et[e];
+                const double* kl = s_Kl + (long)t * ND * ND + (a * DIM) * ND + bb * DIM;
+                const double* km = s_Km + (long)t * ND * ND + (a * DIM) * ND + bb * DIM;
 #pragma unroll
-              for (int i = 0; i < DIM; ++i)
+                for (int i = 0; i < DIM; ++i)
 #pragma unroll
-                for (int j = 0; j < DIM; ++j) {
-                  double v = 0.0;
+                  for (int jj = 0; jj < DIM; ++jj) blk[i][jj] += lam * kl[i * ND + jj] + mu * km[i * ND + jj];
+              } else {
+                for (int qq = 0; qq < nq; ++qq) {
+                  const double* ga = R.grad + ((long)(e * nq + qq) * nen + a) * DIM;
+                  const double* gb = R.grad + ((long)(e * nq + qq) * nen + bb) * DIM;
+                  const double wq = R.wdet[e * nq + qq];
+                  const double* A = Aq + (tq0 + e * nq + qq) * 16;
 #pragma unroll
-                  for (int Jd = 0; Jd < DIM; ++Jd)
+                  for (int i = 0; i < DIM; ++i)
 #pragma unroll
-                    for (int Ld = 0; Ld < DIM; ++Ld) v += ga[Jd] * A[(i * DIM + Jd) * 4 + j * DIM + Ld] * gb[Ld];
-                  blk[i][j] += wq * v;
+                    for (int jj = 0; jj < DIM; ++jj) {
+                      double v = 0.0;
+#pragma unroll
+                      for (int Jd = 0; Jd < DIM; ++Jd)
+#pragma unroll
+                        for (int Ld = 0; Ld < DIM; ++Ld) v += ga[Jd] * A[(i * DIM + Jd) * 4 + jj * DIM + Ld] * gb[Ld];
+                      blk[i][jj] += wq * v;
+                    }
                 }
+              }
             }
+#pragma unroll
+            for (int i = 0; i < DIM; ++i)
+#pragma unroll
+              for (int jj = 0; jj < DIM; ++jj) {
+                const int cc = cq + jj;
+                if (cc >= 0 && cc < TILE) rowbuf[i * TILE + cc] = blk[i][jj];
+              }
           }
         }
+        __syncwarp();
 #pragma unroll
-        for (int i = 0; i < DIM; ++i) {
-          int rr = pr + i - r0;
+        for (int ci = 0; ci < DIM; ++ci) {
+          const int row = p * DIM + ci, rr = row - r0;
           if (rr < 0 || rr >= TILE) continue;
-#pragma unroll
-          for (int j = 0; j < DIM; ++j) {
-            int cc = qc + j - c0;
-            if (cc < 0 || cc >= TILE) continue;
-            tile[rr * TILE + cc] = blk[i][j];
+          double2 v = *reinterpret_cast<const double2*>(rowbuf + ci * TILE + 2 * lane);
+          if (pad || row >= R.npad) {  // identity pad row
+            v.x = (c0 + 2 * lane == row) ? 1.0 : 0.0;
+            v.y = (c0 + 2 * lane + 1 == row) ? 1.0 : 0.0;
           }
+          __stcg(reinterpret_cast<double2*>(gt + rr * TILE + 2 * lane), v);
         }
-      }
-      if (I == J) {  // identity pads: corner class and DOFs beyond N_pad
-        for (int i = tid; i < TILE; i += NTHR) {
-          int g = r0 + i;
-          if (g >= R.npad || g / DIM == R.corner) tile[i * TILE + i] = 1.0;
-        }
-      }
-      __syncthreads();
-      if (tid == 0) {
-        fence_proxy_async();
-        bulk_store(gt, tile, TILE_ELEMS * 8);
-        bulk_commit();
+        __syncwarp();
       }
     }
   }
-  if (tid == 0) bulk_wait_all();
 }
 
 void launch_rve_assemble(const RveDev& R, int b0, int nb, double* Kt, double* Y, double* Cavg,
                          double* Pavg, double* rfn, const double* Aq, const double* Pq,
                          cudaStream_t s) {
-  size_t sm = (size_t)(2 * TILE_ELEMS + NTHR + 2 * R.ne) * sizeof(double);
+  const int dim = R.finite ? 2 : R.dim, nd = 4 * dim * (dim == 2 ? 1 : 2);  // nen*dim
+  size_t sm = (size_t)((NTHR / 32) * dim * TILE + NTHR + 2 * R.ne) * sizeof(double) +
+              (R.finite ? 0 : (size_t)R.ntype * nd * nd * 2 * sizeof(double) + (size_t)R.ne * sizeof(int));
   if (R.finite) {
     auto k = k_rve_assemble<2, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
