@@ -175,13 +175,18 @@ def main():
     args.warmup = max(args.warmup, 3)
 
     from paper_2312_12771_b200 import workloads as W
-    wl = W.make(args.config)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    wl = W.make(args.config)
+    if world > 1:  # weak scaling: one macro problem, its RVEs sharded; ~the same RVE count per GPU
+        nel1 = wl.nel
+        wl = W.make(args.config, nel=int(round(nel1 * world ** (1.0 / wl.dim))))
     config = {"workload": f"{wl.name}: {wl.description}", "config_index": args.config,
               "n_rve": wl.n_rve, "rve_dofs": wl.n_pad, "n_f": wl.n_f, "macro_dof": wl.n_dof,
-              "flop_per_rve": wl.flop_per_rve(), "parallelism": f"replicas{world}" if world > 1 else "single",
+              "flop_per_rve": wl.flop_per_rve(),
+              "parallelism": f"rve-sharded x{world} (C_eff all-gather, replicated macro CG)" if world > 1 else "single",
+              "macro_nel": wl.nel, "rve_per_gpu": wl.n_rve / world,
               "factorization": "tile-sparse" if args.tile_sparse else "dense"}
 
     if args.impl == "reference":
@@ -214,9 +219,15 @@ def main():
         torch.cuda.set_device(0)
     from paper_2312_12771_b200.hom import Homogenizer
 
-    h = Homogenizer.from_workload(wl, tile_sparse=args.tile_sparse)
+    if world > 1:
+        from paper_2312_12771_b200.dist import ShardedHomogenizer
+        sh = ShardedHomogenizer(wl, tile_sparse=args.tile_sparse)
+        h = sh.h
+    else:
+        sh = None
+        h = Homogenizer.from_workload(wl, tile_sparse=args.tile_sparse)
     work = h.work
-    config["l2"] = (f"no flush: each step writes and re-reads the K_ff tile pool ({wl.n_rve * work.g_tiles * 32768 / 1e9:.2f} GB, "
+    config["l2"] = (f"no flush: each step writes and re-reads the K_ff tile pool ({h.sizes.rve_count * work.g_tiles * 32768 / 1e9:.2f} GB, "
                     f"{work.g_tiles} 64x64 tiles per RVE), larger than the 126 MB L2")
     dev = torch.cuda.current_device()
     B, m = h.n_rve, h.m
@@ -229,11 +240,21 @@ def main():
     du = h.empty(h.n_dof) if h.finite else None
     cg_iters = []
 
-    if h.finite:  # a mid-load state: one converged load step first, then time Newton iterations
+    if h.finite and sh is None:  # a mid-load state: one converged load step first, then time Newton iterations
         u0, _ = h.newton(1, tol=1e-9)
         u.copy_(u0)
+    elif h.finite:  # sharded: the first Newton iterations of load step 1 (same per-iteration work)
+        u.zero_()
+        sh.newton_iteration(u, F, C, P_eff, P_avg, du, scale=1.0 / wl.n_steps)
 
     def step():
+        if sh is not None:
+            if h.finite:
+                _, _, info = sh.newton_iteration(u, F, C, P_eff, P_avg, du)
+            else:
+                _, _, _, info = sh.solve_linear(C, u, w)
+            cg_iters.append(info.iterations)
+            return
         if h.finite:
             h.macro_kinematics(u, F)
             h.condense(F, C, P_eff, P_avg)
@@ -280,7 +301,7 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = world * B * args.steps / (ms * 1e-3)
+    value = B * args.steps / (ms * 1e-3)  # B = all RVEs of the (sharded) problem when world > 1
 
     # ---------------- end to end: host inputs (pinned) -> C-ABI -> host results, every step
     ph_host = torch.from_numpy(np.ascontiguousarray(wl.phase if wl.phase.shape[0] > 1 else wl.phase[0])).pin_memory()
@@ -351,13 +372,13 @@ def main():
         "macro_solve_ms": (prof["macro_assemble"][0] + prof["cg"][0]) / args.steps,
         "cg_iterations": statistics.median(cg_iters) if cg_iters else None,
         "assembly": {"kernel": "k_rve_assemble (K1)", "ms_per_launch": asm_ms,
-                     "GBps": asm_bytes_rve * B * args.steps / (prof["rve_assemble"][0] * 1e-3) / 1e9
+                     "GBps": asm_bytes_rve * h.sizes.rve_count * args.steps / (prof["rve_assemble"][0] * 1e-3) / 1e9
                      if prof["rve_assemble"][0] > 0 else None,
                      "bytes": f"{asm_bytes_rve} B/RVE: {work.a_tiles} structurally nonzero 64x64 K_ff tiles + K_fe + <C>"},
         "breakdown": breakdown,
         "gpu_launches": launches,
         "clocks": clocks,
-        "e2e": {"value": world * B * args.steps / (ms_e2e * 1e-3), "unit": "tangents/s",
+        "e2e": {"value": B * args.steps / (ms_e2e * 1e-3), "unit": "tangents/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "what": "hom_set_phases from pinned host + condense + macro solve + recovery + D2H of C_eff, u, w"},
     }

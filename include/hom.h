@@ -112,6 +112,11 @@ typedef struct {
                                symbolic tile-level fill of K_ff's structural pattern are stored
                                and factored; identical arithmetic on those tiles,
                                the skipped products are exact zeros. */
+  int32_t rve_begin;        /* RVE sharding (multi-GPU): this context condenses and */
+  int32_t rve_count;        /* recovers RVEs [rve_begin, rve_begin + rve_count) only (rve_count <= 0:
+                               all B).  C_eff / P_eff / w rows of the other RVEs are left untouched,
+                               so the caller all-gathers C_eff (and P_eff) before hom_macro_solve,
+                               which always solves the full macro problem. */
 } hom_options;
 
 typedef struct {
@@ -124,6 +129,8 @@ typedef struct {
   int32_t macro_nnz;        /* scalar CSR entries of the macro stiffness */
   int32_t rve_chunk;
   double rve_volume;        /* |Omega| */
+  int32_t rve_begin;        /* local RVE range of this context (options.rve_begin / rve_count) */
+  int32_t rve_count;
 } hom_sizes;
 
 /* Work per RVE of the condensation, from the tile structure (hom_get_work).  Tile counts
@@ -192,7 +199,7 @@ int hom_macro_solve(hom_ctx* ctx, const double* d_D, const double* d_S, double d
 /* ||R_F||_2 with R = sum_qp eta B^T S_b - f_body (macro residual, eq:linSys); synchronises. */
 int hom_macro_residual_norm(hom_ctx* ctx, const double* d_S, double* norm, void* stream);
 
-/* Fluctuation recovery (eq:reduction P:388-390 / P:424-427).
+/* Fluctuation recovery (eq:reduction P:388-390 / P:424-427), local RVE range only.
  * Small strain: d_w [B][N_pad] = -X_b eps_b(d_x)           (d_x = u).
  * Finite strain: w += -(X_b dF_b(d_x) + K_ff^-1 r_f,b)       (d_x = du), internal state;
  *                copied to d_w if non-NULL. */

@@ -24,6 +24,7 @@ struct hom_ctx {
   hom_error_info err{};
   int64_t launches = 0;
   int dim = 0, B = 0, m = 0, finite = 0, chunk = 0, macro_free = 0;
+  int b_lo = 0, b_hi = 0;  // local RVE range (options.rve_begin / rve_count)
   RveDev R{};
   MacroDev M{};
   std::vector<void*> allocs;
@@ -499,9 +500,14 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   const size_t tiles = (size_t)R.nslot;
   const size_t per_rve = tiles * hom::TILE_ELEMS * 8 + (size_t)R.NT * hom::RHSW * 8 + 64 * 8 * 2 +
                          (c->finite ? (size_t)R.ne * nq * 20 * 8 : 0);
+  if (c->opt.rve_count > 0 && (c->opt.rve_begin < 0 || c->opt.rve_begin + c->opt.rve_count > c->B))
+    return fail(HOM_ERR_INVALID_ARG, "rve_begin / rve_count outside [0, B)");
+  c->b_lo = c->opt.rve_count > 0 ? c->opt.rve_begin : 0;
+  c->b_hi = c->opt.rve_count > 0 ? c->opt.rve_begin + c->opt.rve_count : c->B;
+  const int nloc = c->b_hi - c->b_lo;
   int chunk = c->opt.rve_chunk > 0 ? c->opt.rve_chunk
-                                   : (int)std::min<double>(c->B, std::floor(c->opt.mem_budget_gb * 1e9 / per_rve));
-  chunk = std::max(1, std::min(chunk, c->B));
+                                   : (int)std::min<double>(nloc, std::floor(c->opt.mem_budget_gb * 1e9 / per_rve));
+  chunk = std::max(1, std::min(chunk, nloc));
   c->chunk = chunk;
 
   R.elem_indep = upload(c, eind, s, &rc);
@@ -541,8 +547,11 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
       }
     }
     R.ntype = c->finite ? 0 : (int)(KlamT.size() / ((size_t)ND * ND));
-    if ((size_t)R.ntype * ND * ND * 2 * sizeof(double) > 96 * 1024)
-      return fail(HOM_ERR_INVALID_ARG, "too many distinct RVE element geometries for the K1 shared-memory tables");
+    if ((size_t)R.ntype * mat->n_phases * ND * ND * sizeof(double) > 96 * 1024)
+      return fail(HOM_ERR_INVALID_ARG, "too many distinct RVE element geometries x phases for the K1 shared-memory tables");
+    int max_deg = 1;
+    for (int pp = 0; pp < R.n_indep; ++pp) max_deg = std::max(max_deg, RP.nbr_ptr[pp + 1] - RP.nbr_ptr[pp]);
+    R.npw = std::max(1, std::min(8, 32 / max_deg));
     R.etype = upload(c, etype, s, &rc);
     R.Klam = upload(c, KlamT, s, &rc);
     R.Kmu = upload(c, KmuT, s, &rc);
@@ -619,6 +628,8 @@ int hom_get_sizes(const hom_ctx* c, hom_sizes* o) {
   o->macro_nnz = c->M.nnz;
   o->rve_chunk = c->chunk;
   o->rve_volume = c->R.vol;
+  o->rve_begin = c->b_lo;
+  o->rve_count = c->b_hi - c->b_lo;
   return HOM_OK;
 }
 
@@ -655,8 +666,8 @@ int hom_condense(hom_ctx* c, const double* d_kin, double* d_C_eff, double* d_P_e
   const RveDev& R = c->R;
   cudaMemsetAsync(c->info, 0, sizeof(int) * c->B, s);
   if (c->finite) cudaMemsetAsync(c->jflag, 0x7f, sizeof(int) * c->B, s);  // = JFLAG_NONE
-  for (int b0 = 0; b0 < c->B; b0 += c->chunk) {
-    int nb = std::min(c->chunk, c->B - b0);
+  for (int b0 = c->b_lo; b0 < c->b_hi; b0 += c->chunk) {
+    int nb = std::min(c->chunk, c->b_hi - b0);
     if (c->finite)
       run(c, HOM_PROF_RVE_ASSEMBLE, s,
           [&] { hom::launch_rve_material_nh(R, b0, nb, d_kin, c->w, c->Aq, c->Pq, c->jflag, s); });
@@ -670,12 +681,16 @@ int hom_condense(hom_ctx* c, const double* d_kin, double* d_C_eff, double* d_P_e
   if (rc || !c->opt.check_info) return rc;
   int h[2] = {INT_MAX, INT_MAX};
   cudaMemcpyAsync(c->first_fail, h, sizeof(h), cudaMemcpyHostToDevice, s);
-  run(c, HOM_PROF_OTHER, s, [&] { hom::launch_first_fail(c->info, c->B, 0, c->first_fail, s); });
+  const int nloc = c->b_hi - c->b_lo;
+  run(c, HOM_PROF_OTHER, s, [&] { hom::launch_first_fail(c->info + c->b_lo, nloc, 0, c->first_fail, s); });
   if (c->finite)
-    run(c, HOM_PROF_OTHER, s, [&] { hom::launch_first_fail(c->jflag, c->B, JFLAG_NONE, c->first_fail + 1, s); });
+    run(c, HOM_PROF_OTHER, s,
+        [&] { hom::launch_first_fail(c->jflag + c->b_lo, nloc, JFLAG_NONE, c->first_fail + 1, s); });
   cudaMemcpyAsync(h, c->first_fail, sizeof(h), cudaMemcpyDeviceToHost, s);
   rc = check_cuda(c, cudaStreamSynchronize(s), "hom_condense sync");
   if (rc) return rc;
+  if (h[0] != INT_MAX) h[0] += c->b_lo;
+  if (h[1] != INT_MAX) h[1] += c->b_lo;
   if (h[1] != INT_MAX) {
     int q = -1;
     cudaMemcpy(&q, c->jflag + h[1], sizeof(int), cudaMemcpyDeviceToHost);
@@ -732,10 +747,12 @@ int hom_recover_fluctuations(hom_ctx* c, const double* d_x, double* d_w, void* s
   cudaStream_t s = (cudaStream_t)stream;
   run(c, HOM_PROF_RECOVER, s, [&] { hom::launch_macro_kin(c->M, d_x, c->kin, 0, s); });
   if (c->finite) {
-    run(c, HOM_PROF_RECOVER, s, [&] { hom::launch_recover(c->R, c->B, c->X, c->kin, c->w, 1, s); });
+    run(c, HOM_PROF_RECOVER, s,
+        [&] { hom::launch_recover(c->R, c->b_lo, c->b_hi - c->b_lo, c->X, c->kin, c->w, 1, s); });
     if (d_w) cudaMemcpyAsync(d_w, c->w, sizeof(double) * (size_t)c->B * c->R.npad, cudaMemcpyDeviceToDevice, s);
   } else {
-    run(c, HOM_PROF_RECOVER, s, [&] { hom::launch_recover(c->R, c->B, c->X, c->kin, d_w, 0, s); });
+    run(c, HOM_PROF_RECOVER, s,
+        [&] { hom::launch_recover(c->R, c->b_lo, c->b_hi - c->b_lo, c->X, c->kin, d_w, 0, s); });
   }
   return check_cuda(c, cudaGetLastError(), "hom_recover_fluctuations");
 }
@@ -744,7 +761,8 @@ int hom_newton_update(hom_ctx* c, double* d_u, const double* d_du, void* stream)
   if (!c || !d_u || !d_du || !c->finite) return set_err(c, HOM_ERR_INVALID_ARG, "hom_newton_update");
   cudaStream_t s = (cudaStream_t)stream;
   run(c, HOM_PROF_RECOVER, s, [&] { hom::launch_macro_kin(c->M, d_du, c->kin, 0, s); });
-  run(c, HOM_PROF_RECOVER, s, [&] { hom::launch_recover(c->R, c->B, c->X, c->kin, c->w, 1, s); });
+  run(c, HOM_PROF_RECOVER, s,
+      [&] { hom::launch_recover(c->R, c->b_lo, c->b_hi - c->b_lo, c->X, c->kin, c->w, 1, s); });
   run(c, HOM_PROF_OTHER, s, [&] { hom::launch_axpy(d_u, d_du, 1.0, c->M.ndof, s); });
   return check_cuda(c, cudaGetLastError(), "hom_newton_update");
 }
@@ -766,7 +784,7 @@ int hom_get_fluctuations(hom_ctx* c, double* d_w, void* stream) {
 int hom_micro_residual_max(hom_ctx* c, double* out, void* stream) {
   if (!c || !out) return set_err(c, HOM_ERR_INVALID_ARG, "hom_micro_residual_max: NULL");
   cudaStream_t s = (cudaStream_t)stream;
-  run(c, HOM_PROF_OTHER, s, [&] { hom::launch_max_reduce(c->rfn, c->B, c->scal + 1, s); });
+  run(c, HOM_PROF_OTHER, s, [&] { hom::launch_max_reduce(c->rfn + c->b_lo, c->b_hi - c->b_lo, c->scal + 1, s); });
   cudaMemcpyAsync(out, c->scal + 1, sizeof(double), cudaMemcpyDeviceToHost, s);
   return check_cuda(c, cudaStreamSynchronize(s), "hom_micro_residual_max");
 }

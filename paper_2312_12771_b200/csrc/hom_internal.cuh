@@ -41,6 +41,7 @@ struct RveDev {
   const double* Kmu;
   const int* etype;               // [ne] element -> type
   int ntype;
+  int npw;                        // K1: RVE nodes gathered per warp iteration (32 / max degree)
   const double* Flam;             // [ne][nen*dim][m]
   const double* Fmu;
   const double* evol;             // [ne] element volume
@@ -105,7 +106,7 @@ bool launch_macro_cg_cluster(const MacroDev& M, int max_slice_nnz, const double*
                              CgState* st, cudaStream_t s);
 void launch_norm(const double* v, int n, double* out, cudaStream_t s);
 void launch_axpy(double* y, const double* x, double a, int n, cudaStream_t s);
-void launch_recover(const RveDev& R, int B, const double* X, const double* kin, double* w,
+void launch_recover(const RveDev& R, int b0, int nb, const double* X, const double* kin, double* w,
                     int accumulate, cudaStream_t s);
 
 }  // namespace hom

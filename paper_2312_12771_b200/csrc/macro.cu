@@ -476,11 +476,12 @@ bool launch_macro_cg_cluster(const MacroDev& M, int max_slice_nnz, const double*
 // ---------------------------------------------------------------- K8 recovery
 // accumulate = 0: w = -X[:, :m] kin            (small strain, kin = eps)
 // accumulate = 1: w += -(X[:, m] + X[:, :m] kin) (finite strain, kin = grad du)
-__global__ void k_recover(RveDev R, int B, const double* __restrict__ X, const double* __restrict__ kin,
+__global__ void k_recover(RveDev R, int b0, int nb, const double* __restrict__ X, const double* __restrict__ kin,
                           double* __restrict__ w, int accumulate) {
   long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long)B * R.npad) return;
-  int b = (int)(t / R.npad), i = (int)(t % R.npad);
+  if (t >= (long)nb * R.npad) return;
+  int b = b0 + (int)(t / R.npad), i = (int)(t % R.npad);
+  t += (long)b0 * R.npad;
   const double* xr = X + ((long)b * R.NT + i) * RHSW;
   const double* kb = kin + (long)b * R.m;
   double v = 0.0;
@@ -489,10 +490,11 @@ __global__ void k_recover(RveDev R, int B, const double* __restrict__ X, const d
   else w[t] = -v;
 }
 
-void launch_recover(const RveDev& R, int B, const double* X, const double* kin, double* w, int accumulate,
-                    cudaStream_t s) {
-  long n = (long)B * R.npad;
-  k_recover<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(R, B, X, kin, w, accumulate);
+void launch_recover(const RveDev& R, int b0, int nb, const double* X, const double* kin, double* w,
+                    int accumulate, cudaStream_t s) {
+  long n = (long)nb * R.npad;
+  if (n <= 0) return;
+  k_recover<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(R, b0, nb, X, kin, w, accumulate);
 }
 
 }  // namespace hom

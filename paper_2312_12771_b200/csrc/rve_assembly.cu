@@ -111,13 +111,12 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
                                                        const double* __restrict__ Aq,
                                                        const double* __restrict__ Pq) {
   extern __shared__ __align__(128) double smem[];
-  double* s_row = smem;                      // [8 warps][DIM][64] tile-row buffers
-  double* red = s_row + (NTHR / 32) * DIM * TILE;  // [NTHR] reduction scratch
+  double* s_row = smem;                      // [8 warps][npw][DIM][64] tile-row buffers
+  double* red = s_row + (NTHR / 32) * R.npw * DIM * TILE;  // [NTHR] reduction scratch
   double* s_lam = red + NTHR;                // [ne] (ISO)
   double* s_mu = s_lam + R.ne;               // [ne] (ISO)
-  double* s_Kl = s_mu + R.ne;                // [ntype][ND][ND] (ISO)
-  double* s_Km = s_Kl + (ISO ? R.ntype * (DIM == 2 ? 64 : 576) : 0);
-  int* s_et = reinterpret_cast<int*>(s_Km + (ISO ? R.ntype * (DIM == 2 ? 64 : 576) : 0));  // [ne]
+  double* s_K = s_mu + R.ne;                 // [ntype][n_phase][ND][ND] element matrices (ISO)
+  int* s_ep = reinterpret_cast<int*>(s_K + (ISO ? R.ntype * R.n_phase * (DIM == 2 ? 64 : 576) : 0));  // [ne]
   const int tid = threadIdx.x;
   const int bl = blockIdx.x;
   const int b = b0 + bl;
@@ -126,11 +125,6 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   const long tq0 = (long)bl * ne * nq;  // offset of this RVE in Aq/Pq (chunk-local)
 
   if (ISO) {
-    for (int i = tid; i < R.ntype * ND * ND; i += NTHR) {
-      s_Kl[i] = R.Klam[i];
-      s_Km[i] = R.Kmu[i];
-    }
-    for (int e = tid; e < ne; e += NTHR) s_et[e] = R.etype[e];
     const uint8_t* ph = R.phase + (R.phase_per_rve ? (long)b * ne : 0);
     const double* mt = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * 2 : 0);
     for (int e = tid; e < ne; e += NTHR) {
@@ -138,6 +132,14 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
       double E = mt[2 * p], nu = mt[2 * p + 1];
       s_lam[e] = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
       s_mu[e] = E / (2.0 * (1.0 + nu));
+      s_ep[e] = R.etype[e] * R.n_phase + p;
+    }
+    // K_e = lam Klam_t + mu Kmu_t for every (element type t, phase) of this RVE
+    for (int i = tid; i < R.ntype * R.n_phase * ND * ND; i += NTHR) {
+      const int t = i / (R.n_phase * ND * ND), pp = (i / (ND * ND)) % R.n_phase, j = i % (ND * ND);
+      const double E = mt[2 * pp], nu = mt[2 * pp + 1];
+      const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)), mu = E / (2.0 * (1.0 + nu));
+      s_K[i] = lam * R.Klam[(long)t * ND * ND + j] + mu * R.Kmu[(long)t * ND * ND + j];
     }
   }
   __syncthreads();
@@ -255,30 +257,33 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   }
 
   // ---- K_ff tiles: node-row gather, coalesced direct stores ----
-  // A warp owns one RVE node p at a time: lane j < deg(p) forms the DIM x DIM block K_pq of
-  // neighbour q = nbr(p, j) (sum over the shared elements, periodic map applied through the
-  // independent-node numbering) into the warp's [DIM][64] row buffer, then every lane stores
-  // its two columns of the DIM rows (512 B per row per warp, 16 B per lane).  Structurally
-  // zero tiles are never touched (k_condense starts their accumulators at zero).
-  const int nt = R.nt;
+  // A warp owns R.npw consecutive RVE nodes p at a time; lane group g = lane / S (S = 32/npw)
+  // serves node p0 + g and its lane j forms the DIM x DIM block K_pq of neighbour q = nbr(p, j)
+  // (sum over the shared elements of the per-(type, phase) element matrix; the periodic map
+  // is applied through the independent-node numbering) into the warp's row buffer; then every
+  // lane stores its two columns of the npw*DIM rows (512 B per row per warp, 16 B per lane).
+  // Structurally zero tiles are never touched (k_condense starts their accumulators at zero).
+  const int nt = R.nt, npw = R.npw, S = 32 / npw;
   double* Kb = Kt + (long)bl * R.nslot * TILE_ELEMS;
   const int lane = tid & 31, warp = tid >> 5;
-  double* rowbuf = s_row + warp * DIM * TILE;
+  double* rowbuf = s_row + warp * npw * DIM * TILE;
+  const int g = lane / S, jl = lane % S;
   for (int I = 0; I < nt; ++I) {
     const int r0 = I * TILE;
-    const int p_lo = r0 / DIM, p_hi = min((r0 + TILE - 1) / DIM, R.NT / DIM);  // nodes touching rows r0..r0+63
+    const int p_lo = r0 / DIM, p_hi = (r0 + TILE - 1) / DIM;  // nodes touching rows r0..r0+63
     for (int J = 0; J <= I; ++J) {
       if (!R.tile_nz[I * nt + J]) continue;
       double* gt = Kb + (long)R.tslot[I * nt + J] * TILE_ELEMS;
       const int c0 = J * TILE;
-      for (int p = p_lo + warp; p <= p_hi; p += NTHR / 32) {
-#pragma unroll
-        for (int ci = 0; ci < DIM; ++ci) *reinterpret_cast<double2*>(rowbuf + ci * TILE + 2 * lane) = make_double2(0.0, 0.0);
+      for (int p0 = p_lo + warp * npw; p0 <= p_hi; p0 += (NTHR / 32) * npw) {
+        for (int i = lane; i < npw * DIM * TILE / 2; i += 32)
+          reinterpret_cast<double2*>(rowbuf)[i] = make_double2(0.0, 0.0);
         __syncwarp();
-        const bool pad = p >= R.n_indep || p == R.corner;  // identity rows (corner class, tail)
-        if (!pad) {
+        const int p = p0 + g;
+        if (g < npw && p <= p_hi && p < R.n_indep && p != R.corner) {
+          double* rb = rowbuf + g * DIM * TILE;
           const int k0 = R.nbr_ptr[p], deg = R.nbr_ptr[p + 1] - k0;
-          for (int j = lane; j < deg; j += 32) {
+          for (int j = jl; j < deg; j += S) {
             const int k = k0 + j, q = R.nbr[k];
             const int cq = q * DIM - c0;  // first column of q in this tile
             if (q == R.corner || cq + DIM <= 0 || cq >= TILE) continue;
@@ -291,14 +296,11 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
               const int code = R.sh[sh];
               const int e = code >> 8, a = (code >> 4) & 15, bb = code & 15;
               if (ISO) {
-                const double lam = s_lam[e], mu = s_mu[e];
-                const int t = s_et[e];
-                const double* kl = s_Kl + (long)t * ND * ND + (a * DIM) * ND + bb * DIM;
-                const double* km = s_Km + (long)t * ND * ND + (a * DIM) * ND + bb * DIM;
+                const double* ke = s_K + (long)s_ep[e] * ND * ND + (a * DIM) * ND + bb * DIM;
 #pragma unroll
                 for (int i = 0; i < DIM; ++i)
 #pragma unroll
-                  for (int jj = 0; jj < DIM; ++jj) blk[i][jj] += lam * kl[i * ND + jj] + mu * km[i * ND + jj];
+                  for (int jj = 0; jj < DIM; ++jj) blk[i][jj] += ke[i * ND + jj];
               } else {
                 for (int qq = 0; qq < nq; ++qq) {
                   const double* ga = R.grad + ((long)(e * nq + qq) * nen + a) * DIM;
@@ -324,21 +326,26 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
 #pragma unroll
               for (int jj = 0; jj < DIM; ++jj) {
                 const int cc = cq + jj;
-                if (cc >= 0 && cc < TILE) rowbuf[i * TILE + cc] = blk[i][jj];
+                if (cc >= 0 && cc < TILE) rb[i * TILE + cc] = blk[i][jj];
               }
           }
         }
         __syncwarp();
+        for (int n = 0; n < npw; ++n) {
+          const int pn = p0 + n;
+          if (pn > p_hi) break;
+          const bool pad = pn >= R.n_indep || pn == R.corner;  // identity rows (corner class, tail)
 #pragma unroll
-        for (int ci = 0; ci < DIM; ++ci) {
-          const int row = p * DIM + ci, rr = row - r0;
-          if (rr < 0 || rr >= TILE) continue;
-          double2 v = *reinterpret_cast<const double2*>(rowbuf + ci * TILE + 2 * lane);
-          if (pad || row >= R.npad) {  // identity pad row
-            v.x = (c0 + 2 * lane == row) ? 1.0 : 0.0;
-            v.y = (c0 + 2 * lane + 1 == row) ? 1.0 : 0.0;
+          for (int ci = 0; ci < DIM; ++ci) {
+            const int row = pn * DIM + ci, rr = row - r0;
+            if (rr < 0 || rr >= TILE) continue;
+            double2 v = *reinterpret_cast<const double2*>(rowbuf + (n * DIM + ci) * TILE + 2 * lane);
+            if (pad || row >= R.npad) {
+              v.x = (c0 + 2 * lane == row) ? 1.0 : 0.0;
+              v.y = (c0 + 2 * lane + 1 == row) ? 1.0 : 0.0;
+            }
+            __stcg(reinterpret_cast<double2*>(gt + rr * TILE + 2 * lane), v);
           }
-          __stcg(reinterpret_cast<double2*>(gt + rr * TILE + 2 * lane), v);
         }
         __syncwarp();
       }
@@ -350,8 +357,8 @@ void launch_rve_assemble(const RveDev& R, int b0, int nb, double* Kt, double* Y,
                          double* Pavg, double* rfn, const double* Aq, const double* Pq,
                          cudaStream_t s) {
   const int dim = R.finite ? 2 : R.dim, nd = 4 * dim * (dim == 2 ? 1 : 2);  // nen*dim
-  size_t sm = (size_t)((NTHR / 32) * dim * TILE + NTHR + 2 * R.ne) * sizeof(double) +
-              (R.finite ? 0 : (size_t)R.ntype * nd * nd * 2 * sizeof(double) + (size_t)R.ne * sizeof(int));
+  size_t sm = (size_t)((NTHR / 32) * R.npw * dim * TILE + NTHR + 2 * R.ne) * sizeof(double) +
+              (R.finite ? 0 : (size_t)R.ntype * R.n_phase * nd * nd * sizeof(double) + (size_t)R.ne * sizeof(int));
   if (R.finite) {
     auto k = k_rve_assemble<2, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

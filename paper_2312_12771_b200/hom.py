@@ -54,13 +54,14 @@ class Materials(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [("finite_strain", ctypes.c_int32), ("cg_rtol", ctypes.c_double), ("cg_max_iter", ctypes.c_int32),
                 ("rve_chunk", ctypes.c_int32), ("check_info", ctypes.c_int32), ("mem_budget_gb", ctypes.c_double),
-                ("tile_sparse", ctypes.c_int32)]
+                ("tile_sparse", ctypes.c_int32), ("rve_begin", ctypes.c_int32), ("rve_count", ctypes.c_int32)]
 
 
 class Sizes(ctypes.Structure):
     _fields_ = [("n_rve", ctypes.c_int32), ("m", ctypes.c_int32), ("n_pad", ctypes.c_int32),
                 ("n_tiles", ctypes.c_int32), ("n_macro_dof", ctypes.c_int32), ("n_macro_free", ctypes.c_int32),
-                ("macro_nnz", ctypes.c_int32), ("rve_chunk", ctypes.c_int32), ("rve_volume", ctypes.c_double)]
+                ("macro_nnz", ctypes.c_int32), ("rve_chunk", ctypes.c_int32), ("rve_volume", ctypes.c_double),
+                ("rve_begin", ctypes.c_int32), ("rve_count", ctypes.c_int32)]
 
 
 class Work(ctypes.Structure):
@@ -142,7 +143,7 @@ class Homogenizer:
 
     def __init__(self, macro_coords, macro_conn, dirichlet_dof, dirichlet_value, body_force,
                  rve_coords, rve_conn, phase, materials, kind="linear", cg_rtol=1e-13, cg_max_iter=20000,
-                 rve_chunk=0, check_info=True, mem_budget_gb=0.0, tile_sparse=False):
+                 rve_chunk=0, check_info=True, mem_budget_gb=0.0, tile_sparse=False, rve_range=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("Homogenizer needs a CUDA device (no CPU fallback)")
@@ -175,8 +176,9 @@ class Homogenizer:
         self.rve = RveMesh(dim, rc_.shape[0], rconn.shape[0], rconn.shape[1], _np_ptr(rc_), _np_ptr(rconn))
         self.phase = PhaseField(per_rve_phase, _np_ptr(ph))
         self.mat = Materials(1 if kind == "nh" else 0, n_phase, per_rve_mat, _np_ptr(mt))
+        rb, rn = (0, 0) if rve_range is None else (int(rve_range[0]), int(rve_range[1]) - int(rve_range[0]))
         self.opt = Options(1 if kind == "nh" else 0, cg_rtol, cg_max_iter, rve_chunk, int(check_info), mem_budget_gb,
-                           int(tile_sparse))
+                           int(tile_sparse), rb, rn)
         self.finite = kind == "nh"
         h = ctypes.c_void_p()
         rc = L.hom_setup(ctypes.byref(h), ctypes.byref(self.macro), ctypes.byref(self.rve),
