@@ -38,6 +38,7 @@ struct hom_ctx {
   CgState* cgst = nullptr;
   size_t phase_bytes = 0, mat_bytes = 0;
   int max_slice_nnz = 0;  // largest CSR slice of a 8-CTA cluster partition (CG smem sizing)
+  int cg2_slice[2][2] = {};  // k_macro_cg_cluster2 largest (rows, nnz) slice for G = 16, 8
   hom_work work{};
   // event profiling (hom_profile_enable / hom_profile_read)
   struct ProfRec {
@@ -287,6 +288,8 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
       int a = (int)((long)M.ndof * g / G), b = (int)((long)M.ndof * (g + 1) / G);
       c->max_slice_nnz = std::max(c->max_slice_nnz, rowptr[b] - rowptr[a]);
     }
+  hom::cg2_slice_sizes(M, rowptr.data(), 16, &c->cg2_slice[0][0], &c->cg2_slice[0][1]);
+  hom::cg2_slice_sizes(M, rowptr.data(), 8, &c->cg2_slice[1][0], &c->cg2_slice[1][1]);
   std::vector<uint8_t> dmask(M.ndof, 0);
   std::vector<double> dval(M.ndof, 0.0), fbody(M.ndof, 0.0);
   if (mac->n_dirichlet > 0 && (!mac->dirichlet_dof || !mac->dirichlet_value))
@@ -711,7 +714,9 @@ int hom_macro_solve(hom_ctx* c, const double* d_D, const double* d_S, double sca
   run(c, HOM_PROF_MACRO_ASSEMBLE, s, [&] { hom::launch_macro_assemble(c->M, d_D, c->val, c->diag, s); });
   run(c, HOM_PROF_MACRO_ASSEMBLE, s, [&] { hom::launch_macro_rhs(c->M, c->val, d_S, scale, c->rhs, nullptr, s); });
   run(c, HOM_PROF_CG, s, [&] {
-    if (!hom::launch_macro_cg_cluster(c->M, c->max_slice_nnz, c->val, c->diag, c->rhs, scale, c->opt.cg_rtol,
+    if (!hom::launch_macro_cg_cluster2(c->M, c->cg2_slice, c->val, c->rhs, scale, c->opt.cg_rtol,
+                                       c->opt.cg_max_iter, d_x, c->cgst, s) &&
+        !hom::launch_macro_cg_cluster(c->M, c->max_slice_nnz, c->val, c->diag, c->rhs, scale, c->opt.cg_rtol,
                                       c->opt.cg_max_iter, d_x, c->cgwork, c->cgst, s))
       hom::launch_macro_cg(c->M, c->val, c->diag, c->rhs, scale, c->opt.cg_rtol, c->opt.cg_max_iter, d_x,
                            c->cgwork, c->cgst, s);

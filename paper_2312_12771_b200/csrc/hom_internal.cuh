@@ -105,6 +105,9 @@ bool launch_macro_cg_cluster(const MacroDev& M, int max_slice_nnz, const double*
                              const double* rhs, double scale, double rtol, int max_iter, double* x, double* p,
                              CgState* st, cudaStream_t s);
 void launch_norm(const double* v, int n, double* out, cudaStream_t s);
+void cg2_slice_sizes(const MacroDev& M, const int* host_rowptr, int G, int* max_nr, int* max_nnz);
+bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const double* val, const double* rhs,
+                              double scale, double rtol, int max_iter, double* x, CgState* st, cudaStream_t s);
 void launch_axpy(double* y, const double* x, double a, int n, cudaStream_t s);
 void launch_recover(const RveDev& R, int b0, int nb, const double* X, const double* kin, double* w,
                     int accumulate, cudaStream_t s);

@@ -8,6 +8,9 @@
 // results are bitwise reproducible.
 #include <cooperative_groups.h>
 
+#include <algorithm>
+#include <vector>
+
 #include "hom_internal.cuh"
 
 namespace cgx = cooperative_groups;
@@ -464,6 +467,249 @@ bool launch_macro_cg_cluster(const MacroDev& M, int max_slice_nnz, const double*
     }
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_macro_cg_cluster, M, val, diag, rhs, scale, rtol, max_iter, x, p,
                                        st, csr);
+    if (e == cudaSuccess) {
+      cached_G = G;
+      return true;
+    }
+    cudaGetLastError();
+  }
+  return false;
+}
+
+// ---------------------------------------------------------------- K6/K7: cluster PCG, v2
+// Chronopoulos-Gear PCG (one fused reduction + one vector broadcast per iteration instead
+// of two reductions + a publish) with a node-block Jacobi preconditioner (the dim x dim
+// diagonal block of every macro node, Dirichlet components removed).  One cluster of G CTAs;
+// CTA g owns the rows of a contiguous node range, keeps that CSR slice and the slices of
+// x, r, p, s, w and of the block inverse in shared memory, and ALSO a full copy of the
+// preconditioned residual z: every CTA scatters its new slice of z into all G copies with
+// DSMEM stores, so the SpMV gathers are shared-memory loads.  Two cluster barriers per
+// iteration; every dot product is summed in a fixed order (bitwise deterministic).
+//   loop: x += a p; r -= a s; z = M^-1 r; [z slices + (r.z, r.r) partials -> all CTAs; sync]
+//         w = A z; [(z.w) partials -> all CTAs; sync]
+//         b = g'/g; a = g'/(d - b g'/a); p = z + b p; s = w + b s
+constexpr int CG2_THR = 256;
+
+__device__ __forceinline__ void cg2_publish(cgx::cluster_group& cl, double* slots, int nv, double* v, double* wred) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int j = 0; j < nv; ++j) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_down_sync(0xffffffffu, v[j], o);
+    if (lane == 0) wred[j * 32 + warp] = v[j];
+  }
+  __syncthreads();
+  const int G = cl.num_blocks();
+  if ((int)threadIdx.x < G) {  // thread t writes this CTA's partials into CTA t's slots
+    double* remote = cl.map_shared_rank(slots, (int)threadIdx.x);
+    for (int j = 0; j < nv; ++j) {
+      double a = 0.0;
+      for (int w = 0; w < CG2_THR / 32; ++w) a += wred[j * 32 + w];
+      remote[j * CGC_MAXG + cl.block_rank()] = a;
+    }
+  }
+}
+__device__ __forceinline__ double cg2_sum(const double* slots, int j, int G) {
+  double a = 0.0;
+  for (int k = 0; k < G; ++k) a += slots[j * CGC_MAXG + k];
+  return a;
+}
+
+__global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const double* __restrict__ val,
+                                                               const double* __restrict__ b, double scale,
+                                                               double rtol, int max_iter, double* __restrict__ xout,
+                                                               CgState* st) {
+  cgx::cluster_group cl = cgx::this_cluster();
+  const int G = cl.num_blocks(), g = cl.block_rank();
+  const int n = M.ndof, dim = M.dim, tid = threadIdx.x;
+  const int nd0 = (int)((long)M.n_nodes * g / G), nd1 = (int)((long)M.n_nodes * (g + 1) / G);
+  const int r0 = nd0 * dim, r1 = nd1 * dim, nr = r1 - r0;
+  extern __shared__ __align__(16) double sm[];
+  double* slotsA = sm;                       // [3][CGC_MAXG]: (r.z, r.r)
+  double* slotsB = slotsA + 3 * CGC_MAXG;    // [3][CGC_MAXG]: (z.w)
+  double* wred = slotsB + 3 * CGC_MAXG;      // [3][32]
+  double* zf = wred + 96;                    // [n] full copy of z
+  double* x = zf + n;
+  double* r = x + nr;
+  double* p = r + nr;
+  double* sv = p + nr;
+  double* w = sv + nr;
+  double* mi = w + nr;                       // [nr][dim] block-Jacobi inverse rows
+  const int nz0 = M.rowptr[r0], nnz = M.rowptr[r1] - nz0;
+  double* sval = mi + nr * dim;
+  int* scol = reinterpret_cast<int*>(sval + nnz);
+  int* srow = scol + nnz;
+  for (int k = tid; k < nnz; k += CG2_THR) { sval[k] = val[nz0 + k]; scol[k] = M.col[nz0 + k]; }
+  for (int i = tid; i <= nr; i += CG2_THR) srow[i] = M.rowptr[r0 + i] - nz0;
+  __syncthreads();
+  // node-block Jacobi: invert the free part of each dim x dim diagonal block
+  for (int nd = nd0 + tid; nd < nd1; nd += CG2_THR) {
+    double a[3][3] = {}, inv[3][3] = {};
+    bool fr[3] = {false, false, false};
+    for (int ci = 0; ci < dim; ++ci) {
+      const int row = nd * dim + ci;
+      fr[ci] = !M.dmask[row];
+      for (int k = srow[row - r0]; k < srow[row - r0 + 1]; ++k) {
+        const int cc = scol[k] - nd * dim;
+        if (cc >= 0 && cc < dim) a[ci][cc] = sval[k];
+      }
+    }
+    for (int ci = 0; ci < 3; ++ci)
+      for (int cj = 0; cj < 3; ++cj)
+        if (ci >= dim || cj >= dim || !fr[ci] || !fr[cj]) a[ci][cj] = (ci == cj) ? 1.0 : 0.0;
+    const double det = a[0][0] * (a[1][1] * a[2][2] - a[1][2] * a[2][1]) -
+                       a[0][1] * (a[1][0] * a[2][2] - a[1][2] * a[2][0]) +
+                       a[0][2] * (a[1][0] * a[2][1] - a[1][1] * a[2][0]);
+    inv[0][0] = (a[1][1] * a[2][2] - a[1][2] * a[2][1]) / det;
+    inv[0][1] = (a[0][2] * a[2][1] - a[0][1] * a[2][2]) / det;
+    inv[0][2] = (a[0][1] * a[1][2] - a[0][2] * a[1][1]) / det;
+    inv[1][0] = (a[1][2] * a[2][0] - a[1][0] * a[2][2]) / det;
+    inv[1][1] = (a[0][0] * a[2][2] - a[0][2] * a[2][0]) / det;
+    inv[1][2] = (a[0][2] * a[1][0] - a[0][0] * a[1][2]) / det;
+    inv[2][0] = (a[1][0] * a[2][1] - a[1][1] * a[2][0]) / det;
+    inv[2][1] = (a[0][1] * a[2][0] - a[0][0] * a[2][1]) / det;
+    inv[2][2] = (a[0][0] * a[1][1] - a[0][1] * a[1][0]) / det;
+    for (int ci = 0; ci < dim; ++ci)
+      for (int cj = 0; cj < dim; ++cj)
+        mi[((nd - nd0) * dim + ci) * dim + cj] = (fr[ci] && fr[cj]) ? inv[ci][cj] : 0.0;
+  }
+  for (int i = tid; i < nr; i += CG2_THR) {
+    const int gi = r0 + i;
+    x[i] = 0.0;
+    r[i] = M.dmask[gi] ? 0.0 : b[gi];
+  }
+  cl.sync();  // every CTA of the cluster is running before the first DSMEM store
+
+  // z = M^-1 r on the local rows, scattered into every CTA's copy; returns (r.z, r.r) partials
+  auto precond_publish = [&](double* part) {
+    double rz = 0.0, rr = 0.0;
+    for (int i = tid; i < nr; i += CG2_THR) {
+      const int nl = i / dim, ci = i % dim;
+      double z = 0.0;
+      for (int cj = 0; cj < dim; ++cj) z += mi[i * dim + cj] * r[nl * dim + cj];
+      rz += r[i] * z;
+      rr += r[i] * r[i];
+      for (int t = 0; t < G; ++t) cl.map_shared_rank(zf, t)[r0 + i] = z;
+      (void)ci;
+    }
+    part[0] = rz;
+    part[1] = rr;
+  };
+  // w = A z (local rows, free DOFs only); returns the (z.w) partial
+  auto spmv = [&]() {
+    double zw = 0.0;
+    for (int i = tid; i < nr; i += CG2_THR) {
+      double s0 = 0.0, s1 = 0.0;
+      if (!M.dmask[r0 + i]) {
+        int k = srow[i];
+        const int ke = srow[i + 1];
+        for (; k + 1 < ke; k += 2) {
+          s0 += sval[k] * zf[scol[k]];
+          s1 += sval[k + 1] * zf[scol[k + 1]];
+        }
+        if (k < ke) s0 += sval[k] * zf[scol[k]];
+      }
+      const double wi = s0 + s1;
+      w[i] = wi;
+      zw += zf[r0 + i] * wi;
+    }
+    return zw;
+  };
+
+  double v[3];
+  precond_publish(v);
+  cg2_publish(cl, slotsA, 2, v, wred);
+  cl.sync();
+  double gam = cg2_sum(slotsA, 0, G), rr = cg2_sum(slotsA, 1, G);
+  const double bnorm = sqrt(rr);
+  int it = 0, status = 0;
+  if (bnorm > 0.0) {
+    v[0] = spmv();
+    cg2_publish(cl, slotsB, 1, v, wred);
+    cl.sync();
+    double del = cg2_sum(slotsB, 0, G);
+    if (!(del > 0.0)) status = 6;
+    double alpha = gam / del;
+    for (int i = tid; i < nr; i += CG2_THR) { p[i] = zf[r0 + i]; sv[i] = w[i]; }
+    for (it = 1; it <= max_iter && status == 0; ++it) {
+      for (int i = tid; i < nr; i += CG2_THR) {
+        x[i] += alpha * p[i];
+        r[i] -= alpha * sv[i];
+      }
+      __syncthreads();  // r complete before the block preconditioner mixes components
+      precond_publish(v);
+      cg2_publish(cl, slotsA, 2, v, wred);
+      cl.sync();
+      const double gn = cg2_sum(slotsA, 0, G);
+      rr = cg2_sum(slotsA, 1, G);
+      if (sqrt(rr) <= rtol * bnorm) break;
+      v[0] = spmv();
+      cg2_publish(cl, slotsB, 1, v, wred);
+      cl.sync();
+      del = cg2_sum(slotsB, 0, G);
+      const double beta = gn / gam;
+      const double den = del - beta * gn / alpha;
+      if (!(den > 0.0)) { status = 6; break; }
+      alpha = gn / den;
+      gam = gn;
+      for (int i = tid; i < nr; i += CG2_THR) {
+        p[i] = zf[r0 + i] + beta * p[i];
+        sv[i] = w[i] + beta * sv[i];
+      }
+    }
+    if (status == 0 && it > max_iter) { status = 5; it = max_iter; }
+  }
+  for (int i = tid; i < nr; i += CG2_THR) {
+    const int gi = r0 + i;
+    xout[gi] = M.dmask[gi] ? scale * M.dval[gi] : x[i];
+  }
+  if (g == 0 && tid == 0) {
+    st->iterations = it;
+    st->status = status;
+    st->rel_residual = bnorm > 0.0 ? sqrt(rr) / bnorm : 0.0;
+    st->rhs_norm = bnorm;
+  }
+  cl.sync();  // no CTA exits while others may still write its shared memory
+}
+
+void cg2_slice_sizes(const MacroDev& M, const int* host_rowptr, int G, int* max_nr, int* max_nnz) {
+  *max_nr = *max_nnz = 0;
+  for (int g = 0; g < G; ++g) {  // node-aligned partition, as in k_macro_cg_cluster2
+    const int nd0 = (int)((long)M.n_nodes * g / G), nd1 = (int)((long)M.n_nodes * (g + 1) / G);
+    *max_nr = std::max(*max_nr, (nd1 - nd0) * M.dim);
+    *max_nnz = std::max(*max_nnz, host_rowptr[nd1 * M.dim] - host_rowptr[nd0 * M.dim]);
+  }
+}
+
+bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const double* val, const double* rhs,
+                              double scale, double rtol, int max_iter, double* x, CgState* st, cudaStream_t s) {
+  static int cached_G = -1;
+  for (int gi = 0; gi < 2; ++gi) {
+    const int G = gi == 0 ? 16 : 8;
+    if (cached_G > 0 && G != cached_G) continue;
+    const int max_nr = slice[gi][0], max_nnz = slice[gi][1];
+    const size_t sm = (size_t)(6 * CGC_MAXG + 96 + M.ndof + 5 * max_nr + max_nr * M.dim) * 8 +
+                      (size_t)max_nnz * 12 + (size_t)(max_nr + 1) * 4 + 64;
+    if (sm > 220 * 1024) continue;
+    cudaFuncSetAttribute(k_macro_cg_cluster2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (G > 8) cudaFuncSetAttribute(k_macro_cg_cluster2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G, 1, 1);
+    cfg.blockDim = dim3(CG2_THR, 1, 1);
+    cfg.dynamicSmemBytes = sm;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, k_macro_cg_cluster2, &cfg) != cudaSuccess || ncl < 1) {
+      cudaGetLastError();
+      continue;
+    }
+    cudaError_t e = cudaLaunchKernelEx(&cfg, k_macro_cg_cluster2, M, val, rhs, scale, rtol, max_iter, x, st);
     if (e == cudaSuccess) {
       cached_G = G;
       return true;
