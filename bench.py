@@ -160,6 +160,47 @@ def cpu_model():
     return "unknown"
 
 
+# ----------------------------------------------------------------------------- scaled SpMV
+def spmv_scaled(C_tile, nel: int = 2048, reps: int = 20):
+    """K6 SpMV roofline on a scaled macro mesh (the config macro matrices are L2-resident, so the
+    HBM-bound SpMV is measured on a 2-D nel x nel Q1 mesh): assemble K from C_eff tiled over all
+    macro qps, then time reps launches of y = K_FF x with CUDA events on the launching stream."""
+    import torch
+
+    from paper_2312_12771_b200 import workloads as W
+    from paper_2312_12771_b200.hom import Homogenizer
+    t0 = time.perf_counter()
+    wl = W.config2(nel=nel, r=2)
+    h = Homogenizer.from_workload(wl, rve_range=(0, 4), check_info=False)  # one element's RVEs condensed
+    t_setup = time.perf_counter() - t0
+    C = C_tile[:1].expand(wl.n_rve, -1, -1).contiguous()
+    h.macro_assemble(C)
+    g = torch.Generator(device="cuda").manual_seed(12771)
+    x = torch.rand(wl.n_dof, dtype=torch.float64, device="cuda", generator=g)
+    x[torch.as_tensor(wl.dir_dof, device="cuda", dtype=torch.long)] = 0.0
+    y = h.empty(wl.n_dof)
+    for _ in range(3):
+        h.macro_spmv(x, y)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(reps):
+        h.macro_spmv(x, y)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / reps
+    nnz, n = h.sizes.macro_nnz, wl.n_dof
+    algo = nnz * 12 + n * (4 + 8 + 8 + 1)  # CSR values + columns, rowptr, y, x (gathered once, L2), Dirichlet mask
+    peak = (load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}).get("hbm_gbs", 6447.8)
+    out = {"kernel": "k_spmv (K6, 8 lanes per CSR row)", "macro_mesh": f"{nel}x{nel} Q1", "macro_dof": n, "nnz": nnz,
+           "ms_per_launch": ms, "bytes_per_launch": algo, "GBps": algo / (ms * 1e-3) / 1e9,
+           "peak_GBps": peak, "frac": algo / (ms * 1e-3) / 1e9 / peak, "setup_s": t_setup,
+           "values": "config-2 C_eff tiled over all macro Gauss points"}
+    h.close()
+    return out
+
+
 # ----------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -169,6 +210,7 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--spmv-nel", type=int, default=2048, help="scaled macro mesh of the K6 SpMV roofline (0: skip)")
     ap.add_argument("--tile-sparse", action="store_true",
                     help="factor only the symbolic tile fill of K_ff (SURVEY §8(f) 3) instead of every lower tile")
     args = ap.parse_args()
@@ -382,6 +424,14 @@ def main():
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "what": "hom_set_phases from pinned host + condense + macro solve + recovery + D2H of C_eff, u, w"},
     }
+    if world == 1 and args.spmv_nel > 0:
+        if m == 3:
+            C_tile = C
+        else:  # 2-D scaled mesh: plane-strain isotropic tangent (E = 1, nu = 0.3)
+            lam, mu = 0.3 / (1.3 * 0.4), 1.0 / 2.6
+            C_tile = torch.tensor([[[lam + 2 * mu, lam, 0.0], [lam, lam + 2 * mu, 0.0], [0.0, 0.0, mu]]],
+                                  dtype=torch.float64, device="cuda")
+        line["spmv_scaled"] = spmv_scaled(C_tile, args.spmv_nel)
     if world == 1 and not args.no_cpu_baseline:
         st, detail = oracle_step_time(wl)
         line["cpu_baseline"] = {"value": wl.n_rve / st, "unit": "tangents/s", "cores": detail["cores"],

@@ -196,6 +196,12 @@ int hom_condense(hom_ctx* ctx, const double* d_kin, double* d_C_eff, double* d_P
 int hom_macro_solve(hom_ctx* ctx, const double* d_D, const double* d_S, double dirichlet_scale,
                     double* d_x, hom_solve_info* info, void* stream);
 
+/* Assemble the macro stiffness K = sum_qp eta B^T D_b B (K5) into
+ * the context's CSR matrix (node-block pattern over all DOFs) without solving.  Enqueue only. */
+int hom_macro_assemble(hom_ctx* ctx, const double* d_D, void* stream);
+/* d_y [n_macro_dof] = K_FF d_x on the free rows of the last assembled macro matrix, 0 on the
+ * Dirichlet rows (K6, the SpMV of the macro CG).  Enqueue only. */
+int hom_macro_spmv(hom_ctx* ctx, const double* d_x, double* d_y, void* stream);
 /* ||R_F||_2 with R = sum_qp eta B^T S_b - f_body (macro residual, eq:linSys); synchronises. */
 int hom_macro_residual_norm(hom_ctx* ctx, const double* d_S, double* norm, void* stream);
 

@@ -336,7 +336,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
   const int nt = R.nt, NT = R.NT;
   double* Kb = Kt + (long)bl * R.nslot * TILE_ELEMS;
   double* Yb = Y + (long)bl * NT * RHSW;
-  double* Xb = X + (long)b * NT * RHSW;
+  double* Xb = X + (long)(b - R.xb0) * NT * RHSW;  // X holds the context's local RVE range only
 
   if (tid == 0) sFail[0] = 0;
   double Sacc = 0.0;  // thread (i,j) = (tid>>3, tid&7), tid < 64: sum_r Y[r][i] Y[r][j]

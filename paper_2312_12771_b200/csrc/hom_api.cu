@@ -35,6 +35,7 @@ struct hom_ctx {
   int *info = nullptr, *jflag = nullptr, *first_fail = nullptr;
   // macro
   double *val = nullptr, *diag = nullptr, *rhs = nullptr, *cgwork = nullptr, *Rfree = nullptr, *scal = nullptr;
+  double *cgl_sc = nullptr, *cgl_part = nullptr;  // grid-wide PCG scalars / block partials
   CgState* cgst = nullptr;
   size_t phase_bytes = 0, mat_bytes = 0;
   int max_slice_nnz = 0;  // largest CSR slice of a 8-CTA cluster partition (CG smem sizing)
@@ -594,7 +595,8 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
     c->Pq = dalloc<double>(c, (size_t)chunk * R.ne * nq * 4, &rc);
     c->w = dalloc<double>(c, (size_t)c->B * R.npad, &rc);
   }
-  c->X = dalloc<double>(c, (size_t)c->B * R.NT * hom::RHSW, &rc);
+  c->X = dalloc<double>(c, (size_t)(c->b_hi - c->b_lo) * R.NT * hom::RHSW, &rc);  // local range only
+  c->R.xb0 = c->b_lo;
   c->rfn = dalloc<double>(c, c->B, &rc);
   c->kin = dalloc<double>(c, (size_t)c->B * c->m, &rc);
   c->info = dalloc<int>(c, c->B, &rc);
@@ -606,6 +608,8 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   c->Rfree = dalloc<double>(c, M.ndof, &rc);
   c->cgwork = dalloc<double>(c, (size_t)4 * M.ndof, &rc);
   c->scal = dalloc<double>(c, 4, &rc);
+  c->cgl_sc = dalloc<double>(c, 16, &rc);
+  c->cgl_part = dalloc<double>(c, 2 * 592 * 4, &rc);
   c->cgst = dalloc<CgState>(c, 1, &rc);
   if (rc) return rc;
   if (c->finite) cudaMemsetAsync(c->w, 0, sizeof(double) * (size_t)c->B * R.npad, s);
@@ -707,16 +711,38 @@ int hom_condense(hom_ctx* c, const double* d_kin, double* d_C_eff, double* d_P_e
   return HOM_OK;
 }
 
+int hom_macro_assemble(hom_ctx* c, const double* d_D, void* stream) {
+  if (!c || !d_D) return set_err(c, HOM_ERR_INVALID_ARG, "hom_macro_assemble: NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  run(c, HOM_PROF_MACRO_ASSEMBLE, s, [&] { hom::launch_macro_assemble(c->M, d_D, c->val, c->diag, s); });
+  return check_cuda(c, cudaGetLastError(), "hom_macro_assemble");
+}
+
+int hom_macro_spmv(hom_ctx* c, const double* d_x, double* d_y, void* stream) {
+  if (!c || !d_x || !d_y) return set_err(c, HOM_ERR_INVALID_ARG, "hom_macro_spmv: NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  run(c, HOM_PROF_CG, s, [&] { hom::launch_spmv(c->M, c->val, d_x, d_y, s); });
+  return check_cuda(c, cudaGetLastError(), "hom_macro_spmv");
+}
+
 int hom_macro_solve(hom_ctx* c, const double* d_D, const double* d_S, double scale, double* d_x,
                     hom_solve_info* info, void* stream) {
   if (!c || !d_D || !d_x) return set_err(c, HOM_ERR_INVALID_ARG, "hom_macro_solve: NULL");
   cudaStream_t s = (cudaStream_t)stream;
   run(c, HOM_PROF_MACRO_ASSEMBLE, s, [&] { hom::launch_macro_assemble(c->M, d_D, c->val, c->diag, s); });
   run(c, HOM_PROF_MACRO_ASSEMBLE, s, [&] { hom::launch_macro_rhs(c->M, c->val, d_S, scale, c->rhs, nullptr, s); });
+  // macro PCG: one cluster with the matrix in shared memory when it fits (config sizes),
+  // else grid-wide kernels (scaled meshes); the cluster kernel with a global CSR as the last resort
   run(c, HOM_PROF_CG, s, [&] {
-    if (!hom::launch_macro_cg_cluster2(c->M, c->cg2_slice, c->val, c->rhs, scale, c->opt.cg_rtol,
-                                       c->opt.cg_max_iter, d_x, c->cgst, s) &&
-        !hom::launch_macro_cg_cluster(c->M, c->max_slice_nnz, c->val, c->diag, c->rhs, scale, c->opt.cg_rtol,
+    if (hom::launch_macro_cg_cluster2(c->M, c->cg2_slice, c->val, c->rhs, scale, c->opt.cg_rtol,
+                                      c->opt.cg_max_iter, d_x, c->cgst, s))
+      return;
+    if (c->M.ndof >= 32768) {
+      hom::launch_macro_cg_large(c->M, c->val, c->diag, c->rhs, scale, c->opt.cg_rtol, c->opt.cg_max_iter, d_x,
+                                 c->cgwork, c->cgl_sc, c->cgl_part, c->cgst, s);
+      return;
+    }
+    if (!hom::launch_macro_cg_cluster(c->M, c->max_slice_nnz, c->val, c->diag, c->rhs, scale, c->opt.cg_rtol,
                                       c->opt.cg_max_iter, d_x, c->cgwork, c->cgst, s))
       hom::launch_macro_cg(c->M, c->val, c->diag, c->rhs, scale, c->opt.cg_rtol, c->opt.cg_max_iter, d_x,
                            c->cgwork, c->cgst, s);

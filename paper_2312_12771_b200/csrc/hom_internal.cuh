@@ -52,6 +52,7 @@ struct RveDev {
   const uint8_t* g_nz;
   const int* tslot;
   int nslot;                      // pool slots (64x64 tiles) per RVE
+  int xb0;                        // first RVE of the influence store X (the context's local range)
 };
 
 struct MacroDev {
@@ -105,6 +106,10 @@ bool launch_macro_cg_cluster(const MacroDev& M, int max_slice_nnz, const double*
                              const double* rhs, double scale, double rtol, int max_iter, double* x, double* p,
                              CgState* st, cudaStream_t s);
 void launch_norm(const double* v, int n, double* out, cudaStream_t s);
+void launch_spmv(const MacroDev& M, const double* val, const double* x, double* y, cudaStream_t s);
+void launch_macro_cg_large(const MacroDev& M, const double* val, const double* diag, const double* rhs,
+                           double scale, double rtol, int max_iter, double* xout, double* work, double* sc,
+                           double* part, CgState* st, cudaStream_t s);
 void cg2_slice_sizes(const MacroDev& M, const int* host_rowptr, int G, int* max_nr, int* max_nnz);
 bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const double* val, const double* rhs,
                               double scale, double rtol, int max_iter, double* x, CgState* st, cudaStream_t s);

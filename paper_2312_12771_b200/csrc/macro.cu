@@ -719,6 +719,203 @@ bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const do
   return false;
 }
 
+// ---------------------------------------------------------------- K6 SpMV + large-problem PCG
+// For macro problems too large for one cluster's shared memory (scaled meshes, multi-GPU
+// weak scaling): grid-wide kernels.  K6 (k_spmv) streams the CSR matrix once per call --
+// HBM-bound, 8 lanes per row (coalesced 64 B of values + 32 B of columns per step), the
+// gathered x stays in L2.  Dot products are reduced per block and then in a fixed order by
+// one block (deterministic); the PCG scalars never leave the device; the host checks
+// convergence every CGL_CHECK iterations.
+constexpr int SPMV_THR = 256, SPMV_LPR = 8, CGL_BLOCKS = 592, CGL_CHECK = 16;
+
+// y = A x on the free rows (Dirichlet rows -> 0); optional partial sums of x.y per block.
+__global__ void __launch_bounds__(SPMV_THR) k_spmv(MacroDev M, const double* __restrict__ val,
+                                                   const double* __restrict__ x, double* __restrict__ y,
+                                                   double* __restrict__ part) {
+  const int lane = threadIdx.x & (SPMV_LPR - 1);
+  const long row0 = ((long)blockIdx.x * SPMV_THR + threadIdx.x) / SPMV_LPR;
+  const long stride = (long)gridDim.x * SPMV_THR / SPMV_LPR;
+  // warp-uniform trip count: every lane reaches the shuffles (rows of a warp are consecutive)
+  const long wrow0 = row0 - (threadIdx.x & 31) / SPMV_LPR;
+  double dot = 0.0;
+  for (long wr = wrow0, row = row0; wr < M.ndof; wr += stride, row += stride) {
+    double s = 0.0;
+    if (row < M.ndof && !M.dmask[row]) {
+      const int k1 = __ldg(M.rowptr + row + 1);
+      for (int k = __ldg(M.rowptr + row) + lane; k < k1; k += SPMV_LPR)
+        s += __ldcs(val + k) * __ldg(x + __ldcs(M.col + k));
+    }
+#pragma unroll
+    for (int o = SPMV_LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0 && row < M.ndof) {
+      y[row] = s;
+      dot += s * x[row];
+    }
+  }
+  if (part) {
+    __shared__ double red[SPMV_THR / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = dot;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < SPMV_THR / 32; ++w) t += red[w];
+      part[blockIdx.x] = t;
+    }
+  }
+}
+void launch_spmv(const MacroDev& M, const double* val, const double* x, double* y, cudaStream_t s) {
+  k_spmv<<<CGL_BLOCKS * 4, SPMV_THR, 0, s>>>(M, val, x, y, nullptr);
+}
+
+// scalars sc: [0] rz, [1] alpha, [2] beta, [3] rr, [4] bnorm^2, [5] status
+__global__ void k_cgl_reduce(const double* __restrict__ part, int nb, int nv, double* __restrict__ out) {
+  __shared__ double red[4][32];
+  for (int v = 0; v < nv; ++v) {
+    double t = 0.0;
+    for (int i = threadIdx.x; i < nb; i += 32) t += part[v * nb + i];  // fixed assignment and order
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (threadIdx.x == 0) red[v][0] = t;
+  }
+  __syncwarp();
+  if (threadIdx.x == 0)
+    for (int v = 0; v < nv; ++v) out[v] = red[v][0];
+}
+
+// init: x = 0, r = b (free), z = D^-1 r, p = z; partials of (r.z, r.r)
+__global__ void k_cgl_init(MacroDev M, const double* __restrict__ b, const double* __restrict__ diag,
+                           double* __restrict__ x, double* __restrict__ r, double* __restrict__ p,
+                           double* __restrict__ part) {
+  double rz = 0.0, rr = 0.0;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < M.ndof; i += (long)gridDim.x * blockDim.x) {
+    const bool d = M.dmask[i];
+    const double ri = d ? 0.0 : b[i], zi = d ? 0.0 : ri / diag[i];
+    x[i] = 0.0;
+    r[i] = ri;
+    p[i] = zi;
+    rz += ri * zi;
+    rr += ri * ri;
+  }
+  __shared__ double red[2][SPMV_THR / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    rz += __shfl_xor_sync(0xffffffffu, rz, o);
+    rr += __shfl_xor_sync(0xffffffffu, rr, o);
+  }
+  if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = rz; red[1][threadIdx.x >> 5] = rr; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, c = 0.0;
+    for (int w = 0; w < SPMV_THR / 32; ++w) { a += red[0][w]; c += red[1][w]; }
+    part[blockIdx.x] = a;
+    part[gridDim.x + blockIdx.x] = c;
+  }
+}
+
+// alpha = rz / pq (sc[1]); breakdown -> status 6
+__global__ void k_cgl_alpha(double* sc, const double* pq) {
+  if (!(pq[0] > 0.0)) sc[5] = 6.0;
+  sc[1] = sc[0] / pq[0];
+}
+
+// x += a p; r -= a q; z = D^-1 r (into q); partials of (r.z, r.r)
+__global__ void k_cgl_update(MacroDev M, const double* __restrict__ diag, const double* __restrict__ sc,
+                             double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                             double* __restrict__ q, double* __restrict__ part) {
+  const double a = sc[1];
+  double rz = 0.0, rr = 0.0;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < M.ndof; i += (long)gridDim.x * blockDim.x) {
+    if (M.dmask[i]) { q[i] = 0.0; continue; }
+    x[i] += a * p[i];
+    const double ri = r[i] - a * q[i];
+    r[i] = ri;
+    const double zi = ri / diag[i];
+    q[i] = zi;
+    rz += ri * zi;
+    rr += ri * ri;
+  }
+  __shared__ double red[2][SPMV_THR / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    rz += __shfl_xor_sync(0xffffffffu, rz, o);
+    rr += __shfl_xor_sync(0xffffffffu, rr, o);
+  }
+  if ((threadIdx.x & 31) == 0) { red[0][threadIdx.x >> 5] = rz; red[1][threadIdx.x >> 5] = rr; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a2 = 0.0, c = 0.0;
+    for (int w = 0; w < SPMV_THR / 32; ++w) { a2 += red[0][w]; c += red[1][w]; }
+    part[blockIdx.x] = a2;
+    part[gridDim.x + blockIdx.x] = c;
+  }
+}
+
+// beta = rz_new / rz; rz = rz_new; rr (sc[3])
+__global__ void k_cgl_beta(double* sc, const double* red) {
+  sc[2] = red[0] / sc[0];
+  sc[0] = red[0];
+  sc[3] = red[1];
+}
+
+// p = z + beta p
+__global__ void k_cgl_p(MacroDev M, const double* __restrict__ sc, const double* __restrict__ z,
+                        double* __restrict__ p) {
+  const double be = sc[2];
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < M.ndof; i += (long)gridDim.x * blockDim.x)
+    p[i] = z[i] + be * p[i];
+}
+
+__global__ void k_cgl_final(MacroDev M, const double* __restrict__ x, double scale, double* __restrict__ xout) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < M.ndof; i += (long)gridDim.x * blockDim.x)
+    xout[i] = M.dmask[i] ? scale * M.dval[i] : x[i];
+}
+
+// work: [x | r | p | q] (4 n) ; sc: >= 6 + 4 doubles; part: >= 2 * CGL_BLOCKS * 4 doubles
+void launch_macro_cg_large(const MacroDev& M, const double* val, const double* diag, const double* rhs,
+                           double scale, double rtol, int max_iter, double* xout, double* work, double* sc,
+                           double* part, CgState* st, cudaStream_t s) {
+  const long n = M.ndof;
+  double *x = work, *r = work + n, *p = work + 2 * n, *q = work + 3 * n;
+  const int nbv = CGL_BLOCKS, nbs = CGL_BLOCKS * 4;
+  double* red = sc + 6;
+  cudaMemsetAsync(sc, 0, 6 * sizeof(double), s);
+  k_cgl_init<<<nbv, SPMV_THR, 0, s>>>(M, rhs, diag, x, r, p, part);
+  k_cgl_reduce<<<1, 32, 0, s>>>(part, nbv, 2, red);
+  double h[2];
+  cudaMemcpyAsync(h, red, 2 * sizeof(double), cudaMemcpyDeviceToHost, s);
+  cudaStreamSynchronize(s);
+  cudaMemcpyAsync(sc, red, sizeof(double), cudaMemcpyDeviceToDevice, s);  // rz
+  const double bnorm = sqrt(h[1]);
+  int it = 0, status = 0;
+  double rr = h[1];
+  if (bnorm > 0.0) {
+    for (it = 1; it <= max_iter; ++it) {
+      k_spmv<<<nbs, SPMV_THR, 0, s>>>(M, val, p, q, part);
+      k_cgl_reduce<<<1, 32, 0, s>>>(part, nbs, 1, red + 2);
+      k_cgl_alpha<<<1, 1, 0, s>>>(sc, red + 2);
+      k_cgl_update<<<nbv, SPMV_THR, 0, s>>>(M, diag, sc, x, r, p, q, part);
+      k_cgl_reduce<<<1, 32, 0, s>>>(part, nbv, 2, red);
+      k_cgl_beta<<<1, 1, 0, s>>>(sc, red);
+      k_cgl_p<<<nbv, SPMV_THR, 0, s>>>(M, sc, q, p);
+      if (it % CGL_CHECK == 0 || it == max_iter) {
+        double hs[6];
+        cudaMemcpyAsync(hs, sc, 6 * sizeof(double), cudaMemcpyDeviceToHost, s);
+        cudaStreamSynchronize(s);
+        rr = hs[3];
+        if (hs[5] != 0.0) { status = 6; break; }
+        if (sqrt(rr) <= rtol * bnorm) break;
+      }
+    }
+    if (status == 0 && it > max_iter) { status = 5; it = max_iter; }
+  }
+  k_cgl_final<<<nbv, SPMV_THR, 0, s>>>(M, x, scale, xout);
+  CgState h_st{it, status, bnorm > 0.0 ? sqrt(rr) / bnorm : 0.0, bnorm};
+  cudaMemcpyAsync(st, &h_st, sizeof(h_st), cudaMemcpyHostToDevice, s);
+  cudaStreamSynchronize(s);
+}
+
 // ---------------------------------------------------------------- K8 recovery
 // accumulate = 0: w = -X[:, :m] kin            (small strain, kin = eps)
 // accumulate = 1: w += -(X[:, m] + X[:, :m] kin) (finite strain, kin = grad du)
@@ -728,7 +925,7 @@ __global__ void k_recover(RveDev R, int b0, int nb, const double* __restrict__ X
   if (t >= (long)nb * R.npad) return;
   int b = b0 + (int)(t / R.npad), i = (int)(t % R.npad);
   t += (long)b0 * R.npad;
-  const double* xr = X + ((long)b * R.NT + i) * RHSW;
+  const double* xr = X + ((long)(b - R.xb0) * R.NT + i) * RHSW;
   const double* kb = kin + (long)b * R.m;
   double v = 0.0;
   for (int k = 0; k < R.m; ++k) v += xr[k] * kb[k];

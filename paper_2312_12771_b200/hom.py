@@ -23,7 +23,7 @@ STATUS = {0: "HOM_OK", 1: "HOM_ERR_INVALID_ARG", 2: "HOM_ERR_MESH", 3: "HOM_ERR_
           7: "HOM_ERR_CUDA", 8: "HOM_ERR_OOM"}
 
 # every symbol include/hom.h declares (checked by tests/test_abi.py)
-EXPORTS = ["hom_setup", "hom_get_sizes", "hom_get_work", "hom_macro_kinematics", "hom_condense", "hom_macro_solve",
+EXPORTS = ["hom_setup", "hom_get_sizes", "hom_get_work", "hom_macro_assemble", "hom_macro_spmv", "hom_macro_kinematics", "hom_condense", "hom_macro_solve",
            "hom_macro_residual_norm", "hom_recover_fluctuations", "hom_newton_update", "hom_set_fluctuations",
            "hom_get_fluctuations", "hom_micro_residual_max", "hom_set_phases", "hom_launch_count",
            "hom_profile_enable", "hom_profile_read", "hom_last_error", "hom_destroy"]
@@ -111,6 +111,8 @@ def lib(build_if_missing: bool = True):
         L.hom_condense.argtypes = [P, P, P, P, P, P]
         L.hom_macro_solve.argtypes = [P, P, P, D, P, ctypes.POINTER(SolveInfo), P]
         L.hom_macro_residual_norm.argtypes = [P, P, ctypes.POINTER(ctypes.c_double), P]
+        L.hom_macro_assemble.argtypes = [P, P, P]
+        L.hom_macro_spmv.argtypes = [P, P, P, P]
         L.hom_recover_fluctuations.argtypes = [P, P, P, P]
         L.hom_newton_update.argtypes = [P, P, P, P]
         L.hom_set_fluctuations.argtypes = [P, P, P]
@@ -253,6 +255,14 @@ class Homogenizer:
         self._check(lib().hom_macro_solve(self.h, self._ptr(D), self._ptr(S), float(scale), self._ptr(x),
                                           ctypes.byref(info), self._stream()), "hom_macro_solve")
         return x, info
+
+    def macro_assemble(self, D):
+        self._check(lib().hom_macro_assemble(self.h, self._ptr(D), self._stream()), "hom_macro_assemble")
+
+    def macro_spmv(self, x, y=None):
+        y = self.empty(self.n_dof) if y is None else y
+        self._check(lib().hom_macro_spmv(self.h, self._ptr(x), self._ptr(y), self._stream()), "hom_macro_spmv")
+        return y
 
     def macro_residual_norm(self, S):
         v = ctypes.c_double()

@@ -289,3 +289,37 @@ def test_rve_range_shards_reassemble_bitwise(torch_cuda):
         w = h.recover(u)
         assert np.array_equal(w[lo:hi].cpu().numpy(), full["w"][lo:hi])
         assert h.sizes.rve_begin == lo and h.sizes.rve_count == hi - lo
+
+
+# ------------------------------------------------------------------ K6 SpMV and the grid-wide PCG (scaled meshes)
+def test_macro_spmv_matches_oracle_operator(torch_cuda):
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = W.config2(nel=8, r=4)
+    h = Homogenizer.from_workload(wl)
+    C = h.condense()
+    h.macro_assemble(C)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(wl.n_dof)
+    x[wl.dir_dof] = 0.0
+    y = h.macro_spmv(torch_cuda.tensor(x, device="cuda")).cpu().numpy()
+    Cn = C.cpu().numpy()
+    Kx = oracle.macro_residual(2, wl.nel, np.einsum("bij,bj->bi", Cn, oracle.macro_kin(2, wl.nel, x)), None)
+    free = np.ones(wl.n_dof, bool)
+    free[wl.dir_dof] = False
+    assert rel(y[free], Kx[free]) <= 1e-13
+    assert np.all(y[~free] == 0.0)
+
+
+def test_large_macro_grid_pcg_matches_direct_solve(torch_cuda):
+    """ndof >= 32768 selects the grid-wide PCG (k_spmv + deterministic block reductions)."""
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = W.config2(nel=128, r=2)
+    h = Homogenizer.from_workload(wl)
+    assert wl.n_dof >= 32768
+    C = h.condense()
+    u, info = h.macro_solve(C)
+    assert info.rel_residual <= 1e-13
+    u_direct = oracle.macro_solve(2, wl.nel, C.cpu().numpy(), wl.dir_dof, wl.dir_val, body=wl.body)
+    assert rel(u.cpu().numpy(), u_direct) <= TOL_U
+    u2, _ = h.macro_solve(C)
+    assert np.array_equal(u.cpu().numpy(), u2.cpu().numpy())  # deterministic reductions
