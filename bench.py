@@ -193,7 +193,7 @@ def spmv_scaled(C_tile, nel: int = 2048, reps: int = 20):
     nnz, n = h.sizes.macro_nnz, wl.n_dof
     algo = nnz * 12 + n * (4 + 8 + 8 + 1)  # CSR values + columns, rowptr, y, x (gathered once, L2), Dirichlet mask
     peak = (load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}).get("hbm_gbs", 6447.8)
-    out = {"kernel": "k_spmv (K6, 8 lanes per CSR row)", "macro_mesh": f"{nel}x{nel} Q1", "macro_dof": n, "nnz": nnz,
+    out = {"kernel": "k_spmv (K6, 4 lanes per CSR row, batched loads)", "macro_mesh": f"{nel}x{nel} Q1", "macro_dof": n, "nnz": nnz,
            "ms_per_launch": ms, "bytes_per_launch": algo, "GBps": algo / (ms * 1e-3) / 1e9,
            "peak_GBps": peak, "frac": algo / (ms * 1e-3) / 1e9 / peak, "setup_s": t_setup,
            "values": "config-2 C_eff tiled over all macro Gauss points"}

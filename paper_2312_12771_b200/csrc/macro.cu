@@ -726,9 +726,14 @@ bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const do
 // gathered x stays in L2.  Dot products are reduced per block and then in a fixed order by
 // one block (deterministic); the PCG scalars never leave the device; the host checks
 // convergence every CGL_CHECK iterations.
-constexpr int SPMV_THR = 256, SPMV_LPR = 8, CGL_BLOCKS = 592, CGL_CHECK = 16;
+constexpr int SPMV_THR = 256, SPMV_LPR = 4, CGL_BLOCKS = 592, CGL_CHECK = 16;
 
 // y = A x on the free rows (Dirichlet rows -> 0); optional partial sums of x.y per block.
+// Latency-bound by construction (row -> rowptr -> col -> x are dependent loads), so the kernel
+// keeps many bytes in flight: every lane issues all (up to SPMV_PASS per pass) value/column
+// loads of its row before any gather, and the next row's rowptr/mask are prefetched under the
+// current row.  SPMV_LPR lanes per row.
+constexpr int SPMV_PASS = 5;
 __global__ void __launch_bounds__(SPMV_THR) k_spmv(MacroDev M, const double* __restrict__ val,
                                                    const double* __restrict__ x, double* __restrict__ y,
                                                    double* __restrict__ part) {
@@ -737,20 +742,47 @@ __global__ void __launch_bounds__(SPMV_THR) k_spmv(MacroDev M, const double* __r
   const long stride = (long)gridDim.x * SPMV_THR / SPMV_LPR;
   // warp-uniform trip count: every lane reaches the shuffles (rows of a warp are consecutive)
   const long wrow0 = row0 - (threadIdx.x & 31) / SPMV_LPR;
+  const long n = M.ndof;
   double dot = 0.0;
-  for (long wr = wrow0, row = row0; wr < M.ndof; wr += stride, row += stride) {
+  int kb = 0, ke = 0;
+  bool act = false;
+  if (row0 < n) {
+    kb = __ldg(M.rowptr + row0);
+    ke = __ldg(M.rowptr + row0 + 1);
+    act = !M.dmask[row0];
+  }
+  for (long wr = wrow0, row = row0; wr < n; wr += stride, row += stride) {
+    double v[SPMV_PASS];
+    int c[SPMV_PASS];
     double s = 0.0;
-    if (row < M.ndof && !M.dmask[row]) {
-      const int k1 = __ldg(M.rowptr + row + 1);
-      for (int k = __ldg(M.rowptr + row) + lane; k < k1; k += SPMV_LPR)
-        s += __ldcs(val + k) * __ldg(x + __ldcs(M.col + k));
+    int k = kb + lane;
+    const int kend = act ? ke : kb;
+#pragma unroll
+    for (int j = 0; j < SPMV_PASS; ++j) {  // all loads of the pass issued together
+      const int kk = k + j * SPMV_LPR;
+      v[j] = kk < kend ? __ldcs(val + kk) : 0.0;
+      c[j] = kk < kend ? __ldcs(M.col + kk) : 0;
+    }
+    const long nrow = row + stride;  // prefetch the next row's range under the gathers
+    int nkb = 0, nke = 0;
+    bool nact = false;
+    if (nrow < n) {
+      nkb = __ldg(M.rowptr + nrow);
+      nke = __ldg(M.rowptr + nrow + 1);
+      nact = !M.dmask[nrow];
     }
 #pragma unroll
+    for (int j = 0; j < SPMV_PASS; ++j) s += v[j] * __ldg(x + c[j]);
+    for (k += SPMV_PASS * SPMV_LPR; k < kend; k += SPMV_LPR) s += __ldcs(val + k) * __ldg(x + __ldcs(M.col + k));
+#pragma unroll
     for (int o = SPMV_LPR / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0 && row < M.ndof) {
+    if (lane == 0 && row < n) {
       y[row] = s;
       dot += s * x[row];
     }
+    kb = nkb;
+    ke = nke;
+    act = nact;
   }
   if (part) {
     __shared__ double red[SPMV_THR / 32];
