@@ -386,14 +386,16 @@ def main():
     cond_ms, cond_n = prof["condense"]
     per_launch = min(h.sizes.rve_chunk, B)
     flop_rve = work.flop_executed if args.tile_sparse else wl.flop_per_rve()
-    flop_launch = flop_rve * per_launch
-    n_cond = max(cond_n, 1)
-    achieved = flop_launch * n_cond / (cond_ms * 1e-3) / 1e12 if cond_ms > 0 else None
+    n_local = h.sizes.rve_count  # RVEs this rank condenses per step (all chunks)
+    achieved = flop_rve * n_local * args.steps / (cond_ms * 1e-3) / 1e12 if cond_ms > 0 else None
     peak, peak_src = fp64_peak()
     step_ms_total = sum(v[0] for v in prof.values())
     breakdown = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
                      "share": (v[0] / step_ms_total if step_ms_total else None)} for k, v in prof.items()}
     asm_ms = prof["rve_assemble"][0] / max(prof["rve_assemble"][1], 1)
+    tr = (load_json(os.path.join(ROOT, "profiles", "traffic.json")) or {}).get(
+        f"cfg{args.config}_{'tilesparse' if args.tile_sparse else 'dense'}")
+    traffic = tr["dram_bytes"] if tr and tr.get("rve_per_launch") == per_launch and world == 1 else None
     # K1 writes the structurally nonzero K_ff tiles + the K_fe / r_f block + <C> (+ <P>)
     asm_bytes_rve = work.a_tiles * 32768 + h.sizes.n_tiles * 64 * 8 * 8 + 2 * 64 * 8
     algo = (f"{flop_rve:.4g} executed DMMA flop/RVE for the tile structure ({work.g_tiles} tiles, {work.gemm_tiles} GEMM + "
@@ -407,9 +409,10 @@ def main():
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
         "roofline": {"bound": "tensor", "kernel": "k_condense (K2-K4 fused FP64 DMMA Cholesky + solves + Schur)",
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": (achieved / peak) if achieved else None, "traffic": None,
+                     "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_source": peak_src,
-                     "algorithmic": f"{algo} x {per_launch} RVEs per launch"},
+                     "algorithmic": f"{algo} x {n_local} RVEs per step ({max(cond_n, 1) // args.steps} launch(es) of "
+                                    f"<= {per_launch} RVEs)"},
         "fp64_tflops_condense": achieved,
         "macro_solve_ms": (prof["macro_assemble"][0] + prof["cg"][0]) / args.steps,
         "cg_iterations": statistics.median(cg_iters) if cg_iters else None,

@@ -9,6 +9,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--nel", type=int, default=0)
+ap.add_argument("--tile-sparse", action="store_true")
 args = ap.parse_args()
 
 import torch  # noqa: E402
@@ -17,7 +18,7 @@ from paper_2312_12771_b200 import workloads as W  # noqa: E402
 from paper_2312_12771_b200.hom import Homogenizer  # noqa: E402
 
 wl = W.make(args.config, **({"nel": args.nel} if args.nel else {}))
-h = Homogenizer.from_workload(wl)
+h = Homogenizer.from_workload(wl, tile_sparse=args.tile_sparse)
 for _ in range(args.steps):
     C = h.condense()
     u, info = h.macro_solve(C)
