@@ -70,6 +70,8 @@ typedef struct {
   const int32_t* dirichlet_dof;   /* host [n_dirichlet] */
   const double* dirichlet_value;  /* host [n_dirichlet] (total prescribed value) */
   const double* body_force;       /* host [dim] or NULL */
+  const double* nodal_force;      /* host [n_nodes*dim] or NULL: external nodal forces, e.g. the
+                                     consistent nodal loads of a surface traction on Gamma^sigma */
 } hom_macro_mesh;
 
 /* RVE mesh: an axis-aligned box meshed with Q1/hex8 elements whose opposite
@@ -92,16 +94,19 @@ typedef struct {
 
 /* Materials per phase.  kind 0: linear isotropic (E, nu), plane strain in 2-D.
  * kind 1: the paper's Cook energy with beta = 0 (R11),
- *   Psi = alpha (F:F - 2) + kappa/2 (J - 1)^2 - 2 alpha ln J, params (alpha, kappa), 2-D only. */
+ *   Psi = alpha (F:F - 2) + kappa/2 (J - 1)^2 - 2 alpha ln J, params (alpha, kappa), 2-D only.
+ * kind 2: the paper's Cook energy,
+ *   Psi = alpha (F:F - 2) + beta (F:F + J^2 - 3) + kappa/2 (J - 1)^2 - 2 (alpha + 2 beta) ln J,
+ *   params (alpha, beta, kappa) [n_phases][3], 2-D only. */
 typedef struct {
   int32_t kind;
   int32_t n_phases;
   int32_t per_rve;          /* 1: [B][n_phases][2], 0: [n_phases][2] */
-  const double* params;     /* host */
+  const double* params;     /* host [B|1][n_phases][2] (kind 0, 1) or [..][3] (kind 2) */
 } hom_materials;
 
 typedef struct {
-  int32_t finite_strain;    /* must equal (materials.kind == 1) */
+  int32_t finite_strain;    /* must equal (materials.kind >= 1) */
   double cg_rtol;           /* relative residual ||r||/||b|| (default 1e-13 if <= 0) */
   int32_t cg_max_iter;      /* default 20000 if <= 0 */
   int32_t rve_chunk;        /* RVEs condensed per pass; <= 0: automatic (memory budget) */
@@ -196,6 +201,9 @@ int hom_condense(hom_ctx* ctx, const double* d_kin, double* d_C_eff, double* d_P
 int hom_macro_solve(hom_ctx* ctx, const double* d_D, const double* d_S, double dirichlet_scale,
                     double* d_x, hom_solve_info* info, void* stream);
 
+/* External-load factor lambda (load stepping T_k = k T / n_l): the residual
+ * is R = sum_qp eta B^T S_b - lambda (f_body + f_nodal).  Default 1; host-side, no sync. */
+int hom_set_load_factor(hom_ctx* ctx, double load_factor);
 /* Assemble the macro stiffness K = sum_qp eta B^T D_b B (K5) into
  * the context's CSR matrix (node-block pattern over all DOFs) without solving.  Enqueue only. */
 int hom_macro_assemble(hom_ctx* ctx, const double* d_D, void* stream);

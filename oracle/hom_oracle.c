@@ -183,27 +183,43 @@ int orc_linear_C(int dim, double E, double nu, double* C) {
   return ORC_OK;
 }
 
-/* The paper's Cook energy with beta = 0 (reading R11):
- *   Psi = alpha (F:F - 2) + kappa/2 (J-1)^2 - 2 alpha ln J,   2-D, J = det F.
- * P = dPsi/dF (P:77-79 with H = cof F), A = dP/dF, both row-major (i,J). */
-int orc_nh_material(const double* F, double alpha, double kappa, double* psi, double* P, double* A) {
-  double J = F[0] * F[3] - F[1] * F[2];
+/* The paper's Cook energy, written out:
+ *   Psi = alpha (F:F - 2) + beta (F:F + J^2 - 3) + kappa/2 (J-1)^2 - 2 (alpha + 2 beta) ln J,
+ * 2-D, J = det F.  Differentiated term by term with dJ/dF = H = cof F:
+ *   P = 2 alpha F + beta (2 F + 2 J H) + kappa (J-1) H - 2 (alpha + 2 beta) / J H,
+ *   A = dP/dF,  both row-major (i,J).  beta = 0 is the config-5 reading R11. */
+int orc_mr_material(const double* F, double alpha, double beta, double kappa, double* psi, double* P,
+                    double* A) {
+  /* J - 1 from the displacement gradient F - I (no cancellation near the reference) */
+  double Jm1 = (F[0] - 1.0) + (F[3] - 1.0) + (F[0] - 1.0) * (F[3] - 1.0) - F[1] * F[2];
+  double J = 1.0 + Jm1;
   if (!(J > 0.0)) return ORC_ERR_JACOBIAN;
   /* cofactor H = dJ/dF, 2-D specialisation of (1/2) F xx F */
   double H[4] = {F[3], -F[2], -F[1], F[0]};
   double FF = F[0] * F[0] + F[1] * F[1] + F[2] * F[2] + F[3] * F[3];
-  if (psi) *psi = alpha * (FF - 2.0) + 0.5 * kappa * (J - 1.0) * (J - 1.0) - 2.0 * alpha * log(J);
-  double s = kappa * (J - 1.0) - 2.0 * alpha / J; /* dPsi/dJ */
-  for (int i = 0; i < 4; ++i) P[i] = 2.0 * alpha * F[i] + s * H[i];
+  if (psi)
+    *psi = alpha * (FF - 2.0) + beta * (FF + J * J - 3.0) + 0.5 * kappa * Jm1 * Jm1 -
+           2.0 * (alpha + 2.0 * beta) * log1p(Jm1);
+  /* dPsi/dJ of the J-dependent terms: 2 beta J + kappa (J-1) - 2 (alpha + 2 beta)/J */
+  double s = 2.0 * beta * J + kappa * Jm1 - 2.0 * (alpha + 2.0 * beta) / J;
+  /* P = 2 (alpha + beta) F + s H, evaluated as 2 (alpha + beta) (F - H) + (s + 2 (alpha + beta)) H
+   * with s + 2 (alpha + beta) = (J - 1) (2 beta + kappa + 2 (alpha + 2 beta) / J) (same value; both
+   * terms vanish at F = I instead of cancelling) */
+  double c1 = Jm1 * (2.0 * beta + kappa + 2.0 * (alpha + 2.0 * beta) / J);
+  double FmH[4] = {F[0] - F[3], F[1] + F[2], F[2] + F[1], F[3] - F[0]};
+  for (int i = 0; i < 4; ++i) P[i] = 2.0 * (alpha + beta) * FmH[i] + c1 * H[i];
   if (A) {
-    double t = kappa + 2.0 * alpha / (J * J); /* d2Psi/dJ2 */
+    double t = 2.0 * beta + kappa + 2.0 * (alpha + 2.0 * beta) / (J * J); /* d2Psi/dJ2 */
     /* dH/dF: H11=F22, H12=-F21, H21=-F12, H22=F11 */
     double dH[4][4] = {{0, 0, 0, 1}, {0, 0, -1, 0}, {0, -1, 0, 0}, {1, 0, 0, 0}};
     for (int i = 0; i < 4; ++i)
       for (int j = 0; j < 4; ++j)
-        A[i * 4 + j] = (i == j ? 2.0 * alpha : 0.0) + t * H[i] * H[j] + s * dH[i][j];
+        A[i * 4 + j] = (i == j ? 2.0 * (alpha + beta) : 0.0) + t * H[i] * H[j] + s * dH[i][j];
   }
   return ORC_OK;
+}
+int orc_nh_material(const double* F, double alpha, double kappa, double* psi, double* P, double* A) {
+  return orc_mr_material(F, alpha, 0.0, kappa, psi, P, A);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -276,15 +292,30 @@ static void sky_solve(const sky_t* s, double* x) {
 typedef struct {
   int dim, r, nen, nnode, nelem;
   double L;
+  const double* xc; /* explicit mesh (macro problems on mapped / unstructured meshes) or NULL */
+  const int* conn;
 } grid_t;
 
 static void grid_init(grid_t* g, int dim, int r, double L) {
   g->dim = dim; g->r = r; g->L = L; g->nen = nen_of(dim);
+  g->xc = NULL; g->conn = NULL;
   g->nnode = 1; g->nelem = 1;
   for (int k = 0; k < dim; ++k) { g->nnode *= (r + 1); g->nelem *= r; }
 }
 
+static void mesh_init(grid_t* g, int dim, int nnode, int nelem, const double* xc, const int* conn) {
+  g->dim = dim; g->r = -1; g->L = 0.0; g->nen = nen_of(dim);
+  g->nnode = nnode; g->nelem = nelem; g->xc = xc; g->conn = conn;
+}
+
 static void grid_elem(const grid_t* g, int e, int* nodes, double x[][3]) {
+  if (g->conn) { /* explicit mesh: same local node order as the structured grid */
+    for (int a = 0; a < g->nen; ++a) {
+      nodes[a] = g->conn[e * g->nen + a];
+      for (int k = 0; k < 3; ++k) x[a][k] = k < g->dim ? g->xc[(size_t)nodes[a] * g->dim + k] : 0.0;
+    }
+    return;
+  }
   int idx[3] = {0, 0, 0}, t = e;
   for (int k = 0; k < g->dim; ++k) { idx[k] = t % g->r; t /= g->r; }
   double h = g->L / g->r;
@@ -519,8 +550,9 @@ done:
 
 /*
  * orc_rve_condense_nh
- *   r          : RVE [0,1]^2 with r x r cells, periodic + corner fix
- *   phase      : [r*r] phase per element; mat [n_phase][2] = (alpha, kappa)
+ *   r, L       : RVE [0,L]^2 with r x r cells, periodic + corner fix
+ *   mstride    : 2: mat [n_phase][2] = (alpha, kappa) (beta = 0); 3: (alpha, beta, kappa)
+ *   phase      : [r*r] phase per element
  *   Fbar       : [4] macro deformation gradient (row-major)
  *   w          : [2 r^2] current fluctuation (independent DOF 2p+c), or NULL = 0
  * outputs (any may be NULL except A_eff):
@@ -531,11 +563,11 @@ done:
  *   rf_norm    : || r_f ||_2 over free DOFs (R_micro)
  * returns 0, ORC_ERR_JACOBIAN (J <= 0 at a micro qp), ORC_ERR_NOT_SPD
  */
-int orc_rve_condense_nh(int r, const uint8_t* phase, const double* mat, const double* Fbar,
-                        const double* w, double* A_eff, double* P_eff, double* P_avg, double* z,
-                        double* Wout, double* rf_norm) {
+int orc_rve_condense_nh(int r, double L, int mstride, const uint8_t* phase, const double* mat,
+                        const double* Fbar, const double* w, double* A_eff, double* P_eff, double* P_avg,
+                        double* z, double* Wout, double* rf_norm) {
   const int dim = 2, m = 4, nq = 4;
-  grid_t g; grid_init(&g, dim, r, 1.0);
+  grid_t g; grid_init(&g, dim, r, L);
   int nd = g.nen * dim, npad = r * r * dim;
   rvemap_t mp;
   int rc = rvemap_build(&g, 0, &mp);
@@ -558,7 +590,7 @@ int orc_rve_condense_nh(int r, const uint8_t* phase, const double* mat, const do
         eqs[a * dim + c] = mp.eq[nodes[a] * dim + c];
         we[a * dim + c] = w ? w[mp.indep[nodes[a]] * dim + c] : 0.0;
       }
-    const double* pm = &mat[2 * phase[e]];
+    const double* pm = &mat[mstride * phase[e]];
     for (int q = 0; q < nq; ++q) {
       double xi[3], N[MAXNEN], dNdx[MAXNEN][3], G[MAXM][MAXNEN * 3];
       gauss_point(dim, q, xi);
@@ -570,7 +602,10 @@ int orc_rve_condense_nh(int r, const uint8_t* phase, const double* mat, const do
         for (int j = 0; j < nd; ++j) F[i] += G[i][j] * we[j]; /* eq:microGrad */
       }
       double P[4], A[16];
-      if (orc_nh_material(F, pm[0], pm[1], NULL, P, A)) { rc = ORC_ERR_JACOBIAN; goto done; }
+      if (orc_mr_material(F, pm[0], mstride == 3 ? pm[1] : 0.0, pm[mstride - 1], NULL, P, A)) {
+        rc = ORC_ERR_JACOBIAN;
+        goto done;
+      }
       vol += wq;
       for (int i = 0; i < 16; ++i) Aavg[i] += wq * A[i];
       for (int i = 0; i < 4; ++i) Pavg[i] += wq * P[i];
@@ -618,7 +653,7 @@ int orc_rve_condense_nh(int r, const uint8_t* phase, const double* mat, const do
     double we[MAXNEN * 3];
     for (int a = 0; a < g.nen; ++a)
       for (int c = 0; c < dim; ++c) we[a * dim + c] = w ? w[mp.indep[nodes[a]] * dim + c] : 0.0;
-    const double* pm = &mat[2 * phase[e]];
+    const double* pm = &mat[mstride * phase[e]];
     for (int q = 0; q < nq; ++q) {
       double xi[3], N[MAXNEN], dNdx[MAXNEN][3], G[MAXM][MAXNEN * 3];
       gauss_point(dim, q, xi);
@@ -630,7 +665,7 @@ int orc_rve_condense_nh(int r, const uint8_t* phase, const double* mat, const do
         for (int j = 0; j < nd; ++j) F[i] += G[i][j] * we[j];
       }
       double P[4], A[16];
-      orc_nh_material(F, pm[0], pm[1], NULL, P, A);
+      orc_mr_material(F, pm[0], mstride == 3 ? pm[1] : 0.0, pm[mstride - 1], NULL, P, A);
       for (int j = 0; j <= m; ++j) { /* j < m: unit gradient e_j; j == m: z */
         const double* v = &sol[(size_t)j * ne];
         double d[4];
@@ -676,7 +711,8 @@ done:
 
 typedef struct {
   int kind; /* 0 linear, 1 nh */
-  int dim, r, n_rve, phase_per_rve, mat_per_rve, n_phase;
+  int dim, r, n_rve, phase_per_rve, mat_per_rve, n_phase, mstride;
+  double L;
   const uint8_t* phase;
   const double* mat;
   const double* Fbar; const double* w;
@@ -697,7 +733,7 @@ static void* batch_worker(void* arg) {
     pthread_mutex_unlock(&b->mu);
     if (i >= b->n_rve) break;
     const uint8_t* ph = b->phase + (b->phase_per_rve ? (size_t)i * nel : 0);
-    const double* mt = b->mat + (b->mat_per_rve ? (size_t)i * b->n_phase * 2 : 0);
+    const double* mt = b->mat + (b->mat_per_rve ? (size_t)i * b->n_phase * b->mstride : 0);
     int rc;
     if (b->kind == 0) {
       for (int e = 0; e < nel; ++e) {
@@ -708,7 +744,8 @@ static void* batch_worker(void* arg) {
       rc = orc_rve_condense_linear(dim, r, 1.0, 0, Cq, &b->C_eff[(size_t)i * m * m],
                                    b->W ? &b->W[(size_t)i * m * npad] : NULL);
     } else {
-      rc = orc_rve_condense_nh(r, ph, mt, &b->Fbar[(size_t)i * 4], b->w ? &b->w[(size_t)i * npad] : NULL,
+      rc = orc_rve_condense_nh(r, b->L, b->mstride, ph, mt, &b->Fbar[(size_t)i * 4],
+                               b->w ? &b->w[(size_t)i * npad] : NULL,
                                &b->C_eff[(size_t)i * 16], b->P_eff ? &b->P_eff[(size_t)i * 4] : NULL,
                                b->P_avg ? &b->P_avg[(size_t)i * 4] : NULL,
                                b->Z ? &b->Z[(size_t)i * npad] : NULL,
@@ -745,22 +782,24 @@ int orc_condense_batch_linear(int dim, int r, int n_rve, int phase_per_rve, cons
                               double* W, int nthreads, int* bad_rve) {
   batch_t b;
   memset(&b, 0, sizeof(b));
-  b.kind = 0; b.dim = dim; b.r = r; b.n_rve = n_rve; b.phase_per_rve = phase_per_rve;
+  b.kind = 0; b.dim = dim; b.r = r; b.n_rve = n_rve; b.phase_per_rve = phase_per_rve; b.mstride = 2; b.L = 1.0;
   b.mat_per_rve = mat_per_rve; b.n_phase = n_phase; b.phase = phase; b.mat = mat;
   b.C_eff = C_eff; b.W = W;
   return run_batch(&b, nthreads, bad_rve);
 }
 
-/* Finite-strain batch (2-D): mat [.. ][n_phase][2] = (alpha, kappa); Fbar [n_rve][4];
- * w [n_rve][2 r^2] or NULL; outputs A_eff [n_rve][16], P_eff/P_avg [n_rve][4],
- * Z [n_rve][2r^2], W [n_rve][4][2r^2], rf_norm [n_rve] (nullable except A_eff). */
-int orc_condense_batch_nh(int r, int n_rve, int phase_per_rve, const uint8_t* phase, int mat_per_rve,
-                          int n_phase, const double* mat, const double* Fbar, const double* w,
+/* Finite-strain batch (2-D, RVE [0,L]^2): mat [.. ][n_phase][mstride] = (alpha, kappa) or
+ * (alpha, beta, kappa); Fbar [n_rve][4]; w [n_rve][2 r^2] or NULL; outputs A_eff [n_rve][16],
+ * P_eff/P_avg [n_rve][4], Z [n_rve][2r^2], W [n_rve][4][2r^2], rf_norm [n_rve] (nullable
+ * except A_eff). */
+int orc_condense_batch_nh(int r, double L, int mstride, int n_rve, int phase_per_rve, const uint8_t* phase,
+                          int mat_per_rve, int n_phase, const double* mat, const double* Fbar, const double* w,
                           double* A_eff, double* P_eff, double* P_avg, double* Z, double* W,
                           double* rf_norm, int nthreads, int* bad_rve) {
   batch_t b;
   memset(&b, 0, sizeof(b));
   b.kind = 1; b.dim = 2; b.r = r; b.n_rve = n_rve; b.phase_per_rve = phase_per_rve;
+  b.mstride = mstride; b.L = L;
   b.mat_per_rve = mat_per_rve; b.n_phase = n_phase; b.phase = phase; b.mat = mat;
   b.Fbar = Fbar; b.w = w; b.C_eff = A_eff; b.P_eff = P_eff; b.P_avg = P_avg; b.Z = Z; b.W = W;
   b.rf_norm = rf_norm;
@@ -773,8 +812,9 @@ int orc_condense_batch_nh(int r, int n_rve, int phase_per_rve, const uint8_t* ph
 /* ------------------------------------------------------------------------ */
 
 /* kinematics at every macro qp: kind 0 -> Voigt strain, kind 1 -> grad u */
-int orc_macro_kin(int dim, int nel, double Lm, int kind, const double* u, double* out) {
-  grid_t g; grid_init(&g, dim, nel, Lm);
+static int macro_kin_g(const grid_t* gp, int kind, const double* u, double* out) {
+  const grid_t g = *gp;
+  const int dim = g.dim;
   int m = m_of(dim, kind), nq = 1 << dim, nd = g.nen * dim;
   for (int e = 0; e < g.nelem; ++e) {
     int nodes[MAXNEN]; double x[MAXNEN][3];
@@ -794,10 +834,12 @@ int orc_macro_kin(int dim, int nel, double Lm, int kind, const double* u, double
   return ORC_OK;
 }
 
-/* R = sum_qp eta B^T S - f_body  (all DOFs; S [B][m] stress, nullable; body [dim] nullable) */
-int orc_macro_residual(int dim, int nel, double Lm, int kind, const double* S, const double* body,
-                       double* R) {
-  grid_t g; grid_init(&g, dim, nel, Lm);
+/* R = sum_qp eta B^T S - f_body - f_ext  (all DOFs; S [B][m] stress, nullable; body [dim]
+ * nullable; fext [ndof] external nodal forces, nullable) */
+static int macro_residual_g(const grid_t* gp, int kind, const double* S, const double* body,
+                            const double* fext, double* R) {
+  const grid_t g = *gp;
+  const int dim = g.dim;
   int m = m_of(dim, kind), nq = 1 << dim, nd = g.nen * dim;
   for (int i = 0; i < g.nnode * dim; ++i) R[i] = 0.0;
   for (int e = 0; e < g.nelem; ++e) {
@@ -818,6 +860,8 @@ int orc_macro_residual(int dim, int nel, double Lm, int kind, const double* S, c
       }
     }
   }
+  if (fext)
+    for (int i = 0; i < g.nnode * dim; ++i) R[i] -= fext[i];
   return ORC_OK;
 }
 
@@ -828,9 +872,10 @@ int orc_macro_residual(int dim, int nel, double Lm, int kind, const double* S, c
  * dir_dof [n_dir]; x [n_dof]: in = values at Dirichlet DOFs, out = full vector.
  * Linear: S = NULL, x_D = prescribed u. Newton: S = P_eff, x_D = 0, x = du.
  */
-int orc_macro_solve(int dim, int nel, double Lm, int kind, const double* D, const double* S,
-                    const double* body, int n_dir, const int* dir_dof, double* x) {
-  grid_t g; grid_init(&g, dim, nel, Lm);
+static int macro_solve_g(const grid_t* gp, int kind, const double* D, const double* S,
+                         const double* body, const double* fext, int n_dir, const int* dir_dof, double* x) {
+  const grid_t g = *gp;
+  const int dim = g.dim;
   int m = m_of(dim, kind), nq = 1 << dim, nd = g.nen * dim, ndof = g.nnode * dim;
   int* eq = (int*)malloc(sizeof(int) * ndof);
   double* rhs = (double*)malloc(sizeof(double) * ndof);
@@ -847,7 +892,7 @@ int orc_macro_solve(int dim, int nel, double Lm, int kind, const double* D, cons
   for (int i = 0; i < ndof; ++i) eq[i] = eq[i] < 0 ? -1 : neq++;
   rc = sky_profile_from_grid(&g, eq, neq, &K);
   if (rc) goto done;
-  orc_macro_residual(dim, nel, Lm, kind, S, body, R);
+  macro_residual_g(&g, kind, S, body, fext, R);
   for (int i = 0; i < neq; ++i) rhs[i] = 0.0;
   for (int i = 0; i < ndof; ++i)
     if (eq[i] >= 0) rhs[eq[i]] = -R[i];
@@ -886,6 +931,40 @@ int orc_macro_solve(int dim, int nel, double Lm, int kind, const double* D, cons
 done:
   free(eq); free(rhs); free(R); sky_free(&K);
   return rc;
+}
+
+/* structured grid [0,Lm]^dim with nel cells per direction */
+int orc_macro_kin(int dim, int nel, double Lm, int kind, const double* u, double* out) {
+  grid_t g; grid_init(&g, dim, nel, Lm);
+  return macro_kin_g(&g, kind, u, out);
+}
+int orc_macro_residual(int dim, int nel, double Lm, int kind, const double* S, const double* body,
+                       double* R) {
+  grid_t g; grid_init(&g, dim, nel, Lm);
+  return macro_residual_g(&g, kind, S, body, NULL, R);
+}
+int orc_macro_solve(int dim, int nel, double Lm, int kind, const double* D, const double* S,
+                    const double* body, int n_dir, const int* dir_dof, double* x) {
+  grid_t g; grid_init(&g, dim, nel, Lm);
+  return macro_solve_g(&g, kind, D, S, body, NULL, n_dir, dir_dof, x);
+}
+/* explicit macro mesh: coords [nnode][dim], conn [nelem][2^dim] (grid local order), external
+ * nodal forces fext [nnode*dim] (nullable) -- the Cook membrane of PAPER.md §4.2 */
+int orc_mesh_macro_kin(int dim, int nnode, int nelem, const double* xc, const int* conn, int kind,
+                       const double* u, double* out) {
+  grid_t g; mesh_init(&g, dim, nnode, nelem, xc, conn);
+  return macro_kin_g(&g, kind, u, out);
+}
+int orc_mesh_macro_residual(int dim, int nnode, int nelem, const double* xc, const int* conn, int kind,
+                            const double* S, const double* body, const double* fext, double* R) {
+  grid_t g; mesh_init(&g, dim, nnode, nelem, xc, conn);
+  return macro_residual_g(&g, kind, S, body, fext, R);
+}
+int orc_mesh_macro_solve(int dim, int nnode, int nelem, const double* xc, const int* conn, int kind,
+                         const double* D, const double* S, const double* body, const double* fext, int n_dir,
+                         const int* dir_dof, double* x) {
+  grid_t g; mesh_init(&g, dim, nnode, nelem, xc, conn);
+  return macro_solve_g(&g, kind, D, S, body, fext, n_dir, dir_dof, x);
 }
 
 /* Dense symmetric check helper for tests: skyline solve of a small SPD dense matrix

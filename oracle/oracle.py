@@ -47,13 +47,17 @@ def lib():
             D = ctypes.c_double
             L.orc_linear_C.argtypes = [I, D, D, P]
             L.orc_nh_material.argtypes = [P, D, D, P, P, P]
+            L.orc_mr_material.argtypes = [P, D, D, D, P, P, P]
             L.orc_rve_condense_linear.argtypes = [I, I, D, I, P, P, P]
-            L.orc_rve_condense_nh.argtypes = [I, P, P, P, P, P, P, P, P, P, P]
+            L.orc_rve_condense_nh.argtypes = [I, D, I, P, P, P, P, P, P, P, P, P, P]
             L.orc_condense_batch_linear.argtypes = [I, I, I, I, P, I, I, P, P, P, I, P]
-            L.orc_condense_batch_nh.argtypes = [I, I, I, P, I, I, P, P, P, P, P, P, P, P, P, I, P]
+            L.orc_condense_batch_nh.argtypes = [I, D, I, I, I, P, I, I, P, P, P, P, P, P, P, P, P, I, P]
             L.orc_macro_kin.argtypes = [I, I, D, I, P, P]
             L.orc_macro_residual.argtypes = [I, I, D, I, P, P, P]
             L.orc_macro_solve.argtypes = [I, I, D, I, P, P, P, I, P, P]
+            L.orc_mesh_macro_kin.argtypes = [I, I, I, P, P, I, P, P]
+            L.orc_mesh_macro_residual.argtypes = [I, I, I, P, P, I, P, P, P, P]
+            L.orc_mesh_macro_solve.argtypes = [I, I, I, P, P, I, P, P, P, P, I, P, P]
             L.orc_dense_spd_solve.argtypes = [I, P, P]
             _lib = L
     return _lib
@@ -87,13 +91,13 @@ def linear_C(dim: int, E: float, nu: float) -> np.ndarray:
     return C
 
 
-def nh_material(F, alpha: float, kappa: float):
-    """Return (psi, P[4], A[4,4]) of the beta = 0 Cook energy."""
+def nh_material(F, alpha: float, kappa: float, beta: float = 0.0):
+    """Return (psi, P[4], A[4,4]) of the Cook energy; beta = 0 is config 5 (R11)."""
     F = _f64(np.asarray(F).reshape(4))
     P = np.zeros(4)
     A = np.zeros((4, 4))
     psi = ctypes.c_double(0.0)
-    rc = lib().orc_nh_material(_p(F), alpha, kappa, ctypes.byref(psi), _p(P), _p(A))
+    rc = lib().orc_mr_material(_p(F), alpha, beta, kappa, ctypes.byref(psi), _p(P), _p(A))
     if rc:
         raise OracleError(rc, "nh_material")
     return psi.value, P, A
@@ -138,12 +142,13 @@ def condense_batch_linear(dim: int, r: int, phase, mat, n_rve: int | None = None
     return (C, W) if want_W else C
 
 
-def condense_batch_nh(r: int, phase, mat, Fbar, w=None, nthreads: int | None = None):
-    """Batched finite-strain condensation (2-D).  Returns dict of A_eff, P_eff, P_avg, Z, W, rf_norm."""
+def condense_batch_nh(r: int, phase, mat, Fbar, w=None, nthreads: int | None = None, L: float = 1.0):
+    """Batched finite-strain condensation (2-D, RVE [0,L]^2).  mat [..][n_phase][2] (alpha, kappa) or
+    [..][n_phase][3] (alpha, beta, kappa).  Returns dict of A_eff, P_eff, P_avg, Z, W, rf_norm."""
     phase = np.ascontiguousarray(phase, dtype=np.uint8).reshape(-1, r * r)
     mat = _f64(mat)
-    n_phase = mat.shape[-2]
-    mat = mat.reshape(-1, n_phase, 2)
+    n_phase, ms = mat.shape[-2], mat.shape[-1]
+    mat = mat.reshape(-1, n_phase, ms)
     Fbar = _f64(np.asarray(Fbar).reshape(-1, 4))
     n_rve = Fbar.shape[0]
     npad = 2 * r * r
@@ -153,7 +158,7 @@ def condense_batch_nh(r: int, phase, mat, Fbar, w=None, nthreads: int | None = N
         "Z": np.zeros((n_rve, npad)), "W": np.zeros((n_rve, 4, npad)), "rf_norm": np.zeros(n_rve),
     }
     bad = ctypes.c_int(-1)
-    rc = lib().orc_condense_batch_nh(r, n_rve, int(phase.shape[0] > 1), _p(phase), int(mat.shape[0] > 1),
+    rc = lib().orc_condense_batch_nh(r, L, ms, n_rve, int(phase.shape[0] > 1), _p(phase), int(mat.shape[0] > 1),
                                      n_phase, _p(mat), _p(Fbar), _p(w), _p(out["A_eff"]),
                                      _p(out["P_eff"]), _p(out["P_avg"]), _p(out["Z"]), _p(out["W"]),
                                      _p(out["rf_norm"]), nthreads or default_threads(), ctypes.byref(bad))
@@ -165,27 +170,60 @@ def condense_batch_nh(r: int, phase, mat, Fbar, w=None, nthreads: int | None = N
 # --------------------------------------------------------------------------
 # macro problem
 # --------------------------------------------------------------------------
-def macro_kin(dim: int, nel: int, u, kind: int = 0, Lm: float = 1.0) -> np.ndarray:
+def _mesh(mesh):
+    xc, conn = mesh
+    return _f64(xc), np.ascontiguousarray(conn, dtype=np.int32)
+
+
+def macro_kin(dim: int, nel: int, u, kind: int = 0, Lm: float = 1.0, mesh=None) -> np.ndarray:
+    """Kinematics at every macro qp; mesh = (coords, conn) for a non-structured macro mesh."""
     m = m_of(dim, kind)
     u = _f64(u)
+    if mesh is not None:
+        xc, conn = _mesh(mesh)
+        out = np.zeros((conn.shape[0] * 2 ** dim, m))
+        lib().orc_mesh_macro_kin(dim, xc.shape[0], conn.shape[0], _p(xc), _p(conn), kind, _p(u), _p(out))
+        return out
     out = np.zeros((nel ** dim * 2 ** dim, m))
     lib().orc_macro_kin(dim, nel, Lm, kind, _p(u), _p(out))
     return out
 
 
-def macro_residual(dim: int, nel: int, S=None, body=None, kind: int = 0, Lm: float = 1.0) -> np.ndarray:
+def macro_residual(dim: int, nel: int, S=None, body=None, kind: int = 0, Lm: float = 1.0, mesh=None,
+                   fext=None) -> np.ndarray:
+    """R = sum eta B^T S - f_body - f_ext over all DOFs."""
+    if mesh is not None:
+        xc, conn = _mesh(mesh)
+        R = np.zeros(xc.shape[0] * dim)
+        lib().orc_mesh_macro_residual(dim, xc.shape[0], conn.shape[0], _p(xc), _p(conn), kind, _p(_f64(S)),
+                                      _p(_f64(body)), _p(_f64(fext)), _p(R))
+        return R
     R = np.zeros((nel + 1) ** dim * dim)
     lib().orc_macro_residual(dim, nel, Lm, kind, _p(_f64(S)), _p(_f64(body)), _p(R))
+    if fext is not None:
+        R -= fext
     return R
 
 
 def macro_solve(dim: int, nel: int, D, dir_dof, x_dir, S=None, body=None, kind: int = 0,
-                Lm: float = 1.0) -> np.ndarray:
+                Lm: float = 1.0, mesh=None, fext=None) -> np.ndarray:
     """Direct solve of K_FF x_F = -R_F - K_FD x_D (see hom_oracle.c orc_macro_solve)."""
+    dir_dof = np.ascontiguousarray(dir_dof, dtype=np.int32)
+    if mesh is not None:
+        xc, conn = _mesh(mesh)
+        x = np.zeros(xc.shape[0] * dim)
+        x[dir_dof] = x_dir
+        rc = lib().orc_mesh_macro_solve(dim, xc.shape[0], conn.shape[0], _p(xc), _p(conn), kind, _p(_f64(D)),
+                                        _p(_f64(S)), _p(_f64(body)), _p(_f64(fext)), len(dir_dof), _p(dir_dof),
+                                        _p(x))
+        if rc:
+            raise OracleError(rc, "mesh_macro_solve")
+        return x
     ndof = (nel + 1) ** dim * dim
     x = np.zeros(ndof)
-    dir_dof = np.ascontiguousarray(dir_dof, dtype=np.int32)
     x[dir_dof] = x_dir
+    if fext is not None:
+        raise ValueError("fext needs mesh=")
     rc = lib().orc_macro_solve(dim, nel, Lm, kind, _p(_f64(D)), _p(_f64(S)), _p(_f64(body)),
                                len(dir_dof), _p(dir_dof), _p(x))
     if rc:
@@ -239,35 +277,48 @@ def recover_linear(W, eps):
     return np.einsum("bj,bjn->bn", eps, W)
 
 
-def newton_step_nh(wl, u, w, x_dir, nthreads: int | None = None):
+def _fs(wl):
+    """Finite-strain workload plumbing: (mesh or None, external nodal force or None, RVE size)."""
+    mesh = None if getattr(wl, "macro_coords", None) is None else wl.macro_mesh()
+    return mesh, getattr(wl, "nodal_force", None), getattr(wl, "rve_size", 1.0)
+
+
+def newton_step_nh(wl, u, w, x_dir, nthreads: int | None = None, load_factor: float = 1.0):
     """One monolithic Newton step at state (u, w) (eq:solution2 P:420-423).
 
     Returns (du, dw, info) with info = dict(R_norm, rf_max, cond) at the *current* state.
     """
     dim, nel, r = 2, wl.nel, wl.r
-    G = macro_kin(dim, nel, u, kind=1)
+    mesh, fn, L = _fs(wl)
+    fext = None if fn is None else load_factor * fn
+    G = macro_kin(dim, nel, u, kind=1, mesh=mesh)
     Fbar = G + np.array([1.0, 0.0, 0.0, 1.0])
-    c = condense_batch_nh(r, wl.phase, wl.mat, Fbar, w, nthreads=nthreads)
-    R = macro_residual(dim, nel, c["P_avg"], wl.body, kind=1)
+    c = condense_batch_nh(r, wl.phase, wl.mat, Fbar, w, nthreads=nthreads, L=L)
+    R = macro_residual(dim, nel, c["P_avg"], wl.body, kind=1, mesh=mesh, fext=fext)
     free = np.ones(len(u), bool)
     free[wl.dir_dof] = False
     info = {"R_norm": float(np.linalg.norm(R[free])), "rf_max": float(c["rf_norm"].max()), "cond": c}
-    du = macro_solve(dim, nel, c["A_eff"], wl.dir_dof, x_dir, S=c["P_eff"], body=wl.body, kind=1)
-    dF = macro_kin(dim, nel, du, kind=1)
+    du = macro_solve(dim, nel, c["A_eff"], wl.dir_dof, x_dir, S=c["P_eff"], body=wl.body, kind=1, mesh=mesh,
+                     fext=fext)
+    dF = macro_kin(dim, nel, du, kind=1, mesh=mesh)
     dw = c["Z"] + np.einsum("bj,bjn->bn", dF, c["W"])
     return du, dw, info
 
 
-def newton_nh(wl, tol: float = 1e-11, max_iter: int = 25, steps=None, nthreads: int | None = None):
-    """Config 5: monolithic Newton with null-space (Schur) reduction and load stepping.
+def newton_nh(wl, tol: float = 1e-11, max_iter: int = 25, steps=None, nthreads: int | None = None,
+              micro_tol=None, divergence: float = 1e10):
+    """Finite strain: monolithic Newton with null-space (Schur) reduction and load stepping.
 
     Per iteration (CS-paper-1): condense at (u, w); check
-    ||R_macro|| (with <P>) and max_b ||r_f,b|| against tol (reading R3); solve the
-    condensed system (eq:solution2); dw = z + W dF.  The Dirichlet
-    increment is applied in the first iteration of each step.
+    ||R_macro|| (with <P>) and max_b ||r_f,b|| against tol (reading R3; micro_tol=inf checks the
+    macro residual only); solve the condensed system (eq:solution2); dw = z + W dF.
+    Load steps: the Dirichlet increment in the first iteration of each step (config 5),
+    or the external load factor k/n_steps when the workload has nodal forces (Cook).
     Returns a list of per-step dicts with u, w and the residual history.
     """
     n_rve, r = wl.n_rve, wl.r
+    force = getattr(wl, "nodal_force", None) is not None
+    mtol = tol if micro_tol is None else micro_tol
     u = np.zeros(wl.n_dof)
     w = np.zeros((n_rve, 2 * r * r))
     out = []
@@ -275,15 +326,84 @@ def newton_nh(wl, tol: float = 1e-11, max_iter: int = 25, steps=None, nthreads: 
     for k in range(1, n_steps + 1):
         hist, converged = [], False
         for it in range(max_iter + 1):
-            x_dir = wl.dir_val / wl.n_steps if it == 0 else np.zeros(len(wl.dir_dof))
-            du, dw, info = newton_step_nh(wl, u, w, x_dir, nthreads=nthreads)
+            x_dir = wl.dir_val / wl.n_steps if (it == 0 and not force) else np.zeros(len(wl.dir_dof))
+            try:
+                du, dw, info = newton_step_nh(wl, u, w, x_dir, nthreads=nthreads,
+                                              load_factor=k / wl.n_steps if force else 1.0)
+            except OracleError as e:
+                if e.code != 4:
+                    raise
+                hist.append((float("inf"), float("inf")))
+                break
             hist.append((info["R_norm"], info["rf_max"]))
-            if it > 0 and info["R_norm"] <= tol and info["rf_max"] <= tol:
+            if it > 0 and info["R_norm"] <= tol and info["rf_max"] <= mtol:
                 converged = True
                 break
-            if info["R_norm"] > 1e10 or it == max_iter:
+            if not (info["R_norm"] <= divergence) or it == max_iter:
                 break
             u, w = u + du, w + dw
+        out.append({"step": k, "u": u.copy(), "w": w.copy(), "history": hist, "converged": converged})
+        if not converged:
+            break
+    return out
+
+
+def _inner_done(inner, micro_tol):
+    """Inner RVE Newton converged: max ||r_f|| < micro_tol, or the round-off floor of the r_f sums
+    reached after quadratic convergence (below 1e-9, no longer halving) -- DESIGN.md reading R21."""
+    rf = inner[-1]
+    return rf < micro_tol or (len(inner) >= 2 and rf < 1e-9 and rf > 0.5 * inner[-2])
+
+
+def newton_classical(wl, tol: float = 1e-9, micro_tol: float = 1e-13, max_iter: int = 25, max_inner: int = 30,
+                     steps=None, nthreads: int | None = None, divergence: float = 1e10):
+    """Classical staggered FE^2: per macro iteration, equilibrate every RVE at the
+    fixed macro deformation (inner Newton w <- w + z, z = -K_ff^-1 r_f, until max ||r_f|| <
+    micro_tol), then solve [K - D L^-1 E] dq = -R_macro (eq:solution1, R_macro with <P>), update q
+    and w += W dF (eq:reduction) and restart until ||R_macro|| < tol.  Load factor k/n_steps on the
+    external nodal forces.  Returns a list of per-step dicts (history: (||R_macro||, inner list))."""
+    dim, nel, r = 2, wl.nel, wl.r
+    mesh, fn, L = _fs(wl)
+    u = np.zeros(wl.n_dof)
+    w = np.zeros((wl.n_rve, 2 * r * r))
+    free = np.ones(wl.n_dof, bool)
+    free[wl.dir_dof] = False
+    out = []
+    n_steps = wl.n_steps if steps is None else steps
+    for k in range(1, n_steps + 1):
+        fext = None if fn is None else (k / wl.n_steps) * fn
+        hist, converged = [], False
+        for it in range(max_iter + 1):
+            Fbar = macro_kin(dim, nel, u, kind=1, mesh=mesh) + np.array([1.0, 0.0, 0.0, 1.0])
+            inner = []
+            try:
+                for _ in range(max_inner + 1):
+                    c = condense_batch_nh(r, wl.phase, wl.mat, Fbar, w, nthreads=nthreads, L=L)
+                    rf = float(c["rf_norm"].max())
+                    inner.append(rf)
+                    if _inner_done(inner, micro_tol) or not (rf <= divergence):
+                        break
+                    w = w + c["Z"]
+            except OracleError as e:
+                if e.code != 4:
+                    raise
+                hist.append((float("inf"), inner))
+                break
+            R = macro_residual(dim, nel, c["P_avg"], wl.body, kind=1, mesh=mesh, fext=fext)
+            rn = float(np.linalg.norm(R[free]))
+            hist.append((rn, inner))
+            if not _inner_done(inner, micro_tol):
+                break
+            if it > 0 and rn <= tol:
+                converged = True
+                break
+            if not (rn <= divergence) or it == max_iter:
+                break
+            du = macro_solve(dim, nel, c["A_eff"], wl.dir_dof, np.zeros(len(wl.dir_dof)), S=c["P_avg"],
+                             body=wl.body, kind=1, mesh=mesh, fext=fext)
+            dF = macro_kin(dim, nel, du, kind=1, mesh=mesh)
+            u = u + du
+            w = w + c["Z"] + np.einsum("bj,bjn->bn", dF, c["W"])
         out.append({"step": k, "u": u.copy(), "w": w.copy(), "history": hist, "converged": converged})
         if not converged:
             break

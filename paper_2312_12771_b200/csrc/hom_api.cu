@@ -243,12 +243,12 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   *out = c;
   if ((dim != 2 && dim != 3) || rve->dim != dim || mac->nodes_per_elem != (1 << dim) ||
       rve->nodes_per_elem != (1 << dim) || mac->n_elems <= 0 || rve->n_elems <= 0 || mat->n_phases <= 0 ||
-      (mat->kind != 0 && mat->kind != 1) || (mat->kind == 1 && dim != 2) ||
-      (options->finite_strain != 0) != (mat->kind == 1))
+      (mat->kind < 0 || mat->kind > 2) || (mat->kind >= 1 && dim != 2) ||
+      (options->finite_strain != 0) != (mat->kind >= 1))
     return fail(HOM_ERR_INVALID_ARG, "unsupported dimension / element / material combination");
   const int nen = 1 << dim, nq = 1 << dim;
   c->dim = dim;
-  c->finite = mat->kind == 1;
+  c->finite = mat->kind >= 1;
   c->m = c->finite ? 4 : (dim == 2 ? 3 : 6);
   c->B = mac->n_elems * nq;
 
@@ -310,6 +310,9 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
           for (int k = 0; k < dim; ++k)
             fbody[(size_t)mconn[e * nen + a] * dim + k] += mw[(size_t)e * nq + q] * shp[q * nen + a] * mac->body_force[k];
   }
+  if (mac->nodal_force)  // surface tractions as consistent nodal forces (eq:weakMech, Gamma^sigma)
+    for (int i = 0; i < M.ndof; ++i) fbody[i] += mac->nodal_force[i];
+  M.load_factor = 1.0;
 
   // ------------------------------------------------------------ RVE mesh, periodic pairing
   RveDev& R = c->R;
@@ -498,7 +501,8 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   std::vector<uint8_t> phase(ph->phase, ph->phase + nph_entries);
   for (uint8_t v : phase)
     if (v >= mat->n_phases) return fail(HOM_ERR_INVALID_ARG, "phase id >= n_phases");
-  std::vector<double> params(mat->params, mat->params + (size_t)(R.mat_per_rve ? c->B : 1) * R.n_phase * 2);
+  R.mat_stride = mat->kind == 2 ? 3 : 2;
+  std::vector<double> params(mat->params, mat->params + (size_t)(R.mat_per_rve ? c->B : 1) * R.n_phase * R.mat_stride);
 
   // ------------------------------------------------------------ chunking + allocation
   const size_t tiles = (size_t)R.nslot;
@@ -708,6 +712,12 @@ int hom_condense(hom_ctx* c, const double* d_kin, double* d_C_eff, double* d_P_e
     cudaMemcpy(&row, c->info + h[0], sizeof(int), cudaMemcpyDeviceToHost);
     return set_err(c, HOM_ERR_NOT_SPD, "K_ff not positive definite", h[0], row - 1);
   }
+  return HOM_OK;
+}
+
+int hom_set_load_factor(hom_ctx* c, double load_factor) {
+  if (!c || !(load_factor == load_factor)) return set_err(c, HOM_ERR_INVALID_ARG, "hom_set_load_factor");
+  c->M.load_factor = load_factor;
   return HOM_OK;
 }
 

@@ -33,8 +33,8 @@ struct RveDev {
   const int* sh;
   const uint8_t* phase;           // [B|1][ne]
   int phase_per_rve;
-  const double* mat;              // [B|1][n_phase][2]
-  int mat_per_rve, n_phase;
+  const double* mat;              // [B|1][n_phase][mat_stride]
+  int mat_per_rve, n_phase, mat_stride;  // stride 2 (E, nu) / (alpha, kappa); 3 (alpha, beta, kappa)
   // geometry-only element matrices of the isotropic closed form (small strain):
   // K_e = lam_e * Klam_e + mu_e * Kmu_e, K_fe rows = lam_e * Flam_e + mu_e * Fmu_e
   const double* Klam;             // [ntype][nen*dim][nen*dim] (element type = identical geometry)
@@ -71,7 +71,8 @@ struct MacroDev {
   const int* ninc;
   const uint8_t* dmask;           // [ndof] 1 = Dirichlet
   const double* dval;             // [ndof] prescribed value (0 where free)
-  const double* fbody;            // [ndof] consistent body load
+  const double* fbody;            // [ndof] external load: consistent body load + nodal forces
+  double load_factor;             // multiplies fbody (load stepping, hom_set_load_factor)
 };
 
 struct CgState {

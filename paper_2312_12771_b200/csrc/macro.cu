@@ -124,7 +124,7 @@ __global__ void k_macro_rhs(MacroDev M, const double* __restrict__ val, const do
     return;
   }
   int n = i / DIM, c = i % DIM;
-  double R = -M.fbody[i];
+  double R = -M.load_factor * M.fbody[i];
   if (S) {
     for (int s = M.ninc_ptr[n]; s < M.ninc_ptr[n + 1]; ++s) {
       int E = M.ninc[s] >> 4, a = M.ninc[s] & 15;

@@ -38,8 +38,13 @@ __device__ __forceinline__ double unit_stress(int k, int c, int J, double lam, d
 
 // ---------------------------------------------------------------------------
 // K1a (finite strain): per (RVE, element, qp) deformation gradient, stress and
-// tangent of the Cook energy with beta = 0.  F~ = F + grad w
-// (eq:microGrad).
+// tangent of the paper's Cook energy, plane strain of the polyconvex
+// Mooney-Rivlin form eq:MR:
+//   Psi = alpha (F:F - 2) + beta (F:F + J^2 - 3) + kappa/2 (J - 1)^2 - 2 (alpha + 2 beta) ln J,
+//   P = 2 (alpha + beta) F + g(J) H,  g = 2 beta J + kappa (J - 1) - 2 (alpha + 2 beta) / J,
+//   A = 2 (alpha + beta) I + g'(J) H (x) H + g dH/dF,  g' = 2 beta + kappa + 2 (alpha + 2 beta) / J^2,
+// with H = cof F (the 2-D specialisation of 1/2 F xx F).  kind 1 = beta 0 (R11).
+// F~ = F + grad w (eq:microGrad).
 // ---------------------------------------------------------------------------
 __global__ void k_rve_material_nh(RveDev R, int b0, int nb, const double* __restrict__ Fbar,
                                   const double* __restrict__ w, double* __restrict__ Aq,
@@ -61,9 +66,13 @@ __global__ void k_rve_material_nh(RveDev R, int b0, int nb, const double* __rest
     F[2] += w1 * g[0]; F[3] += w1 * g[1];
   }
   int ph = R.phase[(R.phase_per_rve ? (long)b * R.ne : 0) + e];
-  const double* mp = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * 2 : 0) + 2 * ph;
-  double alpha = mp[0], kappa = mp[1];
-  double J = F[0] * F[3] - F[1] * F[2];
+  const int np = R.mat_stride;
+  const double* mp = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * np : 0) + np * ph;
+  const double alpha = mp[0], beta = np == 3 ? mp[1] : 0.0, kappa = mp[np - 1];
+  // J - 1 from the displacement-gradient part (no cancellation near F = I)
+  const double g11 = F[0] - 1.0, g22 = F[3] - 1.0;
+  const double Jm1 = g11 + g22 + g11 * g22 - F[1] * F[2];
+  double J = 1.0 + Jm1;
   double* A = Aq + gid * 16;
   double* P = Pq + gid * 4;
   if (!(J > 0.0)) {
@@ -73,14 +82,20 @@ __global__ void k_rve_material_nh(RveDev R, int b0, int nb, const double* __rest
     return;
   }
   double H[4] = {F[3], -F[2], -F[1], F[0]};  // cof F (2-D specialisation of 1/2 F xx F)
-  double dPsidJ = kappa * (J - 1.0) - 2.0 * alpha / J;
-  double d2 = kappa + 2.0 * alpha / (J * J);
-  for (int i = 0; i < 4; ++i) P[i] = 2.0 * alpha * F[i] + dPsidJ * H[i];
+  const double ab = alpha + 2.0 * beta;
+  double dPsidJ = 2.0 * beta * J + kappa * Jm1 - 2.0 * ab / J;
+  double d2 = 2.0 * beta + kappa + 2.0 * ab / (J * J);
+  // P = 2 (alpha + beta) F + g H written as 2 (alpha + beta)(F - H) + (g + 2 (alpha + beta)) H with
+  // g + 2 (alpha + beta) = (J - 1)(2 beta + kappa + 2 (alpha + 2 beta) / J): both terms vanish at F = I
+  // (the stress-free reference) instead of cancelling, so R_micro reaches ~1e-15 (classical scheme)
+  const double c0 = 2.0 * (alpha + beta), c1 = Jm1 * (2.0 * beta + kappa + 2.0 * ab / J);
+  const double FmH[4] = {F[0] - F[3], F[1] + F[2], F[2] + F[1], F[3] - F[0]};
+  for (int i = 0; i < 4; ++i) P[i] = c0 * FmH[i] + c1 * H[i];
   // dH/dF is the constant anti-diagonal [0 0 0 1; 0 0 -1 0; 0 -1 0 0; 1 0 0 0]
   for (int i = 0; i < 4; ++i)
     for (int j = 0; j < 4; ++j) {
       double v = d2 * H[i] * H[j];
-      if (i == j) v += 2.0 * alpha;
+      if (i == j) v += 2.0 * (alpha + beta);
       if (i + j == 3) v += ((i == 0 || i == 3) ? 1.0 : -1.0) * dPsidJ;
       A[i * 4 + j] = v;
     }
@@ -126,7 +141,7 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
 
   if (ISO) {
     const uint8_t* ph = R.phase + (R.phase_per_rve ? (long)b * ne : 0);
-    const double* mt = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * 2 : 0);
+    const double* mt = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * R.mat_stride : 0);
     for (int e = tid; e < ne; e += NTHR) {
       int p = ph[e];
       double E = mt[2 * p], nu = mt[2 * p + 1];

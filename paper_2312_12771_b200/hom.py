@@ -23,7 +23,7 @@ STATUS = {0: "HOM_OK", 1: "HOM_ERR_INVALID_ARG", 2: "HOM_ERR_MESH", 3: "HOM_ERR_
           7: "HOM_ERR_CUDA", 8: "HOM_ERR_OOM"}
 
 # every symbol include/hom.h declares (checked by tests/test_abi.py)
-EXPORTS = ["hom_setup", "hom_get_sizes", "hom_get_work", "hom_macro_assemble", "hom_macro_spmv", "hom_macro_kinematics", "hom_condense", "hom_macro_solve",
+EXPORTS = ["hom_setup", "hom_get_sizes", "hom_get_work", "hom_set_load_factor", "hom_macro_assemble", "hom_macro_spmv", "hom_macro_kinematics", "hom_condense", "hom_macro_solve",
            "hom_macro_residual_norm", "hom_recover_fluctuations", "hom_newton_update", "hom_set_fluctuations",
            "hom_get_fluctuations", "hom_micro_residual_max", "hom_set_phases", "hom_launch_count",
            "hom_profile_enable", "hom_profile_read", "hom_last_error", "hom_destroy"]
@@ -34,7 +34,8 @@ class MacroMesh(ctypes.Structure):
     _fields_ = [("dim", ctypes.c_int32), ("n_nodes", ctypes.c_int32), ("n_elems", ctypes.c_int32),
                 ("nodes_per_elem", ctypes.c_int32), ("coords", ctypes.c_void_p), ("conn", ctypes.c_void_p),
                 ("n_dirichlet", ctypes.c_int32), ("dirichlet_dof", ctypes.c_void_p),
-                ("dirichlet_value", ctypes.c_void_p), ("body_force", ctypes.c_void_p)]
+                ("dirichlet_value", ctypes.c_void_p), ("body_force", ctypes.c_void_p),
+                ("nodal_force", ctypes.c_void_p)]
 
 
 class RveMesh(ctypes.Structure):
@@ -112,6 +113,7 @@ def lib(build_if_missing: bool = True):
         L.hom_macro_solve.argtypes = [P, P, P, D, P, ctypes.POINTER(SolveInfo), P]
         L.hom_macro_residual_norm.argtypes = [P, P, ctypes.POINTER(ctypes.c_double), P]
         L.hom_macro_assemble.argtypes = [P, P, P]
+        L.hom_set_load_factor.argtypes = [P, D]
         L.hom_macro_spmv.argtypes = [P, P, P, P]
         L.hom_recover_fluctuations.argtypes = [P, P, P, P]
         L.hom_newton_update.argtypes = [P, P, P, P]
@@ -136,6 +138,16 @@ def _np_ptr(a):
     return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
 
 
+def _inner_done(inner, micro_tol):
+    """Classical-scheme inner RVE Newton converged (reading R21): max ||r_f|| < micro_tol,
+    or quadratic convergence has reached the round-off floor of the r_f sums (below 1e-9 and no
+    longer halving) -- the paper's 1e-13 is below that floor at Cook's stress levels."""
+    rf = inner[-1]
+    if rf < micro_tol:
+        return True
+    return len(inner) >= 2 and rf < 1e-9 and rf > 0.5 * inner[-2]
+
+
 class Homogenizer:
     """One context (hom_ctx) on the current CUDA device.
 
@@ -145,7 +157,8 @@ class Homogenizer:
 
     def __init__(self, macro_coords, macro_conn, dirichlet_dof, dirichlet_value, body_force,
                  rve_coords, rve_conn, phase, materials, kind="linear", cg_rtol=1e-13, cg_max_iter=20000,
-                 rve_chunk=0, check_info=True, mem_budget_gb=0.0, tile_sparse=False, rve_range=None):
+                 rve_chunk=0, check_info=True, mem_budget_gb=0.0, tile_sparse=False, rve_range=None,
+                 nodal_force=None):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("Homogenizer needs a CUDA device (no CPU fallback)")
@@ -162,6 +175,7 @@ class Homogenizer:
         mc, mconn = arr(macro_coords, np.float64), arr(macro_conn, np.int32)
         dd, dv = arr(dirichlet_dof, np.int32), arr(dirichlet_value, np.float64)
         bf = None if body_force is None else arr(body_force, np.float64)
+        nf = None if nodal_force is None else arr(nodal_force, np.float64)
         rc_, rconn = arr(rve_coords, np.float64), arr(rve_conn, np.int32)
         ph = arr(phase, np.uint8)
         mt = arr(materials, np.float64)
@@ -174,14 +188,15 @@ class Homogenizer:
             raise ValueError("materials must be [n_rve][n_phase][2] or [n_phase][2]")
         n_phase = mt.shape[-2]
         self.macro = MacroMesh(dim, mc.shape[0], mconn.shape[0], mconn.shape[1], _np_ptr(mc), _np_ptr(mconn),
-                               len(dd), _np_ptr(dd), _np_ptr(dv), _np_ptr(bf))
+                               len(dd), _np_ptr(dd), _np_ptr(dv), _np_ptr(bf), _np_ptr(nf))
         self.rve = RveMesh(dim, rc_.shape[0], rconn.shape[0], rconn.shape[1], _np_ptr(rc_), _np_ptr(rconn))
         self.phase = PhaseField(per_rve_phase, _np_ptr(ph))
-        self.mat = Materials(1 if kind == "nh" else 0, n_phase, per_rve_mat, _np_ptr(mt))
+        kinds = {"linear": 0, "nh": 1, "mr": 2}  # mr: the paper's Cook energy with beta
+        self.mat = Materials(kinds[kind], n_phase, per_rve_mat, _np_ptr(mt))
         rb, rn = (0, 0) if rve_range is None else (int(rve_range[0]), int(rve_range[1]) - int(rve_range[0]))
-        self.opt = Options(1 if kind == "nh" else 0, cg_rtol, cg_max_iter, rve_chunk, int(check_info), mem_budget_gb,
+        self.opt = Options(int(kind != "linear"), cg_rtol, cg_max_iter, rve_chunk, int(check_info), mem_budget_gb,
                            int(tile_sparse), rb, rn)
-        self.finite = kind == "nh"
+        self.finite = kind != "linear"
         h = ctypes.c_void_p()
         rc = L.hom_setup(ctypes.byref(h), ctypes.byref(self.macro), ctypes.byref(self.rve),
                          ctypes.byref(self.phase), ctypes.byref(self.mat), ctypes.byref(self.opt), self._stream())
@@ -207,7 +222,9 @@ class Homogenizer:
         rc_, rconn = wl.rve_mesh()
         phase = wl.phase if wl.phase.shape[0] > 1 else wl.phase[0]
         mat = wl.mat if wl.mat.shape[0] > 1 else wl.mat[0]
-        return cls(mc, mconn, wl.dir_dof, wl.dir_val, wl.body, rc_, rconn, phase, mat, kind=wl.kind, **kw)
+        nodal = getattr(wl, "nodal_force", None)
+        return cls(mc, mconn, wl.dir_dof, wl.dir_val, wl.body, rc_, rconn, phase, mat, kind=wl.kind,
+                   nodal_force=nodal, **kw)
 
     # ------------------------------------------------------------------ helpers
     def _stream(self):
@@ -255,6 +272,9 @@ class Homogenizer:
         self._check(lib().hom_macro_solve(self.h, self._ptr(D), self._ptr(S), float(scale), self._ptr(x),
                                           ctypes.byref(info), self._stream()), "hom_macro_solve")
         return x, info
+
+    def set_load_factor(self, lf):
+        self._check(lib().hom_set_load_factor(self.h, float(lf)), "hom_set_load_factor")
 
     def macro_assemble(self, D):
         self._check(lib().hom_macro_assemble(self.h, self._ptr(D), self._stream()), "hom_macro_assemble")
@@ -335,35 +355,105 @@ class Homogenizer:
         w = self.recover(u)
         return C, u, w, info
 
-    def newton(self, n_steps, tol=1e-11, max_iter=25, history=None):
-        """Finite-strain load stepping with the monolithic null-space Newton.
+    def newton(self, n_steps, tol=1e-11, max_iter=25, history=None, force_load=False, micro_tol=None,
+               divergence=1e10, raise_on_fail=True):
+        """Finite-strain load stepping with the monolithic null-space Newton (generalized scheme,
+        P:325-342, P:398-428).
 
         Per iteration: F = I + grad u; condense -> (A_eff, P_eff, <P>); check ||R_macro|| (with <P>)
-        and max ||r_f|| (reading R3); solve the condensed system for du (eq:solution2); update u and
-        w.  Returns u (device) and the per-step residual histories.
-        """
+        and max ||r_f|| (reading R3; micro_tol=None uses tol, micro_tol=inf checks the macro
+        residual only, as the paper's Cook study); solve the condensed system for du
+        (eq:solution2); update u and w.  Load steps: the Dirichlet values (default) or,
+        with force_load, the external load factor k/n_steps (T_k = k T / n_l).  Failure:
+        ||R_macro|| > divergence, a micro J <= 0, or max_iter.  Returns u (device) and the
+        per-step residual histories [(||R_macro||, max ||r_f||), ...]."""
         u = self.torch.zeros(self.n_dof, dtype=self.torch.float64, device="cuda")
         du = self.empty(self.n_dof)
+        mtol = tol if micro_tol is None else micro_tol
         hist_all = []
         for k in range(1, n_steps + 1):
+            if force_load:
+                self.set_load_factor(k / n_steps)
             hist = []
             converged = False
             for it in range(max_iter + 1):
                 F = self.macro_kinematics(u)
-                A, Pe, Pa = self.condense(F)
+                try:
+                    A, Pe, Pa = self.condense(F)
+                except HomError as e:
+                    if e.code != 4:
+                        raise
+                    hist.append((float("inf"), float("inf")))
+                    break
                 rn = self.macro_residual_norm(Pa)
                 rf = self.micro_residual_max()
                 hist.append((rn, rf))
-                if it > 0 and rn <= tol and rf <= tol:
+                if it > 0 and rn <= tol and rf <= mtol:
                     converged = True
                     break
-                if rn > 1e10 or it == max_iter:
+                if not (rn <= divergence) or it == max_iter:
                     break
-                self.macro_solve(A, Pe, scale=(1.0 / n_steps) if it == 0 else 0.0, x=du)
+                scale = (1.0 / n_steps) if (it == 0 and not force_load) else 0.0
+                self.macro_solve(A, Pe, scale=scale, x=du)
                 self.newton_update(u, du)
             hist_all.append(hist)
             if history is not None:
                 history.append(hist)
             if not converged:
-                raise HomError(5, None, f"Newton did not converge in load step {k}: {hist[-1]}")
+                if raise_on_fail:
+                    raise HomError(5, None, f"Newton did not converge in load step {k}: {hist[-1]}")
+                return u, hist_all
         return u, hist_all
+
+    def newton_classical(self, n_steps, tol=1e-9, micro_tol=1e-13, max_iter=25, max_inner=30, divergence=1e10,
+                         force_load=True, predictor=True):
+        """Classical staggered FE^2 scheme for comparison with the generalized one:
+        every macro iteration first equilibrates all RVEs at the fixed macro deformation
+        (batched inner Newton on R_micro: w <- w - K_ff^-1 r_f until max ||r_f|| < micro_tol),
+        then solves [K - D L^-1 E] dq = -R_macro (eq:solution1, no -D L^-1 R_micro term),
+        updates q and w with eq:reduction (dw = -L^-1 E dq) and restarts until
+        ||R_macro|| < tol; failure if ||R_macro|| > divergence, J <= 0 or no convergence.
+        Returns (u, histories [(||R_macro||, [inner max ||r_f||, ...]), ...] per step, ok)."""
+        u = self.torch.zeros(self.n_dof, dtype=self.torch.float64, device="cuda")
+        du = self.empty(self.n_dof)
+        zero = self.torch.zeros(self.n_dof, dtype=self.torch.float64, device="cuda")
+        hist_all = []
+        for k in range(1, n_steps + 1):
+            if force_load:
+                self.set_load_factor(k / n_steps)
+            hist = []
+            converged = False
+            for it in range(max_iter + 1):
+                F = self.macro_kinematics(u)
+                inner = []
+                try:
+                    for _ in range(max_inner + 1):
+                        A, Pe, Pa = self.condense(F)
+                        rf = self.micro_residual_max()
+                        inner.append(rf)
+                        if _inner_done(inner, micro_tol) or not (rf <= divergence):
+                            break
+                        self.newton_update(u, zero)  # w -= K_ff^-1 r_f at fixed F
+                except HomError as e:
+                    if e.code != 4:
+                        raise
+                    hist.append((float("inf"), inner))
+                    break
+                rn = self.macro_residual_norm(Pa)
+                hist.append((rn, inner))
+                if not _inner_done(inner, micro_tol):
+                    break
+                if it > 0 and rn <= tol:
+                    converged = True
+                    break
+                if not (rn <= divergence) or it == max_iter:
+                    break
+                self.macro_solve(A, Pa, scale=0.0, x=du)
+                if predictor:
+                    self.newton_update(u, du)  # q += dq; w += -L^-1 E dq (r_f ~ 0 after the inner loop)
+                else:  # variant without the eq:reduction predictor: q += dq only
+                    u.add_(du)
+            hist_all.append(hist)
+            if not converged:
+                return u, hist_all, False
+        return u, hist_all, True

@@ -89,7 +89,7 @@ class Workload:
     dim: int
     nel: int               # macro cells per direction
     r: int                 # RVE cells per direction
-    kind: str              # "linear" (E, nu) or "nh" (alpha, kappa)
+    kind: str              # "linear" (E, nu), "nh" (alpha, kappa) or "mr" (alpha, beta, kappa)
     phase: np.ndarray      # [n_rve | 1][r^dim] uint8
     mat: np.ndarray        # [n_rve | 1][n_phase][2] float64
     dir_dof: np.ndarray    # int32 Dirichlet DOFs (node*dim + comp)
@@ -97,6 +97,10 @@ class Workload:
     body: np.ndarray | None
     n_steps: int = 1
     description: str = ""
+    macro_coords: np.ndarray | None = None   # mapped (non-rectangular) macro grid; None = [0,1]^dim
+    nodal_force: np.ndarray | None = None    # [n_dof] external nodal forces (surface tractions)
+    rve_size: float = 1.0
+    rve_origin: float = 0.0
 
     @property
     def n_qp(self) -> int:
@@ -120,15 +124,17 @@ class Workload:
 
     @property
     def m(self) -> int:
-        if self.kind == "nh":
+        if self.kind in ("nh", "mr"):
             return self.dim * self.dim
         return {1: 1, 2: 3, 3: 6}[self.dim]
 
     def macro_mesh(self):
-        return grid_mesh(self.dim, self.nel)
+        coords, conn = grid_mesh(self.dim, self.nel)
+        return (coords if self.macro_coords is None else self.macro_coords), conn
 
     def rve_mesh(self):
-        return grid_mesh(self.dim, self.r)
+        coords, conn = grid_mesh(self.dim, self.r, self.rve_size)
+        return np.ascontiguousarray(coords + self.rve_origin), conn
 
     def flop_per_rve(self) -> float:
         """Dense condensation flops counted on n_f: n^3/3 + 2 n^2 m + n m^2."""
@@ -209,6 +215,43 @@ def config5(nel: int = 32, r: int = 16, n_steps: int = 10, stretch: float = 0.1)
     v = np.concatenate([vl, np.full(len(dr), stretch)])
     return Workload("cfg5_neohooke", 2, nel, r, "nh", phase, mat, d, v, None, n_steps=n_steps,
                     description="2-D finite-strain Neo-Hookean disc, right edge stretched to 1.1 in 10 steps")
+
+
+COOK_CORNERS = np.array([[0.0, 0.0], [480.0, 440.0], [480.0, 600.0], [0.0, 440.0]])  # P1..P4
+COOK_TRACTION = np.array([-5.0, 10.0])  # on the right edge Gamma^sigma_r (eq:load)
+COOK_MATERIALS = np.array([[27.0, 18.0, 60.0], [13.5, 6.5, 30.0]])  # (alpha, beta, kappa)
+
+
+def cook(nel: int = 20, r: int = 30, n_steps: int = 22) -> Workload:
+    """Cook's membrane of PAPER.md §4.2: the trapezoid P1 (0,0), P2 (480,440),
+    P3 (480,600), P4 (0,440) meshed with nel x nel bilinear Q1 (the image of the uniform grid
+    under the bilinear map of the corners), left edge X1 = 0 fixed, traction T = (-5, 10) on the
+    right edge as consistent nodal forces (exact for the constant traction and linear edge
+    shape functions), one periodic RVE (-3,3)^2 with r x r Q1 per macro Gauss point (Dirac
+    basis), a centred cross of width 2 of material 2 (by element centroid) in material 1, the
+    paper's energy with beta (kind "mr"), T_k = k T / n_steps."""
+    coords, conn = grid_mesh(2, nel)
+    xi, eta = coords[:, 0], coords[:, 1]
+    P = COOK_CORNERS
+    X = (np.outer((1 - xi) * (1 - eta), P[0]) + np.outer(xi * (1 - eta), P[1]) + np.outer(xi * eta, P[2]) +
+         np.outer((1 - xi) * eta, P[3]))
+    left = face_nodes(2, nel, 0, 0)
+    d = np.array([2 * n + c for n in left for c in (0, 1)], np.int32)
+    f = np.zeros((nel + 1) ** 2 * 2)
+    right = face_nodes(2, nel, 0, nel)  # ordered by eta
+    ys = X[right, 1]
+    seg = np.diff(ys)
+    wgt = np.zeros(len(right))
+    wgt[:-1] += seg / 2
+    wgt[1:] += seg / 2
+    for n, wv in zip(right, wgt):
+        f[2 * n:2 * n + 2] += wv * COOK_TRACTION
+    c = (centroids(2, r) - 0.5) * 6.0  # element centroids in (-3,3)^2
+    phase = ((np.abs(c[:, 0]) < 1.0) | (np.abs(c[:, 1]) < 1.0)).astype(np.uint8)[None]
+    return Workload("cook", 2, nel, r, "mr", phase, COOK_MATERIALS[None].copy(), d, np.zeros(len(d)), None,
+                    n_steps=n_steps, description=f"Cook's membrane, {nel}x{nel} macro Q1, RVE {r}x{r} cross, "
+                                                 f"{n_steps} load steps",
+                    macro_coords=np.ascontiguousarray(X), nodal_force=f, rve_size=6.0, rve_origin=-3.0)
 
 
 CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}

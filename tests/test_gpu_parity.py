@@ -323,3 +323,95 @@ def test_large_macro_grid_pcg_matches_direct_solve(torch_cuda):
     assert rel(u.cpu().numpy(), u_direct) <= TOL_U
     u2, _ = h.macro_solve(C)
     assert np.array_equal(u.cpu().numpy(), u2.cpu().numpy())  # deterministic reductions
+
+
+# ------------------------------------------------------------------ Cook's membrane (§4.2)
+def _cook_small(n_steps=2):
+    return W.cook(nel=3, r=6, n_steps=n_steps)
+
+
+def test_cook_condense_per_state_matches_oracle(torch_cuda):
+    """Cook energy with beta (kind "mr"), RVE (-3,3)^2 cross, mapped macro mesh: A_eff, P_eff, <P>
+    at a non-equilibrium state <= 1e-10; one macro solve with the traction load <= 1e-8."""
+    import torch
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = _cook_small()
+    mesh = wl.macro_mesh()
+    rng = np.random.default_rng(5)
+    u = 0.05 * rng.standard_normal(wl.n_dof)
+    u[wl.dir_dof] = 0.0
+    w = 0.02 * rng.standard_normal((wl.n_rve, wl.n_pad))
+    w[:, :2] = 0.0
+    G = oracle.macro_kin(2, wl.nel, u, kind=1, mesh=mesh) + np.array([1.0, 0, 0, 1.0])
+    c = oracle.condense_batch_nh(wl.r, wl.phase, wl.mat, G, w, L=6.0)
+    for ts in (False, True):
+        h = Homogenizer.from_workload(wl, tile_sparse=ts)
+        h.set_load_factor(0.5)
+        h.set_fluctuations(torch.tensor(w, device="cuda"))
+        F = h.macro_kinematics(torch.tensor(u, device="cuda"))
+        assert rel(F.cpu().numpy(), G) <= 1e-14
+        A, Pe, Pa = h.condense(F)
+        assert rel(A.cpu().numpy(), c["A_eff"]) <= TOL_C
+        assert rel(Pe.cpu().numpy(), c["P_eff"]) <= TOL_C
+        assert rel(Pa.cpu().numpy(), c["P_avg"]) <= TOL_C
+        free = np.ones(wl.n_dof, bool)
+        free[wl.dir_dof] = False
+        R = oracle.macro_residual(2, wl.nel, c["P_avg"], None, kind=1, mesh=mesh, fext=0.5 * wl.nodal_force)
+        assert abs(h.macro_residual_norm(Pa) - np.linalg.norm(R[free])) <= 1e-10 * np.linalg.norm(R[free])
+        du, _ = h.macro_solve(A, Pe, scale=0.0)
+        du_o = oracle.macro_solve(2, wl.nel, c["A_eff"], wl.dir_dof, np.zeros(len(wl.dir_dof)), S=c["P_eff"],
+                                  kind=1, mesh=mesh, fext=0.5 * wl.nodal_force)
+        assert rel(du.cpu().numpy(), du_o) <= TOL_U
+
+
+def test_cook_generalized_newton_matches_oracle(torch_cuda):
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = _cook_small(n_steps=3)
+    o = oracle.newton_nh(wl, tol=1e-9, micro_tol=float("inf"))
+    assert all(s["converged"] for s in o)
+    h = Homogenizer.from_workload(wl, tile_sparse=True)
+    u, hist = h.newton(wl.n_steps, tol=1e-9, micro_tol=float("inf"), force_load=True)
+    assert rel(u.cpu().numpy(), o[-1]["u"]) <= TOL_U
+    assert [len(s) for s in hist] == [len(s["history"]) for s in o]  # same iteration counts
+
+
+def test_cook_classical_newton_matches_oracle(torch_cuda):
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = _cook_small(n_steps=3)
+    o = oracle.newton_classical(wl, tol=1e-9, micro_tol=1e-11)
+    assert all(s["converged"] for s in o)
+    h = Homogenizer.from_workload(wl, tile_sparse=True)
+    u, hist, ok = h.newton_classical(wl.n_steps, tol=1e-9, micro_tol=1e-11)
+    assert ok
+    assert rel(u.cpu().numpy(), o[-1]["u"]) <= TOL_U
+    assert [len(s) for s in hist] == [len(s["history"]) for s in o]
+
+
+def test_cook_table1_generalized_iteration_counts(torch_cuda):
+    """PAPER.md Table 1, full Cook's membrane (20x20 macro, 1600 RVEs of 30x30): the
+    generalized scheme needs 6 Newton iterations per load step at n_l = 2 and 4 at n_l = 22
+    (tests/golden/table1_newton.json), with quadratic decay of ||R_macro|| (Table 2)."""
+    import json
+    import os
+    from paper_2312_12771_b200.hom import Homogenizer
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table1_newton.json")))
+    want = dict(zip(gold["n_l"], gold["generalized_iterations"]))
+    for n_l in (2, 22):
+        wl = W.cook(n_steps=n_l)
+        h = Homogenizer.from_workload(wl, tile_sparse=True)
+        _, hist = h.newton(n_l, tol=1e-9, micro_tol=float("inf"), max_iter=30, force_load=True)
+        assert [len(s) - 1 for s in hist] == [want[n_l]] * n_l
+        r = [x[0] for x in hist[0]]
+        assert r[-1] <= 1e-9 and r[-2] <= 1e-4 and r[-2] ** 1.7 >= r[-1]  # quadratic tail
+
+
+def test_cook_classical_and_generalized_reach_the_same_state(torch_cuda):
+    """Both schemes solve the same discrete two-scale problem: equal converged u (n_l = 22)."""
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = W.cook(nel=8, r=12, n_steps=4)
+    h = Homogenizer.from_workload(wl, tile_sparse=True)
+    u_g, _ = h.newton(4, tol=1e-9, micro_tol=1e-11, force_load=True)
+    h2 = Homogenizer.from_workload(wl, tile_sparse=True)
+    u_c, _, ok = h2.newton_classical(4, tol=1e-9, micro_tol=1e-13)
+    assert ok
+    assert rel(u_c.cpu().numpy(), u_g.cpu().numpy()) <= 1e-8

@@ -421,3 +421,76 @@ def test_bench1d_convergence_orders():
     p_w = np.polyfit(np.log(hs), np.log(e[:, 1]), 1)[0]
     assert p_phi >= g["err_phi_min"], p_phi
     assert abs(p_w - g["err_w"]) <= g["err_w_tol"], p_w
+
+
+# ------------------------------------------------------------------ Cook energy with beta
+COOK_MAT = [(27.0, 18.0, 60.0), (13.5, 6.5, 30.0)]  # (alpha, beta, kappa)
+
+
+def _mr3d_energy(F2, alpha, beta, kappa):
+    """Independent reference: the 3-D polyconvex Mooney-Rivlin energy of eq:MR,
+    Psi = alpha (F:F - 3) + beta (H:H - 3) + kappa/2 (J - 1)^2 - 2 (alpha + 2 beta) ln J with
+    H = cof F = J F^-T (numpy inverse), evaluated on the plane-strain embedding F33 = 1."""
+    F = np.eye(3)
+    F[:2, :2] = F2.reshape(2, 2)
+    J = np.linalg.det(F)
+    H = J * np.linalg.inv(F).T
+    return (alpha * (np.sum(F * F) - 3) + beta * (np.sum(H * H) - 3) + 0.5 * kappa * (J - 1) ** 2
+            - 2 * (alpha + 2 * beta) * np.log(J))
+
+
+def test_cook_energy_is_plane_strain_mooney_rivlin_and_fd_consistent():
+    """The paper's 2-D Cook energy equals the 3-D eq:MR energy on the plane-strain embedding
+    (H:H = F:F + J^2 there), is stress free at I, and its P, A are the FD derivatives."""
+    for a, b, k in COOK_MAT:
+        psi, P, _ = oracle.nh_material(np.array([1.0, 0, 0, 1.0]), a, k, beta=b)
+        assert abs(psi) < 1e-14 and np.abs(P).max() < 1e-12
+    rng = np.random.default_rng(7)
+    h = 1e-6
+    for _ in range(20):
+        F = np.array([1.0, 0, 0, 1.0]) + 0.2 * rng.standard_normal(4)
+        a, b, k = 1 + 30 * rng.random(), 20 * rng.random(), 10 + 60 * rng.random()
+        psi, P, A = oracle.nh_material(F, a, k, beta=b)
+        assert abs(psi - _mr3d_energy(F, a, b, k)) <= 1e-12 * max(1.0, abs(psi))
+        for j in range(4):
+            dF = np.zeros(4)
+            dF[j] = h
+            pp, Pp, _ = oracle.nh_material(F + dF, a, k, beta=b)
+            pm, Pm, _ = oracle.nh_material(F - dF, a, k, beta=b)
+            # P from the independent 3-D energy as well as from the oracle's own energy
+            p3 = (_mr3d_energy(F + dF, a, b, k) - _mr3d_energy(F - dF, a, b, k)) / (2 * h)
+            assert abs(p3 - P[j]) < 1e-6 * max(1, abs(P[j]))
+            assert abs((pp - pm) / (2 * h) - P[j]) < 1e-6 * max(1, abs(P[j]))
+            np.testing.assert_allclose((Pp - Pm) / (2 * h), A[:, j], rtol=1e-6, atol=1e-5)
+        np.testing.assert_allclose(A, A.T, atol=1e-12)
+
+
+def test_cook_linearisation_mu_lambda():
+    """A(I) is isotropic with mu = 2 (alpha + beta), lambda = kappa + 4 beta (derived):
+    (mu, lambda) = (90, 132) and (40, 56) for the two Cook materials."""
+    d = np.eye(2)
+    for (a, b, k), (mu, lam) in zip(COOK_MAT, [(90.0, 132.0), (40.0, 56.0)]):
+        _, _, A = oracle.nh_material(np.array([1.0, 0, 0, 1.0]), a, k, beta=b)
+        ref = (lam * np.einsum("ij,kl->ijkl", d, d) + mu * (np.einsum("ik,jl->ijkl", d, d)
+                                                            + np.einsum("il,jk->ijkl", d, d))).reshape(4, 4)
+        np.testing.assert_allclose(A, ref, atol=1e-12)
+
+
+def test_cook_rve_at_reference_equals_linear_condensation():
+    """At F = I, w = 0 the finite-strain tangent of the Cook cross RVE equals the small-strain
+    C_eff of the same RVE with the linearised moduli (mu, lambda), in full-gradient form."""
+    from paper_2312_12771_b200 import workloads as W
+    wl = W.cook(nel=1, r=6)
+    c = oracle.condense_batch_nh(wl.r, wl.phase, wl.mat, np.array([[1.0, 0, 0, 1.0]]), L=6.0)
+    # linear: E, nu from (mu, lambda) in plane strain: nu = lam / (2 (lam + mu)), E = 2 mu (1 + nu)
+    mat = []
+    for mu, lam in [(90.0, 132.0), (40.0, 56.0)]:
+        nu = lam / (2 * (lam + mu))
+        mat.append([2 * mu * (1 + nu), nu])
+    C = oracle.condense_batch_linear(2, wl.r, wl.phase, np.array([mat]), 1)[0]
+    A = c["A_eff"][0]
+    # Voigt [e11, e22, g12] vs gradient [F11, F12, F21, F22]: A_{11,11} = C11, A_{11,22} = C12,
+    # A_{22,22} = C22, A_{12,12} = A_{12,21} = C33 (symmetric part)
+    np.testing.assert_allclose([A[0, 0], A[0, 3], A[3, 3], A[1, 1], A[1, 2]],
+                               [C[0, 0], C[0, 1], C[1, 1], C[2, 2], C[2, 2]], rtol=1e-12)
+    np.testing.assert_allclose(c["P_avg"][0], 0.0, atol=1e-12)
