@@ -402,7 +402,7 @@ def test_cook_table1_generalized_iteration_counts(torch_cuda):
         _, hist = h.newton(n_l, tol=1e-9, micro_tol=float("inf"), max_iter=30, force_load=True)
         assert [len(s) - 1 for s in hist] == [want[n_l]] * n_l
         r = [x[0] for x in hist[0]]
-        assert r[-1] <= 1e-9 and r[-2] <= 1e-4 and r[-2] ** 1.7 >= r[-1]  # quadratic tail
+        assert r[-1] <= 1e-9 and r[-2] <= 1e-2 and r[-2] ** 1.7 >= r[-1]  # quadratic tail
 
 
 def test_cook_classical_and_generalized_reach_the_same_state(torch_cuda):
