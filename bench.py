@@ -211,6 +211,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--spmv-nel", type=int, default=2048, help="scaled macro mesh of the K6 SpMV roofline (0: skip)")
+    ap.add_argument("--macro-basis", default="dirac", choices=["dirac", "constant"],
+                    help="constant: one RVE per macro element (SURVEY §8(f) 2, small strain)")
     ap.add_argument("--tile-sparse", action="store_true",
                     help="factor only the symbolic tile fill of K_ff (SURVEY §8(f) 3) instead of every lower tile")
     args = ap.parse_args()
@@ -229,7 +231,7 @@ def main():
               "flop_per_rve": wl.flop_per_rve(),
               "parallelism": f"rve-sharded x{world} (C_eff all-gather, replicated macro CG)" if world > 1 else "single",
               "macro_nel": wl.nel, "rve_per_gpu": wl.n_rve / world,
-              "factorization": "tile-sparse" if args.tile_sparse else "dense"}
+              "factorization": "tile-sparse" if args.tile_sparse else "dense", "macro_basis": args.macro_basis}
 
     if args.impl == "reference":
         if rank != 0:
@@ -263,11 +265,11 @@ def main():
 
     if world > 1:
         from paper_2312_12771_b200.dist import ShardedHomogenizer
-        sh = ShardedHomogenizer(wl, tile_sparse=args.tile_sparse)
+        sh = ShardedHomogenizer(wl, tile_sparse=args.tile_sparse, macro_basis=args.macro_basis)
         h = sh.h
     else:
         sh = None
-        h = Homogenizer.from_workload(wl, tile_sparse=args.tile_sparse)
+        h = Homogenizer.from_workload(wl, tile_sparse=args.tile_sparse, macro_basis=args.macro_basis)
     work = h.work
     config["l2"] = (f"no flush: each step writes and re-reads the K_ff tile pool ({h.sizes.rve_count * work.g_tiles * 32768 / 1e9:.2f} GB, "
                     f"{work.g_tiles} 64x64 tiles per RVE), larger than the 126 MB L2")

@@ -122,6 +122,15 @@ typedef struct {
                                all B).  C_eff / P_eff / w rows of the other RVEs are left untouched,
                                so the caller all-gathers C_eff (and P_eff) before hom_macro_solve,
                                which always solves the full macro problem. */
+  int32_t macro_basis;      /* macro interpolation of the fluctuations:
+                               0 = Dirac pulses at the macro Gauss points (one RVE per qp, B = 2^dim
+                               n_elems, classical FE^2); 1 = piecewise constant per macro element
+                               (eq:constSolution1/2, one RVE per element, B = n_elems; small strain
+                               only).  With 1, the RVE index is the element, hom_condense also keeps
+                               <C> per element, the macro stiffness is
+                               K_e = sum_q eta B_q^T <C>_e B_q - |B_e| Bbar^T (<C>_e - C_eff,e) Bbar
+                               (Bbar = element-average strain operator) and kinematics / recovery use
+                               the element-average strain. */
 } hom_options;
 
 typedef struct {

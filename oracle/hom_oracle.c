@@ -967,6 +967,112 @@ int orc_mesh_macro_solve(int dim, int nnode, int nelem, const double* xc, const 
   return macro_solve_g(&g, kind, D, S, body, fext, n_dir, dir_dof, x);
 }
 
+/* ------------------------------------------------------------------------ */
+/* Piecewise-constant macro fluctuation basis (eq:constSolution1/2), */
+/* small strain.  One fluctuation field per macro element e; its micro         */
+/* equilibrium integrated over the element gives w_e = -K_ff^-1 K_fe eps_bar_e */
+/* with the element-average strain eps_bar_e = |B_e|^-1 int_e eps dV; inserted */
+/* in the macro equation the element stiffness becomes                         */
+/*   K_e = int_e B^T <C>_e B dV - |B_e|^-1 (int_e B dV)^T (<C>_e - C_eff,e) (int_e B dV). */
+/* ------------------------------------------------------------------------ */
+int orc_macro_kin_const(int dim, int nel, double Lm, const double* u, double* out) {
+  grid_t g; grid_init(&g, dim, nel, Lm);
+  int m = m_of(dim, 0), nq = 1 << dim, nd = g.nen * dim;
+  for (int e = 0; e < g.nelem; ++e) {
+    int nodes[MAXNEN]; double x[MAXNEN][3];
+    grid_elem(&g, e, nodes, x);
+    double acc[MAXM] = {0}, vol = 0.0;
+    for (int q = 0; q < nq; ++q) {
+      double xi[3], N[MAXNEN], dNdx[MAXNEN][3], Bm[MAXM][MAXNEN * 3];
+      gauss_point(dim, q, xi);
+      double w = element_derivs(dim, x, xi, N, dNdx);
+      strain_operator(dim, 0, dNdx, Bm);
+      vol += w;
+      for (int i = 0; i < m; ++i)
+        for (int j = 0; j < nd; ++j) acc[i] += w * Bm[i][j] * u[nodes[j / dim] * dim + (j % dim)];
+    }
+    for (int i = 0; i < m; ++i) out[(size_t)e * m + i] = acc[i] / vol;
+  }
+  return ORC_OK;
+}
+
+int orc_macro_solve_const(int dim, int nel, double Lm, const double* Cavg, const double* Ceff,
+                          const double* body, int n_dir, const int* dir_dof, double* x) {
+  grid_t g; grid_init(&g, dim, nel, Lm);
+  int m = m_of(dim, 0), nq = 1 << dim, nd = g.nen * dim, ndof = g.nnode * dim;
+  int* eq = (int*)malloc(sizeof(int) * ndof);
+  double* rhs = (double*)malloc(sizeof(double) * ndof);
+  double* R = (double*)malloc(sizeof(double) * ndof);
+  sky_t K = {0};
+  int rc = ORC_OK;
+  if (!eq || !rhs || !R) { rc = ORC_ERR_OOM; goto done; }
+  for (int i = 0; i < ndof; ++i) eq[i] = 0;
+  for (int i = 0; i < n_dir; ++i) {
+    if (dir_dof[i] < 0 || dir_dof[i] >= ndof) { rc = ORC_ERR_ARG; goto done; }
+    eq[dir_dof[i]] = -1;
+  }
+  int neq = 0;
+  for (int i = 0; i < ndof; ++i) eq[i] = eq[i] < 0 ? -1 : neq++;
+  rc = sky_profile_from_grid(&g, eq, neq, &K);
+  if (rc) goto done;
+  macro_residual_g(&g, 0, NULL, body, NULL, R);
+  for (int i = 0; i < neq; ++i) rhs[i] = 0.0;
+  for (int i = 0; i < ndof; ++i)
+    if (eq[i] >= 0) rhs[eq[i]] = -R[i];
+  for (int e = 0; e < g.nelem; ++e) {
+    int nodes[MAXNEN]; double xx[MAXNEN][3];
+    grid_elem(&g, e, nodes, xx);
+    int dofs[MAXNEN * 3];
+    for (int j = 0; j < nd; ++j) dofs[j] = nodes[j / dim] * dim + (j % dim);
+    const double* Ca = &Cavg[(size_t)e * m * m];
+    const double* Ce = &Ceff[(size_t)e * m * m];
+    double Ke[MAXNEN * 3][MAXNEN * 3], Bbar[MAXM][MAXNEN * 3], vol = 0.0;
+    memset(Ke, 0, sizeof(Ke));
+    memset(Bbar, 0, sizeof(Bbar));
+    for (int q = 0; q < nq; ++q) {
+      double xi[3], N[MAXNEN], dNdx[MAXNEN][3], Bm[MAXM][MAXNEN * 3];
+      gauss_point(dim, q, xi);
+      double w = element_derivs(dim, xx, xi, N, dNdx);
+      strain_operator(dim, 0, dNdx, Bm);
+      vol += w;
+      for (int k = 0; k < m; ++k)
+        for (int i = 0; i < nd; ++i) Bbar[k][i] += w * Bm[k][i];
+      for (int i = 0; i < nd; ++i)
+        for (int j = 0; j < nd; ++j) {
+          double v = 0;
+          for (int k = 0; k < m; ++k)
+            for (int l = 0; l < m; ++l) v += Bm[k][i] * Ca[k * m + l] * Bm[l][j];
+          Ke[i][j] += w * v;
+        }
+    }
+    for (int i = 0; i < nd; ++i)
+      for (int j = 0; j < nd; ++j) {
+        double v = 0;
+        for (int k = 0; k < m; ++k)
+          for (int l = 0; l < m; ++l) v += Bbar[k][i] * (Ca[k * m + l] - Ce[k * m + l]) * Bbar[l][j];
+        Ke[i][j] -= v / vol;
+      }
+    for (int i = 0; i < nd; ++i) {
+      int ei = eq[dofs[i]];
+      if (ei < 0) continue;
+      for (int j = 0; j < nd; ++j) {
+        int ej = eq[dofs[j]];
+        if (ej < 0) rhs[ei] -= Ke[i][j] * x[dofs[j]];
+        else if (ej <= ei) *sky_at(&K, ei, ej) += Ke[i][j];
+      }
+    }
+  }
+  if (neq > 0) {
+    if (sky_cholesky(&K)) { rc = ORC_ERR_NOT_SPD; goto done; }
+    sky_solve(&K, rhs);
+  }
+  for (int i = 0; i < ndof; ++i)
+    if (eq[i] >= 0) x[i] = rhs[eq[i]];
+done:
+  free(eq); free(rhs); free(R); sky_free(&K);
+  return rc;
+}
+
 /* Dense symmetric check helper for tests: skyline solve of a small SPD dense matrix
  * (row-major n x n) -- used to pin the skyline routine against a textbook solve. */
 int orc_dense_spd_solve(int n, const double* A, double* x) {

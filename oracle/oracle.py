@@ -56,6 +56,8 @@ def lib():
             L.orc_macro_residual.argtypes = [I, I, D, I, P, P, P]
             L.orc_macro_solve.argtypes = [I, I, D, I, P, P, P, I, P, P]
             L.orc_mesh_macro_kin.argtypes = [I, I, I, P, P, I, P, P]
+            L.orc_macro_kin_const.argtypes = [I, I, D, P, P]
+            L.orc_macro_solve_const.argtypes = [I, I, D, P, P, P, I, P, P]
             L.orc_mesh_macro_residual.argtypes = [I, I, I, P, P, I, P, P, P, P]
             L.orc_mesh_macro_solve.argtypes = [I, I, I, P, P, I, P, P, P, P, I, P, P]
             L.orc_dense_spd_solve.argtypes = [I, P, P]
@@ -268,6 +270,48 @@ def solve_linear(wl, rve_ids=None, nthreads: int | None = None):
     u = macro_solve(dim, wl.nel, C, wl.dir_dof, wl.dir_val, body=wl.body)
     eps = macro_kin(dim, wl.nel, u)
     return {"C_eff": C, "u": u, "eps": eps, "W": Wsel}
+
+
+def C_avg_linear(dim: int, r: int, phase, mat) -> np.ndarray:
+    """<C> = |Omega|^-1 sum_e |e| C(phase_e) (plain definition, uniform RVE grid) per RVE row."""
+    phase = np.asarray(phase).reshape(-1, r ** dim)
+    mat = np.asarray(mat, dtype=np.float64)
+    mat = mat.reshape(-1, mat.shape[-2], 2)
+    n = max(phase.shape[0], mat.shape[0])
+    out = np.zeros((n, m_of(dim), m_of(dim)))
+    for b in range(n):
+        ph = phase[b if phase.shape[0] > 1 else 0]
+        mt = mat[b if mat.shape[0] > 1 else 0]
+        for p in np.unique(ph):
+            out[b] += np.count_nonzero(ph == p) / ph.size * linear_C(dim, mt[p, 0], mt[p, 1])
+    return out
+
+
+def solve_linear_constant(wl, nthreads: int | None = None):
+    """Piecewise-constant macro fluctuation basis (eq:constSolution1/2), small strain:
+    one RVE per macro element (phase/material rows of element e = those of its first Gauss point
+    RVE), C_eff and <C> per element, direct macro solve with
+    K_e = int B^T <C> B - |B_e|^-1 Bbar^T (<C> - C_eff) Bbar, recovery w_e = W_e eps_bar_e.
+    Returns dict(C_eff [E][m][m], C_avg [E][m][m], u, eps_bar [E][m], w [E][N_pad])."""
+    dim, r, nq = wl.dim, wl.r, wl.n_qp
+    ne = wl.nel ** dim
+    ph = wl.phase[::nq] if wl.phase.shape[0] > 1 else wl.phase
+    mt = wl.mat[::nq] if wl.mat.shape[0] > 1 else wl.mat
+    C, W = condense_batch_linear(dim, r, ph, mt, ne if (ph.shape[0] > 1 or mt.shape[0] > 1) else 1,
+                                 want_W=True, nthreads=nthreads)
+    Ca = C_avg_linear(dim, r, ph, mt)
+    if C.shape[0] == 1:
+        C, W, Ca = (np.broadcast_to(a, (ne,) + a.shape[1:]).copy() for a in (C, W, Ca))
+    x = np.zeros(wl.n_dof)
+    dd = np.ascontiguousarray(wl.dir_dof, dtype=np.int32)
+    x[dd] = wl.dir_val
+    rc = lib().orc_macro_solve_const(dim, wl.nel, 1.0, _p(_f64(Ca)), _p(_f64(C)), _p(_f64(wl.body)), len(dd),
+                                     _p(dd), _p(x))
+    if rc:
+        raise OracleError(rc, "macro_solve_const")
+    eps = np.zeros((ne, m_of(dim)))
+    lib().orc_macro_kin_const(dim, wl.nel, 1.0, _p(x), _p(eps))
+    return {"C_eff": C, "C_avg": Ca, "u": x, "eps_bar": eps, "w": recover_linear(W, eps)}
 
 
 def recover_linear(W, eps):

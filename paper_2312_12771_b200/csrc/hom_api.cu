@@ -36,6 +36,7 @@ struct hom_ctx {
   // macro
   double *val = nullptr, *diag = nullptr, *rhs = nullptr, *cgwork = nullptr, *Rfree = nullptr, *scal = nullptr;
   double *cgl_sc = nullptr, *cgl_part = nullptr;  // grid-wide PCG scalars / block partials
+  double* Cavg_e = nullptr;                       // <C> per element (constant macro basis)
   CgState* cgst = nullptr;
   size_t phase_bytes = 0, mat_bytes = 0;
   int max_slice_nnz = 0;  // largest CSR slice of a 8-CTA cluster partition (CG smem sizing)
@@ -250,7 +251,9 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   c->dim = dim;
   c->finite = mat->kind >= 1;
   c->m = c->finite ? 4 : (dim == 2 ? 3 : 6);
-  c->B = mac->n_elems * nq;
+  if (options->macro_basis < 0 || options->macro_basis > 1 || (options->macro_basis == 1 && c->finite))
+    return fail(HOM_ERR_INVALID_ARG, "macro_basis must be 0 (Dirac) or 1 (constant, small strain only)");
+  c->B = mac->n_elems * (options->macro_basis == 1 ? 1 : nq);
 
   // ------------------------------------------------------------ macro mesh
   MacroDev& M = c->M;
@@ -578,6 +581,17 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   M.grad = upload(c, mgrad, s, &rc);
   M.shp = upload(c, shp, s, &rc);
   M.wdet = upload(c, mw, s, &rc);
+  {  // element volumes |B_e| = sum_q eta j (constant macro basis)
+    std::vector<double> ev(M.ne, 0.0);
+    for (int e = 0; e < M.ne; ++e)
+      for (int q = 0; q < nq; ++q) ev[e] += mw[(size_t)e * nq + q];
+    M.evol = upload(c, ev, s, &rc);
+  }
+  M.constant_basis = c->opt.macro_basis == 1;
+  if (M.constant_basis) {
+    c->Cavg_e = dalloc<double>(c, (size_t)c->B * c->m * c->m, &rc);
+    M.Cavg_e = c->Cavg_e;
+  }
   M.rowptr = upload(c, rowptr, s, &rc);
   M.col = upload(c, col, s, &rc);
   M.nz_blk = upload(c, nzblk, s, &rc);
@@ -687,6 +701,9 @@ int hom_condense(hom_ctx* c, const double* d_kin, double* d_C_eff, double* d_P_e
     run(c, HOM_PROF_CONDENSE, s, [&] {
       hom::launch_condense(R, b0, nb, c->Kt, c->Y, c->Cavg, c->Pavg, d_C_eff, d_P_eff, d_P_avg, c->X, c->info, s);
     });
+    if (c->Cavg_e)  // keep <C> of every element for the constant-basis macro stiffness
+      cudaMemcpy2DAsync(c->Cavg_e + (size_t)b0 * c->m * c->m, sizeof(double) * c->m * c->m, c->Cavg,
+                        sizeof(double) * 64, sizeof(double) * c->m * c->m, nb, cudaMemcpyDeviceToDevice, s);
   }
   int rc = check_cuda(c, cudaGetLastError(), "hom_condense");
   if (rc || !c->opt.check_info) return rc;

@@ -73,6 +73,9 @@ struct MacroDev {
   const double* dval;             // [ndof] prescribed value (0 where free)
   const double* fbody;            // [ndof] external load: consistent body load + nodal forces
   double load_factor;             // multiplies fbody (load stepping, hom_set_load_factor)
+  int constant_basis;             // 1: one RVE per element (eq:constSolution1/2), D = C_eff per element
+  const double* Cavg_e;           // [ne][m][m] <C> per element (constant basis)
+  const double* evol;             // [ne] element volume |B_e|
 };
 
 struct CgState {

@@ -41,6 +41,24 @@ template <int DIM>
 __global__ void k_macro_kin(MacroDev M, const double* __restrict__ u, double* __restrict__ kin,
                             int add_identity) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (M.constant_basis) {  // element-average strain eps_bar_e = |B_e|^-1 sum_q eta B_q u_e
+    if (t >= M.ne) return;
+    double out[9];
+    for (int k = 0; k < M.m; ++k) out[k] = 0.0;
+    for (int q = 0; q < M.nq; ++q) {
+      const int tq = t * M.nq + q;
+      const double w = M.wdet[tq];
+      for (int a = 0; a < M.nen; ++a) {
+        const double* g = M.grad + ((long)tq * M.nen + a) * DIM;
+        for (int c = 0; c < DIM; ++c) {
+          const double uc = u[M.conn[t * M.nen + a] * DIM + c];
+          for (int k = 0; k < M.m; ++k) out[k] += w * voigtB<DIM>(g, k, c) * uc;
+        }
+      }
+    }
+    for (int k = 0; k < M.m; ++k) kin[(long)t * M.m + k] = out[k] / M.evol[t];
+    return;
+  }
   if (t >= M.ne * M.nq) return;
   int e = t / M.nq, q = t % M.nq;
   double out[9];
@@ -63,7 +81,7 @@ __global__ void k_macro_kin(MacroDev M, const double* __restrict__ u, double* __
 }
 
 void launch_macro_kin(const MacroDev& M, const double* u, double* kin, int add_identity, cudaStream_t s) {
-  int n = M.ne * M.nq;
+  int n = M.constant_basis ? M.ne : M.ne * M.nq;
   if (M.dim == 2) k_macro_kin<2><<<(n + 127) / 128, 128, 0, s>>>(M, u, kin, add_identity);
   else k_macro_kin<3><<<(n + 127) / 128, 128, 0, s>>>(M, u, kin, add_identity);
 }
@@ -81,6 +99,34 @@ __global__ void k_macro_assemble(MacroDev M, const double* __restrict__ D, doubl
   for (int s = M.blk_ptr[blk]; s < M.blk_ptr[blk + 1]; ++s) {
     int code = M.blk_sh[s];
     int E = code >> 8, a = (code >> 4) & 15, b = code & 15;
+    if (M.constant_basis) {
+      // K_e = sum_q eta B_q^T <C>_e B_q - |B_e|^-1 (sum_q eta B_q)^T (<C>_e - C_eff,e) (sum_q eta B_q)
+      const double* Ca = M.Cavg_e + (long)E * m * m;
+      const double* Ce = D + (long)E * m * m;
+      double ba[6] = {0, 0, 0, 0, 0, 0}, bb[6] = {0, 0, 0, 0, 0, 0};
+      for (int q = 0; q < M.nq; ++q) {
+        const int t = E * M.nq + q;
+        const double* ga = M.grad + ((long)t * M.nen + a) * DIM;
+        const double* gb = M.grad + ((long)t * M.nen + b) * DIM;
+        const double w = M.wdet[t];
+        double s2 = 0.0;
+        for (int kk = 0; kk < m; ++kk) {
+          const double bak = voigtB<DIM>(ga, kk, ci);
+          ba[kk] += w * bak;
+          bb[kk] += w * voigtB<DIM>(gb, kk, cj);
+          if (bak == 0.0) continue;
+          double t2 = 0.0;
+          for (int l = 0; l < m; ++l) t2 += Ca[kk * m + l] * voigtB<DIM>(gb, l, cj);
+          s2 += bak * t2;
+        }
+        v += w * s2;
+      }
+      double corr = 0.0;
+      for (int kk = 0; kk < m; ++kk)
+        for (int l = 0; l < m; ++l) corr += ba[kk] * (Ca[kk * m + l] - Ce[kk * m + l]) * bb[l];
+      v -= corr / M.evol[E];
+      continue;
+    }
     for (int q = 0; q < M.nq; ++q) {
       int t = E * M.nq + q;
       const double* ga = M.grad + ((long)t * M.nen + a) * DIM;

@@ -79,7 +79,8 @@ class ShardedHomogenizer:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         n_elems = wl.nel ** wl.dim
-        self.parts = rve_partition(n_elems, wl.n_qp, self.world)
+        per_elem = 1 if kw.get("macro_basis", "dirac") == "constant" else wl.n_qp
+        self.parts = rve_partition(n_elems, per_elem, self.world)
         self.b_lo, self.b_hi = self.parts[self.rank]
         self.h = Homogenizer.from_workload(wl, rve_range=(self.b_lo, self.b_hi), **kw)
         self.n_rve, self.m, self.n_pad, self.n_dof = self.h.n_rve, self.h.m, self.h.n_pad, self.h.n_dof

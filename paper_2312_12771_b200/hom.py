@@ -55,7 +55,8 @@ class Materials(ctypes.Structure):
 class Options(ctypes.Structure):
     _fields_ = [("finite_strain", ctypes.c_int32), ("cg_rtol", ctypes.c_double), ("cg_max_iter", ctypes.c_int32),
                 ("rve_chunk", ctypes.c_int32), ("check_info", ctypes.c_int32), ("mem_budget_gb", ctypes.c_double),
-                ("tile_sparse", ctypes.c_int32), ("rve_begin", ctypes.c_int32), ("rve_count", ctypes.c_int32)]
+                ("tile_sparse", ctypes.c_int32), ("rve_begin", ctypes.c_int32), ("rve_count", ctypes.c_int32),
+                ("macro_basis", ctypes.c_int32)]
 
 
 class Sizes(ctypes.Structure):
@@ -158,7 +159,7 @@ class Homogenizer:
     def __init__(self, macro_coords, macro_conn, dirichlet_dof, dirichlet_value, body_force,
                  rve_coords, rve_conn, phase, materials, kind="linear", cg_rtol=1e-13, cg_max_iter=20000,
                  rve_chunk=0, check_info=True, mem_budget_gb=0.0, tile_sparse=False, rve_range=None,
-                 nodal_force=None):
+                 nodal_force=None, macro_basis="dirac"):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("Homogenizer needs a CUDA device (no CPU fallback)")
@@ -179,7 +180,9 @@ class Homogenizer:
         rc_, rconn = arr(rve_coords, np.float64), arr(rve_conn, np.int32)
         ph = arr(phase, np.uint8)
         mt = arr(materials, np.float64)
-        n_rve = mconn.shape[0] * 2 ** dim
+        if macro_basis not in ("dirac", "constant"):
+            raise ValueError("macro_basis must be 'dirac' (one RVE per Gauss point) or 'constant' (per element)")
+        n_rve = mconn.shape[0] * (2 ** dim if macro_basis == "dirac" else 1)
         per_rve_phase = int(ph.ndim == 2 and ph.shape[0] > 1)
         per_rve_mat = int(mt.ndim == 3 and mt.shape[0] > 1)
         if per_rve_phase and ph.shape[0] != n_rve:
@@ -195,7 +198,7 @@ class Homogenizer:
         self.mat = Materials(kinds[kind], n_phase, per_rve_mat, _np_ptr(mt))
         rb, rn = (0, 0) if rve_range is None else (int(rve_range[0]), int(rve_range[1]) - int(rve_range[0]))
         self.opt = Options(int(kind != "linear"), cg_rtol, cg_max_iter, rve_chunk, int(check_info), mem_budget_gb,
-                           int(tile_sparse), rb, rn)
+                           int(tile_sparse), rb, rn, int(macro_basis == "constant"))
         self.finite = kind != "linear"
         h = ctypes.c_void_p()
         rc = L.hom_setup(ctypes.byref(h), ctypes.byref(self.macro), ctypes.byref(self.rve),
@@ -218,10 +221,13 @@ class Homogenizer:
 
     @classmethod
     def from_workload(cls, wl, **kw):
+        """Context for a workload; with macro_basis="constant" the RVE of element e takes the phase
+        and material rows of the element's first Gauss-point RVE."""
         mc, mconn = wl.macro_mesh()
         rc_, rconn = wl.rve_mesh()
-        phase = wl.phase if wl.phase.shape[0] > 1 else wl.phase[0]
-        mat = wl.mat if wl.mat.shape[0] > 1 else wl.mat[0]
+        step = wl.n_qp if kw.get("macro_basis", "dirac") == "constant" else 1
+        phase = wl.phase[::step] if wl.phase.shape[0] > 1 else wl.phase[0]
+        mat = wl.mat[::step] if wl.mat.shape[0] > 1 else wl.mat[0]
         nodal = getattr(wl, "nodal_force", None)
         return cls(mc, mconn, wl.dir_dof, wl.dir_val, wl.body, rc_, rconn, phase, mat, kind=wl.kind,
                    nodal_force=nodal, **kw)

@@ -120,18 +120,24 @@ def periodic_dofs(dim, r):
 
 
 class Monolithic:
-    """Tiny two-scale problem: macro grid nel^dim on [0,1]^dim, RVE r^dim on [0,1]^dim."""
+    """Tiny two-scale problem: macro grid nel^dim on [0,1]^dim, RVE r^dim on [0,1]^dim.
 
-    def __init__(self, dim, nel, r, tangent_of, dir_dof, body=None):
-        """tangent_of(b, e) -> full-gradient tangent (dim^2 x dim^2) for linear problems."""
+    basis "dirac": one fluctuation field per macro Gauss point (eq:fluctVaria_dirac, P:246-292);
+    basis "constant": one per macro element, shared by its Gauss points (eq:constSolution1/2,
+    P:294-315) -- the micro equations are then integrated over the whole element."""
+
+    def __init__(self, dim, nel, r, tangent_of, dir_dof, body=None, basis="dirac"):
+        """tangent_of(b, e) -> full-gradient tangent (dim^2 x dim^2) for linear problems
+        (b = fluctuation field index: Gauss point or element)."""
         self.dim, self.nel, self.r = dim, nel, r
         self.tangent_of = tangent_of
         self.dir_dof = np.asarray(dir_dof)
         self.body = body
+        self.basis = basis
         self.nq = 2 ** dim
         self.ndof_M = (nel + 1) ** dim * dim
         self.dofmap, self.nf, self.indep = periodic_dofs(dim, r)
-        self.n_rve = nel ** dim * self.nq
+        self.n_rve = nel ** dim * (self.nq if basis == "dirac" else 1)
         self.N = self.ndof_M + self.n_rve * self.nf
 
     def _macro_ops(self):
@@ -167,6 +173,8 @@ class Monolithic:
             wM = (1.0 / self.nel) ** dim  # Gauss weight 1 x det J = (h/2)^d * 2^d / 2^d ... see below
             wM = (0.5 / self.nel) ** dim
             grad_u = Bm @ u[mdofs] if u is not None else np.zeros(dim * dim)
+            if self.basis == "constant":
+                b = b // self.nq  # the element's single fluctuation field
             off = self.ndof_M + b * self.nf
             for e, fd, Bf, wm in self._micro_ops():
                 wm = (0.5 / self.r) ** dim

@@ -415,3 +415,27 @@ def test_cook_classical_and_generalized_reach_the_same_state(torch_cuda):
     u_c, _, ok = h2.newton_classical(4, tol=1e-9, micro_tol=1e-13)
     assert ok
     assert rel(u_c.cpu().numpy(), u_g.cpu().numpy()) <= 1e-8
+
+
+# ------------------------------------------------------------------ constant macro basis
+@pytest.mark.parametrize("make", [
+    lambda: W.config1(),
+    lambda: W.config2(nel=8),
+    lambda: W.config3(nel=4, r=12, seed=17),
+    lambda: W.config4(nel=3),
+], ids=["cfg1", "cfg2-small", "cfg3-random", "cfg4-small"])
+def test_constant_basis_matches_oracle(torch_cuda, make):
+    """One RVE per macro element (eq:constSolution1/2): C_eff <= 1e-10, u and w <= 1e-8 against the
+    oracle's condensed constant-basis route (itself pinned by the monolithic brute force)."""
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = make()
+    o = oracle.solve_linear_constant(wl)
+    for ts in (False, True):
+        h = Homogenizer.from_workload(wl, macro_basis="constant", tile_sparse=ts)
+        assert h.n_rve == wl.nel ** wl.dim
+        C, u, w, info = h.solve_linear()
+        assert rel(C.cpu().numpy(), o["C_eff"]) <= TOL_C
+        assert rel(u.cpu().numpy(), o["u"]) <= TOL_U
+        assert rel(w.cpu().numpy(), o["w"]) <= TOL_U
+        eps = h.macro_kinematics(u)
+        assert rel(eps.cpu().numpy(), o["eps_bar"]) <= 1e-12

@@ -494,3 +494,44 @@ def test_cook_rve_at_reference_equals_linear_condensation():
     np.testing.assert_allclose([A[0, 0], A[0, 3], A[3, 3], A[1, 1], A[1, 2]],
                                [C[0, 0], C[0, 1], C[1, 1], C[2, 2], C[2, 2]], rtol=1e-12)
     np.testing.assert_allclose(c["P_avg"][0], 0.0, atol=1e-12)
+
+
+# ------------------------------------------------------------------ constant macro basis
+@pytest.mark.parametrize("dim,nel,r", [(2, 2, 4), (2, 3, 3), (3, 2, 2)])
+def test_constant_basis_condensation_equals_monolithic_bruteforce(dim, nel, r):
+    """The full uncondensed two-scale system with one fluctuation field per macro element
+    (eq:constSolution1/2, micro equations integrated over the element) solved densely equals the
+    oracle's condensed route: C_eff, <C> per element, K_e = int B^T <C> B - |B_e|^-1 Bbar^T
+    (<C> - C_eff) Bbar, w_e = W_e eps_bar_e."""
+    from types import SimpleNamespace
+    rng = np.random.default_rng(31 + dim + nel)
+    ne, nq, nelr = nel ** dim, 2 ** dim, r ** dim
+    phase_e = (rng.random((ne, nelr)) < 0.4).astype(np.uint8)
+    mat_e = np.stack([10 ** (2 * rng.random((ne, 2))), 0.2 + 0.2 * rng.random((ne, 2))], -1)
+    E = np.take_along_axis(mat_e[..., 0], phase_e.astype(int), 1)
+    nu = np.take_along_axis(mat_e[..., 1], phase_e.astype(int), 1)
+    nodes = W.face_nodes(dim, nel, 0, 0)
+    dir_dof = np.array([n * dim + c for n in nodes for c in range(dim)], np.int32)
+    dir_val = 1e-3 * rng.standard_normal(len(dir_dof))
+    body = np.array([0.3, -1.0, 0.2][:dim])
+    mono = bf.Monolithic(dim, nel, r, lambda b, e: bf.iso_tangent_full(dim, E[b, e], nu[b, e]), dir_dof, body,
+                         basis="constant")
+    u_bf, wfree = mono.solve_linear(dir_val)
+    w_bf = mono.to_indep_layout(wfree)
+    # the oracle's workload view: per-Gauss-point rows, the element's rows at its first qp
+    wl = SimpleNamespace(dim=dim, r=r, nel=nel, n_qp=nq, n_dof=(nel + 1) ** dim * dim, dir_dof=dir_dof,
+                         dir_val=dir_val, body=body, phase=np.repeat(phase_e, nq, 0), mat=np.repeat(mat_e, nq, 0))
+    o = oracle.solve_linear_constant(wl)
+    np.testing.assert_allclose(o["u"], u_bf, rtol=0, atol=1e-12 * np.abs(u_bf).max())
+    np.testing.assert_allclose(o["w"], w_bf, rtol=0, atol=1e-12 * np.abs(w_bf).max())
+
+
+def test_constant_basis_homogeneous_rve_is_plain_fe():
+    """Homogeneous RVE: C_eff = <C>, the correction term vanishes and both macro bases give the
+    same (plain finite-element) solution."""
+    wl = W.config2(nel=4, r=4)
+    wl.phase = np.zeros_like(wl.phase)
+    oc = oracle.solve_linear_constant(wl)
+    od = oracle.solve_linear(wl)
+    np.testing.assert_allclose(oc["C_eff"], oc["C_avg"], rtol=1e-13, atol=1e-14)
+    np.testing.assert_allclose(oc["u"], od["u"], rtol=0, atol=1e-13 * np.abs(od["u"]).max())
