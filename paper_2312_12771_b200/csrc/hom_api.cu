@@ -145,7 +145,10 @@ bool element_tables(int dim, const double* x /*[nen][dim]*/, double* grad, doubl
       for (int i = 0; i < dim; ++i)
         for (int j = 0; j < dim; ++j) J[i][j] += x[a * dim + i] * dN[a][j];
     double det, Ji[3][3];
-    if (dim == 2) {
+    if (dim == 1) {
+      det = J[0][0];
+      Ji[0][0] = 1.0 / det;
+    } else if (dim == 2) {
       det = J[0][0] * J[1][1] - J[0][1] * J[1][0];
       Ji[0][0] = J[1][1] / det; Ji[0][1] = -J[0][1] / det;
       Ji[1][0] = -J[1][0] / det; Ji[1][1] = J[0][0] / det;
@@ -242,7 +245,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   cudaGetDevice(&c->device);
   const int dim = mac->dim;
   *out = c;
-  if ((dim != 2 && dim != 3) || rve->dim != dim || mac->nodes_per_elem != (1 << dim) ||
+  if ((dim < 1 || dim > 3) || rve->dim != dim || mac->nodes_per_elem != (1 << dim) ||
       rve->nodes_per_elem != (1 << dim) || mac->n_elems <= 0 || rve->n_elems <= 0 || mat->n_phases <= 0 ||
       (mat->kind < 0 || mat->kind > 2) || (mat->kind >= 1 && dim != 2) ||
       (options->finite_strain != 0) != (mat->kind >= 1))
@@ -250,7 +253,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   const int nen = 1 << dim, nq = 1 << dim;
   c->dim = dim;
   c->finite = mat->kind >= 1;
-  c->m = c->finite ? 4 : (dim == 2 ? 3 : 6);
+  c->m = c->finite ? 4 : (dim == 1 ? 1 : (dim == 2 ? 3 : 6));
   if (options->macro_basis < 0 || options->macro_basis > 1 || (options->macro_basis == 1 && c->finite))
     return fail(HOM_ERR_INVALID_ARG, "macro_basis must be 0 (Dirac) or 1 (constant, small strain only)");
   c->B = mac->n_elems * (options->macro_basis == 1 ? 1 : nq);

@@ -20,6 +20,7 @@ namespace hom {
 // Voigt strain-displacement entry B_a[k][c] from the gradient g of N_a.
 template <int DIM>
 __device__ __forceinline__ double voigtB(const double* g, int k, int c) {
+  if (DIM == 1) return g[0];  // eps11 = du/dX
   if (DIM == 2) {
     if (k == 0) return c == 0 ? g[0] : 0.0;
     if (k == 1) return c == 1 ? g[1] : 0.0;
@@ -82,7 +83,8 @@ __global__ void k_macro_kin(MacroDev M, const double* __restrict__ u, double* __
 
 void launch_macro_kin(const MacroDev& M, const double* u, double* kin, int add_identity, cudaStream_t s) {
   int n = M.constant_basis ? M.ne : M.ne * M.nq;
-  if (M.dim == 2) k_macro_kin<2><<<(n + 127) / 128, 128, 0, s>>>(M, u, kin, add_identity);
+  if (M.dim == 1) k_macro_kin<1><<<(n + 127) / 128, 128, 0, s>>>(M, u, kin, add_identity);
+  else if (M.dim == 2) k_macro_kin<2><<<(n + 127) / 128, 128, 0, s>>>(M, u, kin, add_identity);
   else k_macro_kin<3><<<(n + 127) / 128, 128, 0, s>>>(M, u, kin, add_identity);
 }
 
@@ -153,7 +155,8 @@ __global__ void k_macro_assemble(MacroDev M, const double* __restrict__ D, doubl
 }
 
 void launch_macro_assemble(const MacroDev& M, const double* D, double* val, double* diag, cudaStream_t s) {
-  if (M.dim == 2) k_macro_assemble<2><<<(M.nnz + 255) / 256, 256, 0, s>>>(M, D, val, diag);
+  if (M.dim == 1) k_macro_assemble<1><<<(M.nnz + 255) / 256, 256, 0, s>>>(M, D, val, diag);
+  else if (M.dim == 2) k_macro_assemble<2><<<(M.nnz + 255) / 256, 256, 0, s>>>(M, D, val, diag);
   else k_macro_assemble<3><<<(M.nnz + 255) / 256, 256, 0, s>>>(M, D, val, diag);
 }
 
@@ -203,7 +206,8 @@ __global__ void k_macro_rhs(MacroDev M, const double* __restrict__ val, const do
 
 void launch_macro_rhs(const MacroDev& M, const double* val, const double* S, double scale, double* rhs,
                       double* Rfree, cudaStream_t s) {
-  if (M.dim == 2) k_macro_rhs<2><<<(M.ndof + 255) / 256, 256, 0, s>>>(M, val, S, scale, rhs, Rfree);
+  if (M.dim == 1) k_macro_rhs<1><<<(M.ndof + 255) / 256, 256, 0, s>>>(M, val, S, scale, rhs, Rfree);
+  else if (M.dim == 2) k_macro_rhs<2><<<(M.ndof + 255) / 256, 256, 0, s>>>(M, val, S, scale, rhs, Rfree);
   else k_macro_rhs<3><<<(M.ndof + 255) / 256, 256, 0, s>>>(M, val, S, scale, rhs, Rfree);
 }
 

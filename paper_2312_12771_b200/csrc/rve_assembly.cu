@@ -131,12 +131,12 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   double* s_lam = red + NTHR;                // [ne] (ISO)
   double* s_mu = s_lam + R.ne;               // [ne] (ISO)
   double* s_K = s_mu + R.ne;                 // [ntype][n_phase][ND][ND] element matrices (ISO)
-  int* s_ep = reinterpret_cast<int*>(s_K + (ISO ? R.ntype * R.n_phase * (DIM == 2 ? 64 : 576) : 0));  // [ne]
+  int* s_ep = reinterpret_cast<int*>(s_K + (ISO ? R.ntype * R.n_phase * ((1 << DIM) * DIM) * ((1 << DIM) * DIM) : 0));
   const int tid = threadIdx.x;
   const int bl = blockIdx.x;
   const int b = b0 + bl;
   const int nen = R.nen, nq = R.nq, ne = R.ne;
-  constexpr int ND = ISO ? (DIM == 2 ? 8 : 24) : 8;  // nen*dim
+  constexpr int ND = ISO ? (1 << DIM) * DIM : 8;  // nen*dim
   const long tq0 = (long)bl * ne * nq;  // offset of this RVE in Aq/Pq (chunk-local)
 
   if (ISO) {
@@ -371,11 +371,15 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
 void launch_rve_assemble(const RveDev& R, int b0, int nb, double* Kt, double* Y, double* Cavg,
                          double* Pavg, double* rfn, const double* Aq, const double* Pq,
                          cudaStream_t s) {
-  const int dim = R.finite ? 2 : R.dim, nd = 4 * dim * (dim == 2 ? 1 : 2);  // nen*dim
+  const int dim = R.finite ? 2 : R.dim, nd = (1 << dim) * dim;  // nen*dim
   size_t sm = (size_t)((NTHR / 32) * R.npw * dim * TILE + NTHR + 2 * R.ne) * sizeof(double) +
               (R.finite ? 0 : (size_t)R.ntype * R.n_phase * nd * nd * sizeof(double) + (size_t)R.ne * sizeof(int));
   if (R.finite) {
     auto k = k_rve_assemble<2, false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    k<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, rfn, Aq, Pq);
+  } else if (R.dim == 1) {  // the paper's 1-D benchmark on the device
+    auto k = k_rve_assemble<1, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     k<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, rfn, Aq, Pq);
   } else if (R.dim == 2) {

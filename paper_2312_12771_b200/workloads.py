@@ -254,6 +254,28 @@ def cook(nel: int = 20, r: int = 30, n_steps: int = 22) -> Workload:
                     macro_coords=np.ascontiguousarray(X), nodal_force=f, rve_size=6.0, rve_origin=-3.0)
 
 
+def bench1d(k: int) -> Workload:
+    """The paper's 1-D analytical benchmark (§5.1), Dirac basis [delta,1]:
+    B_0 = (0,1000) with 2^k P1 macro elements (2 Gauss points), RVE (0,1) with 2^k P1 elements,
+    lambda(X~) = 20 / cos(2 pi X~/3 - pi/3), Psi~ = lambda (F~^2 - 1) -> tangent 2 lambda (R14),
+    body load B = 1, phi(0) = 0, phi(1000) = 37575 sqrt(3) / (2 pi); the unknown is the position
+    phi (linear problem).  For P1 elements only the element average of the tangent enters, so each
+    RVE element carries its own "phase" with E = 2 * (2-point Gauss average of lambda), nu = 0
+    (1-D C = lambda_Lame + 2 mu = E); 2^k <= 255."""
+    n = 2 ** k
+    if n > 255:
+        raise ValueError("bench1d: one phase per RVE element, 2^k <= 255")
+    g = 1.0 / np.sqrt(3.0)
+    xc = (np.arange(n)[:, None] + 0.5 + 0.5 * np.array([-g, g])[None, :]) / n
+    lam = 20.0 / np.cos(2 * np.pi * xc / 3 - np.pi / 3)
+    mat = np.stack([2.0 * lam.mean(1), np.zeros(n)], -1)[None]
+    coords, _ = grid_mesh(1, n, 1000.0)
+    phi1000 = 37575.0 * np.sqrt(3.0) / (2.0 * np.pi)  # P:459 (DESIGN.md R14)
+    return Workload(f"bench1d_k{k}", 1, n, n, "linear", np.arange(n, dtype=np.uint8)[None], mat,
+                    np.array([0, n], np.int32), np.array([0.0, phi1000]), np.array([1.0]),
+                    description=f"paper 1-D benchmark, 2^{k} elements per scale", macro_coords=coords)
+
+
 CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}
 
 

@@ -439,3 +439,78 @@ def test_constant_basis_matches_oracle(torch_cuda, make):
         assert rel(w.cpu().numpy(), o["w"]) <= TOL_U
         eps = h.macro_kinematics(u)
         assert rel(eps.cpu().numpy(), o["eps_bar"]) <= 1e-12
+
+
+# ------------------------------------------------------------------ dim = 1: the paper's 1-D benchmark on the GPU (§8(f) 4)
+def _gpu_bench1d(k):
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = W.bench1d(k)
+    h = Homogenizer.from_workload(wl)
+    C, phi, w, _ = h.solve_linear()
+    F = h.macro_kinematics(phi)
+    return wl, C.cpu().numpy(), phi.cpu().numpy(), F.cpu().numpy()[:, 0], w.cpu().numpy()
+
+
+def test_bench1d_gpu_closed_forms_and_oracle(torch_cuda):
+    """C^h = 2 / sum(h_e / lambda_bar_e) and the exact nodal phi of P1 (R14) on the device, and
+    phi, w against the oracle's [delta,1] solution."""
+    import math
+    for k in (3, 5, 7):
+        wl, C, phi, F, w = _gpu_bench1d(k)
+        n = 2 ** k
+        lam_bar = wl.mat[0, :, 0] / 2
+        Ch = 2.0 / np.sum((1.0 / n) / lam_bar)
+        assert np.abs(C[:, 0, 0] - Ch).max() <= 1e-12 * Ch
+        X = np.linspace(0, 1000.0, n + 1)
+        a = (wl.dir_val[1] + 1000.0 ** 2 / (2 * Ch)) / 1000.0
+        np.testing.assert_allclose(phi, -X ** 2 / (2 * Ch) + a * X, rtol=1e-11, atol=1e-8)
+        xg = np.array([-1 / math.sqrt(3), 1 / math.sqrt(3)])
+        Cq = (2 * 20.0 / np.cos(2 * math.pi * ((np.arange(n)[:, None] + 0.5 + 0.5 * xg) / n) / 3 - math.pi / 3))
+        Co, Wf = oracle.rve_condense_linear(1, n, Cq[:, :, None, None], want_W=True)
+        w_o = np.outer(F, Wf[0])
+        assert rel(w, w_o) <= TOL_U
+
+
+def test_bench1d_gpu_convergence_orders(torch_cuda):
+    """PAPER.md P:531-541, [delta,1]: fitted L2 orders over k = 4..7 from the GPU solution:
+    err_phi >= 1.95 (R16), err_w = 1 +- 0.2 (golden bench1d.json)."""
+    import json
+    import math
+    import os
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "bench1d.json")))
+    c2, c1 = gold["phi_a_c2"], gold["phi_a_c1"]
+    xs, ws = np.polynomial.legendre.leggauss(5)
+    xq = np.array([-1 / math.sqrt(3), 1 / math.sqrt(3)])
+    errs = []
+    for k in (4, 5, 6, 7):
+        wl, C, phi, F, w = _gpu_bench1d(k)
+        n, L = 2 ** k, 1000.0
+        h, hm = L / n, 1.0 / n
+        num = den = 0.0
+        for e in range(n):
+            X = e * h + (xs + 1) * h / 2
+            ph = phi[e] + (phi[e + 1] - phi[e]) * (xs + 1) / 2
+            pa = c2 * X ** 2 + c1 * X
+            num += np.sum(ws * h / 2 * (ph - pa) ** 2)
+            den += np.sum(ws * h / 2 * pa ** 2)
+        e_phi = math.sqrt(num / den)
+        num = den = 0.0
+        for e in range(n):
+            for q in range(2):
+                Xk = e * h + (xq[q] + 1) * h / 2
+                Fa = 2 * c2 * Xk + c1
+                wn = np.concatenate([w[2 * e + q], w[2 * e + q][:1]])  # node n == node 0 (corner class)
+                for c in range(n):
+                    xt = c * hm + (xs + 1) * hm / 2
+                    wh = wn[c] + (wn[c + 1] - wn[c]) * (xs + 1) / 2
+                    wa = Fa * (np.sin(2 * math.pi * xt / 3 - math.pi / 3) / math.sqrt(3) - xt + 0.5)
+                    num += h / 2 * np.sum(ws * hm / 2 * (wh - wa) ** 2)
+                    den += h / 2 * np.sum(ws * hm / 2 * wa ** 2)
+        errs.append((e_phi, math.sqrt(num / den)))
+    e = np.array(errs)
+    hs = np.array([1000.0 / 2 ** k for k in (4, 5, 6, 7)])
+    p_phi = np.polyfit(np.log(hs), np.log(e[:, 0]), 1)[0]
+    p_w = np.polyfit(np.log(hs), np.log(e[:, 1]), 1)[0]
+    od = gold["orders_delta1"]
+    assert p_phi >= od["err_phi_min"], p_phi
+    assert abs(p_w - od["err_w"]) <= od["err_w_tol"], p_w
