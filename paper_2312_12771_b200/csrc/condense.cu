@@ -40,6 +40,15 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // swizzled word index inside a [rows][KC] k-chunk and a [rows][64] tile (row-chunk)
 __device__ __forceinline__ int sw32(int r, int k) { return r * KC + (k ^ ((r & 3) << 2)); }
 __device__ __forceinline__ int sw64(int r, int c) { return r * TILE + (c ^ ((r & 3) << 2)); }
+// Diagonal-tile buffer: only the 10 lower 16x16 blocks of the 64x64 tile, block (bi, bj <= bi) at
+// (bi(bi+1)/2 + bj) * 256, each block row-major with the same XOR swizzle (2560 doubles instead of
+// 4096 -> 4 CTAs per SM).  Callers never address a strictly upper block.
+constexpr int SD_DBL = 10 * 256;
+__device__ __forceinline__ int sd(int r, int c) {
+  const int bi = r >> 4, bj = c >> 4;
+  return (((bi * (bi + 1)) >> 1) + bj) * 256 + (r & 15) * 16 + ((c & 15) ^ ((r & 3) << 2));
+}
+__device__ __forceinline__ bool sd_upper(int r, int c) { return (c >> 4) > (r >> 4); }
 // [rows][8] right-hand-side block
 __device__ __forceinline__ int swy(int k, int n) { return k * RHSW + (n ^ (((k >> 1) & 1) << 2)); }
 
@@ -116,7 +125,7 @@ __device__ __forceinline__ int chol16_inv_inplace(double* sD, int k0, int lane) 
   const int r = lane & 15;
   double a[16], ip[16];
 #pragma unroll
-  for (int c = 0; c < 16; ++c) a[c] = (c <= r) ? sD[sw64(k0 + r, k0 + c)] : 0.0;
+  for (int c = 0; c < 16; ++c) a[c] = (c <= r) ? sD[sd(k0 + r, k0 + c)] : 0.0;
   int fail = 16;
   // Pivot chain: one rsqrt per pivot (no sqrt, no division); every lane keeps 1/L_kk.
 #pragma unroll
@@ -136,7 +145,7 @@ __device__ __forceinline__ int chol16_inv_inplace(double* sD, int k0, int lane) 
   if (lane < 16) {
 #pragma unroll
     for (int c = 0; c < 16; ++c)
-      if (c <= r) sD[sw64(k0 + r, k0 + c)] = a[c];
+      if (c <= r) sD[sd(k0 + r, k0 + c)] = a[c];
   }
   __syncwarp();
   // X = L^-1: lane c builds column c by forward substitution (L rows read as smem
@@ -148,15 +157,15 @@ __device__ __forceinline__ int chol16_inv_inplace(double* sD, int k0, int lane) 
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll
     for (int k = 0; k < 16; k += 2) {
-      if (k < rr) s0 = fma(sD[sw64(k0 + rr, k0 + k)], x[k], s0);
-      if (k + 1 < rr) s1 = fma(sD[sw64(k0 + rr, k0 + k + 1)], x[k + 1], s1);
+      if (k < rr) s0 = fma(sD[sd(k0 + rr, k0 + k)], x[k], s0);
+      if (k + 1 < rr) s1 = fma(sD[sd(k0 + rr, k0 + k + 1)], x[k + 1], s1);
     }
     x[rr] = (rr >= c) ? (((rr == c) ? 1.0 : 0.0) - (s0 + s1)) * ip[rr] : 0.0;
   }
   __syncwarp();
   if (lane < 16) {
 #pragma unroll
-    for (int rr = 0; rr < 16; ++rr) sD[sw64(k0 + rr, k0 + c)] = x[rr];
+    for (int rr = 0; rr < 16; ++rr) sD[sd(k0 + rr, k0 + c)] = x[rr];
   }
   __syncwarp();
   return fail;
@@ -193,9 +202,9 @@ __device__ __forceinline__ bool factor_invert_diag(double* sD, double* sScr, int
         p[u][0] = p[u][1] = p[u][2] = p[u][3] = 0.0;
 #pragma unroll
         for (int kk = 0; kk < 16; kk += 4) {
-          const double a = sD[sw64(r, k0 + kk + lc)];
-          if (kk < 8) dmma(p[u][0], p[u][1], a, sD[sw64(k0 + lr, k0 + kk + lc)]);
-          dmma(p[u][2], p[u][3], a, sD[sw64(k0 + 8 + lr, k0 + kk + lc)]);
+          const double a = sD[sd(r, k0 + kk + lc)];
+          if (kk < 8) dmma(p[u][0], p[u][1], a, sD[sd(k0 + lr, k0 + kk + lc)]);
+          dmma(p[u][2], p[u][3], a, sD[sd(k0 + 8 + lr, k0 + kk + lc)]);
         }
       }
     }
@@ -205,10 +214,10 @@ __device__ __forceinline__ bool factor_invert_diag(double* sD, double* sScr, int
       const int ti = warp + 4 * u;
       if (ti < nrt) {
         const int r = rb0 + 8 * ti + lr;
-        sD[sw64(r, k0 + 2 * lc)] = p[u][0];
-        sD[sw64(r, k0 + 2 * lc + 1)] = p[u][1];
-        sD[sw64(r, k0 + 8 + 2 * lc)] = p[u][2];
-        sD[sw64(r, k0 + 8 + 2 * lc + 1)] = p[u][3];
+        sD[sd(r, k0 + 2 * lc)] = p[u][0];
+        sD[sd(r, k0 + 2 * lc + 1)] = p[u][1];
+        sD[sd(r, k0 + 8 + 2 * lc)] = p[u][2];
+        sD[sd(r, k0 + 8 + 2 * lc + 1)] = p[u][3];
       }
     }
     __syncthreads();
@@ -220,12 +229,12 @@ __device__ __forceinline__ bool factor_invert_diag(double* sD, double* sScr, int
       while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
       const int tj = t - ti * (ti + 1) / 2;
       const int r = rb0 + 8 * ti, cb = rb0 + 8 * tj;
-      double acc0 = sD[sw64(r + lr, cb + 2 * lc)], acc1 = sD[sw64(r + lr, cb + 2 * lc + 1)];
+      double acc0 = sD[sd(r + lr, cb + 2 * lc)], acc1 = sD[sd(r + lr, cb + 2 * lc + 1)];
 #pragma unroll
       for (int kk = 0; kk < 16; kk += 4)
-        dmma(acc0, acc1, neg(sD[sw64(r + lr, k0 + kk + lc)]), sD[sw64(cb + lr, k0 + kk + lc)]);
-      sD[sw64(r + lr, cb + 2 * lc)] = acc0;
-      sD[sw64(r + lr, cb + 2 * lc + 1)] = acc1;
+        dmma(acc0, acc1, neg(sD[sd(r + lr, k0 + kk + lc)]), sD[sd(cb + lr, k0 + kk + lc)]);
+      sD[sd(r + lr, cb + 2 * lc)] = acc0;
+      sD[sd(r + lr, cb + 2 * lc + 1)] = acc1;
     }
     __syncthreads();
   }
@@ -242,8 +251,8 @@ __device__ __forceinline__ bool factor_invert_diag(double* sD, double* sScr, int
 #pragma unroll
         for (int kk = 0; kk < 16; kk += 4) {
           if (j == k && tc == 1 && kk < 8) continue;  // X_kk[kk][8+n] = 0 for kk < 8
-          dmma(t0, t1, sD[sw64(16 * i + 8 * tr + lr, 16 * j + kk + lc)],
-               sD[sw64(16 * j + kk + lc, 16 * k + 8 * tc + lr)]);
+          dmma(t0, t1, sD[sd(16 * i + 8 * tr + lr, 16 * j + kk + lc)],
+               sD[sd(16 * j + kk + lc, 16 * k + 8 * tc + lr)]);
         }
       }
       double* W = sScr + k * 320;
@@ -258,11 +267,11 @@ __device__ __forceinline__ bool factor_invert_diag(double* sD, double* sScr, int
 #pragma unroll
       for (int kk = 0; kk < 16; kk += 4) {
         if (tr == 0 && kk >= 8) continue;  // X_ii lower
-        dmma(o0, o1, neg(sD[sw64(16 * i + 8 * tr + lr, 16 * i + kk + lc)]), W[(kk + lc) * 20 + 8 * tc + lr]);
+        dmma(o0, o1, neg(sD[sd(16 * i + 8 * tr + lr, 16 * i + kk + lc)]), W[(kk + lc) * 20 + 8 * tc + lr]);
       }
       const int r = 16 * i + 8 * tr + lr, cc = 16 * k + 8 * tc + 2 * lc;
-      sD[sw64(r, cc)] = o0;  // only X_ii and sScr are read in this phase: in-place write is safe
-      sD[sw64(r, cc + 1)] = o1;
+      sD[sd(r, cc)] = o0;  // only X_ii and sScr are read in this phase: in-place write is safe
+      sD[sd(r, cc + 1)] = o1;
     }
     __syncthreads();
   }
@@ -306,26 +315,30 @@ __device__ __forceinline__ void load_frag(double (&acc)[4][4][2], const double* 
     }
 }
 
-// Smem (doubles): sT 64x64 | stage[2] x (A 64xKC + B 64xKC + Yc KCx8) | sY 64x8 | misc.
-// The stage area doubles as: factor scratch (3 x 16x20), Y_J (64x8), the full S_IJ tile of
-// the TRSM (64x64) and the backward row chunks -- never at the same time.
+// Smem (doubles): sT (packed lower 16x16 blocks) | stage[2] x (A 64xKC + B 64xKC + Yc KCx8) | misc.
+// The stage area doubles as: factor scratch (3 x 16x20 at 0), Y_J (64x8 at 0), Kfe_J - sum (64x8
+// at SY_F, forward) / Y_J - xacc (at SY_B, backward), the full S_IJ tile of the TRSM (64x64) and
+// the backward row chunks -- never two of them at the same time.
 constexpr int STAGE_DBL = 2 * 64 * KC + KC * RHSW;
-constexpr int SMEM_DBL = TILE_ELEMS + 2 * STAGE_DBL + 64 * RHSW + 64;
-static_assert(SMEM_DBL * 8 <= 73 * 1024, "three CTAs per SM");
+constexpr int SY_F = 1024, SY_B = 3456;
+constexpr int SMEM_DBL = SD_DBL + 2 * STAGE_DBL + 64;
+static_assert(SMEM_DBL * 8 + 1024 <= 57 * 1024, "four CTAs per SM");
+static_assert(3 * 320 <= SY_F && SY_F + 64 * RHSW <= 2 * STAGE_DBL, "forward stage-area aliases");
+static_assert(STAGE_DBL + 16 * TILE + 16 * RHSW <= SY_B && SY_B + 64 * RHSW <= 2 * STAGE_DBL, "backward aliases");
 static_assert(TILE_ELEMS <= 2 * STAGE_DBL, "S tile fits in the stage area");
 static_assert(16 * TILE + 16 * RHSW <= STAGE_DBL, "backward row chunk fits in a stage");
 
 // ------------------------------------------------------------------ kernel
-__global__ void __launch_bounds__(NTC, 3)
+__global__ void __launch_bounds__(NTC, 4)
 k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
            const double* __restrict__ Cavg, const double* __restrict__ Pavg,
            double* __restrict__ Ceff, double* __restrict__ Peff, double* __restrict__ PavgOut,
            double* __restrict__ X, int* __restrict__ info) {
   extern __shared__ __align__(128) double smem[];
-  double* sT = smem;                        // 64x64 swizzled: S_JJ -> G_JJ^-1
-  double* sStage = sT + TILE_ELEMS;         // 2 stages | S tile | factor scratch | Y_J
-  double* sY = sStage + 2 * STAGE_DBL;      // 64x8 swizzled: Kfe_J - sum_K G_JK Y_K
-  int* sFail = reinterpret_cast<int*>(sY + 64 * RHSW);
+  double* sT = smem;                        // packed lower 64x64 (sd): S_JJ -> G_JJ^-1
+  double* sStage = sT + SD_DBL;             // 2 stages | S tile | factor scratch | Y_J | sY
+  double* sY = sStage + SY_F;               // 64x8 swizzled: Kfe_J - sum_K G_JK Y_K (forward)
+  int* sFail = reinterpret_cast<int*>(sStage + 2 * STAGE_DBL);
   double* sY2 = sStage;                     // Y_J (after the factorisation, before the off-diagonal tiles)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -387,8 +400,9 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni) {
           const int r = R0 + 8 * mi + lr, cc = C0 + 8 * ni + 2 * lc;
-          sT[sw64(r, cc)] = (cc <= r) ? acc[mi][ni][0] : 0.0;
-          sT[sw64(r, cc + 1)] = (cc + 1 <= r) ? acc[mi][ni][1] : 0.0;
+          if (sd_upper(r, cc)) continue;  // strictly upper 16x16 block: not stored
+          sT[sd(r, cc)] = (cc <= r) ? acc[mi][ni][0] : 0.0;
+          sT[sd(r, cc + 1)] = (cc + 1 <= r) ? acc[mi][ni][1] : 0.0;
         }
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
@@ -410,7 +424,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
         const int r = 16 * warp + 8 * u;
         double y0 = 0.0, y1 = 0.0;
         for (int k0 = 0; k0 < r + 8; k0 += 4)  // G_JJ^-1 lower
-          dmma(y0, y1, sT[sw64(r + lr, k0 + lc)], sY[swy(k0 + lc, lr)]);
+          dmma(y0, y1, sT[sd(r + lr, k0 + lc)], sY[swy(k0 + lc, lr)]);
         const int rr = r + lr, cc = 2 * lc;
         sY2[swy(rr, cc)] = y0;
         sY2[swy(rr, cc + 1)] = y1;
@@ -419,7 +433,8 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
       double* Gjj = tile_ptr(Kb, R, J, J);
       for (int idx = tid; idx < TILE_ELEMS / 2; idx += NTC) {
         const int r = idx >> 5, cc = 2 * (idx & 31);
-        *reinterpret_cast<double2*>(Gjj + r * TILE + cc) = make_double2(sT[sw64(r, cc)], sT[sw64(r, cc + 1)]);
+        *reinterpret_cast<double2*>(Gjj + r * TILE + cc) =
+            sd_upper(r, cc) ? make_double2(0.0, 0.0) : make_double2(sT[sd(r, cc)], sT[sd(r, cc + 1)]);
       }
     }
     __syncthreads();
@@ -484,7 +499,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
       double g[8][2][2] = {};
       int k0 = 0;
       for (; k0 < 8 * (cLo + 1); k0 += 4) {
-        const double bl0 = sT[sw64(8 * cLo + lr, k0 + lc)], bh0 = sT[sw64(8 * cHi + lr, k0 + lc)];
+        const double bl0 = sT[sd(8 * cLo + lr, k0 + lc)], bh0 = sT[sd(8 * cHi + lr, k0 + lc)];
 #pragma unroll
         for (int mi = 0; mi < 8; ++mi) {
           const double a = sS[sw64(8 * mi + lr, k0 + lc)];
@@ -493,7 +508,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
         }
       }
       for (; k0 < 8 * (cHi + 1); k0 += 4) {
-        const double bh0 = sT[sw64(8 * cHi + lr, k0 + lc)];
+        const double bh0 = sT[sd(8 * cHi + lr, k0 + lc)];
 #pragma unroll
         for (int mi = 0; mi < 8; ++mi) dmma(g[mi][1][0], g[mi][1][1], sS[sw64(8 * mi + lr, k0 + lc)], bh0);
       }
@@ -519,7 +534,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
 
   // ======================= K4 epilogue: C_eff, P_eff ==========================
   {
-    double* sSum = sY;  // reuse: 8x8 plain
+    double* sSum = sStage;  // reuse: 8x8 plain
     __syncthreads();
     if (tid < 64) sSum[tid] = Sacc;
     __syncthreads();
@@ -579,8 +594,15 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
       I = I2; rq = rq2; par ^= 1;
     }
     // r = Y_J - xacc ; X_J = G_JJ^-T r
-    stage_rows(sT, tile_ptr(Kb, R, J, J), 0, TILE, tid);
+    {  // G_JJ^-1 (lower 16x16 blocks) into the packed buffer
+      const double* src = tile_ptr(Kb, R, J, J);
+      for (int idx = tid; idx < TILE * 32; idx += NTC) {
+        const int r = idx >> 5, c2 = 2 * (idx & 31);
+        if (!sd_upper(r, c2)) cp_async16(sT + sd(r, c2), src + r * TILE + c2);
+      }
+    }
     cp_async_commit();
+    sY = sStage + SY_B;
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
       const int r = 16 * warp + 8 * u + lr, cc = 2 * lc;
@@ -595,7 +617,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
       const int r = 16 * warp + 8 * u;
       double x0 = 0.0, x1 = 0.0;
       for (int k0 = r; k0 < TILE; k0 += 4)  // (G_JJ^-1)^T upper: row j needs k >= j
-        dmma(x0, x1, sT[sw64(k0 + lc, r + lr)], sY[swy(k0 + lc, lr)]);
+        dmma(x0, x1, sT[sd(k0 + lc, r + lr)], sY[swy(k0 + lc, lr)]);
       const int rr = r + lr, cc = 2 * lc;
       *reinterpret_cast<double2*>(Xb + (long)(J * TILE + rr) * RHSW + cc) = make_double2(x0, x1);
     }
