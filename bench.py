@@ -201,6 +201,51 @@ def spmv_scaled(C_tile, nel: int = 2048, reps: int = 20):
     return out
 
 
+# ----------------------------------------------------------------------------- tile-sparse companion
+def tile_sparse_line(wl, C_dense, steps: int, warmup: int):
+    """The same linear step with the tile-sparse factorisation: tangents/s and the
+    k_condense roofline on the executed tile-structure flops, plus the bitwise check against the
+    dense tangents of the main line (every skipped product is an exact zero)."""
+    import torch
+
+    from paper_2312_12771_b200.hom import Homogenizer
+    h = Homogenizer.from_workload(wl, tile_sparse=True)
+    C = h.empty(h.n_rve, h.m, h.m)
+    u = h.empty(h.n_dof)
+    w = h.empty(h.n_rve, h.n_pad)
+
+    def step():
+        h.condense(None, C)
+        h.macro_solve(C, None, 1.0, u)
+        h.recover(u, w)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    h.profile(True)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    prof = h.profile_read()
+    h.profile(False)
+    cond_ms = prof["condense"][0]
+    achieved = h.work.flop_executed * h.sizes.rve_count * steps / (cond_ms * 1e-3) / 1e12
+    peak, _ = fp64_peak()
+    out = {"value": wl.n_rve * steps / (ms * 1e-3), "unit": "tangents/s", "ms_per_step": ms / steps,
+           "condense_ms_per_step": cond_ms / steps,
+           "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                        "frac": achieved / peak,
+                        "algorithmic": f"{h.work.flop_executed:.4g} executed DMMA flop/RVE ({h.work.g_tiles} tiles)"},
+           "bitwise_equal_to_dense": bool(torch.equal(C, C_dense))}
+    h.close()
+    return out
+
+
 # ----------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
@@ -429,6 +474,8 @@ def main():
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "what": "hom_set_phases from pinned host + condense + macro solve + recovery + D2H of C_eff, u, w"},
     }
+    if world == 1 and not args.tile_sparse and not h.finite and args.macro_basis == "dirac":
+        line["tile_sparse"] = tile_sparse_line(wl, C, args.steps, args.warmup)
     if world == 1 and args.spmv_nel > 0:
         if m == 3:
             C_tile = C

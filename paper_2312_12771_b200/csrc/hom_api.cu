@@ -513,7 +513,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   // ------------------------------------------------------------ chunking + allocation
   const size_t tiles = (size_t)R.nslot;
   const size_t per_rve = tiles * hom::TILE_ELEMS * 8 + (size_t)R.NT * hom::RHSW * 8 + 64 * 8 * 2 +
-                         (c->finite ? (size_t)R.ne * nq * 20 * 8 : 0);
+                         (c->finite ? (size_t)R.ne * 124 * 8 : 0);
   if (c->opt.rve_count > 0 && (c->opt.rve_begin < 0 || c->opt.rve_begin + c->opt.rve_count > c->B))
     return fail(HOM_ERR_INVALID_ARG, "rve_begin / rve_count outside [0, B)");
   c->b_lo = c->opt.rve_count > 0 ? c->opt.rve_begin : 0;
@@ -612,8 +612,8 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   c->Cavg = dalloc<double>(c, (size_t)64 * chunk, &rc);
   c->Pavg = dalloc<double>(c, (size_t)8 * chunk, &rc);
   if (c->finite) {
-    c->Aq = dalloc<double>(c, (size_t)chunk * R.ne * nq * 16, &rc);
-    c->Pq = dalloc<double>(c, (size_t)chunk * R.ne * nq * 4, &rc);
+    c->Aq = dalloc<double>(c, (size_t)chunk * R.ne * 124, &rc);  // element table of k_rve_element_nh
+    c->Pq = nullptr;
     c->w = dalloc<double>(c, (size_t)c->B * R.npad, &rc);
   }
   c->X = dalloc<double>(c, (size_t)(c->b_hi - c->b_lo) * R.NT * hom::RHSW, &rc);  // local range only

@@ -46,48 +46,26 @@ __device__ __forceinline__ double unit_stress(int k, int c, int J, double lam, d
 // with H = cof F (the 2-D specialisation of 1/2 F xx F).  kind 1 = beta 0 (R11).
 // F~ = F + grad w (eq:microGrad).
 // ---------------------------------------------------------------------------
-__global__ void k_rve_material_nh(RveDev R, int b0, int nb, const double* __restrict__ Fbar,
-                                  const double* __restrict__ w, double* __restrict__ Aq,
-                                  double* __restrict__ Pq, int* __restrict__ jflag) {
-  const int per = R.ne * R.nq;
-  long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= (long)nb * per) return;
-  int bl = (int)(gid / per), eq = (int)(gid % per);
-  int e = eq / R.nq, q = eq % R.nq;
-  int b = b0 + bl;
-  const double* Fb = Fbar + (long)b * 4;
-  double F[4] = {Fb[0], Fb[1], Fb[2], Fb[3]};
-  const double* wb = w + (long)b * R.npad;
-  for (int a = 0; a < R.nen; ++a) {
-    int p = R.elem_indep[e * R.nen + a];
-    const double* g = R.grad + ((long)(e * R.nq + q) * R.nen + a) * 2;
-    double w0 = wb[2 * p], w1 = wb[2 * p + 1];
-    F[0] += w0 * g[0]; F[1] += w0 * g[1];
-    F[2] += w1 * g[0]; F[3] += w1 * g[1];
-  }
-  int ph = R.phase[(R.phase_per_rve ? (long)b * R.ne : 0) + e];
-  const int np = R.mat_stride;
-  const double* mp = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * np : 0) + np * ph;
-  const double alpha = mp[0], beta = np == 3 ? mp[1] : 0.0, kappa = mp[np - 1];
+// Element quantities per (RVE, element), 124 doubles (EL_STRIDE): K_e [8][8] = sum_q eta G_q^T A_q G_q,
+// F_e [8][4] = sum_q eta G_q^T A_q, r_e [8] = sum_q eta G_q^T P_q (the element parts of K_ff, K_fF and
+// r_f, eq:discreteSys_D/L), and the qp sums sum_q eta A_q [16], sum_q eta P_q [4] for <A>, <P>.
+// One thread per element row (a, i): the material point is re-evaluated by the 8 row threads.
+constexpr int EL_STRIDE = 124, EL_F = 64, EL_R = 96, EL_A = 104, EL_P = 120;
+
+__device__ __forceinline__ bool cook_material(const double* F, double alpha, double beta, double kappa, double* P,
+                                              double* A) {
   // J - 1 from the displacement-gradient part (no cancellation near F = I)
   const double g11 = F[0] - 1.0, g22 = F[3] - 1.0;
   const double Jm1 = g11 + g22 + g11 * g22 - F[1] * F[2];
-  double J = 1.0 + Jm1;
-  double* A = Aq + gid * 16;
-  double* P = Pq + gid * 4;
-  if (!(J > 0.0)) {
-    atomicMin(&jflag[b], eq);  // first failing qp of this RVE (jflag init INT_MAX)
-    for (int i = 0; i < 16; ++i) A[i] = 0.0;
-    for (int i = 0; i < 4; ++i) P[i] = 0.0;
-    return;
-  }
-  double H[4] = {F[3], -F[2], -F[1], F[0]};  // cof F (2-D specialisation of 1/2 F xx F)
+  const double J = 1.0 + Jm1;
+  if (!(J > 0.0)) return false;
+  const double H[4] = {F[3], -F[2], -F[1], F[0]};  // cof F (2-D specialisation of 1/2 F xx F)
   const double ab = alpha + 2.0 * beta;
-  double dPsidJ = 2.0 * beta * J + kappa * Jm1 - 2.0 * ab / J;
-  double d2 = 2.0 * beta + kappa + 2.0 * ab / (J * J);
+  const double dPsidJ = 2.0 * beta * J + kappa * Jm1 - 2.0 * ab / J;
+  const double d2 = 2.0 * beta + kappa + 2.0 * ab / (J * J);
   // P = 2 (alpha + beta) F + g H written as 2 (alpha + beta)(F - H) + (g + 2 (alpha + beta)) H with
   // g + 2 (alpha + beta) = (J - 1)(2 beta + kappa + 2 (alpha + 2 beta) / J): both terms vanish at F = I
-  // (the stress-free reference) instead of cancelling, so R_micro reaches ~1e-15 (classical scheme)
+  // (the stress-free reference) instead of cancelling
   const double c0 = 2.0 * (alpha + beta), c1 = Jm1 * (2.0 * beta + kappa + 2.0 * ab / J);
   const double FmH[4] = {F[0] - F[3], F[1] + F[2], F[2] + F[1], F[3] - F[0]};
   for (int i = 0; i < 4; ++i) P[i] = c0 * FmH[i] + c1 * H[i];
@@ -99,13 +77,74 @@ __global__ void k_rve_material_nh(RveDev R, int b0, int nb, const double* __rest
       if (i + j == 3) v += ((i == 0 || i == 3) ? 1.0 : -1.0) * dPsidJ;
       A[i * 4 + j] = v;
     }
+  return true;
+}
+
+__global__ void k_rve_element_nh(RveDev R, int b0, int nb, const double* __restrict__ Fbar,
+                                 const double* __restrict__ w, double* __restrict__ EL, int* __restrict__ jflag) {
+  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int ne = R.ne, nq = R.nq;
+  if (gid >= (long)nb * ne * 8) return;
+  const int row = (int)(gid & 7);
+  const long ge = gid >> 3;
+  const int bl = (int)(ge / ne), e = (int)(ge % ne), b = b0 + bl;
+  const int a = row >> 1, i = row & 1;
+  const double* Fb = Fbar + (long)b * 4;
+  const double* wb = w + (long)b * R.npad;
+  const int ph = R.phase[(R.phase_per_rve ? (long)b * ne : 0) + e];
+  const int np = R.mat_stride;
+  const double* mp = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * np : 0) + np * ph;
+  const double alpha = mp[0], beta = np == 3 ? mp[1] : 0.0, kappa = mp[np - 1];
+  double we[8];
+  for (int aa = 0; aa < 4; ++aa) {
+    const int p = R.elem_indep[e * 4 + aa];
+    we[2 * aa] = wb[2 * p];
+    we[2 * aa + 1] = wb[2 * p + 1];
+  }
+  double ke[8] = {}, fe[4] = {}, re = 0.0, As[16] = {}, Ps[4] = {};
+  bool ok = true;
+  for (int q = 0; q < nq; ++q) {
+    const double* G = R.grad + (long)(e * nq + q) * 4 * 2;  // [nen][2]
+    double F[4] = {Fb[0], Fb[1], Fb[2], Fb[3]};
+    for (int aa = 0; aa < 4; ++aa) {  // F~ = F + grad w (eq:microGrad)
+      F[0] += we[2 * aa] * G[2 * aa]; F[1] += we[2 * aa] * G[2 * aa + 1];
+      F[2] += we[2 * aa + 1] * G[2 * aa]; F[3] += we[2 * aa + 1] * G[2 * aa + 1];
+    }
+    double P[4], A[16];
+    if (!cook_material(F, alpha, beta, kappa, P, A)) {
+      if (row == 0) atomicMin(&jflag[b], e * nq + q);  // first failing qp of this RVE (init INT_MAX)
+      ok = false;
+      break;
+    }
+    const double wq = R.wdet[e * nq + q];
+    const double ga0 = G[2 * a], ga1 = G[2 * a + 1];
+    // row (a, i): t[k] = sum_J g_a[J] A[(i,J), k]
+    double t[4];
+    for (int k = 0; k < 4; ++k) t[k] = ga0 * A[(2 * i) * 4 + k] + ga1 * A[(2 * i + 1) * 4 + k];
+    for (int k = 0; k < 4; ++k) fe[k] += wq * t[k];
+    re += wq * (ga0 * P[2 * i] + ga1 * P[2 * i + 1]);
+    for (int bb = 0; bb < 4; ++bb)
+      for (int j = 0; j < 2; ++j)  // column (b, j): sum_L t[(j,L)] g_b[L]
+        ke[2 * bb + j] += wq * (t[2 * j] * G[2 * bb] + t[2 * j + 1] * G[2 * bb + 1]);
+    if (row == 0) {
+      for (int k = 0; k < 16; ++k) As[k] += wq * A[k];
+      for (int k = 0; k < 4; ++k) Ps[k] += wq * P[k];
+    }
+  }
+  double* out = EL + ge * EL_STRIDE;
+  for (int k = 0; k < 8; ++k) out[row * 8 + k] = ok ? ke[k] : 0.0;
+  for (int k = 0; k < 4; ++k) out[EL_F + row * 4 + k] = ok ? fe[k] : 0.0;
+  out[EL_R + row] = ok ? re : 0.0;
+  if (row == 0) {
+    for (int k = 0; k < 16; ++k) out[EL_A + k] = ok ? As[k] : 0.0;
+    for (int k = 0; k < 4; ++k) out[EL_P + k] = ok ? Ps[k] : 0.0;
+  }
 }
 
 void launch_rve_material_nh(const RveDev& R, int b0, int nb, const double* F, const double* w,
-                            double* Aq, double* Pq, int* jflag, cudaStream_t s) {
-  long n = (long)nb * R.ne * R.nq;
-  int thr = 256;
-  k_rve_material_nh<<<(unsigned)((n + thr - 1) / thr), thr, 0, s>>>(R, b0, nb, F, w, Aq, Pq, jflag);
+                            double* EL, double* /*unused*/, int* jflag, cudaStream_t s) {
+  const long n = (long)nb * R.ne * 8;
+  k_rve_element_nh<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(R, b0, nb, F, w, EL, jflag);
 }
 
 // ---------------------------------------------------------------------------
@@ -137,7 +176,6 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   const int b = b0 + bl;
   const int nen = R.nen, nq = R.nq, ne = R.ne;
   constexpr int ND = ISO ? (1 << DIM) * DIM : 8;  // nen*dim
-  const long tq0 = (long)bl * ne * nq;  // offset of this RVE in Aq/Pq (chunk-local)
 
   if (ISO) {
     const uint8_t* ph = R.phase + (R.phase_per_rve ? (long)b * ne : 0);
@@ -172,14 +210,12 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
         acc[1] += v * s_mu[e];
       }
     } else {
-      for (int eq = tid; eq < ne * nq; eq += NTHR) {
-        double wq = R.wdet[eq];
-        const double* A = Aq + (tq0 + eq) * 16;
-        const double* P = Pq + (tq0 + eq) * 4;
+      for (int e = tid; e < ne; e += NTHR) {
+        const double* el = Aq + ((long)bl * ne + e) * EL_STRIDE;
 #pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] += wq * A[i];
+        for (int i = 0; i < 16; ++i) acc[i] += el[EL_A + i];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) acc[16 + i] += wq * P[i];
+        for (int i = 0; i < 4; ++i) acc[16 + i] += el[EL_P + i];
       }
     }
     // one pass: warp shuffles, then NV partial rows in smem
@@ -235,22 +271,10 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
             for (int k = 0; k < RHSW; ++k)
               if (k < R.m) out[k] += lam * fl[k] + mu * fm[k];
           } else {
-            for (int q = 0; q < nq; ++q) {
-              const double* g = R.grad + ((long)(e * nq + q) * nen + a) * DIM;
-              double wq = R.wdet[e * nq + q];
-              const double* A = Aq + (tq0 + e * nq + q) * 16;
-              const double* P = Pq + (tq0 + e * nq + q) * 4;
-              for (int k = 0; k < 4; ++k) {
-                double v = 0.0;
-#pragma unroll
-                for (int J = 0; J < DIM; ++J) v += g[J] * A[(c * DIM + J) * 4 + k];
-                out[k] += wq * v;
-              }
-              double v = 0.0;
-#pragma unroll
-              for (int J = 0; J < DIM; ++J) v += g[J] * P[c * DIM + J];
-              out[4] += wq * v;
-            }
+            const double* el = Aq + ((long)bl * ne + e) * EL_STRIDE;
+            const int rw = a * DIM + c;
+            for (int k = 0; k < 4; ++k) out[k] += el[EL_F + rw * 4 + k];
+            out[4] += el[EL_R + rw];
           }
         }
         if (!ISO) rr += out[4] * out[4];
@@ -317,23 +341,11 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
 #pragma unroll
                   for (int jj = 0; jj < DIM; ++jj) blk[i][jj] += ke[i * ND + jj];
               } else {
-                for (int qq = 0; qq < nq; ++qq) {
-                  const double* ga = R.grad + ((long)(e * nq + qq) * nen + a) * DIM;
-                  const double* gb = R.grad + ((long)(e * nq + qq) * nen + bb) * DIM;
-                  const double wq = R.wdet[e * nq + qq];
-                  const double* A = Aq + (tq0 + e * nq + qq) * 16;
+                const double* ke = Aq + ((long)bl * ne + e) * EL_STRIDE + (a * DIM) * 8 + bb * DIM;
 #pragma unroll
-                  for (int i = 0; i < DIM; ++i)
+                for (int i = 0; i < DIM; ++i)
 #pragma unroll
-                    for (int jj = 0; jj < DIM; ++jj) {
-                      double v = 0.0;
-#pragma unroll
-                      for (int Jd = 0; Jd < DIM; ++Jd)
-#pragma unroll
-                        for (int Ld = 0; Ld < DIM; ++Ld) v += ga[Jd] * A[(i * DIM + Jd) * 4 + jj * DIM + Ld] * gb[Ld];
-                      blk[i][jj] += wq * v;
-                    }
-                }
+                  for (int jj = 0; jj < DIM; ++jj) blk[i][jj] += ke[i * 8 + jj];
               }
             }
 #pragma unroll
