@@ -537,7 +537,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   {  // element types: (Klam, Kmu) geometry blocks equal to 1e-13 relative share one table (a uniform
      // grid has one; the representative differs from the others only by coordinate rounding)
     std::vector<int> etype(R.ne, 0);
-    std::vector<double> KlamT, KmuT;
+    std::vector<double> KlamT, KmuT, FlamT, FmuT;
     if (!c->finite) {
       const size_t blk = (size_t)ND * ND;
       for (int e = 0; e < R.ne; ++e) {
@@ -550,18 +550,25 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
           for (size_t i = 0; i < blk && same; ++i)
             same = std::fabs(Klam[e * blk + i] - KlamT[t * blk + i]) <= tol &&
                    std::fabs(Kmu[e * blk + i] - KmuT[t * blk + i]) <= tol;
+          const size_t fb = (size_t)ND * m;  // K_fe tables must match too (same geometry)
+          for (size_t i = 0; i < fb && same; ++i)
+            same = std::fabs(Flam[e * fb + i] - FlamT[t * fb + i]) <= tol &&
+                   std::fabs(Fmu[e * fb + i] - FmuT[t * fb + i]) <= tol;
           if (same) found = t;
         }
         if (found < 0) {
           found = (int)(KlamT.size() / blk);
           KlamT.insert(KlamT.end(), Klam.begin() + e * blk, Klam.begin() + (e + 1) * blk);
           KmuT.insert(KmuT.end(), Kmu.begin() + e * blk, Kmu.begin() + (e + 1) * blk);
+          const size_t fb = (size_t)ND * m;  // the element's K_fe tables (same geometry type)
+          FlamT.insert(FlamT.end(), Flam.begin() + e * fb, Flam.begin() + (e + 1) * fb);
+          FmuT.insert(FmuT.end(), Fmu.begin() + e * fb, Fmu.begin() + (e + 1) * fb);
         }
         etype[e] = found;
       }
     }
     R.ntype = c->finite ? 0 : (int)(KlamT.size() / ((size_t)ND * ND));
-    if ((size_t)R.ntype * mat->n_phases * ND * ND * sizeof(double) > 96 * 1024)
+    if ((size_t)R.ntype * mat->n_phases * ND * (ND + m) * sizeof(double) > 96 * 1024)
       return fail(HOM_ERR_INVALID_ARG, "too many distinct RVE element geometries x phases for the K1 shared-memory tables");
     int max_deg = 1;
     for (int pp = 0; pp < R.n_indep; ++pp) max_deg = std::max(max_deg, RP.nbr_ptr[pp + 1] - RP.nbr_ptr[pp]);
@@ -569,12 +576,22 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
     R.etype = upload(c, etype, s, &rc);
     R.Klam = upload(c, KlamT, s, &rc);
     R.Kmu = upload(c, KmuT, s, &rc);
+    R.FlamT = upload(c, FlamT, s, &rc);
+    R.FmuT = upload(c, FmuT, s, &rc);
   }
   R.Flam = upload(c, Flam, s, &rc);
   R.Fmu = upload(c, Fmu, s, &rc);
   R.evol = upload(c, evol, s, &rc);
   R.tile_nz = upload(c, tile_nz, s, &rc);
   R.g_nz = upload(c, g_nz, s, &rc);
+  {
+    std::vector<int> alist;
+    for (int I = 0; I < nt_; ++I)
+      for (int J = 0; J <= I; ++J)
+        if (tile_nz[(size_t)I * nt_ + J]) alist.push_back((I << 16) | J);
+    R.n_a = (int)alist.size();
+    R.a_list = upload(c, alist, s, &rc);
+  }
   R.tslot = upload(c, tslot, s, &rc);
   R.phase = upload(c, phase, s, &rc);
   R.mat = upload(c, params, s, &rc);

@@ -40,6 +40,8 @@ struct RveDev {
   const double* Klam;             // [ntype][nen*dim][nen*dim] (element type = identical geometry)
   const double* Kmu;
   const int* etype;               // [ne] element -> type
+  const double* FlamT;            // [ntype][nen*dim][m] K_fe tables per element type
+  const double* FmuT;
   int ntype;
   int npw;                        // K1: RVE nodes gathered per warp iteration (32 / max degree)
   const double* Flam;             // [ne][nen*dim][m]
@@ -52,6 +54,8 @@ struct RveDev {
   const uint8_t* g_nz;
   const int* tslot;
   int nslot;                      // pool slots (64x64 tiles) per RVE
+  const int* a_list;              // [n_a] (I << 16 | J) of the structurally nonzero lower tiles (K1)
+  int n_a;
   int xb0;                        // first RVE of the influence store X (the context's local range)
 };
 

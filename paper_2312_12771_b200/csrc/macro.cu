@@ -9,6 +9,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "hom_internal.cuh"
@@ -733,8 +734,13 @@ void cg2_slice_sizes(const MacroDev& M, const int* host_rowptr, int G, int* max_
 bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const double* val, const double* rhs,
                               double scale, double rtol, int max_iter, double* x, CgState* st, cudaStream_t s) {
   static int cached_G = -1;
+  static const int force_G = [] {
+    const char* e = getenv("HOM_CG_CLUSTER");  // experiment knob: 8 or 16
+    return e ? atoi(e) : 0;
+  }();
   for (int gi = 0; gi < 2; ++gi) {
     const int G = gi == 0 ? 16 : 8;
+    if (force_G && G != force_G) continue;
     if (cached_G > 0 && G != cached_G) continue;
     const int max_nr = slice[gi][0], max_nnz = slice[gi][1];
     const size_t sm = (size_t)(6 * CGC_MAXG + 96 + M.ndof + 5 * max_nr + max_nr * M.dim) * 8 +

@@ -170,7 +170,8 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   double* s_lam = red + NTHR;                // [ne] (ISO)
   double* s_mu = s_lam + R.ne;               // [ne] (ISO)
   double* s_K = s_mu + R.ne;                 // [ntype][n_phase][ND][ND] element matrices (ISO)
-  int* s_ep = reinterpret_cast<int*>(s_K + (ISO ? R.ntype * R.n_phase * ((1 << DIM) * DIM) * ((1 << DIM) * DIM) : 0));
+  double* s_F = s_K + (ISO ? R.ntype * R.n_phase * ((1 << DIM) * DIM) * ((1 << DIM) * DIM) : 0);  // [type][phase][ND][m]
+  int* s_ep = reinterpret_cast<int*>(s_F + (ISO ? R.ntype * R.n_phase * ((1 << DIM) * DIM) * R.m : 0));
   const int tid = threadIdx.x;
   const int bl = blockIdx.x;
   const int b = b0 + bl;
@@ -193,6 +194,12 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
       const double E = mt[2 * pp], nu = mt[2 * pp + 1];
       const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)), mu = E / (2.0 * (1.0 + nu));
       s_K[i] = lam * R.Klam[(long)t * ND * ND + j] + mu * R.Kmu[(long)t * ND * ND + j];
+    }
+    for (int i = tid; i < R.ntype * R.n_phase * ND * R.m; i += NTHR) {  // K_fe element tables
+      const int t = i / (R.n_phase * ND * R.m), pp = (i / (ND * R.m)) % R.n_phase, j = i % (ND * R.m);
+      const double E = mt[2 * pp], nu = mt[2 * pp + 1];
+      const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)), mu = E / (2.0 * (1.0 + nu));
+      s_F[i] = lam * R.FlamT[(long)t * ND * R.m + j] + mu * R.FmuT[(long)t * ND * R.m + j];
     }
   }
   __syncthreads();
@@ -264,12 +271,10 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
         for (int s = R.inc_ptr[p]; s < R.inc_ptr[p + 1]; ++s) {
           int e = R.inc[s] >> 4, a = R.inc[s] & 15;
           if (ISO) {
-            const double lam = s_lam[e], mu = s_mu[e];
-            const double* fl = R.Flam + ((long)e * ND + a * DIM + c) * R.m;
-            const double* fm = R.Fmu + ((long)e * ND + a * DIM + c) * R.m;
+            const double* fe = s_F + ((long)s_ep[e] * ND + a * DIM + c) * R.m;
 #pragma unroll
             for (int k = 0; k < RHSW; ++k)
-              if (k < R.m) out[k] += lam * fl[k] + mu * fm[k];
+              if (k < R.m) out[k] += fe[k];
           } else {
             const double* el = Aq + ((long)bl * ne + e) * EL_STRIDE;
             const int rw = a * DIM + c;
@@ -307,12 +312,13 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   const int lane = tid & 31, warp = tid >> 5;
   double* rowbuf = s_row + warp * npw * DIM * TILE;
   const int g = lane / S, jl = lane % S;
-  for (int I = 0; I < nt; ++I) {
+  for (int t = 0; t < R.n_a; ++t) {  // compact list of the structurally nonzero lower tiles
+    const int code = __ldg(R.a_list + t);
+    const int I = code >> 16, J = code & 0xffff;
     const int r0 = I * TILE;
     const int p_lo = r0 / DIM, p_hi = (r0 + TILE - 1) / DIM;  // nodes touching rows r0..r0+63
-    for (int J = 0; J <= I; ++J) {
-      if (!R.tile_nz[I * nt + J]) continue;
-      double* gt = Kb + (long)R.tslot[I * nt + J] * TILE_ELEMS;
+    {
+      double* gt = Kb + (long)__ldg(R.tslot + I * nt + J) * TILE_ELEMS;
       const int c0 = J * TILE;
       for (int p0 = p_lo + warp * npw; p0 <= p_hi; p0 += (NTHR / 32) * npw) {
         for (int i = lane; i < npw * DIM * TILE / 2; i += 32)
@@ -385,7 +391,7 @@ void launch_rve_assemble(const RveDev& R, int b0, int nb, double* Kt, double* Y,
                          cudaStream_t s) {
   const int dim = R.finite ? 2 : R.dim, nd = (1 << dim) * dim;  // nen*dim
   size_t sm = (size_t)((NTHR / 32) * R.npw * dim * TILE + NTHR + 2 * R.ne) * sizeof(double) +
-              (R.finite ? 0 : (size_t)R.ntype * R.n_phase * nd * nd * sizeof(double) + (size_t)R.ne * sizeof(int));
+              (R.finite ? 0 : (size_t)R.ntype * R.n_phase * nd * (nd + R.m) * sizeof(double) + (size_t)R.ne * sizeof(int));
   if (R.finite) {
     auto k = k_rve_assemble<2, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
