@@ -572,7 +572,22 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
       return fail(HOM_ERR_INVALID_ARG, "too many distinct RVE element geometries x phases for the K1 shared-memory tables");
     int max_deg = 1;
     for (int pp = 0; pp < R.n_indep; ++pp) max_deg = std::max(max_deg, RP.nbr_ptr[pp + 1] - RP.nbr_ptr[pp]);
-    R.npw = std::max(1, std::min(8, 32 / max_deg));
+
+    {  // flattened gather records: one dependent load per (node, neighbour) in K1
+      int max_sh = 0;
+      for (size_t k = 0; k + 1 < RP.sh_ptr.size(); ++k) max_sh = std::max(max_sh, RP.sh_ptr[k + 1] - RP.sh_ptr[k]);
+      R.maxdeg = max_deg;
+      R.rs4 = (2 + max_sh + 3) / 4;
+      std::vector<int> rec((size_t)R.n_indep * max_deg * R.rs4 * 4, -1);
+      for (int pp = 0; pp < R.n_indep; ++pp)
+        for (int k = RP.nbr_ptr[pp]; k < RP.nbr_ptr[pp + 1]; ++k) {
+          int* r = rec.data() + ((size_t)pp * max_deg + (k - RP.nbr_ptr[pp])) * R.rs4 * 4;
+          r[0] = RP.nbr[k] == R.corner ? -1 : RP.nbr[k];
+          r[1] = RP.sh_ptr[k + 1] - RP.sh_ptr[k];
+          for (int sidx = RP.sh_ptr[k]; sidx < RP.sh_ptr[k + 1]; ++sidx) r[2 + sidx - RP.sh_ptr[k]] = RP.sh[sidx];
+        }
+      R.nrec = reinterpret_cast<const int4*>(upload(c, rec, s, &rc));
+    }
     R.etype = upload(c, etype, s, &rc);
     R.Klam = upload(c, KlamT, s, &rc);
     R.Kmu = upload(c, KmuT, s, &rc);
@@ -591,6 +606,44 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
         if (tile_nz[(size_t)I * nt_ + J]) alist.push_back((I << 16) | J);
     R.n_a = (int)alist.size();
     R.a_list = upload(c, alist, s, &rc);
+    R.npw = hom::rve_assemble_npw(R);
+    // K1 warp work items: the row nodes of each nonzero tile packed greedily into items of
+    // <= npw consecutive nodes and <= 32 in-tile neighbour records (one per lane), dealt
+    // round-robin over the warps
+    const int dK = c->finite ? 2 : R.dim;
+    std::vector<int> witem, wlist;
+    for (int t = 0; t < R.n_a; ++t) {
+      const int r0 = (alist[t] >> 16) * 64, c0 = (alist[t] & 0xffff) * 64;
+      const int p_lo = r0 / dK, p_hi = (r0 + 63) / dK;
+      int p0 = p_lo, nn = 0;
+      std::vector<int> lanes;
+      auto flush = [&]() {
+        if (nn == 0) return;
+        witem.insert(witem.end(), {t, p0, nn, 0});
+        lanes.resize(32, -1);
+        wlist.insert(wlist.end(), lanes.begin(), lanes.end());
+        lanes.clear();
+        p0 += nn;
+        nn = 0;
+      };
+      for (int pp = p_lo; pp <= p_hi; ++pp) {
+        std::vector<int> mine;
+        if (pp < R.n_indep && pp != R.corner)
+          for (int k = RP.nbr_ptr[pp]; k < RP.nbr_ptr[pp + 1]; ++k) {
+            const int q = RP.nbr[k], cq = q * dK - c0;
+            if (q != R.corner && cq + dK > 0 && cq < 64) mine.push_back(pp * R.maxdeg + (k - RP.nbr_ptr[pp]));
+          }
+        if ((int)mine.size() > 32) return fail(HOM_ERR_INVALID_ARG, "K1: more than 32 neighbour blocks of one node in one tile");
+        if (nn == R.npw || lanes.size() + mine.size() > 32) flush();
+        for (int ridx : mine) lanes.push_back((nn << 24) | ridx);
+        ++nn;
+      }
+      flush();
+    }
+    if ((long)R.n_indep * R.maxdeg >= (1L << 24)) return fail(HOM_ERR_INVALID_ARG, "K1: RVE too large for 24-bit record indices");
+    R.n_witem = (int)(witem.size() / 4);
+    R.witem = reinterpret_cast<const int4*>(upload(c, witem, s, &rc));
+    R.wlist = upload(c, wlist, s, &rc);
   }
   R.tslot = upload(c, tslot, s, &rc);
   R.phase = upload(c, phase, s, &rc);

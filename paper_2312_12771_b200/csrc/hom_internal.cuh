@@ -43,7 +43,7 @@ struct RveDev {
   const double* FlamT;            // [ntype][nen*dim][m] K_fe tables per element type
   const double* FmuT;
   int ntype;
-  int npw;                        // K1: RVE nodes gathered per warp iteration (32 / max degree)
+  int npw;                        // K1: row-buffer capacity in RVE nodes per warp (12 / dim)
   const double* Flam;             // [ne][nen*dim][m]
   const double* Fmu;
   const double* evol;             // [ne] element volume
@@ -56,6 +56,15 @@ struct RveDev {
   int nslot;                      // pool slots (64x64 tiles) per RVE
   const int* a_list;              // [n_a] (I << 16 | J) of the structurally nonzero lower tiles (K1)
   int n_a;
+  // K1 gather records: node p, neighbour slot j < maxdeg -> rs4 int4s
+  // {q (-1: none / corner), n_sh, code_0 .. code_{n_sh-1}, -1 ...}, code = e<<8 | a<<4 | b
+  const int4* nrec;
+  int maxdeg, rs4;
+  // K1 warp work items: {tile t, first row node p0, node count nn, 0}, and per item one record
+  // per lane: (g << 24 | record index) for node p0 + g, -1 = idle lane (<= 32 records, <= npw nodes)
+  const int4* witem;
+  const int* wlist;
+  int n_witem;
   int xb0;                        // first RVE of the influence store X (the context's local range)
 };
 
@@ -92,6 +101,8 @@ struct CgState {
 // ---- kernels (launch wrappers; all enqueue on `s`) ----
 void launch_rve_material_nh(const RveDev& R, int b0, int nb, const double* F, const double* w,
                             double* Aq, double* Pq, int* jflag, cudaStream_t s);
+size_t rve_assemble_smem(const RveDev& R, int npw);  // K1 dynamic shared memory
+int rve_assemble_npw(const RveDev& R);              // K1 row-buffer nodes per warp
 void launch_rve_assemble(const RveDev& R, int b0, int nb, double* Kt, double* Y, double* Cavg,
                          double* Pavg, double* rfn, const double* Aq, const double* Pq,
                          cudaStream_t s);

@@ -167,9 +167,7 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   extern __shared__ __align__(128) double smem[];
   double* s_row = smem;                      // [8 warps][npw][DIM][64] tile-row buffers
   double* red = s_row + (NTHR / 32) * R.npw * DIM * TILE;  // [NTHR] reduction scratch
-  double* s_lam = red + NTHR;                // [ne] (ISO)
-  double* s_mu = s_lam + R.ne;               // [ne] (ISO)
-  double* s_K = s_mu + R.ne;                 // [ntype][n_phase][ND][ND] element matrices (ISO)
+  double* s_K = red + NTHR;                  // [ntype][n_phase][ND][ND] element matrices (ISO)
   double* s_F = s_K + (ISO ? R.ntype * R.n_phase * ((1 << DIM) * DIM) * ((1 << DIM) * DIM) : 0);  // [type][phase][ND][m]
   int* s_ep = reinterpret_cast<int*>(s_F + (ISO ? R.ntype * R.n_phase * ((1 << DIM) * DIM) * R.m : 0));
   const int tid = threadIdx.x;
@@ -181,13 +179,7 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   if (ISO) {
     const uint8_t* ph = R.phase + (R.phase_per_rve ? (long)b * ne : 0);
     const double* mt = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * R.mat_stride : 0);
-    for (int e = tid; e < ne; e += NTHR) {
-      int p = ph[e];
-      double E = mt[2 * p], nu = mt[2 * p + 1];
-      s_lam[e] = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
-      s_mu[e] = E / (2.0 * (1.0 + nu));
-      s_ep[e] = R.etype[e] * R.n_phase + p;
-    }
+    for (int e = tid; e < ne; e += NTHR) s_ep[e] = R.etype[e] * R.n_phase + ph[e];
     // K_e = lam Klam_t + mu Kmu_t for every (element type t, phase) of this RVE
     for (int i = tid; i < R.ntype * R.n_phase * ND * ND; i += NTHR) {
       const int t = i / (R.n_phase * ND * ND), pp = (i / (ND * ND)) % R.n_phase, j = i % (ND * ND);
@@ -211,10 +203,13 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
 #pragma unroll
     for (int i = 0; i < NV; ++i) acc[i] = 0.0;
     if (ISO) {
+      const uint8_t* ph = R.phase + (R.phase_per_rve ? (long)b * ne : 0);
+      const double* mt = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * R.mat_stride : 0);
       for (int e = tid; e < ne; e += NTHR) {
-        double v = R.evol[e];
-        acc[0] += v * s_lam[e];
-        acc[1] += v * s_mu[e];
+        const int p = ph[e];
+        const double E = mt[2 * p], nu = mt[2 * p + 1], v = R.evol[e];
+        acc[0] += v * (E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)));
+        acc[1] += v * (E / (2.0 * (1.0 + nu)));
       }
     } else {
       for (int e = tid; e < ne; e += NTHR) {
@@ -301,44 +296,49 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   }
 
   // ---- K_ff tiles: node-row gather, coalesced direct stores ----
-  // A warp owns R.npw consecutive RVE nodes p at a time; lane group g = lane / S (S = 32/npw)
-  // serves node p0 + g and its lane j forms the DIM x DIM block K_pq of neighbour q = nbr(p, j)
-  // (sum over the shared elements of the per-(type, phase) element matrix; the periodic map
-  // is applied through the independent-node numbering) into the warp's row buffer; then every
-  // lane stores its two columns of the npw*DIM rows (512 B per row per warp, 16 B per lane).
+  // A work item is nn <= R.npw consecutive row nodes of one tile whose in-tile neighbour blocks
+  // (<= 32, packed on the host) are one per lane: the lane forms the DIM x DIM block K_pq of
+  // its record (sum over the shared elements of the per-(type, phase) element matrix; the
+  // periodic map is applied through the independent-node numbering) in the warp's row buffer;
+  // then every lane stores its two columns of the nn*DIM rows (512 B per row per warp).
   // Structurally zero tiles are never touched (k_condense starts their accumulators at zero).
-  const int nt = R.nt, npw = R.npw, S = 32 / npw;
+  const int nt = R.nt;
   double* Kb = Kt + (long)bl * R.nslot * TILE_ELEMS;
   const int lane = tid & 31, warp = tid >> 5;
-  double* rowbuf = s_row + warp * npw * DIM * TILE;
-  const int g = lane / S, jl = lane % S;
-  for (int t = 0; t < R.n_a; ++t) {  // compact list of the structurally nonzero lower tiles
-    const int code = __ldg(R.a_list + t);
+  double* rowbuf = s_row + warp * R.npw * DIM * TILE;
+  // work items {tile, first row node p0, nn nodes} with one in-tile neighbour record per lane
+  for (int it = warp; it < R.n_witem; it += NTHR / 32) {
+    const int4 wi = __ldg(R.witem + it);
+    const int lw = __ldg(R.wlist + (long)it * 32 + lane);
+    const int code = __ldg(R.a_list + wi.x);
     const int I = code >> 16, J = code & 0xffff;
     const int r0 = I * TILE;
-    const int p_lo = r0 / DIM, p_hi = (r0 + TILE - 1) / DIM;  // nodes touching rows r0..r0+63
+    const int p0 = wi.y, nn = wi.z;
     {
       double* gt = Kb + (long)__ldg(R.tslot + I * nt + J) * TILE_ELEMS;
       const int c0 = J * TILE;
-      for (int p0 = p_lo + warp * npw; p0 <= p_hi; p0 += (NTHR / 32) * npw) {
-        for (int i = lane; i < npw * DIM * TILE / 2; i += 32)
+      {
+        for (int i = lane; i < nn * DIM * TILE / 2; i += 32)
           reinterpret_cast<double2*>(rowbuf)[i] = make_double2(0.0, 0.0);
         __syncwarp();
-        const int p = p0 + g;
-        if (g < npw && p <= p_hi && p < R.n_indep && p != R.corner) {
-          double* rb = rowbuf + g * DIM * TILE;
-          const int k0 = R.nbr_ptr[p], deg = R.nbr_ptr[p + 1] - k0;
-          for (int j = jl; j < deg; j += S) {
-            const int k = k0 + j, q = R.nbr[k];
+        if (lw >= 0) {
+          double* rb = rowbuf + (lw >> 24) * DIM * TILE;
+          {
+            const int4* rec = R.nrec + (long)(lw & 0xffffff) * R.rs4;
+            const int4 hd = __ldg(rec);
+            const int q = hd.x;
             const int cq = q * DIM - c0;  // first column of q in this tile
-            if (q == R.corner || cq + DIM <= 0 || cq >= TILE) continue;
             double blk[DIM][DIM];
 #pragma unroll
             for (int i = 0; i < DIM; ++i)
 #pragma unroll
               for (int jj = 0; jj < DIM; ++jj) blk[i][jj] = 0.0;
-            for (int sh = R.sh_ptr[k]; sh < R.sh_ptr[k + 1]; ++sh) {
-              const int code = R.sh[sh];
+            const int nsh = hd.y;
+            int4 cur = hd;
+            for (int sidx = 0; sidx < nsh; ++sidx) {
+              const int slot = sidx + 2;
+              if ((slot & 3) == 0) cur = __ldg(rec + (slot >> 2));
+              const int code = (slot & 3) == 0 ? cur.x : (slot & 3) == 1 ? cur.y : (slot & 3) == 2 ? cur.z : cur.w;
               const int e = code >> 8, a = (code >> 4) & 15, bb = code & 15;
               if (ISO) {
                 const double* ke = s_K + (long)s_ep[e] * ND * ND + (a * DIM) * ND + bb * DIM;
@@ -364,9 +364,8 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
           }
         }
         __syncwarp();
-        for (int n = 0; n < npw; ++n) {
+        for (int n = 0; n < nn; ++n) {
           const int pn = p0 + n;
-          if (pn > p_hi) break;
           const bool pad = pn >= R.n_indep || pn == R.corner;  // identity rows (corner class, tail)
 #pragma unroll
           for (int ci = 0; ci < DIM; ++ci) {
@@ -386,12 +385,25 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   }
 }
 
+size_t rve_assemble_smem(const RveDev& R, int npw) {
+  const int dim = R.finite ? 2 : R.dim, nd = (1 << dim) * dim;  // nen*dim
+  return (size_t)((NTHR / 32) * npw * dim * TILE + NTHR) * sizeof(double) +
+         (R.finite ? 0 : (size_t)R.ntype * R.n_phase * nd * (nd + R.m) * sizeof(double) + (size_t)R.ne * sizeof(int));
+}
+
+int rve_assemble_npw(const RveDev& R) {
+  // largest row buffer (<= 16 rows per warp) that keeps 4 CTAs per SM (<= 56 KB each)
+  const int dim = R.finite ? 2 : R.dim;
+  int npw = 16 / dim;
+  while (npw > 1 && rve_assemble_smem(R, npw) > 56 * 1024) --npw;
+  return npw;
+}
+
 void launch_rve_assemble(const RveDev& R, int b0, int nb, double* Kt, double* Y, double* Cavg,
                          double* Pavg, double* rfn, const double* Aq, const double* Pq,
                          cudaStream_t s) {
   const int dim = R.finite ? 2 : R.dim, nd = (1 << dim) * dim;  // nen*dim
-  size_t sm = (size_t)((NTHR / 32) * R.npw * dim * TILE + NTHR + 2 * R.ne) * sizeof(double) +
-              (R.finite ? 0 : (size_t)R.ntype * R.n_phase * nd * (nd + R.m) * sizeof(double) + (size_t)R.ne * sizeof(int));
+  const size_t sm = rve_assemble_smem(R, R.npw);
   if (R.finite) {
     auto k = k_rve_assemble<2, false>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
