@@ -202,14 +202,14 @@ def spmv_scaled(C_tile, nel: int = 2048, reps: int = 20):
 
 
 # ----------------------------------------------------------------------------- tile-sparse companion
-def tile_sparse_line(wl, C_dense, steps: int, warmup: int):
+def tile_sparse_line(wl, C_dense, steps: int, warmup: int, ordering="folded"):
     """The same linear step with the tile-sparse factorisation: tangents/s and the
     k_condense roofline on the executed tile-structure flops, plus the bitwise check against the
     dense tangents of the main line (every skipped product is an exact zero)."""
     import torch
 
     from paper_2312_12771_b200.hom import Homogenizer
-    h = Homogenizer.from_workload(wl, tile_sparse=True)
+    h = Homogenizer.from_workload(wl, tile_sparse=True, rve_ordering=ordering)
     C = h.empty(h.n_rve, h.m, h.m)
     u = h.empty(h.n_dof)
     w = h.empty(h.n_rve, h.n_pad)
@@ -260,6 +260,8 @@ def main():
                     help="constant: one RVE per macro element (SURVEY §8(f) 2, small strain)")
     ap.add_argument("--tile-sparse", action="store_true",
                     help="factor only the symbolic tile fill of K_ff (SURVEY §8(f) 3) instead of every lower tile")
+    ap.add_argument("--rve-ordering", default="folded", choices=["folded", "natural"],
+                    help="internal order of the RVE nodes (rows of K_ff); w at the API is natural either way")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -276,7 +278,8 @@ def main():
               "flop_per_rve": wl.flop_per_rve(),
               "parallelism": f"rve-sharded x{world} (C_eff all-gather, replicated macro CG)" if world > 1 else "single",
               "macro_nel": wl.nel, "rve_per_gpu": wl.n_rve / world,
-              "factorization": "tile-sparse" if args.tile_sparse else "dense", "macro_basis": args.macro_basis}
+              "factorization": "tile-sparse" if args.tile_sparse else "dense", "macro_basis": args.macro_basis,
+              "rve_ordering": args.rve_ordering}
 
     if args.impl == "reference":
         if rank != 0:
@@ -310,11 +313,13 @@ def main():
 
     if world > 1:
         from paper_2312_12771_b200.dist import ShardedHomogenizer
-        sh = ShardedHomogenizer(wl, tile_sparse=args.tile_sparse, macro_basis=args.macro_basis)
+        sh = ShardedHomogenizer(wl, tile_sparse=args.tile_sparse, macro_basis=args.macro_basis,
+                                rve_ordering=args.rve_ordering)
         h = sh.h
     else:
         sh = None
-        h = Homogenizer.from_workload(wl, tile_sparse=args.tile_sparse, macro_basis=args.macro_basis)
+        h = Homogenizer.from_workload(wl, tile_sparse=args.tile_sparse, macro_basis=args.macro_basis,
+                                      rve_ordering=args.rve_ordering)
     work = h.work
     config["l2"] = (f"no flush: each step writes and re-reads the K_ff tile pool ({h.sizes.rve_count * work.g_tiles * 32768 / 1e9:.2f} GB, "
                     f"{work.g_tiles} 64x64 tiles per RVE), larger than the 126 MB L2")
@@ -475,7 +480,7 @@ def main():
                 "what": "hom_set_phases from pinned host + condense + macro solve + recovery + D2H of C_eff, u, w"},
     }
     if world == 1 and not args.tile_sparse and not h.finite and args.macro_basis == "dirac":
-        line["tile_sparse"] = tile_sparse_line(wl, C, args.steps, args.warmup)
+        line["tile_sparse"] = tile_sparse_line(wl, C, args.steps, args.warmup, args.rve_ordering)
     if world == 1 and args.spmv_nel > 0:
         if m == 3:
             C_tile = C

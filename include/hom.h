@@ -131,6 +131,14 @@ typedef struct {
                                K_e = sum_q eta B_q^T <C>_e B_q - |B_e| Bbar^T (<C>_e - C_eff,e) Bbar
                                (Bbar = element-average strain operator) and kinematics / recovery use
                                the element-average strain. */
+  int32_t rve_ordering;     /* internal order of the RVE's independent nodes (the rows of K_ff):
+                               0 = folded (default): along every axis the periodic images are
+                               interleaved 0, r-1, 1, r-2, ... (slowest axis first), so wrap-around
+                               neighbours are adjacent and K_ff is banded without a periodic frame
+                               (fewer fill tiles for tile_sparse); 1 = natural
+                               (first appearance in the mesh).  The layout of w at the API (d_w of
+                               hom_recover_fluctuations / hom_set_fluctuations / hom_get_fluctuations)
+                               is always the natural one. */
 } hom_options;
 
 typedef struct {

@@ -382,6 +382,28 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
     if (it == indep_of.end()) return fail(HOM_ERR_MESH, "RVE has no node at its lower corner");
     R.corner = it->second;
   }
+  if (options->rve_ordering != 0 && options->rve_ordering != 1)
+    return fail(HOM_ERR_INVALID_ARG, "rve_ordering must be 0 (folded) or 1 (natural)");
+  if (options->rve_ordering == 0) {  // folded order: interleave the periodic images on every axis
+    std::vector<std::vector<long long>> fkey(R.n_indep);
+    for (auto& kv : indep_of) {
+      std::vector<long long> f;
+      for (int k = dim - 1; k >= 0; --k) {  // slowest axis first, like the natural grid order
+        const long long L = std::llround((hi[k] - lo[k]) / (1e-7 * Lmax)), x = kv.first[k];
+        f.push_back(std::min(x, L - x));
+        f.push_back(2 * x > L ? 0 : 1);  // the upper image of a pair first: 0, r-1, 1, r-2, ...
+      }
+      fkey[kv.second] = f;
+    }
+    std::vector<int> order(R.n_indep);
+    for (int p = 0; p < R.n_indep; ++p) order[p] = p;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return fkey[a] < fkey[b]; });
+    std::vector<int> int_of(R.n_indep);
+    for (int p = 0; p < R.n_indep; ++p) int_of[order[p]] = p;
+    for (int n = 0; n < rn; ++n) indep[n] = int_of[indep[n]];
+    R.corner = int_of[R.corner];
+    R.nat_of = upload(c, order, s, &rc);  // internal p -> natural order[p]
+  }
   R.npad = dim * R.n_indep;
   R.nt = (R.npad + hom::TILE - 1) / hom::TILE;
   R.NT = R.nt * hom::TILE;
@@ -880,7 +902,7 @@ int hom_recover_fluctuations(hom_ctx* c, const double* d_x, double* d_w, void* s
   if (c->finite) {
     run(c, HOM_PROF_RECOVER, s,
         [&] { hom::launch_recover(c->R, c->b_lo, c->b_hi - c->b_lo, c->X, c->kin, c->w, 1, s); });
-    if (d_w) cudaMemcpyAsync(d_w, c->w, sizeof(double) * (size_t)c->B * c->R.npad, cudaMemcpyDeviceToDevice, s);
+    if (d_w) run(c, HOM_PROF_RECOVER, s, [&] { hom::launch_permute_w(c->R, c->B, c->w, d_w, 1, s); });
   } else {
     run(c, HOM_PROF_RECOVER, s,
         [&] { hom::launch_recover(c->R, c->b_lo, c->b_hi - c->b_lo, c->X, c->kin, d_w, 0, s); });
@@ -900,15 +922,13 @@ int hom_newton_update(hom_ctx* c, double* d_u, const double* d_du, void* stream)
 
 int hom_set_fluctuations(hom_ctx* c, const double* d_w, void* stream) {
   if (!c || !d_w || !c->finite) return set_err(c, HOM_ERR_INVALID_ARG, "hom_set_fluctuations");
-  cudaMemcpyAsync(c->w, d_w, sizeof(double) * (size_t)c->B * c->R.npad, cudaMemcpyDeviceToDevice,
-                  (cudaStream_t)stream);
+  hom::launch_permute_w(c->R, c->B, d_w, c->w, 0, (cudaStream_t)stream);
   return check_cuda(c, cudaGetLastError(), "hom_set_fluctuations");
 }
 
 int hom_get_fluctuations(hom_ctx* c, double* d_w, void* stream) {
   if (!c || !d_w || !c->finite) return set_err(c, HOM_ERR_INVALID_ARG, "hom_get_fluctuations");
-  cudaMemcpyAsync(d_w, c->w, sizeof(double) * (size_t)c->B * c->R.npad, cudaMemcpyDeviceToDevice,
-                  (cudaStream_t)stream);
+  hom::launch_permute_w(c->R, c->B, c->w, d_w, 1, (cudaStream_t)stream);
   return check_cuda(c, cudaGetLastError(), "hom_get_fluctuations");
 }
 

@@ -66,6 +66,7 @@ struct RveDev {
   const int* wlist;
   int n_witem;
   int xb0;                        // first RVE of the influence store X (the context's local range)
+  const int* nat_of;              // [n_indep] internal node -> natural (API) node; nullptr = identity
 };
 
 struct MacroDev {
@@ -133,6 +134,8 @@ void cg2_slice_sizes(const MacroDev& M, const int* host_rowptr, int G, int* max_
 bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const double* val, const double* rhs,
                               double scale, double rtol, int max_iter, double* x, CgState* st, cudaStream_t s);
 void launch_axpy(double* y, const double* x, double a, int n, cudaStream_t s);
+// w between the natural (API) and the internal node order (to_api: internal -> natural)
+void launch_permute_w(const RveDev& R, int B, const double* src, double* dst, int to_api, cudaStream_t s);
 void launch_recover(const RveDev& R, int b0, int nb, const double* X, const double* kin, double* w,
                     int accumulate, cudaStream_t s);
 

@@ -1018,7 +1018,32 @@ __global__ void k_recover(RveDev R, int b0, int nb, const double* __restrict__ X
   double v = 0.0;
   for (int k = 0; k < R.m; ++k) v += xr[k] * kb[k];
   if (accumulate) w[t] -= xr[R.m] + v;
-  else w[t] = -v;
+  else if (R.nat_of) {  // external (natural) layout
+    const int dr = R.npad / R.n_indep;
+    w[(long)b * R.npad + (long)__ldg(R.nat_of + i / dr) * dr + i % dr] = -v;
+  } else w[t] = -v;
+}
+
+__global__ void k_permute_w(RveDev R, long n, const double* __restrict__ src, double* __restrict__ dst,
+                            int to_api) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const int dr = R.npad / R.n_indep;
+  const long b = t / R.npad;
+  const int i = (int)(t % R.npad);  // internal index
+  const long e = b * R.npad + (long)__ldg(R.nat_of + i / dr) * dr + i % dr;
+  if (to_api) dst[e] = src[t];
+  else dst[t] = src[e];
+}
+
+void launch_permute_w(const RveDev& R, int B, const double* src, double* dst, int to_api, cudaStream_t s) {
+  const long n = (long)B * R.npad;
+  if (n <= 0) return;
+  if (!R.nat_of) {
+    cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDeviceToDevice, s);
+    return;
+  }
+  k_permute_w<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(R, n, src, dst, to_api);
 }
 
 void launch_recover(const RveDev& R, int b0, int nb, const double* X, const double* kin, double* w,

@@ -263,6 +263,88 @@ def test_tile_sparse_finite_strain_per_state(torch_cuda):
         assert np.array_equal(a, b)
 
 
+# ------------------------------------------------------------------ internal RVE node order (hom_options.rve_ordering)
+def _expected_tile_fill(r, d, ordering):
+    """The test's own symbolic tile-level Cholesky fill of K_ff (shares nothing with libhom): the
+    periodic r^d grid, Q1/hex8 node couplings (all 3^d neighbours, wrapped), the corner node
+    removed (identity pad), dofs node-major in the given node order, 64x64 tiles.  Returns
+    (structurally nonzero lower tiles, lower tiles of the factor after fill)."""
+    import itertools
+
+    def fold(i):  # 0, r-1, 1, r-2, ...
+        return 2 * i if i < (r + 1) // 2 else 2 * (r - 1 - i) + 1
+    grid = list(itertools.product(range(r), repeat=d))  # (slowest .. fastest) axis indices
+    if ordering == "natural":
+        rank = {n: k for k, n in enumerate(grid)}
+    else:
+        srt = sorted(grid, key=lambda n: tuple(fold(i) for i in n))
+        rank = {n: k for k, n in enumerate(srt)}
+    nt = (d * len(grid) + 63) // 64
+    T = np.eye(nt, dtype=bool)
+    corner = (0,) * d
+    for n in grid:
+        if n == corner:
+            continue
+        for off in itertools.product((-1, 0, 1), repeat=d):
+            q = tuple((a + o) % r for a, o in zip(n, off))
+            if q == corner:
+                continue
+            for c1 in range(d):
+                for c2 in range(d):
+                    i, j = rank[n] * d + c1, rank[q] * d + c2
+                    if i >= j:
+                        T[i // 64, j // 64] = True
+    G = T.copy()
+    for J in range(nt):
+        for I in range(J, nt):
+            if any(G[I, K] and G[J, K] for K in range(J)):
+                G[I, J] = True
+    return int(np.tril(T).sum()), int(np.tril(G).sum())
+
+
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg4"])
+def test_rve_ordering_folded_and_natural(torch_cuda, cfg):
+    """Both internal orders match the oracle, give the same C_eff / u / w at the API (w in the
+    natural layout either way), and their tile structure equals an independent symbolic fill;
+    the folded order removes the periodic frame (config 2's RVE: 21 -> 15 factor tiles)."""
+    wl = W.config2(nel=2) if cfg == "cfg2" else W.config4(nel=1)
+    res = {}
+    for o in ("natural", "folded"):
+        g, _ = check_linear_against_oracle(wl, tile_sparse=True, rve_ordering=o)
+        wk = g["h"].work
+        assert (wk.a_tiles, wk.g_tiles) == _expected_tile_fill(wl.r, wl.dim, o)
+        res[o] = g
+    for k in ("C", "u", "w"):
+        assert rel(res["folded"][k], res["natural"][k]) <= 1e-12
+    assert res["folded"]["h"].work.g_tiles < res["natural"]["h"].work.g_tiles
+    if cfg == "cfg2":
+        assert (res["natural"]["h"].work.g_tiles, res["folded"]["h"].work.g_tiles) == (21, 15)
+
+
+def test_fluctuations_keep_the_natural_layout(torch_cuda):
+    """Finite strain: set/get of w round-trips bit for bit through the folded internal order, and a
+    condensation at a given (u, w) state is the same under both orders."""
+    import torch
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = W.config5(nel=2, n_steps=2)
+    rng = np.random.default_rng(5)
+    w = 1e-3 * rng.standard_normal((wl.n_rve, wl.n_pad))
+    w[:, :2] = 0.0
+    u = 1e-2 * rng.standard_normal(wl.n_dof)
+    out = {}
+    for o in ("natural", "folded"):
+        h = Homogenizer.from_workload(wl, rve_ordering=o)
+        wt = torch.tensor(w, device="cuda")
+        h.set_fluctuations(wt)
+        back = torch.empty_like(wt)
+        h.get_fluctuations(back)
+        assert torch.equal(back, wt)
+        F = h.macro_kinematics(torch.tensor(u, device="cuda"))
+        out[o] = [t.cpu().numpy() for t in h.condense(F)]
+    for a, b in zip(out["natural"], out["folded"]):
+        assert rel(b, a) <= 1e-12
+
+
 # ------------------------------------------------------------------ RVE sharding (multi-GPU path, DESIGN.md §7)
 def test_rve_range_shards_reassemble_bitwise(torch_cuda):
     """Two contexts condensing disjoint, element-aligned RVE ranges (what two ranks do), rows
