@@ -302,6 +302,67 @@ __device__ __forceinline__ void mma_chunk(double (&acc)[4][4][2], const double* 
   }
 }
 
+// Diagonal tile S_JJ = A_JJ - sum_K G_JK G_JK^T balanced over the 4 warps: warp W owns the lower
+// 8x8 blocks of block rows W and 7-W (9 blocks each; 32x32 quadrants would give 16/10/10/0).
+// A and B fragments of a chunk are the same words (G_JK against itself): 8-W loads per k-step.
+template <int W>
+__device__ __forceinline__ void diag_load(double (&acc)[9][2], const double* T, int lane) {
+  const int lr = lane >> 2, lc = lane & 3;
+  int t = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = h ? 7 - W : W;
+#pragma unroll
+    for (int c = 0; c <= r; ++c, ++t) {
+      const double2 v = __ldcg(reinterpret_cast<const double2*>(T + (8 * r + lr) * TILE + 8 * c + 2 * lc));
+      acc[t][0] = v.x;
+      acc[t][1] = v.y;
+    }
+  }
+}
+template <int W>
+__device__ __forceinline__ void diag_chunk(double (&acc)[9][2], const double* sA, int lane) {
+  const int lr = lane >> 2, lc = lane & 3;
+#pragma unroll
+  for (int k0 = 0; k0 < KC; k0 += 4) {
+    double b[8 - W];
+#pragma unroll
+    for (int c = 0; c < 8 - W; ++c) b[c] = sA[sw32(8 * c + lr, k0 + lc)];
+    const double a0 = neg(b[W]), a1 = neg(b[7 - W]);
+    int t = 0;
+#pragma unroll
+    for (int c = 0; c <= W; ++c, ++t) dmma(acc[t][0], acc[t][1], a0, b[c]);
+#pragma unroll
+    for (int c = 0; c <= 7 - W; ++c, ++t) dmma(acc[t][0], acc[t][1], a1, b[c]);
+  }
+}
+// sT = lower(S_JJ): exact zeros above the diagonal inside the stored 16x16 blocks
+template <int W>
+__device__ __forceinline__ void diag_store(const double (&acc)[9][2], double* sT, int lane) {
+  const int lr = lane >> 2, lc = lane & 3;
+  int t = 0;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int r = h ? 7 - W : W, row = 8 * r + lr;
+#pragma unroll
+    for (int c = 0; c <= r; ++c, ++t) {
+      const int cc = 8 * c + 2 * lc;
+      sT[sd(row, cc)] = (c < r || cc <= row) ? acc[t][0] : 0.0;
+      sT[sd(row, cc + 1)] = (c < r || cc + 1 <= row) ? acc[t][1] : 0.0;
+    }
+  }
+  const int row = 16 * W + lr, cc = 16 * W + 8 + 2 * lc;  // upper 8x8 half of diagonal block W
+  sT[sd(row, cc)] = 0.0;
+  sT[sd(row, cc + 1)] = 0.0;
+}
+#define DIAG_DISPATCH(fn, ...)           \
+  switch (warp) {                        \
+    case 0: fn<0>(__VA_ARGS__); break;   \
+    case 1: fn<1>(__VA_ARGS__); break;   \
+    case 2: fn<2>(__VA_ARGS__); break;   \
+    default: fn<3>(__VA_ARGS__); break;  \
+  }
+
 // acc := this thread's accumulator-layout fragment of the quadrant of a row-major 64x64 global tile
 __device__ __forceinline__ void load_frag(double (&acc)[4][4][2], const double* T, int R0, int C0, int lane) {
   const int lr = lane >> 2, lc = lane & 3;
@@ -360,9 +421,9 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
     // ---------- S_JJ = A_JJ - sum_K G_JK G_JK^T ; yacc = sum_K G_JK Y_K ----------
     // k-chunks (K, kc) run over the K < J with G_JK != 0, two-stage cp.async pipeline
     {
-      double acc[4][4][2];
+      double dacc[9][2];
       double yacc[2][2] = {};
-      load_frag(acc, tile_ptr(Kb, R, J, J), R0, C0, lane);
+      DIAG_DISPATCH(diag_load, dacc, tile_ptr(Kb, R, J, J), lane);
       int K = next_pair(R, J, J, 0), kc = 0, par = 0;
       if (K < J) {
         stage_chunk(sStage, tile_ptr(Kb, R, J, K), 0, tid);
@@ -383,7 +444,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
         }
         __syncthreads();
         const double* st = sStage + par * STAGE_DBL;
-        mma_chunk<true>(acc, st, st, R0, C0, lane);
+        DIAG_DISPATCH(diag_chunk, dacc, st, lane);
         const double* sYc = st + 2 * 64 * KC;  // yacc rows 16*warp.. (2 blocks) x 8 RHS columns
 #pragma unroll
         for (int k0 = 0; k0 < KC; k0 += 4) {
@@ -394,16 +455,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
         __syncthreads();
         K = K2; kc = kc2; par ^= 1;
       }
-      // sT = lower(S_JJ), exact zeros above the diagonal
-#pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-        for (int ni = 0; ni < 4; ++ni) {
-          const int r = R0 + 8 * mi + lr, cc = C0 + 8 * ni + 2 * lc;
-          if (sd_upper(r, cc)) continue;  // strictly upper 16x16 block: not stored
-          sT[sd(r, cc)] = (cc <= r) ? acc[mi][ni][0] : 0.0;
-          sT[sd(r, cc + 1)] = (cc + 1 <= r) ? acc[mi][ni][1] : 0.0;
-        }
+      DIAG_DISPATCH(diag_store, dacc, sT, lane);
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int r = 16 * warp + 8 * u + lr, cc = 2 * lc;

@@ -37,6 +37,16 @@ int main(int argc, char** argv) {
   cudaMemset(info, 0, nb * 4);
   hom::RveDev R{};
   R.dim = 2; R.nt = nt; R.NT = n; R.npad = n; R.m = 3; R.ncol = 3; R.vol = 1.0;
+  {  // dense tile structure: every lower tile processed, slot I(I+1)/2 + J
+    std::vector<int> ts((size_t)nt * nt, -1);
+    std::vector<uint8_t> gz((size_t)nt * nt, 0);
+    for (int I = 0; I < nt; ++I)
+      for (int J = 0; J <= I; ++J) { ts[(size_t)I * nt + J] = I * (I + 1) / 2 + J; gz[(size_t)I * nt + J] = 1; }
+    int* dts; uint8_t* dgz;
+    cudaMalloc(&dts, ts.size() * 4); cudaMemcpy(dts, ts.data(), ts.size() * 4, cudaMemcpyHostToDevice);
+    cudaMalloc(&dgz, gz.size()); cudaMemcpy(dgz, gz.data(), gz.size(), cudaMemcpyHostToDevice);
+    R.tslot = dts; R.g_nz = dgz; R.tile_nz = dgz; R.nslot = (int)tiles; R.xb0 = 0;
+  }
   std::vector<double> hk(per * nb);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
