@@ -123,49 +123,100 @@ __device__ __forceinline__ void stage_rhs(double* dst, const double* src, int n,
 __device__ __forceinline__ int chol16_inv_inplace(double* sD, int k0, int lane) {
   const unsigned FULL = 0xffffffffu;
   const int r = lane & 15;
-  double a[16], ip[16];
-#pragma unroll
-  for (int c = 0; c < 16; ++c) a[c] = (c <= r) ? sD[sd(k0 + r, k0 + c)] : 0.0;
+  const int lr = lane >> 2, lc = lane & 3;
+  double ip[16];
   int fail = 16;
-  // Pivot chain: one rsqrt per pivot (no sqrt, no division); every lane keeps 1/L_kk.
+  // Right-looking in four 4-column panels: the pivot chain and the in-panel updates on the
+  // registers of lane r = row r (one rsqrt per pivot, every lane keeps 1/L_kk), the rank-4
+  // update of the trailing rows/columns on DMMA (k = 4 = the panel) -- the FP64 pipe is shared
+  // with the other CTAs' DMMA, so the chain is kept to as few FP64 instructions as possible.
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    double dkk = __shfl_sync(FULL, a[k], k);
-    if (!(dkk > 0.0) && fail == 16) fail = k;
-    ip[k] = rsqrt(dkk);
-    a[k] = (r == k) ? dkk * ip[k] : a[k] * ip[k];
+  for (int p = 0; p < 4; ++p) {
+    const int c0 = 4 * p;
+    double a[4];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      if (j > k) {  // compile-time after unrolling: a[] stays in registers
-        double ljk = __shfl_sync(FULL, a[k], j);
-        if (r >= j) a[j] = fma(-a[k], ljk, a[j]);
+    for (int q = 0; q < 4; ++q) a[q] = (r >= c0 + q) ? sD[sd(k0 + r, k0 + c0 + q)] : 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double dkk = __shfl_sync(FULL, a[k], c0 + k);
+      if (!(dkk > 0.0) && fail == 16) fail = c0 + k;
+      ip[c0 + k] = rsqrt(dkk);
+      a[k] = (r == c0 + k) ? dkk * ip[c0 + k] : a[k] * ip[c0 + k];
+#pragma unroll
+      for (int j = k + 1; j < 4; ++j) {
+        const double ljk = __shfl_sync(FULL, a[k], c0 + j);
+        if (r >= c0 + j) a[j] = fma(-a[k], ljk, a[j]);
       }
     }
-  }
-  if (lane < 16) {
+    if (lane < 16 && r >= c0) {
 #pragma unroll
-    for (int c = 0; c < 16; ++c)
-      if (c <= r) sD[sd(k0 + r, k0 + c)] = a[c];
-  }
-  __syncwarp();
-  // X = L^-1: lane c builds column c by forward substitution (L rows read as smem
-  // broadcasts), two partial sums to halve the dependent FMA chain.
-  const int c = lane & 15;
-  double x[16];
-#pragma unroll
-  for (int rr = 0; rr < 16; ++rr) {
-    double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-    for (int k = 0; k < 16; k += 2) {
-      if (k < rr) s0 = fma(sD[sd(k0 + rr, k0 + k)], x[k], s0);
-      if (k + 1 < rr) s1 = fma(sD[sd(k0 + rr, k0 + k + 1)], x[k + 1], s1);
+      for (int q = 0; q < 4; ++q)
+        if (c0 + q <= r) sD[sd(k0 + r, k0 + c0 + q)] = a[q];
     }
-    x[rr] = (rr >= c) ? (((rr == c) ? 1.0 : 0.0) - (s0 + s1)) * ip[rr] : 0.0;
+    __syncwarp();
+    if (p < 3) {  // trailing rows/cols >= c0 + 4: C -= L_panel L_panel^T (rows above masked to 0)
+      const int t0 = c0 + 4;
+#pragma unroll
+      for (int blk = 0; blk < 3; ++blk) {
+        const int bi = blk == 0 ? 0 : 1, bj = blk == 2 ? 1 : 0;
+        if (8 * bi + 7 < t0 || 8 * bj + 7 < t0) continue;  // block outside the trailing part
+        const int ra = 8 * bi + lr, rb = 8 * bj + lr;
+        const double av = ra >= t0 ? neg(sD[sd(k0 + ra, k0 + c0 + lc)]) : 0.0;
+        const double bv = rb >= t0 ? sD[sd(k0 + rb, k0 + c0 + lc)] : 0.0;
+        const int cc = 8 * bj + 2 * lc;
+        double c0v = sD[sd(k0 + ra, k0 + cc)], c1v = sD[sd(k0 + ra, k0 + cc + 1)];
+        dmma(c0v, c1v, av, bv);
+        __syncwarp();
+        if (ra >= t0) {
+          sD[sd(k0 + ra, k0 + cc)] = c0v;
+          sD[sd(k0 + ra, k0 + cc + 1)] = c1v;
+        }
+      }
+      __syncwarp();
+    }
   }
   __syncwarp();
-  if (lane < 16) {
+  // X = L^-1 blockwise (8x8 blocks): X00 = L00^-1 and X11 = L11^-1 together (lane c builds column
+  // c & 7 of block c >> 3 by forward substitution, L rows read as smem broadcasts), then
+  // X10 = -X11 (L10 X00) as two 8x8x8 DMMA products (T = L10 X00 is parked over L10).
+  {
+    const int c = lane & 15, bq = c >> 3, cb = c & 7, o = 8 * bq;
+    double x[8];
 #pragma unroll
-    for (int rr = 0; rr < 16; ++rr) sD[sd(k0 + rr, k0 + c)] = x[rr];
+    for (int rr = 0; rr < 8; ++rr) {
+      double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+      for (int k = 0; k < 8; k += 2) {
+        if (k < rr) s0 = fma(sD[sd(k0 + o + rr, k0 + o + k)], x[k], s0);
+        if (k + 1 < rr) s1 = fma(sD[sd(k0 + o + rr, k0 + o + k + 1)], x[k + 1], s1);
+      }
+      const double ipr = bq ? ip[8 + rr] : ip[rr];
+      x[rr] = (rr >= cb) ? (((rr == cb) ? 1.0 : 0.0) - (s0 + s1)) * ipr : 0.0;
+    }
+    __syncwarp();
+    if (lane < 16) {
+#pragma unroll
+      for (int rr = 0; rr < 8; ++rr) {
+        sD[sd(k0 + o + rr, k0 + c)] = x[rr];
+        if (bq) sD[sd(k0 + rr, k0 + c)] = 0.0;  // strictly upper 8x8 block
+      }
+    }
+    __syncwarp();
+    double t0 = 0.0, t1 = 0.0;  // T = L10 X00 (rows 8..15, cols 0..7)
+#pragma unroll
+    for (int kk = 0; kk < 8; kk += 4)
+      dmma(t0, t1, sD[sd(k0 + 8 + lr, k0 + kk + lc)], sD[sd(k0 + kk + lc, k0 + lr)]);
+    __syncwarp();
+    sD[sd(k0 + 8 + lr, k0 + 2 * lc)] = t0;
+    sD[sd(k0 + 8 + lr, k0 + 2 * lc + 1)] = t1;
+    __syncwarp();
+    double y0 = 0.0, y1 = 0.0;  // X10 = -X11 T
+#pragma unroll
+    for (int kk = 0; kk < 8; kk += 4)
+      dmma(y0, y1, neg(sD[sd(k0 + 8 + lr, k0 + 8 + kk + lc)]), sD[sd(k0 + 8 + kk + lc, k0 + lr)]);
+    __syncwarp();
+    sD[sd(k0 + 8 + lr, k0 + 2 * lc)] = y0;
+    sD[sd(k0 + 8 + lr, k0 + 2 * lc + 1)] = y1;
   }
   __syncwarp();
   return fail;
@@ -189,6 +240,7 @@ __device__ __forceinline__ bool factor_invert_diag(double* sD, double* sScr, int
       if (f < 16 && lane == 0) sFail[0] = J * TILE + k0 + f + 1;
     }
     __syncthreads();
+    if (kb == 0) TMARK(5);
     if (sFail[0]) return false;
     if (kb == 3) break;
     const int rb0 = k0 + 16, nrt = (TILE - rb0) / 8;
@@ -238,6 +290,7 @@ __device__ __forceinline__ bool factor_invert_diag(double* sD, double* sScr, int
     }
     __syncthreads();
   }
+  TMARK(6);
   // off-diagonal blocks of the inverse, in place, block rows i ascending:
   //   T_k = sum_{j=k}^{i-1} L_ij X_jk (all k < i in parallel; X_jk of rows j < i are final),
   //   X_ik = -X_ii T_k written over L_ik after every T_k is formed.

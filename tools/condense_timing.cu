@@ -76,5 +76,15 @@ int main(int argc, char** argv) {
   }
   printf("sum | %6.1f | %6.1f | %8.1f | %7.1f | %5.1f\n", tot[0] / 64e3, tot[1] / 64e3, tot[2] / 64e3, tot[3] / 64e3,
          tot[4] / 64e3);
+  {  // inside the factor: first chol16 (+ its barrier), the blocked loop, the off-diagonal inverse
+    double f[3] = {};
+    for (int J = 0; J < nt && J < 40; ++J)
+      for (int b = 0; b < 64; ++b) {
+        long long* m = tm[b][J];
+        f[0] += m[5] - m[1]; f[1] += m[6] - m[1]; f[2] += m[2] - m[6];
+      }
+    printf("factor split (k-cycles summed over J): chol16(0) %.1f | 4-block loop %.1f | inverse %.1f\n",
+           f[0] / 64e3, f[1] / 64e3, f[2] / 64e3);
+  }
   return 0;
 }
