@@ -52,16 +52,26 @@ __device__ __forceinline__ bool sd_upper(int r, int c) { return (c >> 4) > (r >>
 // [rows][8] right-hand-side block
 __device__ __forceinline__ int swy(int k, int n) { return k * RHSW + (n ^ (((k >> 1) & 1) << 2)); }
 
-// lower tile (I,J) of this RVE's pool (slot map RveDev::tslot; every lower tile in the dense path)
+// lower tile (I,J) of this RVE's pool: slot map RveDev::tslot (tile-sparse), or the row-major
+// lower slot I(I+1)/2 + J when every lower tile is stored (dense: no table loads)
+template <bool SP>
 __device__ __forceinline__ double* tile_ptr(double* Kb, const RveDev& R, int I, int J) {
-  return Kb + (long)__ldg(R.tslot + I * R.nt + J) * TILE_ELEMS;
+  if (SP) return Kb + (long)__ldg(R.tslot + I * R.nt + J) * TILE_ELEMS;
+  return Kb + (long)(((I * (I + 1)) >> 1) + J) * TILE_ELEMS;
 }
-// G(I,K) and G(J,K) both structurally nonzero (always true in the dense path)
+// G(I,J) structurally nonzero (always true in the dense path)
+template <bool SP>
+__device__ __forceinline__ bool gnz(const RveDev& R, int I, int J) {
+  return !SP || __ldg(R.g_nz + I * R.nt + J);
+}
+// G(I,K) and G(J,K) both structurally nonzero
+template <bool SP>
 __device__ __forceinline__ bool pair_nz(const RveDev& R, int I, int J, int K) {
-  return __ldg(R.g_nz + I * R.nt + K) && __ldg(R.g_nz + J * R.nt + K);
+  return !SP || (__ldg(R.g_nz + I * R.nt + K) && __ldg(R.g_nz + J * R.nt + K));
 }
+template <bool SP>
 __device__ __forceinline__ int next_pair(const RveDev& R, int I, int J, int K) {
-  while (K < J && !pair_nz(R, I, J, K)) ++K;
+  while (SP && K < J && !pair_nz<SP>(R, I, J, K)) ++K;
   return K;
 }
 
@@ -443,6 +453,7 @@ static_assert(TILE_ELEMS <= 2 * STAGE_DBL, "S tile fits in the stage area");
 static_assert(16 * TILE + 16 * RHSW <= STAGE_DBL, "backward row chunk fits in a stage");
 
 // ------------------------------------------------------------------ kernel
+template <bool SP>
 __global__ void __launch_bounds__(NTC, 4)
 k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
            const double* __restrict__ Cavg, const double* __restrict__ Pavg,
@@ -476,19 +487,19 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
     {
       double dacc[9][2];
       double yacc[2][2] = {};
-      DIAG_DISPATCH(diag_load, dacc, tile_ptr(Kb, R, J, J), lane);
-      int K = next_pair(R, J, J, 0), kc = 0, par = 0;
+      DIAG_DISPATCH(diag_load, dacc, tile_ptr<SP>(Kb, R, J, J), lane);
+      int K = next_pair<SP>(R, J, J, 0), kc = 0, par = 0;
       if (K < J) {
-        stage_chunk(sStage, tile_ptr(Kb, R, J, K), 0, tid);
+        stage_chunk(sStage, tile_ptr<SP>(Kb, R, J, K), 0, tid);
         stage_rhs(sStage + 2 * 64 * KC, Yb + (long)(K * TILE) * RHSW, KC, tid);
         cp_async_commit();
       }
       while (K < J) {
         int K2 = K, kc2 = kc + 1;
-        if (kc2 == CPT) { kc2 = 0; K2 = next_pair(R, J, J, K + 1); }
+        if (kc2 == CPT) { kc2 = 0; K2 = next_pair<SP>(R, J, J, K + 1); }
         if (K2 < J) {
           double* st = sStage + (par ^ 1) * STAGE_DBL;
-          stage_chunk(st, tile_ptr(Kb, R, J, K2), kc2, tid);
+          stage_chunk(st, tile_ptr<SP>(Kb, R, J, K2), kc2, tid);
           stage_rhs(st + 2 * 64 * KC, Yb + (long)(K2 * TILE + kc2 * KC) * RHSW, KC, tid);
           cp_async_commit();
           cp_async_wait<1>();
@@ -535,7 +546,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
         sY2[swy(rr, cc + 1)] = y1;
         *reinterpret_cast<double2*>(Yb + (long)(J * TILE + rr) * RHSW + cc) = make_double2(y0, y1);
       }
-      double* Gjj = tile_ptr(Kb, R, J, J);
+      double* Gjj = tile_ptr<SP>(Kb, R, J, J);
       for (int idx = tid; idx < TILE_ELEMS / 2; idx += NTC) {
         const int r = idx >> 5, cc = 2 * (idx & 31);
         *reinterpret_cast<double2*>(Gjj + r * TILE + cc) =
@@ -553,9 +564,9 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
     TMARK(3);
     // ---------- off-diagonal tiles of column J: S_IJ, then G_IJ = S_IJ G_JJ^-T ----------
     for (int I = J + 1; I < nt; ++I) {
-      if (!__ldg(R.g_nz + I * nt + J)) continue;  // structurally zero tile of G (tile-sparse path)
+      if (!gnz<SP>(R, I, J)) continue;  // structurally zero tile of G (tile-sparse path)
       double acc[4][4][2];
-      double* Aij = tile_ptr(Kb, R, I, J);
+      double* Aij = tile_ptr<SP>(Kb, R, I, J);
       if (__ldg(R.tile_nz + I * nt + J)) {
         load_frag(acc, Aij, R0, C0, lane);
       } else {  // fill tile: A_IJ = 0 (never written by K1)
@@ -564,19 +575,19 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
 #pragma unroll
           for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
       }
-      int K = next_pair(R, I, J, 0), kc = 0, par = 0;
+      int K = next_pair<SP>(R, I, J, 0), kc = 0, par = 0;
       if (K < J) {
-        stage_chunk(sStage, tile_ptr(Kb, R, I, K), 0, tid);
-        stage_chunk(sStage + 64 * KC, tile_ptr(Kb, R, J, K), 0, tid);
+        stage_chunk(sStage, tile_ptr<SP>(Kb, R, I, K), 0, tid);
+        stage_chunk(sStage + 64 * KC, tile_ptr<SP>(Kb, R, J, K), 0, tid);
         cp_async_commit();
       }
       while (K < J) {
         int K2 = K, kc2 = kc + 1;
-        if (kc2 == CPT) { kc2 = 0; K2 = next_pair(R, I, J, K + 1); }
+        if (kc2 == CPT) { kc2 = 0; K2 = next_pair<SP>(R, I, J, K + 1); }
         if (K2 < J) {
           double* st = sStage + (par ^ 1) * STAGE_DBL;
-          stage_chunk(st, tile_ptr(Kb, R, I, K2), kc2, tid);
-          stage_chunk(st + 64 * KC, tile_ptr(Kb, R, J, K2), kc2, tid);
+          stage_chunk(st, tile_ptr<SP>(Kb, R, I, K2), kc2, tid);
+          stage_chunk(st + 64 * KC, tile_ptr<SP>(Kb, R, J, K2), kc2, tid);
           cp_async_commit();
           cp_async_wait<1>();
         } else {
@@ -662,14 +673,14 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
   // warp owns rows j = 16*warp .. +15 (2 blocks).
   constexpr int RC = 16, RPT = TILE / RC;
   auto next_row = [&](int J, int I) {  // next I with G_IJ structurally nonzero
-    while (I < nt && !__ldg(R.g_nz + I * nt + J)) ++I;
+    while (I < nt && !gnz<SP>(R, I, J)) ++I;
     return I;
   };
   for (int J = nt - 1; J >= 0; --J) {
     double xacc[2][2] = {};
     int I = next_row(J, J + 1), rq = 0, par = 0;
     if (I < nt) {
-      stage_rows(sStage, tile_ptr(Kb, R, I, J), 0, RC, tid);
+      stage_rows(sStage, tile_ptr<SP>(Kb, R, I, J), 0, RC, tid);
       stage_rhs(sStage + RC * TILE, Xb + (long)I * TILE * RHSW, RC, tid);
       cp_async_commit();
     }
@@ -678,7 +689,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
       if (rq2 == RPT) { rq2 = 0; I2 = next_row(J, I + 1); }
       if (I2 < nt) {
         double* nb = sStage + (par ^ 1) * STAGE_DBL;
-        stage_rows(nb, tile_ptr(Kb, R, I2, J), rq2 * RC, RC, tid);
+        stage_rows(nb, tile_ptr<SP>(Kb, R, I2, J), rq2 * RC, RC, tid);
         stage_rhs(nb + RC * TILE, Xb + (long)(I2 * TILE + rq2 * RC) * RHSW, RC, tid);
         cp_async_commit();
         cp_async_wait<1>();
@@ -700,7 +711,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
     }
     // r = Y_J - xacc ; X_J = G_JJ^-T r
     {  // G_JJ^-1 (lower 16x16 blocks) into the packed buffer
-      const double* src = tile_ptr(Kb, R, J, J);
+      const double* src = tile_ptr<SP>(Kb, R, J, J);
       for (int idx = tid; idx < TILE * 32; idx += NTC) {
         const int r = idx >> 5, c2 = 2 * (idx & 31);
         if (!sd_upper(r, c2)) cp_async16(sT + sd(r, c2), src + r * TILE + c2);
@@ -734,8 +745,9 @@ void launch_condense(const RveDev& R, int b0, int nb, double* Kt, double* Y, con
                      const double* Pavg, double* Ceff, double* Peff, double* PavgOut, double* X,
                      int* info, cudaStream_t s) {
   size_t sm = (size_t)SMEM_DBL * sizeof(double);
-  cudaFuncSetAttribute(k_condense, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_condense<<<nb, NTC, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, Ceff, Peff, PavgOut, X, info);
+  auto k = R.dense_tiles ? k_condense<false> : k_condense<true>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k<<<nb, NTC, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, Ceff, Peff, PavgOut, X, info);
 }
 
 // ------------------------------------------------------------------ small reductions

@@ -499,6 +499,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
     for (int J = 0; J <= I; ++J)
       if (g_nz[(size_t)I * nt_ + J]) tslot[(size_t)I * nt_ + J] = nslot++;
   R.nslot = nslot;
+  R.dense_tiles = nslot == nt_ * (nt_ + 1) / 2;
   {  // work per RVE in 64^3 tile products (hom_get_work)
     auto& W = c->work;
     W = hom_work{};

@@ -54,6 +54,7 @@ struct RveDev {
   const uint8_t* g_nz;
   const int* tslot;
   int nslot;                      // pool slots (64x64 tiles) per RVE
+  int dense_tiles;                // 1: every lower tile stored at slot I(I+1)/2 + J (no table lookups)
   const int* a_list;              // [n_a] (I << 16 | J) of the structurally nonzero lower tiles (K1)
   int n_a;
   // K1 gather records: node p, neighbour slot j < maxdeg -> rs4 int4s

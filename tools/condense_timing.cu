@@ -45,7 +45,7 @@ int main(int argc, char** argv) {
     int* dts; uint8_t* dgz;
     cudaMalloc(&dts, ts.size() * 4); cudaMemcpy(dts, ts.data(), ts.size() * 4, cudaMemcpyHostToDevice);
     cudaMalloc(&dgz, gz.size()); cudaMemcpy(dgz, gz.data(), gz.size(), cudaMemcpyHostToDevice);
-    R.tslot = dts; R.g_nz = dgz; R.tile_nz = dgz; R.nslot = (int)tiles; R.xb0 = 0;
+    R.tslot = dts; R.g_nz = dgz; R.tile_nz = dgz; R.nslot = (int)tiles; R.xb0 = 0; R.dense_tiles = 1;
   }
   std::vector<double> hk(per * nb);
   cudaEvent_t e0, e1;
