@@ -52,27 +52,43 @@ __device__ __forceinline__ bool sd_upper(int r, int c) { return (c >> 4) > (r >>
 // [rows][8] right-hand-side block
 __device__ __forceinline__ int swy(int k, int n) { return k * RHSW + (n ^ (((k >> 1) & 1) << 2)); }
 
-// lower tile (I,J) of this RVE's pool: slot map RveDev::tslot (tile-sparse), or the row-major
-// lower slot I(I+1)/2 + J when every lower tile is stored (dense: no table loads)
-template <bool SP>
-__device__ __forceinline__ double* tile_ptr(double* Kb, const RveDev& R, int I, int J) {
-  if (SP) return Kb + (long)__ldg(R.tslot + I * R.nt + J) * TILE_ELEMS;
+// Tile structure, MODE 0: every lower tile stored at the row-major lower slot I(I+1)/2 + J
+// (dense; no lookups).  MODE 1: tile-sparse with nt <= 64, bitmasks in the kernel parameter
+// space (TileMask).  MODE 2: tile-sparse, any nt, tables in global memory (g_nz, tslot).
+template <int MODE>
+__device__ __forceinline__ double* tile_ptr(double* Kb, const RveDev& R, const TileMask& tm, int I, int J) {
+  if (MODE == 2) return Kb + (long)__ldg(R.tslot + I * R.nt + J) * TILE_ELEMS;
+  if (MODE == 1) return Kb + (long)(tm.rowstart[I] + __popcll(tm.row[I] & ((1ull << J) - 1ull))) * TILE_ELEMS;
   return Kb + (long)(((I * (I + 1)) >> 1) + J) * TILE_ELEMS;
 }
-// G(I,J) structurally nonzero (always true in the dense path)
-template <bool SP>
-__device__ __forceinline__ bool gnz(const RveDev& R, int I, int J) {
-  return !SP || __ldg(R.g_nz + I * R.nt + J);
+// G(I,J) structurally nonzero
+template <int MODE>
+__device__ __forceinline__ bool gnz(const RveDev& R, const TileMask& tm, int I, int J) {
+  if (MODE == 2) return __ldg(R.g_nz + I * R.nt + J);
+  if (MODE == 1) return (tm.row[I] >> J) & 1ull;
+  return true;
 }
-// G(I,K) and G(J,K) both structurally nonzero
-template <bool SP>
-__device__ __forceinline__ bool pair_nz(const RveDev& R, int I, int J, int K) {
-  return !SP || (__ldg(R.g_nz + I * R.nt + K) && __ldg(R.g_nz + J * R.nt + K));
-}
-template <bool SP>
-__device__ __forceinline__ int next_pair(const RveDev& R, int I, int J, int K) {
-  while (SP && K < J && !pair_nz<SP>(R, I, J, K)) ++K;
+// first K' >= K, K' < J, with G(I,K') and G(J,K') both structurally nonzero (J if none)
+template <int MODE>
+__device__ __forceinline__ int next_pair(const RveDev& R, const TileMask& tm, int I, int J, int K) {
+  if (MODE == 0 || K >= J) return K;
+  if (MODE == 1) {
+    const unsigned long long m = tm.row[I] & tm.row[J] & ((1ull << J) - 1ull) & (~0ull << K);
+    return m ? __ffsll((long long)m) - 1 : J;
+  }
+  while (K < J && !(__ldg(R.g_nz + I * R.nt + K) && __ldg(R.g_nz + J * R.nt + K))) ++K;
   return K;
+}
+// first I' >= I with G(I',J) structurally nonzero (nt if none)
+template <int MODE>
+__device__ __forceinline__ int next_row(const RveDev& R, const TileMask& tm, int J, int I) {
+  if (MODE == 0 || I >= R.nt) return I;
+  if (MODE == 1) {
+    const unsigned long long m = tm.col[J] & (~0ull << I);
+    return m ? min(__ffsll((long long)m) - 1, R.nt) : R.nt;
+  }
+  while (I < R.nt && !__ldg(R.g_nz + I * R.nt + J)) ++I;
+  return I;
 }
 
 // ------------------------------------------------------------------ CTA shape
@@ -453,9 +469,9 @@ static_assert(TILE_ELEMS <= 2 * STAGE_DBL, "S tile fits in the stage area");
 static_assert(16 * TILE + 16 * RHSW <= STAGE_DBL, "backward row chunk fits in a stage");
 
 // ------------------------------------------------------------------ kernel
-template <bool SP>
+template <int MODE>
 __global__ void __launch_bounds__(NTC, 4)
-k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
+k_condense(RveDev R, const __grid_constant__ TileMask tm, int b0, double* __restrict__ Kt, double* __restrict__ Y,
            const double* __restrict__ Cavg, const double* __restrict__ Pavg,
            double* __restrict__ Ceff, double* __restrict__ Peff, double* __restrict__ PavgOut,
            double* __restrict__ X, int* __restrict__ info) {
@@ -487,19 +503,19 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
     {
       double dacc[9][2];
       double yacc[2][2] = {};
-      DIAG_DISPATCH(diag_load, dacc, tile_ptr<SP>(Kb, R, J, J), lane);
-      int K = next_pair<SP>(R, J, J, 0), kc = 0, par = 0;
+      DIAG_DISPATCH(diag_load, dacc, tile_ptr<MODE>(Kb, R, tm, J, J), lane);
+      int K = next_pair<MODE>(R, tm, J, J, 0), kc = 0, par = 0;
       if (K < J) {
-        stage_chunk(sStage, tile_ptr<SP>(Kb, R, J, K), 0, tid);
+        stage_chunk(sStage, tile_ptr<MODE>(Kb, R, tm, J, K), 0, tid);
         stage_rhs(sStage + 2 * 64 * KC, Yb + (long)(K * TILE) * RHSW, KC, tid);
         cp_async_commit();
       }
       while (K < J) {
         int K2 = K, kc2 = kc + 1;
-        if (kc2 == CPT) { kc2 = 0; K2 = next_pair<SP>(R, J, J, K + 1); }
+        if (kc2 == CPT) { kc2 = 0; K2 = next_pair<MODE>(R, tm, J, J, K + 1); }
         if (K2 < J) {
           double* st = sStage + (par ^ 1) * STAGE_DBL;
-          stage_chunk(st, tile_ptr<SP>(Kb, R, J, K2), kc2, tid);
+          stage_chunk(st, tile_ptr<MODE>(Kb, R, tm, J, K2), kc2, tid);
           stage_rhs(st + 2 * 64 * KC, Yb + (long)(K2 * TILE + kc2 * KC) * RHSW, KC, tid);
           cp_async_commit();
           cp_async_wait<1>();
@@ -546,7 +562,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
         sY2[swy(rr, cc + 1)] = y1;
         *reinterpret_cast<double2*>(Yb + (long)(J * TILE + rr) * RHSW + cc) = make_double2(y0, y1);
       }
-      double* Gjj = tile_ptr<SP>(Kb, R, J, J);
+      double* Gjj = tile_ptr<MODE>(Kb, R, tm, J, J);
       for (int idx = tid; idx < TILE_ELEMS / 2; idx += NTC) {
         const int r = idx >> 5, cc = 2 * (idx & 31);
         *reinterpret_cast<double2*>(Gjj + r * TILE + cc) =
@@ -564,9 +580,9 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
     TMARK(3);
     // ---------- off-diagonal tiles of column J: S_IJ, then G_IJ = S_IJ G_JJ^-T ----------
     for (int I = J + 1; I < nt; ++I) {
-      if (!gnz<SP>(R, I, J)) continue;  // structurally zero tile of G (tile-sparse path)
+      if (!gnz<MODE>(R, tm, I, J)) continue;  // structurally zero tile of G (tile-sparse path)
       double acc[4][4][2];
-      double* Aij = tile_ptr<SP>(Kb, R, I, J);
+      double* Aij = tile_ptr<MODE>(Kb, R, tm, I, J);
       if (__ldg(R.tile_nz + I * nt + J)) {
         load_frag(acc, Aij, R0, C0, lane);
       } else {  // fill tile: A_IJ = 0 (never written by K1)
@@ -575,19 +591,19 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
 #pragma unroll
           for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
       }
-      int K = next_pair<SP>(R, I, J, 0), kc = 0, par = 0;
+      int K = next_pair<MODE>(R, tm, I, J, 0), kc = 0, par = 0;
       if (K < J) {
-        stage_chunk(sStage, tile_ptr<SP>(Kb, R, I, K), 0, tid);
-        stage_chunk(sStage + 64 * KC, tile_ptr<SP>(Kb, R, J, K), 0, tid);
+        stage_chunk(sStage, tile_ptr<MODE>(Kb, R, tm, I, K), 0, tid);
+        stage_chunk(sStage + 64 * KC, tile_ptr<MODE>(Kb, R, tm, J, K), 0, tid);
         cp_async_commit();
       }
       while (K < J) {
         int K2 = K, kc2 = kc + 1;
-        if (kc2 == CPT) { kc2 = 0; K2 = next_pair<SP>(R, I, J, K + 1); }
+        if (kc2 == CPT) { kc2 = 0; K2 = next_pair<MODE>(R, tm, I, J, K + 1); }
         if (K2 < J) {
           double* st = sStage + (par ^ 1) * STAGE_DBL;
-          stage_chunk(st, tile_ptr<SP>(Kb, R, I, K2), kc2, tid);
-          stage_chunk(st + 64 * KC, tile_ptr<SP>(Kb, R, J, K2), kc2, tid);
+          stage_chunk(st, tile_ptr<MODE>(Kb, R, tm, I, K2), kc2, tid);
+          stage_chunk(st + 64 * KC, tile_ptr<MODE>(Kb, R, tm, J, K2), kc2, tid);
           cp_async_commit();
           cp_async_wait<1>();
         } else {
@@ -672,15 +688,12 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
   // xacc[j][n] = sum_{I>J} sum_k G_IJ[k][j] X_I[k][n], streamed in 16-row chunks of G_IJ;
   // warp owns rows j = 16*warp .. +15 (2 blocks).
   constexpr int RC = 16, RPT = TILE / RC;
-  auto next_row = [&](int J, int I) {  // next I with G_IJ structurally nonzero
-    while (I < nt && !gnz<SP>(R, I, J)) ++I;
-    return I;
-  };
+  auto next_row = [&](int J, int I) { return hom::next_row<MODE>(R, tm, J, I); };
   for (int J = nt - 1; J >= 0; --J) {
     double xacc[2][2] = {};
     int I = next_row(J, J + 1), rq = 0, par = 0;
     if (I < nt) {
-      stage_rows(sStage, tile_ptr<SP>(Kb, R, I, J), 0, RC, tid);
+      stage_rows(sStage, tile_ptr<MODE>(Kb, R, tm, I, J), 0, RC, tid);
       stage_rhs(sStage + RC * TILE, Xb + (long)I * TILE * RHSW, RC, tid);
       cp_async_commit();
     }
@@ -689,7 +702,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
       if (rq2 == RPT) { rq2 = 0; I2 = next_row(J, I + 1); }
       if (I2 < nt) {
         double* nb = sStage + (par ^ 1) * STAGE_DBL;
-        stage_rows(nb, tile_ptr<SP>(Kb, R, I2, J), rq2 * RC, RC, tid);
+        stage_rows(nb, tile_ptr<MODE>(Kb, R, tm, I2, J), rq2 * RC, RC, tid);
         stage_rhs(nb + RC * TILE, Xb + (long)(I2 * TILE + rq2 * RC) * RHSW, RC, tid);
         cp_async_commit();
         cp_async_wait<1>();
@@ -711,7 +724,7 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
     }
     // r = Y_J - xacc ; X_J = G_JJ^-T r
     {  // G_JJ^-1 (lower 16x16 blocks) into the packed buffer
-      const double* src = tile_ptr<SP>(Kb, R, J, J);
+      const double* src = tile_ptr<MODE>(Kb, R, tm, J, J);
       for (int idx = tid; idx < TILE * 32; idx += NTC) {
         const int r = idx >> 5, c2 = 2 * (idx & 31);
         if (!sd_upper(r, c2)) cp_async16(sT + sd(r, c2), src + r * TILE + c2);
@@ -743,11 +756,12 @@ k_condense(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y,
 
 void launch_condense(const RveDev& R, int b0, int nb, double* Kt, double* Y, const double* Cavg,
                      const double* Pavg, double* Ceff, double* Peff, double* PavgOut, double* X,
-                     int* info, cudaStream_t s) {
+                     int* info, cudaStream_t s, const TileMask* tm) {
   size_t sm = (size_t)SMEM_DBL * sizeof(double);
-  auto k = R.dense_tiles ? k_condense<false> : k_condense<true>;
+  static const TileMask none{};
+  auto k = R.dense_tiles ? k_condense<0> : (tm ? k_condense<1> : k_condense<2>);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k<<<nb, NTC, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, Ceff, Peff, PavgOut, X, info);
+  k<<<nb, NTC, sm, s>>>(R, tm ? *tm : none, b0, Kt, Y, Cavg, Pavg, Ceff, Peff, PavgOut, X, info);
 }
 
 // ------------------------------------------------------------------ small reductions

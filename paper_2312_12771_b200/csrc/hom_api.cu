@@ -40,7 +40,9 @@ struct hom_ctx {
   CgState* cgst = nullptr;
   size_t phase_bytes = 0, mat_bytes = 0;
   int max_slice_nnz = 0;  // largest CSR slice of a 8-CTA cluster partition (CG smem sizing)
-  int cg2_slice[2][2] = {};  // k_macro_cg_cluster2 largest (rows, nnz) slice for G = 16, 8
+  int cg2_slice[2][2] = {};
+  hom::TileMask tmask{};     // tile-sparse structure as bitmasks (nt <= 64), k_condense MODE 1
+  bool has_tmask = false;  // k_macro_cg_cluster2 largest (rows, nnz) slice for G = 16, 8
   hom_work work{};
   // event profiling (hom_profile_enable / hom_profile_read)
   struct ProfRec {
@@ -500,6 +502,20 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
       if (g_nz[(size_t)I * nt_ + J]) tslot[(size_t)I * nt_ + J] = nslot++;
   R.nslot = nslot;
   R.dense_tiles = nslot == nt_ * (nt_ + 1) / 2;
+  if (!R.dense_tiles && nt_ <= 64) {
+    int slot = 0;
+    for (int I = 0; I < nt_; ++I) {
+      c->tmask.rowstart[I] = slot;
+      for (int J = 0; J <= I; ++J)
+        if (g_nz[(size_t)I * nt_ + J]) {
+          c->tmask.row[I] |= 1ull << J;
+          c->tmask.col[J] |= 1ull << I;
+          if (tslot[(size_t)I * nt_ + J] != slot) return fail(HOM_ERR_INVALID_ARG, "tile slot order");
+          ++slot;
+        }
+    }
+    c->has_tmask = true;
+  }
   {  // work per RVE in 64^3 tile products (hom_get_work)
     auto& W = c->work;
     W = hom_work{};
@@ -795,7 +811,8 @@ int hom_condense(hom_ctx* c, const double* d_kin, double* d_C_eff, double* d_P_e
     run(c, HOM_PROF_RVE_ASSEMBLE, s,
         [&] { hom::launch_rve_assemble(R, b0, nb, c->Kt, c->Y, c->Cavg, c->Pavg, c->rfn, c->Aq, c->Pq, s); });
     run(c, HOM_PROF_CONDENSE, s, [&] {
-      hom::launch_condense(R, b0, nb, c->Kt, c->Y, c->Cavg, c->Pavg, d_C_eff, d_P_eff, d_P_avg, c->X, c->info, s);
+      hom::launch_condense(R, b0, nb, c->Kt, c->Y, c->Cavg, c->Pavg, d_C_eff, d_P_eff, d_P_avg, c->X, c->info, s,
+                           c->has_tmask ? &c->tmask : nullptr);
     });
     if (c->Cavg_e)  // keep <C> of every element for the constant-basis macro stiffness
       cudaMemcpy2DAsync(c->Cavg_e + (size_t)b0 * c->m * c->m, sizeof(double) * c->m * c->m, c->Cavg,

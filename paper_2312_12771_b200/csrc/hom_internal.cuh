@@ -93,6 +93,14 @@ struct MacroDev {
   const double* evol;             // [ne] element volume |B_e|
 };
 
+// Tile structure of a tile-sparse factor with nt <= 64, passed to k_condense by value (kernel
+// parameter space = constant bank: warp-uniform lookups without global loads): bit J of row[I] /
+// bit I of col[J] = G(I,J) stored; rowstart[I] = slot of row I's first stored tile.
+struct TileMask {
+  unsigned long long row[64], col[64];
+  int rowstart[64];
+};
+
 struct CgState {
   int iterations;
   int status;                     // 0 ok, 5 not converged, 6 breakdown
@@ -110,7 +118,8 @@ void launch_rve_assemble(const RveDev& R, int b0, int nb, double* Kt, double* Y,
                          cudaStream_t s);
 void launch_condense(const RveDev& R, int b0, int nb, double* Kt, double* Y, const double* Cavg,
                      const double* Pavg, double* Ceff, double* Peff, double* PavgOut, double* X,
-                     int* info, cudaStream_t s);
+                     int* info, cudaStream_t s,
+                     const struct TileMask* tm = nullptr);
 void launch_first_fail(const int* flags, int n, int sentinel, int* out, cudaStream_t s);
 void launch_max_reduce(const double* v, int n, double* out, cudaStream_t s);
 

@@ -242,6 +242,17 @@ def test_tile_sparse_config3_full_rve_fewer_tiles(torch_cuda):
     assert w.flop_executed < w.flop_dense / 10
 
 
+def test_tile_sparse_table_path_large_rve(torch_cuda):
+    """nt > 64 tiles (N_pad = 2 * 46^2 = 4232): the tile-sparse factor uses the global-table
+    structure path instead of the kernel-parameter bitmasks; bitwise equal to dense."""
+    wl = W.config3(nel=1, r=46, seed=3)
+    d = gpu_linear(wl)
+    t = gpu_linear(wl, tile_sparse=True)
+    assert t["h"].sizes.n_tiles > 64
+    assert np.array_equal(t["C"], d["C"]) and np.array_equal(t["u"], d["u"]) and np.array_equal(t["w"], d["w"])
+    assert t["h"].work.g_tiles < d["h"].work.g_tiles
+
+
 def test_tile_sparse_finite_strain_per_state(torch_cuda):
     import torch
     from paper_2312_12771_b200.hom import Homogenizer
