@@ -80,71 +80,97 @@ __device__ __forceinline__ bool cook_material(const double* F, double alpha, dou
   return true;
 }
 
-__global__ void k_rve_element_nh(RveDev R, int b0, int nb, const double* __restrict__ Fbar,
-                                 const double* __restrict__ w, double* __restrict__ EL, int* __restrict__ jflag) {
-  const long gid = (long)blockIdx.x * blockDim.x + threadIdx.x;
-  const int ne = R.ne, nq = R.nq;
-  if (gid >= (long)nb * ne * 8) return;
-  const int row = (int)(gid & 7);
-  const long ge = gid >> 3;
-  const int bl = (int)(ge / ne), e = (int)(ge % ne), b = b0 + bl;
-  const int a = row >> 1, i = row & 1;
-  const double* Fb = Fbar + (long)b * 4;
-  const double* wb = w + (long)b * R.npad;
-  const int ph = R.phase[(R.phase_per_rve ? (long)b * ne : 0) + e];
-  const int np = R.mat_stride;
-  const double* mp = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * np : 0) + np * ph;
-  const double alpha = mp[0], beta = np == 3 ? mp[1] : 0.0, kappa = mp[np - 1];
-  double we[8];
-  for (int aa = 0; aa < 4; ++aa) {
-    const int p = R.elem_indep[e * 4 + aa];
-    we[2 * aa] = wb[2 * p];
-    we[2 * aa + 1] = wb[2 * p + 1];
-  }
-  double ke[8] = {}, fe[4] = {}, re = 0.0, As[16] = {}, Ps[4] = {};
-  bool ok = true;
-  for (int q = 0; q < nq; ++q) {
-    const double* G = R.grad + (long)(e * nq + q) * 4 * 2;  // [nen][2]
-    double F[4] = {Fb[0], Fb[1], Fb[2], Fb[3]};
-    for (int aa = 0; aa < 4; ++aa) {  // F~ = F + grad w (eq:microGrad)
-      F[0] += we[2 * aa] * G[2 * aa]; F[1] += we[2 * aa] * G[2 * aa + 1];
-      F[2] += we[2 * aa + 1] * G[2 * aa]; F[3] += we[2 * aa + 1] * G[2 * aa + 1];
-    }
-    double P[4], A[16];
-    if (!cook_material(F, alpha, beta, kappa, P, A)) {
-      if (row == 0) atomicMin(&jflag[b], e * nq + q);  // first failing qp of this RVE (init INT_MAX)
-      ok = false;
-      break;
-    }
-    const double wq = R.wdet[e * nq + q];
-    const double ga0 = G[2 * a], ga1 = G[2 * a + 1];
-    // row (a, i): t[k] = sum_J g_a[J] A[(i,J), k]
-    double t[4];
-    for (int k = 0; k < 4; ++k) t[k] = ga0 * A[(2 * i) * 4 + k] + ga1 * A[(2 * i + 1) * 4 + k];
-    for (int k = 0; k < 4; ++k) fe[k] += wq * t[k];
-    re += wq * (ga0 * P[2 * i] + ga1 * P[2 * i + 1]);
-    for (int bb = 0; bb < 4; ++bb)
-      for (int j = 0; j < 2; ++j)  // column (b, j): sum_L t[(j,L)] g_b[L]
-        ke[2 * bb + j] += wq * (t[2 * j] * G[2 * bb] + t[2 * j + 1] * G[2 * bb + 1]);
-    if (row == 0) {
-      for (int k = 0; k < 16; ++k) As[k] += wq * A[k];
-      for (int k = 0; k < 4; ++k) Ps[k] += wq * P[k];
+// Block of NH_ELB consecutive (RVE, element) pairs, NH_THR threads: phase 1, one thread per
+// (element, qp) evaluates F~, P, A once (shared memory); phase 2, one thread per element row (a, i)
+// forms its rows of K_e, F_e, r_e from them; the block's NH_ELB x EL_STRIDE outputs are staged in
+// shared memory and written back as one contiguous, coalesced range.
+constexpr int NH_ELB = 16, NH_THR = 128;
+
+__global__ void __launch_bounds__(NH_THR) k_rve_element_nh(RveDev R, int b0, int nb, const double* __restrict__ Fbar,
+                                                          const double* __restrict__ w, double* __restrict__ EL,
+                                                          int* __restrict__ jflag) {
+  __shared__ double sQ[NH_ELB * 4][20];  // per (element, qp): A [16], P [4]
+  __shared__ double sOut[NH_ELB * EL_STRIDE];
+  __shared__ int sOk[NH_ELB];
+  const int ne = R.ne, nq = R.nq, tid = threadIdx.x;
+  const long ge0 = (long)blockIdx.x * NH_ELB, n_el = (long)nb * ne;
+  if (tid < NH_ELB) sOk[tid] = 1;
+  __syncthreads();
+  // ---- phase 1: material point per (element, qp) ----
+  if (tid < NH_ELB * 4) {
+    const int le = tid >> 2, q = tid & 3;
+    const long ge = ge0 + le;
+    if (ge < n_el && q < nq) {
+      const int bl = (int)(ge / ne), e = (int)(ge % ne), b = b0 + bl;
+      const double* Fb = Fbar + (long)b * 4;
+      const double* wb = w + (long)b * R.npad;
+      const int ph = R.phase[(R.phase_per_rve ? (long)b * ne : 0) + e];
+      const int np = R.mat_stride;
+      const double* mp = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * np : 0) + np * ph;
+      const double alpha = mp[0], beta = np == 3 ? mp[1] : 0.0, kappa = mp[np - 1];
+      const double* G = R.grad + (long)(e * nq + q) * 4 * 2;  // [nen][2]
+      double F[4] = {Fb[0], Fb[1], Fb[2], Fb[3]};
+      for (int aa = 0; aa < 4; ++aa) {  // F~ = F + grad w (eq:microGrad)
+        const int p = R.elem_indep[e * 4 + aa];
+        const double w0 = wb[2 * p], w1 = wb[2 * p + 1];
+        F[0] += w0 * G[2 * aa]; F[1] += w0 * G[2 * aa + 1];
+        F[2] += w1 * G[2 * aa]; F[3] += w1 * G[2 * aa + 1];
+      }
+      double* Q = sQ[tid];
+      if (!cook_material(F, alpha, beta, kappa, Q + 16, Q)) {
+        atomicMin(&jflag[b], e * nq + q);  // first failing qp of this RVE (init INT_MAX)
+        sOk[le] = 0;
+      }
     }
   }
-  double* out = EL + ge * EL_STRIDE;
-  for (int k = 0; k < 8; ++k) out[row * 8 + k] = ok ? ke[k] : 0.0;
-  for (int k = 0; k < 4; ++k) out[EL_F + row * 4 + k] = ok ? fe[k] : 0.0;
-  out[EL_R + row] = ok ? re : 0.0;
-  if (row == 0) {
-    for (int k = 0; k < 16; ++k) out[EL_A + k] = ok ? As[k] : 0.0;
-    for (int k = 0; k < 4; ++k) out[EL_P + k] = ok ? Ps[k] : 0.0;
+  __syncthreads();
+  // ---- phase 2: element rows (a, i) ----
+  {
+    const int le = tid >> 3, row = tid & 7, a = row >> 1, i = row & 1;
+    const long ge = ge0 + le;
+    double* out = sOut + le * EL_STRIDE;
+    if (ge < n_el) {
+      const int e = (int)(ge % ne);
+      const bool ok = sOk[le];
+      double ke[8] = {}, fe[4] = {}, re = 0.0;
+      for (int q = 0; q < nq; ++q) {
+        const double* G = R.grad + (long)(e * nq + q) * 4 * 2;
+        const double* A = sQ[le * 4 + q];
+        const double* P = A + 16;
+        const double wq = R.wdet[e * nq + q];
+        const double ga0 = G[2 * a], ga1 = G[2 * a + 1];
+        double t[4];  // row (a, i): t[k] = sum_J g_a[J] A[(i,J), k]
+        for (int k = 0; k < 4; ++k) t[k] = ga0 * A[(2 * i) * 4 + k] + ga1 * A[(2 * i + 1) * 4 + k];
+        for (int k = 0; k < 4; ++k) fe[k] += wq * t[k];
+        re += wq * (ga0 * P[2 * i] + ga1 * P[2 * i + 1]);
+        for (int bb = 0; bb < 4; ++bb)
+          for (int j = 0; j < 2; ++j)  // column (b, j): sum_L t[(j,L)] g_b[L]
+            ke[2 * bb + j] += wq * (t[2 * j] * G[2 * bb] + t[2 * j + 1] * G[2 * bb + 1]);
+      }
+      for (int k = 0; k < 8; ++k) out[row * 8 + k] = ok ? ke[k] : 0.0;
+      for (int k = 0; k < 4; ++k) out[EL_F + row * 4 + k] = ok ? fe[k] : 0.0;
+      out[EL_R + row] = ok ? re : 0.0;
+      if (row < 5) {  // qp sums of A (rows 0-3: 4 entries each) and P (row 4)
+        double sv[4] = {};
+        for (int q = 0; q < nq; ++q) {
+          const double wq = R.wdet[e * nq + q];
+          for (int k = 0; k < 4; ++k) sv[k] += wq * sQ[le * 4 + q][row * 4 + k];
+        }
+        for (int k = 0; k < 4; ++k) out[EL_A + row * 4 + k] = ok ? sv[k] : 0.0;
+      }
+    }
   }
+  __syncthreads();
+  // ---- coalesced write-back of the block's contiguous element records ----
+  const long nrec = min((long)NH_ELB, n_el - ge0);
+  double* dst = EL + ge0 * EL_STRIDE;
+  for (int k = tid; k < nrec * EL_STRIDE; k += NH_THR) __stcg(dst + k, sOut[k]);
 }
 
 void launch_rve_material_nh(const RveDev& R, int b0, int nb, const double* F, const double* w,
                             double* EL, double* /*unused*/, int* jflag, cudaStream_t s) {
-  const long n = (long)nb * R.ne * 8;
-  k_rve_element_nh<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(R, b0, nb, F, w, EL, jflag);
+  const long n = (long)nb * R.ne;
+  k_rve_element_nh<<<(unsigned)((n + NH_ELB - 1) / NH_ELB), NH_THR, 0, s>>>(R, b0, nb, F, w, EL, jflag);
 }
 
 // ---------------------------------------------------------------------------
