@@ -658,7 +658,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
       std::vector<int> lanes;
       auto flush = [&]() {
         if (nn == 0) return;
-        witem.insert(witem.end(), {t, p0, nn, 0});
+        witem.insert(witem.end(), {alist[t], p0, nn, tslot[(size_t)(alist[t] >> 16) * nt_ + (alist[t] & 0xffff)]});
         lanes.resize(32, -1);
         wlist.insert(wlist.end(), lanes.begin(), lanes.end());
         lanes.clear();

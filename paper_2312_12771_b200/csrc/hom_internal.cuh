@@ -61,7 +61,7 @@ struct RveDev {
   // {q (-1: none / corner), n_sh, code_0 .. code_{n_sh-1}, -1 ...}, code = e<<8 | a<<4 | b
   const int4* nrec;
   int maxdeg, rs4;
-  // K1 warp work items: {tile t, first row node p0, node count nn, 0}, and per item one record
+  // K1 warp work items: {tile code I<<16|J, first row node p0, node count nn, pool slot}, and per item one record
   // per lane: (g << 24 | record index) for node p0 + g, -1 = idle lane (<= 32 records, <= npw nodes)
   const int4* witem;
   const int* wlist;

@@ -336,12 +336,11 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   for (int it = warp; it < R.n_witem; it += NTHR / 32) {
     const int4 wi = __ldg(R.witem + it);
     const int lw = __ldg(R.wlist + (long)it * 32 + lane);
-    const int code = __ldg(R.a_list + wi.x);
-    const int I = code >> 16, J = code & 0xffff;
+    const int I = wi.x >> 16, J = wi.x & 0xffff;
     const int r0 = I * TILE;
     const int p0 = wi.y, nn = wi.z;
     {
-      double* gt = Kb + (long)__ldg(R.tslot + I * nt + J) * TILE_ELEMS;
+      double* gt = Kb + (long)wi.w * TILE_ELEMS;
       const int c0 = J * TILE;
       {
         for (int i = lane; i < nn * DIM * TILE / 2; i += 32)
@@ -351,20 +350,47 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
           double* rb = rowbuf + (lw >> 24) * DIM * TILE;
           {
             const int4* rec = R.nrec + (long)(lw & 0xffffff) * R.rs4;
-            const int4 hd = __ldg(rec);
-            const int q = hd.x;
+            // the whole record in one round of independent loads (2^DIM shared elements fit
+            // RS4M int4s; longer records -- tiny periodic meshes -- fall back to extra loads)
+            constexpr int RS4M = DIM == 3 ? 3 : (DIM == 2 ? 2 : 1);
+            int rv[4 * RS4M];
+#pragma unroll
+            for (int u = 0; u < RS4M; ++u) {
+              const int4 v = u < R.rs4 ? __ldg(rec + u) : make_int4(-1, -1, -1, -1);
+              rv[4 * u] = v.x; rv[4 * u + 1] = v.y; rv[4 * u + 2] = v.z; rv[4 * u + 3] = v.w;
+            }
+            const int q = rv[0];
             const int cq = q * DIM - c0;  // first column of q in this tile
             double blk[DIM][DIM];
 #pragma unroll
             for (int i = 0; i < DIM; ++i)
 #pragma unroll
               for (int jj = 0; jj < DIM; ++jj) blk[i][jj] = 0.0;
-            const int nsh = hd.y;
-            int4 cur = hd;
-            for (int sidx = 0; sidx < nsh; ++sidx) {
-              const int slot = sidx + 2;
-              if ((slot & 3) == 0) cur = __ldg(rec + (slot >> 2));
-              const int code = (slot & 3) == 0 ? cur.x : (slot & 3) == 1 ? cur.y : (slot & 3) == 2 ? cur.z : cur.w;
+            const int nsh = rv[1];
+#pragma unroll
+            for (int sidx = 0; sidx < 4 * RS4M - 2 + 1; ++sidx) {
+              if (sidx >= nsh) break;
+              int code;
+              if (sidx < 4 * RS4M - 2) {
+                code = rv[sidx + 2];
+              } else {  // rare: records longer than RS4M int4s
+                for (int s2 = sidx; s2 < nsh; ++s2) {
+                  const int slot = s2 + 2;
+                  const int4 v = __ldg(rec + (slot >> 2));
+                  const int c2 = (slot & 3) == 0 ? v.x : (slot & 3) == 1 ? v.y : (slot & 3) == 2 ? v.z : v.w;
+                  const int e = c2 >> 8, a = (c2 >> 4) & 15, bb = c2 & 15;
+                  if (ISO) {
+                    const double* ke = s_K + (long)s_ep[e] * ND * ND + (a * DIM) * ND + bb * DIM;
+                    for (int i = 0; i < DIM; ++i)
+                      for (int jj = 0; jj < DIM; ++jj) blk[i][jj] += ke[i * ND + jj];
+                  } else {
+                    const double* ke = Aq + ((long)bl * ne + e) * EL_STRIDE + (a * DIM) * 8 + bb * DIM;
+                    for (int i = 0; i < DIM; ++i)
+                      for (int jj = 0; jj < DIM; ++jj) blk[i][jj] += ke[i * 8 + jj];
+                  }
+                }
+                break;
+              }
               const int e = code >> 8, a = (code >> 4) & 15, bb = code & 15;
               if (ISO) {
                 const double* ke = s_K + (long)s_ep[e] * ND * ND + (a * DIM) * ND + bb * DIM;
@@ -393,11 +419,14 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
         for (int n = 0; n < nn; ++n) {
           const int pn = p0 + n;
           const bool pad = pn >= R.n_indep || pn == R.corner;  // identity rows (corner class, tail)
+          double2 vr[DIM];  // all rows of the node loaded before the first store
+#pragma unroll
+          for (int ci = 0; ci < DIM; ++ci) vr[ci] = *reinterpret_cast<const double2*>(rowbuf + (n * DIM + ci) * TILE + 2 * lane);
 #pragma unroll
           for (int ci = 0; ci < DIM; ++ci) {
             const int row = pn * DIM + ci, rr = row - r0;
             if (rr < 0 || rr >= TILE) continue;
-            double2 v = *reinterpret_cast<const double2*>(rowbuf + (n * DIM + ci) * TILE + 2 * lane);
+            double2 v = vr[ci];
             if (pad || row >= R.npad) {
               v.x = (c0 + 2 * lane == row) ? 1.0 : 0.0;
               v.y = (c0 + 2 * lane + 1 == row) ? 1.0 : 0.0;
