@@ -332,10 +332,31 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   double* Kb = Kt + (long)bl * R.nslot * TILE_ELEMS;
   const int lane = tid & 31, warp = tid >> 5;
   double* rowbuf = s_row + warp * R.npw * DIM * TILE;
-  // work items {tile, first row node p0, nn nodes} with one in-tile neighbour record per lane
-  for (int it = warp; it < R.n_witem; it += NTHR / 32) {
-    const int4 wi = __ldg(R.witem + it);
-    const int lw = __ldg(R.wlist + (long)it * 32 + lane);
+  // work items {tile, first row node p0, nn nodes} with one in-tile neighbour record per lane,
+  // software-pipelined: the next item's header and gather record and the lane word of the item
+  // after it are in flight while the current item is formed and stored
+  constexpr int RS4M = DIM == 3 ? 3 : (DIM == 2 ? 2 : 1);  // record int4s for 2^DIM shared elements
+  constexpr int WSTRIDE = NTHR / 32;
+  const int nw = R.n_witem;
+  auto load_rec = [&](int (&rv)[4 * RS4M], int lwv) {
+#pragma unroll
+    for (int u = 0; u < RS4M; ++u) {
+      const int4 v = (lwv >= 0 && u < R.rs4) ? __ldg(R.nrec + (long)(lwv & 0xffffff) * R.rs4 + u)
+                                             : make_int4(-1, -1, -1, -1);
+      rv[4 * u] = v.x; rv[4 * u + 1] = v.y; rv[4 * u + 2] = v.z; rv[4 * u + 3] = v.w;
+    }
+  };
+  int4 wi = warp < nw ? __ldg(R.witem + warp) : make_int4(0, 0, 0, 0);
+  int lw = warp < nw ? __ldg(R.wlist + (long)warp * 32 + lane) : -1;
+  int rv[4 * RS4M];
+  load_rec(rv, lw);
+  int lw1 = warp + WSTRIDE < nw ? __ldg(R.wlist + (long)(warp + WSTRIDE) * 32 + lane) : -1;
+  for (int it = warp; it < nw; it += WSTRIDE) {
+    const int itn = it + WSTRIDE;
+    const int4 wi_n = itn < nw ? __ldg(R.witem + itn) : wi;
+    int rv_n[4 * RS4M];
+    load_rec(rv_n, lw1);
+    const int lw2 = itn + WSTRIDE < nw ? __ldg(R.wlist + (long)(itn + WSTRIDE) * 32 + lane) : -1;
     const int I = wi.x >> 16, J = wi.x & 0xffff;
     const int r0 = I * TILE;
     const int p0 = wi.y, nn = wi.z;
@@ -350,15 +371,8 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
           double* rb = rowbuf + (lw >> 24) * DIM * TILE;
           {
             const int4* rec = R.nrec + (long)(lw & 0xffffff) * R.rs4;
-            // the whole record in one round of independent loads (2^DIM shared elements fit
-            // RS4M int4s; longer records -- tiny periodic meshes -- fall back to extra loads)
-            constexpr int RS4M = DIM == 3 ? 3 : (DIM == 2 ? 2 : 1);
-            int rv[4 * RS4M];
-#pragma unroll
-            for (int u = 0; u < RS4M; ++u) {
-              const int4 v = u < R.rs4 ? __ldg(rec + u) : make_int4(-1, -1, -1, -1);
-              rv[4 * u] = v.x; rv[4 * u + 1] = v.y; rv[4 * u + 2] = v.z; rv[4 * u + 3] = v.w;
-            }
+            // the record was loaded a round earlier (rv); records longer than RS4M int4s (tiny
+            // periodic meshes) fall back to extra loads
             const int q = rv[0];
             const int cq = q * DIM - c0;  // first column of q in this tile
             double blk[DIM][DIM];
@@ -437,6 +451,11 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
         __syncwarp();
       }
     }
+    wi = wi_n;
+    lw = lw1;
+#pragma unroll
+    for (int u = 0; u < 4 * RS4M; ++u) rv[u] = rv_n[u];
+    lw1 = lw2;
   }
 }
 
