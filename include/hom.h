@@ -176,7 +176,8 @@ typedef struct {
 typedef struct {
   int32_t code;
   int32_t rve;              /* offending RVE or -1 */
-  int32_t row;              /* Cholesky row (NOT_SPD) or micro qp (JACOBIAN), or -1 */
+  int32_t row;              /* NOT_SPD: the fluctuation DOF (natural [N_pad] layout) whose pivot
+                               failed in the factorisation order; JACOBIAN: micro qp; or -1 */
   int32_t cuda_error;
   char message[256];
 } hom_error_info;

@@ -42,7 +42,8 @@ struct hom_ctx {
   int max_slice_nnz = 0;  // largest CSR slice of a 8-CTA cluster partition (CG smem sizing)
   int cg2_slice[2][2] = {};
   hom::TileMask tmask{};     // tile-sparse structure as bitmasks (nt <= 64), k_condense MODE 1
-  bool has_tmask = false;  // k_macro_cg_cluster2 largest (rows, nnz) slice for G = 16, 8
+  bool has_tmask = false;
+  std::vector<int> nat_of;   // internal RVE node -> natural (API) node (empty: identity)  // k_macro_cg_cluster2 largest (rows, nnz) slice for G = 16, 8
   hom_work work{};
   // event profiling (hom_profile_enable / hom_profile_read)
   struct ProfRec {
@@ -405,6 +406,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
     for (int n = 0; n < rn; ++n) indep[n] = int_of[indep[n]];
     R.corner = int_of[R.corner];
     R.nat_of = upload(c, order, s, &rc);  // internal p -> natural order[p]
+    c->nat_of = order;
   }
   R.npad = dim * R.n_indep;
   R.nt = (R.npad + hom::TILE - 1) / hom::TILE;
@@ -840,7 +842,10 @@ int hom_condense(hom_ctx* c, const double* d_kin, double* d_C_eff, double* d_P_e
   if (h[0] != INT_MAX) {
     int row = -1;
     cudaMemcpy(&row, c->info + h[0], sizeof(int), cudaMemcpyDeviceToHost);
-    return set_err(c, HOM_ERR_NOT_SPD, "K_ff not positive definite", h[0], row - 1);
+    --row;  // internal K_ff row -> DOF of the natural (API) fluctuation layout
+    const int dr = c->R.npad / c->R.n_indep;
+    if (!c->nat_of.empty() && row >= 0 && row < c->R.npad) row = c->nat_of[row / dr] * dr + row % dr;
+    return set_err(c, HOM_ERR_NOT_SPD, "K_ff not positive definite", h[0], row);
   }
   return HOM_OK;
 }

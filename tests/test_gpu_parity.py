@@ -191,6 +191,21 @@ def test_not_spd_reports_rve(torch_cuda):
     assert e.value.code == 3 and e.value.rve == 5
 
 
+@pytest.mark.parametrize("ordering", ["natural", "folded"])
+def test_not_spd_reports_first_failing_dof_in_api_layout(torch_cuda, ordering):
+    """Every phase of RVE 5 with negative stiffness: K_ff is negative definite, so the first
+    pivot after the corner pad fails -- the first DOF of the second node in the factorisation
+    order: node 1 (natural order) or node (x = r-1, y = 0) = natural node r-1 (folded order)."""
+    from paper_2312_12771_b200.hom import Homogenizer, HomError
+    wl = W.config3(nel=2, r=6, seed=3)
+    wl.mat = wl.mat.copy()
+    wl.mat[5, :, 0] = -1.0
+    with pytest.raises(HomError) as e:
+        Homogenizer.from_workload(wl, rve_ordering=ordering).condense()
+    assert e.value.code == 3 and e.value.rve == 5
+    assert e.value.row == (2 * 1 if ordering == "natural" else 2 * (wl.r - 1))
+
+
 def test_jacobian_reports_rve(torch_cuda):
     import torch
     from paper_2312_12771_b200.hom import Homogenizer, HomError
