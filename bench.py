@@ -128,9 +128,10 @@ def oracle_step_time(wl, target_s: float = 10.0):
         return time.perf_counter() - t0, C
 
     n = max(nthreads, 8)
-    t, _ = sample(n)
-    while t < 0.25 * target_s and n < wl.n_rve:
-        n = min(wl.n_rve, max(n * 2, int(n * 0.3 * target_s / max(t, 1e-3))))
+    t, C = sample(n)
+    # grow the sample to ~target_s of CPU work (RVEs repeat cyclically past n_rve, never deduplicated)
+    while t < 0.6 * target_s and n < 256 * wl.n_rve:
+        n = min(256 * wl.n_rve, max(n * 2, int(n * 0.8 * target_s / max(t, 1e-3))))
         t, C = sample(n)
     t_rve = t / n
     # macro direct solve at full size with representative tangents
@@ -144,7 +145,9 @@ def oracle_step_time(wl, target_s: float = 10.0):
                            body=wl.body, kind=1)
     t_macro = time.perf_counter() - t0
     step = t_rve * wl.n_rve + t_macro
-    detail = {"cores": nthreads, "sample": f"{n} of {wl.n_rve} RVEs condensed (skyline Cholesky, unit-strain route, "
+    what = (f"{n} of {wl.n_rve} RVEs" if n <= wl.n_rve else
+            f"{n} RVE condensations (the {wl.n_rve} RVEs of the step, cyclically)")
+    detail = {"cores": nthreads, "sample": f"{what} condensed (skyline Cholesky, unit-strain route, "
                                              f"{t:.1f} s) + 1 full-size direct macro solve ({t_macro:.2f} s); "
                                              f"scaled to a full step", "t_rve_s": t_rve, "t_macro_s": t_macro}
     return step, detail
