@@ -687,6 +687,9 @@ k_condense(RveDev R, const __grid_constant__ TileMask tm, int b0, double* __rest
   // ======================= backward: X = G^-T Y ===============================
   // xacc[j][n] = sum_{I>J} sum_k G_IJ[k][j] X_I[k][n], streamed in 16-row chunks of G_IJ;
   // warp owns rows j = 16*warp .. +15 (2 blocks).
+#ifdef HOM_TIMING
+  if (blockIdx.x < 64 && threadIdx.x == 0) g_tm[blockIdx.x][39][0] = clk_ordered();
+#endif
   constexpr int RC = 16, RPT = TILE / RC;
   auto next_row = [&](int J, int I) { return hom::next_row<MODE>(R, tm, J, I); };
   for (int J = nt - 1; J >= 0; --J) {
@@ -752,6 +755,9 @@ k_condense(RveDev R, const __grid_constant__ TileMask tm, int b0, double* __rest
     }
     __syncthreads();
   }
+#ifdef HOM_TIMING
+  if (blockIdx.x < 64 && threadIdx.x == 0) g_tm[blockIdx.x][39][1] = clk_ordered();
+#endif
 }
 
 void launch_condense(const RveDev& R, int b0, int nb, double* Kt, double* Y, const double* Cavg,

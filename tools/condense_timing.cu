@@ -85,6 +85,9 @@ int main(int argc, char** argv) {
       }
     printf("factor split (k-cycles summed over J): chol16(0) %.1f | 4-block loop %.1f | inverse %.1f\n",
            f[0] / 64e3, f[1] / 64e3, f[2] / 64e3);
+    double bw = 0.0;
+    for (int b = 0; b < 64; ++b) bw += tm[b][39][1] - tm[b][39][0];
+    printf("backward X = G^-T Y (k-cycles, after the C_eff epilogue): %.1f\n", bw / 64e3);
   }
   return 0;
 }
