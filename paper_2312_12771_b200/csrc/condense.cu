@@ -14,6 +14,9 @@
 // shared memory with cp.async (16 B) into an XOR-swizzled layout that makes the
 // DMMA fragment reads bank-conflict free; diagonal tiles are stored inverted
 // (G_JJ^-1) so that the triangular solves are DMMA GEMMs too.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "hom_internal.cuh"
 
 namespace hom {
@@ -37,8 +40,39 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
+// ---- TMA (cp.async.bulk.tensor) staging of the k-chunks, completion on mbarriers ----
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done)
+                 : "r"(s_u32(bar)), "r"(parity)
+                 : "memory");
+}
+// generic-proxy writes of this CTA (ordered by a preceding barrier) before async-proxy writes
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int r0, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          s_u32(dst)),
+      "l"(map), "r"(c0), "r"(r0), "r"(s_u32(bar))
+      : "memory");
+}
+// TMA 128-byte swizzle of a [rows][16] FP64 k-chunk (rows of 128 B, 16-byte units XOR row & 7)
+__device__ __forceinline__ int swt(int r, int k) { return r * KC + ((((k >> 1) ^ (r & 7)) << 1) | (k & 1)); }
+
 // swizzled word index inside a [rows][KC] k-chunk and a [rows][64] tile (row-chunk)
 __device__ __forceinline__ int sw32(int r, int k) { return r * KC + (k ^ ((r & 3) << 2)); }
+// k-chunk layout: TMA's 128-byte swizzle (dense, TMA-staged) or sw32 (tile-sparse, cp.async)
+template <bool TS>
+__device__ __forceinline__ int swk(int r, int k) { return TS ? swt(r, k) : sw32(r, k); }
 __device__ __forceinline__ int sw64(int r, int c) { return r * TILE + (c ^ ((r & 3) << 2)); }
 // Diagonal-tile buffer: only the 10 lower 16x16 blocks of the 64x64 tile, block (bi, bj <= bi) at
 // (bi(bi+1)/2 + bj) * 256, each block row-major with the same XOR swizzle (2560 doubles instead of
@@ -60,6 +94,12 @@ __device__ __forceinline__ double* tile_ptr(double* Kb, const RveDev& R, const T
   if (MODE == 2) return Kb + (long)__ldg(R.tslot + I * R.nt + J) * TILE_ELEMS;
   if (MODE == 1) return Kb + (long)(tm.rowstart[I] + __popcll(tm.row[I] & ((1ull << J) - 1ull))) * TILE_ELEMS;
   return Kb + (long)(((I * (I + 1)) >> 1) + J) * TILE_ELEMS;
+}
+template <int MODE>
+__device__ __forceinline__ int tile_slot(const RveDev& R, const TileMask& tm, int I, int J) {
+  if (MODE == 2) return __ldg(R.tslot + I * R.nt + J);
+  if (MODE == 1) return tm.rowstart[I] + __popcll(tm.row[I] & ((1ull << J) - 1ull));
+  return ((I * (I + 1)) >> 1) + J;
 }
 // G(I,J) structurally nonzero
 template <int MODE>
@@ -361,7 +401,7 @@ __device__ __forceinline__ bool factor_invert_diag(double* sD, double* sScr, int
 // acc[4][4][2] += (-A(64xKC chunk)) * B(64xKC chunk)^T for the warp quadrant (R0, C0): acc starts
 // as the original tile, so the result is A_IJ - sum_K G_IK G_JK^T.  DIAG: skip the 8x8 blocks
 // strictly above the diagonal (the upper half is never used; frees the pipe for the other CTAs).
-template <bool DIAG>
+template <bool DIAG, bool TS>
 __device__ __forceinline__ void mma_chunk(double (&acc)[4][4][2], const double* sA, const double* sB,
                                           int R0, int C0, int lane) {
   if (DIAG && C0 > R0 + 24) return;  // quadrant entirely above the diagonal
@@ -370,9 +410,9 @@ __device__ __forceinline__ void mma_chunk(double (&acc)[4][4][2], const double* 
   for (int k0 = 0; k0 < KC; k0 += 4) {
     double a[4], b[4];
 #pragma unroll
-    for (int mi = 0; mi < 4; ++mi) a[mi] = neg(sA[sw32(R0 + 8 * mi + lr, k0 + lc)]);
+    for (int mi = 0; mi < 4; ++mi) a[mi] = neg(sA[swk<TS>(R0 + 8 * mi + lr, k0 + lc)]);
 #pragma unroll
-    for (int ni = 0; ni < 4; ++ni) b[ni] = sB[sw32(C0 + 8 * ni + lr, k0 + lc)];
+    for (int ni = 0; ni < 4; ++ni) b[ni] = sB[swk<TS>(C0 + 8 * ni + lr, k0 + lc)];
 #pragma unroll
     for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
@@ -399,14 +439,14 @@ __device__ __forceinline__ void diag_load(double (&acc)[9][2], const double* T, 
     }
   }
 }
-template <int W>
+template <int W, bool TS>
 __device__ __forceinline__ void diag_chunk(double (&acc)[9][2], const double* sA, int lane) {
   const int lr = lane >> 2, lc = lane & 3;
 #pragma unroll
   for (int k0 = 0; k0 < KC; k0 += 4) {
     double b[8 - W];
 #pragma unroll
-    for (int c = 0; c < 8 - W; ++c) b[c] = sA[sw32(8 * c + lr, k0 + lc)];
+    for (int c = 0; c < 8 - W; ++c) b[c] = sA[swk<TS>(8 * c + lr, k0 + lc)];
     const double a0 = neg(b[W]), a1 = neg(b[7 - W]);
     int t = 0;
 #pragma unroll
@@ -471,11 +511,12 @@ static_assert(16 * TILE + 16 * RHSW <= STAGE_DBL, "backward row chunk fits in a 
 // ------------------------------------------------------------------ kernel
 template <int MODE>
 __global__ void __launch_bounds__(NTC, 4)
-k_condense(RveDev R, const __grid_constant__ TileMask tm, int b0, double* __restrict__ Kt, double* __restrict__ Y,
+k_condense(RveDev R, const __grid_constant__ TileMask tm, const __grid_constant__ CUtensorMap kmap,
+           const __grid_constant__ CUtensorMap ymap, int b0, double* __restrict__ Kt, double* __restrict__ Y,
            const double* __restrict__ Cavg, const double* __restrict__ Pavg,
            double* __restrict__ Ceff, double* __restrict__ Peff, double* __restrict__ PavgOut,
            double* __restrict__ X, int* __restrict__ info) {
-  extern __shared__ __align__(128) double smem[];
+  extern __shared__ __align__(1024) double smem[];
   double* sT = smem;                        // packed lower 64x64 (sd): S_JJ -> G_JJ^-1
   double* sStage = sT + SD_DBL;             // 2 stages | S tile | factor scratch | Y_J | sY
   double* sY = sStage + SY_F;               // 64x8 swizzled: Kfe_J - sum_K G_JK Y_K (forward)
@@ -492,7 +533,25 @@ k_condense(RveDev R, const __grid_constant__ TileMask tm, int b0, double* __rest
   double* Yb = Y + (long)bl * NT * RHSW;
   double* Xb = X + (long)(b - R.xb0) * NT * RHSW;  // X holds the context's local RVE range only
 
-  if (tid == 0) sFail[0] = 0;
+  // two k-chunk stages filled by TMA: full[s] completes when the stage's bytes have landed
+  uint64_t* full = reinterpret_cast<uint64_t*>(sStage + 2 * STAGE_DBL + 8);
+  uint32_t ph0 = 0, ph1 = 0;  // parity of the next completion of full[0], full[1]
+  if (tid == 0) {
+    sFail[0] = 0;
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto wait_stage = [&](int st) {
+    if (st == 0) { mbar_wait(&full[0], ph0); ph0 ^= 1u; }
+    else { mbar_wait(&full[1], ph1); ph1 ^= 1u; }
+  };
+  // k-chunks: TMA + mbarriers for the dense structure (long pipelines); 16-byte cp.async for the
+  // tile-sparse modes (one or two chunks per tile: the TMA round trip measured slower there)
+  constexpr bool TMA_STAGING = MODE == 0;
+  const long krow0 = (long)bl * R.nslot * TILE;  // first pool row of this RVE (kmap rows)
+  const long yrow0 = (long)bl * NT;              // first Y row of this RVE (ymap rows)
   double Sacc = 0.0;  // thread (i,j) = (tid>>3, tid&7), tid < 64: sum_r Y[r][i] Y[r][j]
 
   // ======================= forward: factor + Y ==============================
@@ -505,32 +564,49 @@ k_condense(RveDev R, const __grid_constant__ TileMask tm, int b0, double* __rest
       double yacc[2][2] = {};
       DIAG_DISPATCH(diag_load, dacc, tile_ptr<MODE>(Kb, R, tm, J, J), lane);
       int K = next_pair<MODE>(R, tm, J, J, 0), kc = 0, par = 0;
-      if (K < J) {
-        stage_chunk(sStage, tile_ptr<MODE>(Kb, R, tm, J, K), 0, tid);
-        stage_rhs(sStage + 2 * 64 * KC, Yb + (long)(K * TILE) * RHSW, KC, tid);
+      auto issue_d = [&](int stg, int KK, int kcc) {  // G_JK chunk kcc + Y_K rows, one thread
+        double* st = sStage + stg * STAGE_DBL;
+        fence_proxy_async();
+        mbar_expect(&full[stg], (64 * KC + KC * RHSW) * 8);
+        tma_load_2d(st, &kmap, kcc * KC, (int)(krow0 + (long)tile_slot<MODE>(R, tm, J, KK) * TILE), &full[stg]);
+        tma_load_2d(st + 2 * 64 * KC, &ymap, 0, (int)(yrow0 + KK * TILE + kcc * KC), &full[stg]);
+      };
+      auto stage_d = [&](int stg, int KK, int kcc) {  // cp.async variant (tile-sparse modes)
+        double* st = sStage + stg * STAGE_DBL;
+        stage_chunk(st, tile_ptr<MODE>(Kb, R, tm, J, KK), kcc, tid);
+        stage_rhs(st + 2 * 64 * KC, Yb + (long)(KK * TILE + kcc * KC) * RHSW, KC, tid);
         cp_async_commit();
+      };
+      if (K < J) {
+        if (TMA_STAGING) { if (tid == 0) issue_d(0, K, 0); }
+        else stage_d(0, K, 0);
       }
       while (K < J) {
         int K2 = K, kc2 = kc + 1;
         if (kc2 == CPT) { kc2 = 0; K2 = next_pair<MODE>(R, tm, J, J, K + 1); }
-        if (K2 < J) {
-          double* st = sStage + (par ^ 1) * STAGE_DBL;
-          stage_chunk(st, tile_ptr<MODE>(Kb, R, tm, J, K2), kc2, tid);
-          stage_rhs(st + 2 * 64 * KC, Yb + (long)(K2 * TILE + kc2 * KC) * RHSW, KC, tid);
-          cp_async_commit();
-          cp_async_wait<1>();
+        if (TMA_STAGING) {
+          if (K2 < J && tid == 0) issue_d(par ^ 1, K2, kc2);
+          wait_stage(par);
         } else {
-          cp_async_wait<0>();
+          if (K2 < J) { stage_d(par ^ 1, K2, kc2); cp_async_wait<1>(); }
+          else cp_async_wait<0>();
+          __syncthreads();
         }
-        __syncthreads();
         const double* st = sStage + par * STAGE_DBL;
-        DIAG_DISPATCH(diag_chunk, dacc, st, lane);
+        switch (warp) {
+          case 0: diag_chunk<0, TMA_STAGING>(dacc, st, lane); break;
+          case 1: diag_chunk<1, TMA_STAGING>(dacc, st, lane); break;
+          case 2: diag_chunk<2, TMA_STAGING>(dacc, st, lane); break;
+          default: diag_chunk<3, TMA_STAGING>(dacc, st, lane); break;
+        }
         const double* sYc = st + 2 * 64 * KC;  // yacc rows 16*warp.. (2 blocks) x 8 RHS columns
 #pragma unroll
         for (int k0 = 0; k0 < KC; k0 += 4) {
-          const double bb = sYc[swy(k0 + lc, lr)];
+          // TMA chunk unswizzled [KC][8]; cp.async chunk in the swy layout
+          const double bb = TMA_STAGING ? sYc[(k0 + lc) * RHSW + lr] : sYc[swy(k0 + lc, lr)];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) dmma(yacc[u][0], yacc[u][1], st[sw32(16 * warp + 8 * u + lr, k0 + lc)], bb);
+          for (int u = 0; u < 2; ++u)
+            dmma(yacc[u][0], yacc[u][1], st[swk<TMA_STAGING>(16 * warp + 8 * u + lr, k0 + lc)], bb);
         }
         __syncthreads();
         K = K2; kc = kc2; par ^= 1;
@@ -592,26 +668,37 @@ k_condense(RveDev R, const __grid_constant__ TileMask tm, int b0, double* __rest
           for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
       }
       int K = next_pair<MODE>(R, tm, I, J, 0), kc = 0, par = 0;
-      if (K < J) {
-        stage_chunk(sStage, tile_ptr<MODE>(Kb, R, tm, I, K), 0, tid);
-        stage_chunk(sStage + 64 * KC, tile_ptr<MODE>(Kb, R, tm, J, K), 0, tid);
+      auto issue_o = [&](int stg, int KK, int kcc) {  // G_IK and G_JK chunks kcc, one thread
+        double* st = sStage + stg * STAGE_DBL;
+        fence_proxy_async();
+        mbar_expect(&full[stg], 2 * 64 * KC * 8);
+        tma_load_2d(st, &kmap, kcc * KC, (int)(krow0 + (long)tile_slot<MODE>(R, tm, I, KK) * TILE), &full[stg]);
+        tma_load_2d(st + 64 * KC, &kmap, kcc * KC, (int)(krow0 + (long)tile_slot<MODE>(R, tm, J, KK) * TILE),
+                    &full[stg]);
+      };
+      auto stage_o = [&](int stg, int KK, int kcc) {  // cp.async variant (tile-sparse modes)
+        double* st = sStage + stg * STAGE_DBL;
+        stage_chunk(st, tile_ptr<MODE>(Kb, R, tm, I, KK), kcc, tid);
+        stage_chunk(st + 64 * KC, tile_ptr<MODE>(Kb, R, tm, J, KK), kcc, tid);
         cp_async_commit();
+      };
+      if (K < J) {
+        if (TMA_STAGING) { if (tid == 0) issue_o(0, K, 0); }
+        else stage_o(0, K, 0);
       }
       while (K < J) {
         int K2 = K, kc2 = kc + 1;
         if (kc2 == CPT) { kc2 = 0; K2 = next_pair<MODE>(R, tm, I, J, K + 1); }
-        if (K2 < J) {
-          double* st = sStage + (par ^ 1) * STAGE_DBL;
-          stage_chunk(st, tile_ptr<MODE>(Kb, R, tm, I, K2), kc2, tid);
-          stage_chunk(st + 64 * KC, tile_ptr<MODE>(Kb, R, tm, J, K2), kc2, tid);
-          cp_async_commit();
-          cp_async_wait<1>();
+        if (TMA_STAGING) {
+          if (K2 < J && tid == 0) issue_o(par ^ 1, K2, kc2);
+          wait_stage(par);
         } else {
-          cp_async_wait<0>();
+          if (K2 < J) { stage_o(par ^ 1, K2, kc2); cp_async_wait<1>(); }
+          else cp_async_wait<0>();
+          __syncthreads();
         }
-        __syncthreads();
         const double* st = sStage + par * STAGE_DBL;
-        mma_chunk<false>(acc, st, st + 64 * KC, R0, C0, lane);
+        mma_chunk<false, TMA_STAGING>(acc, st, st + 64 * KC, R0, C0, lane);
         __syncthreads();
         K = K2; kc = kc2; par ^= 1;
       }
@@ -760,14 +847,43 @@ k_condense(RveDev R, const __grid_constant__ TileMask tm, int b0, double* __rest
 #endif
 }
 
+__global__ void k_first_fail(const int* __restrict__ f, int n, int sentinel, int* out);
+
 void launch_condense(const RveDev& R, int b0, int nb, double* Kt, double* Y, const double* Cavg,
                      const double* Pavg, double* Ceff, double* Peff, double* PavgOut, double* X,
                      int* info, cudaStream_t s, const TileMask* tm) {
   size_t sm = (size_t)SMEM_DBL * sizeof(double);
   static const TileMask none{};
+  // tensor maps of this launch's K_ff pool ([rows][64] FP64, 16x64 boxes, 128-byte swizzle) and
+  // right-hand sides ([rows][8], 8x16 boxes)
+  CUtensorMap kmap, ymap;
+  {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        fn = nullptr;
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode) {  // surfaces as a launch error through the caller's error check
+      cudaLaunchKernel((const void*)k_first_fail, dim3(0), dim3(0), nullptr, 0, s);
+      return;
+    }
+    const cuuint64_t kdim[2] = {(cuuint64_t)TILE, (cuuint64_t)nb * R.nslot * TILE};
+    const cuuint64_t kstr[1] = {(cuuint64_t)TILE * sizeof(double)};
+    const cuuint32_t kbox[2] = {(cuuint32_t)KC, (cuuint32_t)TILE}, one[2] = {1, 1};
+    encode(&kmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, Kt, kdim, kstr, kbox, one, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const cuuint64_t ydim[2] = {(cuuint64_t)RHSW, (cuuint64_t)nb * R.NT};
+    const cuuint64_t ystr[1] = {(cuuint64_t)RHSW * sizeof(double)};
+    const cuuint32_t ybox[2] = {(cuuint32_t)RHSW, (cuuint32_t)KC};
+    encode(&ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, Y, ydim, ystr, ybox, one, CU_TENSOR_MAP_INTERLEAVE_NONE,
+           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
   auto k = R.dense_tiles ? k_condense<0> : (tm ? k_condense<1> : k_condense<2>);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k<<<nb, NTC, sm, s>>>(R, tm ? *tm : none, b0, Kt, Y, Cavg, Pavg, Ceff, Peff, PavgOut, X, info);
+  k<<<nb, NTC, sm, s>>>(R, tm ? *tm : none, kmap, ymap, b0, Kt, Y, Cavg, Pavg, Ceff, Peff, PavgOut, X, info);
 }
 
 // ------------------------------------------------------------------ small reductions
