@@ -592,6 +592,10 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
   for (int k = tid; k < nnz; k += CG2_THR) { sval[k] = val[nz0 + k]; scol[k] = M.col[nz0 + k]; }
   for (int i = tid; i <= nr; i += CG2_THR) srow[i] = M.rowptr[r0 + i] - nz0;
   __syncthreads();
+  // remote copies of z: this CTA's slice in every CTA of the cluster (addresses mapped once)
+  double* zrem[CGC_MAXG];
+#pragma unroll
+  for (int t = 0; t < CGC_MAXG; ++t) zrem[t] = t < G ? cl.map_shared_rank(zf, t) + r0 : nullptr;
   // node-block Jacobi: invert the free part of each dim x dim diagonal block
   for (int nd = nd0 + tid; nd < nd1; nd += CG2_THR) {
     double a[3][3] = {}, inv[3][3] = {};
@@ -623,10 +627,13 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
       for (int cj = 0; cj < dim; ++cj)
         mi[((nd - nd0) * dim + ci) * dim + cj] = (fr[ci] && fr[cj]) ? inv[ci][cj] : 0.0;
   }
+  __syncthreads();  // the block-Jacobi setup has read the diagonal blocks
   for (int i = tid; i < nr; i += CG2_THR) {
     const int gi = r0 + i;
     x[i] = 0.0;
     r[i] = M.dmask[gi] ? 0.0 : b[gi];
+    if (M.dmask[gi])  // Dirichlet row: w_i = 0 without a mask test in the SpMV
+      for (int k = srow[i]; k < srow[i + 1]; ++k) sval[k] = 0.0;
   }
   cl.sync();  // every CTA of the cluster is running before the first DSMEM store
 
@@ -639,7 +646,9 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
       for (int cj = 0; cj < dim; ++cj) z += mi[i * dim + cj] * r[nl * dim + cj];
       rz += r[i] * z;
       rr += r[i] * r[i];
-      for (int t = 0; t < G; ++t) cl.map_shared_rank(zf, t)[r0 + i] = z;
+#pragma unroll
+      for (int t = 0; t < CGC_MAXG; ++t)
+        if (t < G) zrem[t][i] = z;
       (void)ci;
     }
     part[0] = rz;
@@ -650,7 +659,7 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
     double zw = 0.0;
     for (int i = tid; i < nr; i += CG2_THR) {
       double s0 = 0.0, s1 = 0.0;
-      if (!M.dmask[r0 + i]) {
+      {  // Dirichlet rows have zero values (set up above)
         int k = srow[i];
         const int ke = srow[i + 1];
         for (; k + 1 < ke; k += 2) {
