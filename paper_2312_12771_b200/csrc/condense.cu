@@ -778,29 +778,36 @@ k_condense(RveDev R, const __grid_constant__ TileMask tm, const __grid_constant_
   if (blockIdx.x < 64 && threadIdx.x == 0) g_tm[blockIdx.x][39][0] = clk_ordered();
 #endif
   constexpr int RC = 16, RPT = TILE / RC;
+  constexpr int NSTB = 4, BST = RC * TILE + RC * RHSW;  // backward stages (doubles each)
+  static_assert(NSTB * BST <= SD_DBL + SY_B, "backward stages overlap sY");
   auto next_row = [&](int J, int I) { return hom::next_row<MODE>(R, tm, J, I); };
   for (int J = nt - 1; J >= 0; --J) {
     double xacc[2][2] = {};
-    int I = next_row(J, J + 1), rq = 0, par = 0;
-    if (I < nt) {
-      stage_rows(sStage, tile_ptr<MODE>(Kb, R, tm, I, J), 0, RC, tid);
-      stage_rhs(sStage + RC * TILE, Xb + (long)I * TILE * RHSW, RC, tid);
+    // 16-row chunks (I, rq) of the G_IJ column, NSTB-deep cp.async pipeline in the diagonal-tile
+    // buffer + stage area (sT is reloaded with G_JJ^-1 only after the chunks; sY at SY_B is free)
+    int I = next_row(J, J + 1), rq = 0;
+    int nis = 0, ncon = 0;
+    auto issue_b = [&]() {
+      double* nb = smem + (nis % NSTB) * BST;
+      stage_rows(nb, tile_ptr<MODE>(Kb, R, tm, I, J), rq * RC, RC, tid);
+      stage_rhs(nb + RC * TILE, Xb + (long)(I * TILE + rq * RC) * RHSW, RC, tid);
       cp_async_commit();
-    }
-    while (I < nt) {
-      int I2 = I, rq2 = rq + 1;
-      if (rq2 == RPT) { rq2 = 0; I2 = next_row(J, I + 1); }
-      if (I2 < nt) {
-        double* nb = sStage + (par ^ 1) * STAGE_DBL;
-        stage_rows(nb, tile_ptr<MODE>(Kb, R, tm, I2, J), rq2 * RC, RC, tid);
-        stage_rhs(nb + RC * TILE, Xb + (long)(I2 * TILE + rq2 * RC) * RHSW, RC, tid);
-        cp_async_commit();
-        cp_async_wait<1>();
+      ++nis;
+      if (++rq == RPT) { rq = 0; I = next_row(J, I + 1); }
+    };
+    while (nis < NSTB - 1 && I < nt) issue_b();
+    while (ncon < nis) {
+      if (I < nt) {
+        issue_b();
+        cp_async_wait<NSTB - 1>();
       } else {
-        cp_async_wait<0>();
+        const int ahead = nis - ncon - 1;  // groups allowed to stay in flight
+        if (ahead >= 2) cp_async_wait<2>();
+        else if (ahead == 1) cp_async_wait<1>();
+        else cp_async_wait<0>();
       }
       __syncthreads();
-      const double* tl = sStage + par * STAGE_DBL;
+      const double* tl = smem + (ncon % NSTB) * BST;
       const double* xi = tl + RC * TILE;
 #pragma unroll
       for (int k0 = 0; k0 < RC; k0 += 4) {
@@ -810,7 +817,7 @@ k_condense(RveDev R, const __grid_constant__ TileMask tm, const __grid_constant_
           dmma(xacc[u][0], xacc[u][1], tl[sw64(k0 + lc, 16 * warp + 8 * u + lr)], bb);
       }
       __syncthreads();
-      I = I2; rq = rq2; par ^= 1;
+      ++ncon;
     }
     // r = Y_J - xacc ; X_J = G_JJ^-T r
     {  // G_JJ^-1 (lower 16x16 blocks) into the packed buffer
