@@ -115,9 +115,10 @@ __device__ __forceinline__ int next_pair(const RveDev& R, const TileMask& tm, in
   if (MODE == 1) {
     const unsigned long long m = tm.row[I] & tm.row[J] & ((1ull << J) - 1ull) & (~0ull << K);
     return m ? __ffsll((long long)m) - 1 : J;
+  } else {
+    while (K < J && !(__ldg(R.g_nz + I * R.nt + K) && __ldg(R.g_nz + J * R.nt + K))) ++K;
+    return K;
   }
-  while (K < J && !(__ldg(R.g_nz + I * R.nt + K) && __ldg(R.g_nz + J * R.nt + K))) ++K;
-  return K;
 }
 // first I' >= I with G(I',J) structurally nonzero (nt if none)
 template <int MODE>
@@ -126,9 +127,10 @@ __device__ __forceinline__ int next_row(const RveDev& R, const TileMask& tm, int
   if (MODE == 1) {
     const unsigned long long m = tm.col[J] & (~0ull << I);
     return m ? min(__ffsll((long long)m) - 1, R.nt) : R.nt;
+  } else {
+    while (I < R.nt && !__ldg(R.g_nz + I * R.nt + J)) ++I;
+    return I;
   }
-  while (I < R.nt && !__ldg(R.g_nz + I * R.nt + J)) ++I;
-  return I;
 }
 
 // ------------------------------------------------------------------ CTA shape

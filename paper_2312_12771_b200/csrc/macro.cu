@@ -62,7 +62,7 @@ __global__ void k_macro_kin(MacroDev M, const double* __restrict__ u, double* __
     return;
   }
   if (t >= M.ne * M.nq) return;
-  int e = t / M.nq, q = t % M.nq;
+  const int e = t / M.nq;  // qp t % nq: grad is indexed by t directly
   double out[9];
   for (int k = 0; k < M.m; ++k) out[k] = 0.0;
   for (int a = 0; a < M.nen; ++a) {

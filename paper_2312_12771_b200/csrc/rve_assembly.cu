@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   const int tid = threadIdx.x;
   const int bl = blockIdx.x;
   const int b = b0 + bl;
-  const int nen = R.nen, nq = R.nq, ne = R.ne;
+  const int ne = R.ne;
   constexpr int ND = ISO ? (1 << DIM) * DIM : 8;  // nen*dim
 
   if (ISO) {
@@ -328,7 +328,6 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   // periodic map is applied through the independent-node numbering) in the warp's row buffer;
   // then every lane stores its two columns of the nn*DIM rows (512 B per row per warp).
   // Structurally zero tiles are never touched (k_condense starts their accumulators at zero).
-  const int nt = R.nt;
   double* Kb = Kt + (long)bl * R.nslot * TILE_ELEMS;
   const int lane = tid & 31, warp = tid >> 5;
   double* rowbuf = s_row + warp * R.npw * DIM * TILE;
@@ -476,7 +475,6 @@ int rve_assemble_npw(const RveDev& R) {
 void launch_rve_assemble(const RveDev& R, int b0, int nb, double* Kt, double* Y, double* Cavg,
                          double* Pavg, double* rfn, const double* Aq, const double* Pq,
                          cudaStream_t s) {
-  const int dim = R.finite ? 2 : R.dim, nd = (1 << dim) * dim;  // nen*dim
   const size_t sm = rve_assemble_smem(R, R.npw);
   if (R.finite) {
     auto k = k_rve_assemble<2, false>;
