@@ -690,13 +690,55 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
     if (!(del > 0.0)) status = 6;
     double alpha = gam / del;
     for (int i = tid; i < nr; i += CG2_THR) { p[i] = zf[r0 + i]; sv[i] = w[i]; }
-    for (it = 1; it <= max_iter && status == 0; ++it) {
-      for (int i = tid; i < nr; i += CG2_THR) {
-        x[i] += alpha * p[i];
-        r[i] -= alpha * sv[i];
+    // 2-D: the direction update of the previous iteration, the x / r update and z = M^-1 r in one
+    // pass -- threads i and i^1 hold the two rows of a node (node-aligned slices), the 2x2 block
+    // preconditioner takes the sibling residual by a shuffle: no CTA barrier (same arithmetic)
+    double beta = 0.0;
+    auto fused2 = [&](bool first, double* part) {
+      double rz = 0.0, rr2 = 0.0;
+      for (int base = 0; base < nr; base += CG2_THR) {
+        const int i = base + tid;
+        const bool act = i < nr;
+        double ri = 0.0;
+        if (act) {
+          double pi = p[i], si = sv[i];
+          if (!first) {
+            pi = zf[r0 + i] + beta * pi;
+            si = w[i] + beta * si;
+            p[i] = pi;
+            sv[i] = si;
+          }
+          x[i] += alpha * pi;
+          ri = r[i] - alpha * si;
+          r[i] = ri;
+        }
+        const double rsib = __shfl_xor_sync(0xffffffffu, ri, 1);
+        if (act) {
+          const double re = (i & 1) ? rsib : ri, ro = (i & 1) ? ri : rsib;
+          double z = 0.0;
+          z += mi[i * 2] * re;
+          z += mi[i * 2 + 1] * ro;
+          rz += ri * z;
+          rr2 += ri * ri;
+#pragma unroll
+          for (int t = 0; t < CGC_MAXG; ++t)
+            if (t < G) zrem[t][i] = z;
+        }
       }
-      __syncthreads();  // r complete before the block preconditioner mixes components
-      precond_publish(v);
+      part[0] = rz;
+      part[1] = rr2;
+    };
+    for (it = 1; it <= max_iter && status == 0; ++it) {
+      if (dim == 2) {
+        fused2(it == 1, v);
+      } else {
+        for (int i = tid; i < nr; i += CG2_THR) {
+          x[i] += alpha * p[i];
+          r[i] -= alpha * sv[i];
+        }
+        __syncthreads();  // r complete before the block preconditioner mixes components
+        precond_publish(v);
+      }
       cg2_publish(cl, slotsA, 2, v, wred);
       cl.sync();
       const double gn = cg2_sum(slotsA, 0, G);
@@ -706,15 +748,16 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
       cg2_publish(cl, slotsB, 1, v, wred);
       cl.sync();
       del = cg2_sum(slotsB, 0, G);
-      const double beta = gn / gam;
+      beta = gn / gam;
       const double den = del - beta * gn / alpha;
       if (!(den > 0.0)) { status = 6; break; }
       alpha = gn / den;
       gam = gn;
-      for (int i = tid; i < nr; i += CG2_THR) {
-        p[i] = zf[r0 + i] + beta * p[i];
-        sv[i] = w[i] + beta * sv[i];
-      }
+      if (dim != 2)
+        for (int i = tid; i < nr; i += CG2_THR) {
+          p[i] = zf[r0 + i] + beta * p[i];
+          sv[i] = w[i] + beta * sv[i];
+        }
     }
     if (status == 0 && it > max_iter) { status = 5; it = max_iter; }
   }
