@@ -84,13 +84,14 @@ __device__ __forceinline__ bool cook_material(const double* F, double alpha, dou
 // (element, qp) evaluates F~, P, A once (shared memory); phase 2, one thread per element row (a, i)
 // forms its rows of K_e, F_e, r_e from them; the block's NH_ELB x EL_STRIDE outputs are staged in
 // shared memory and written back as one contiguous, coalesced range.
-constexpr int NH_ELB = 16, NH_THR = 128;
+constexpr int NH_ELB = 32, NH_THR = 256;
 
 __global__ void __launch_bounds__(NH_THR) k_rve_element_nh(RveDev R, int b0, int nb, const double* __restrict__ Fbar,
                                                           const double* __restrict__ w, double* __restrict__ EL,
                                                           int* __restrict__ jflag) {
-  __shared__ double sQ[NH_ELB * 4][20];  // per (element, qp): A [16], P [4]
-  __shared__ double sOut[NH_ELB * EL_STRIDE];
+  extern __shared__ double nh_smem[];
+  double (*sQ)[20] = reinterpret_cast<double (*)[20]>(nh_smem);  // [NH_ELB * 4][20]: A [16], P [4] per qp
+  double* sOut = nh_smem + NH_ELB * 4 * 20;                      // [NH_ELB][EL_STRIDE]
   __shared__ int sOk[NH_ELB];
   const int ne = R.ne, nq = R.nq, tid = threadIdx.x;
   const long ge0 = (long)blockIdx.x * NH_ELB, n_el = (long)nb * ne;
@@ -170,7 +171,9 @@ __global__ void __launch_bounds__(NH_THR) k_rve_element_nh(RveDev R, int b0, int
 void launch_rve_material_nh(const RveDev& R, int b0, int nb, const double* F, const double* w,
                             double* EL, double* /*unused*/, int* jflag, cudaStream_t s) {
   const long n = (long)nb * R.ne;
-  k_rve_element_nh<<<(unsigned)((n + NH_ELB - 1) / NH_ELB), NH_THR, 0, s>>>(R, b0, nb, F, w, EL, jflag);
+  const size_t sm = (size_t)NH_ELB * (4 * 20 + EL_STRIDE) * sizeof(double);
+  cudaFuncSetAttribute(k_rve_element_nh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  k_rve_element_nh<<<(unsigned)((n + NH_ELB - 1) / NH_ELB), NH_THR, sm, s>>>(R, b0, nb, F, w, EL, jflag);
 }
 
 // ---------------------------------------------------------------------------
