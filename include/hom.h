@@ -228,6 +228,12 @@ int hom_macro_assemble(hom_ctx* ctx, const double* d_D, void* stream);
 /* d_y [n_macro_dof] = K_FF d_x on the free rows of the last assembled macro matrix, 0 on the
  * Dirichlet rows (K6, the SpMV of the macro CG).  Enqueue only. */
 int hom_macro_spmv(hom_ctx* ctx, const double* d_x, double* d_y, void* stream);
+/* Inspection of K1 (test / verification use): assembles RVE `rve` (small strain only) with the
+ * production kernel into the context's scratch pool and expands its lower K_ff tiles into the
+ * dense symmetric d_Kff [N_pad][N_pad] in the natural fluctuation layout (PAPER.md
+ * eq:discreteSys_L, un-normalised: sum_e sum_qp eta~ B_f^T C B_f; the corner class is an
+ * identity pad).  Overwrites the scratch pool (call between condensations); synchronises. */
+int hom_debug_rve_kff(hom_ctx* ctx, int rve, double* d_Kff, void* stream);
 /* ||R_F||_2 with R = sum_qp eta B^T S_b - f_body (macro residual, eq:linSys); synchronises. */
 int hom_macro_residual_norm(hom_ctx* ctx, const double* d_S, double* norm, void* stream);
 

@@ -406,6 +406,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
     for (int n = 0; n < rn; ++n) indep[n] = int_of[indep[n]];
     R.corner = int_of[R.corner];
     R.nat_of = upload(c, order, s, &rc);  // internal p -> natural order[p]
+    R.int_of = upload(c, int_of, s, &rc);
     c->nat_of = order;
   }
   R.npad = dim * R.n_indep;
@@ -868,6 +869,16 @@ int hom_macro_spmv(hom_ctx* c, const double* d_x, double* d_y, void* stream) {
   cudaStream_t s = (cudaStream_t)stream;
   run(c, HOM_PROF_CG, s, [&] { hom::launch_spmv(c->M, c->val, d_x, d_y, s); });
   return check_cuda(c, cudaGetLastError(), "hom_macro_spmv");
+}
+
+int hom_debug_rve_kff(hom_ctx* c, int rve, double* d_Kff, void* stream) {
+  if (!c || !d_Kff) return set_err(c, HOM_ERR_INVALID_ARG, "hom_debug_rve_kff: NULL");
+  if (c->finite) return set_err(c, HOM_ERR_INVALID_ARG, "hom_debug_rve_kff: small strain only");
+  if (rve < c->b_lo || rve >= c->b_hi) return set_err(c, HOM_ERR_INVALID_ARG, "hom_debug_rve_kff: RVE out of range");
+  cudaStream_t s = (cudaStream_t)stream;
+  hom::launch_rve_assemble(c->R, rve, 1, c->Kt, c->Y, c->Cavg, c->Pavg, c->rfn, c->Aq, c->Pq, s);
+  hom::launch_expand_kff(c->R, c->Kt, d_Kff, s);
+  return check_cuda(c, cudaStreamSynchronize(s), "hom_debug_rve_kff");
 }
 
 int hom_macro_solve(hom_ctx* c, const double* d_D, const double* d_S, double scale, double* d_x,

@@ -68,6 +68,7 @@ struct RveDev {
   int n_witem;
   int xb0;                        // first RVE of the influence store X (the context's local range)
   const int* nat_of;              // [n_indep] internal node -> natural (API) node; nullptr = identity
+  const int* int_of;              // [n_indep] natural node -> internal node; nullptr = identity
 };
 
 struct MacroDev {
@@ -146,6 +147,8 @@ bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const do
 void launch_axpy(double* y, const double* x, double a, int n, cudaStream_t s);
 // w between the natural (API) and the internal node order (to_api: internal -> natural)
 void launch_permute_w(const RveDev& R, int B, const double* src, double* dst, int to_api, cudaStream_t s);
+// dense natural-layout K_ff [npad][npad] from the lower tiles of one RVE's pool (Kb)
+void launch_expand_kff(const RveDev& R, const double* Kb, double* out, cudaStream_t s);
 void launch_recover(const RveDev& R, int b0, int nb, const double* X, const double* kin, double* w,
                     int accumulate, cudaStream_t s);
 

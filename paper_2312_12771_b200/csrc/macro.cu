@@ -1088,6 +1088,29 @@ __global__ void k_permute_w(RveDev R, long n, const double* __restrict__ src, do
   else dst[t] = src[e];
 }
 
+__global__ void k_expand_kff(RveDev R, const double* __restrict__ Kb, double* __restrict__ out) {
+  const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = R.npad;
+  if (t >= (long)n * n) return;
+  const int i = (int)(t / n), j = (int)(t % n), dr = n / R.n_indep;
+  int ii = i, jj = j;  // natural -> internal DOF
+  if (R.int_of) {
+    ii = __ldg(R.int_of + i / dr) * dr + i % dr;
+    jj = __ldg(R.int_of + j / dr) * dr + j % dr;
+  }
+  if (ii < jj) { const int x = ii; ii = jj; jj = x; }  // lower tiles only (symmetric)
+  const int I = ii / TILE, J = jj / TILE;
+  double v = 0.0;
+  const int slot = __ldg(R.tslot + I * R.nt + J);
+  if (slot >= 0 && R.tile_nz[I * R.nt + J]) v = Kb[(long)slot * TILE_ELEMS + (ii % TILE) * TILE + jj % TILE];
+  out[t] = v;
+}
+
+void launch_expand_kff(const RveDev& R, const double* Kb, double* out, cudaStream_t s) {
+  const long n = (long)R.npad * R.npad;
+  k_expand_kff<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(R, Kb, out);
+}
+
 void launch_permute_w(const RveDev& R, int B, const double* src, double* dst, int to_api, cudaStream_t s) {
   const long n = (long)B * R.npad;
   if (n <= 0) return;

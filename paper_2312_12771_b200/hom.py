@@ -23,7 +23,7 @@ STATUS = {0: "HOM_OK", 1: "HOM_ERR_INVALID_ARG", 2: "HOM_ERR_MESH", 3: "HOM_ERR_
           7: "HOM_ERR_CUDA", 8: "HOM_ERR_OOM"}
 
 # every symbol include/hom.h declares (checked by tests/test_abi.py)
-EXPORTS = ["hom_setup", "hom_get_sizes", "hom_get_work", "hom_set_load_factor", "hom_macro_assemble", "hom_macro_spmv", "hom_macro_kinematics", "hom_condense", "hom_macro_solve",
+EXPORTS = ["hom_setup", "hom_get_sizes", "hom_get_work", "hom_debug_rve_kff", "hom_set_load_factor", "hom_macro_assemble", "hom_macro_spmv", "hom_macro_kinematics", "hom_condense", "hom_macro_solve",
            "hom_macro_residual_norm", "hom_recover_fluctuations", "hom_newton_update", "hom_set_fluctuations",
            "hom_get_fluctuations", "hom_micro_residual_max", "hom_set_phases", "hom_launch_count",
            "hom_profile_enable", "hom_profile_read", "hom_last_error", "hom_destroy"]
@@ -116,6 +116,7 @@ def lib(build_if_missing: bool = True):
         L.hom_macro_assemble.argtypes = [P, P, P]
         L.hom_set_load_factor.argtypes = [P, D]
         L.hom_macro_spmv.argtypes = [P, P, P, P]
+        L.hom_debug_rve_kff.argtypes = [P, I, P, P]
         L.hom_recover_fluctuations.argtypes = [P, P, P, P]
         L.hom_newton_update.argtypes = [P, P, P, P]
         L.hom_set_fluctuations.argtypes = [P, P, P]
@@ -285,6 +286,12 @@ class Homogenizer:
 
     def macro_assemble(self, D):
         self._check(lib().hom_macro_assemble(self.h, self._ptr(D), self._stream()), "hom_macro_assemble")
+
+    def debug_rve_kff(self, rve):
+        """K1 output of one RVE as a dense [N_pad][N_pad] tensor in the natural layout (verification)."""
+        out = self.empty(self.n_pad, self.n_pad)
+        self._check(lib().hom_debug_rve_kff(self.h, int(rve), self._ptr(out), self._stream()), "hom_debug_rve_kff")
+        return out
 
     def macro_spmv(self, x, y=None):
         y = self.empty(self.n_dof) if y is None else y

@@ -371,6 +371,40 @@ def test_fluctuations_keep_the_natural_layout(torch_cuda):
         assert rel(b, a) <= 1e-12
 
 
+# ------------------------------------------------------------------ K1 alone (hom_debug_rve_kff)
+@pytest.mark.parametrize("dim,r,ordering,tile_sparse", [(2, 5, "folded", False), (2, 6, "natural", True),
+                                                        (2, 12, "folded", True), (3, 3, "folded", False)])
+def test_k1_kff_equals_bruteforce_micro_block(torch_cuda, dim, r, ordering, tile_sparse):
+    """The assembled K_ff of one RVE, entry by entry, against the micro-micro block L of the
+    brute-force monolithic assembly (tests/bruteforce.py, own shape functions and periodic map):
+    L_b = eta_M K_ff (R2), with random per-element phases and per-RVE moduli."""
+    from paper_2312_12771_b200.hom import Homogenizer
+
+    from . import bruteforce as bf
+    rng = np.random.default_rng(40 + r)
+    if dim == 2:
+        wl = W.config3(nel=1, r=r, seed=17 + r)
+    else:
+        wl = W.config4(nel=1, r=r)
+        wl.phase = (rng.random((wl.n_rve, r ** 3)) < 0.4).astype(np.uint8)
+        wl.mat = np.stack([np.array([[1.0 + rng.random(), 0.25], [20.0 * rng.random() + 1.0, 0.3]])
+                           for _ in range(wl.n_rve)])
+    b = 1
+    h = Homogenizer.from_workload(wl, rve_ordering=ordering, tile_sparse=tile_sparse)
+    K = h.debug_rve_kff(b).cpu().numpy()
+    ph = wl.phase[b] if wl.phase.shape[0] > 1 else wl.phase[0]
+    mt = wl.mat[b] if wl.mat.ndim == 3 and wl.mat.shape[0] > 1 else (wl.mat[0] if wl.mat.ndim == 3 else wl.mat)
+    E = np.array([mt[p, 0] for p in ph]).reshape(1, -1).repeat(wl.n_rve, 0)
+    nu = np.array([mt[p, 1] for p in ph]).reshape(1, -1).repeat(wl.n_rve, 0)
+    mono = bf.Monolithic(dim, 1, r, lambda bb, e: bf.iso_tangent_full(dim, E[bb, e], nu[bb, e]), wl.dir_dof)
+    Kg, _ = mono.assemble(u=np.zeros(mono.ndof_M))
+    off = mono.ndof_M + b * mono.nf
+    L = Kg[off:off + mono.nf, off:off + mono.nf] / (0.5 / 1) ** dim  # / eta_M of the 1-element macro mesh
+    assert rel(K[dim:, dim:], L) <= 1e-13
+    assert np.array_equal(K[:dim, :dim], np.eye(dim)) and not K[:dim, dim:].any() and not K[dim:, :dim].any()
+    assert np.array_equal(K, K.T)
+
+
 # ------------------------------------------------------------------ RVE sharding (multi-GPU path, DESIGN.md §7)
 def test_rve_range_shards_reassemble_bitwise(torch_cuda):
     """Two contexts condensing disjoint, element-aligned RVE ranges (what two ranks do), rows
