@@ -624,8 +624,21 @@ k_condense(RveDev R, const __grid_constant__ TileMask tm, const __grid_constant_
     }
     __syncthreads();
     TMARK(1);
+    // dense (TMA): the first chunk of the first off-diagonal tile (J+1, J) is fetched into stage 1
+    // now -- stage 1 is untouched by the factor and Y phases -- so it lands under the pivot chain
+    const bool pre_o = TMA_STAGING && J > 0 && J + 1 < nt;
+    if (pre_o && tid == 0) {
+      double* st = sStage + STAGE_DBL;
+      fence_proxy_async();
+      mbar_expect(&full[1], 2 * 64 * KC * 8);
+      tma_load_2d(st, &kmap, 0, (int)(krow0 + (long)tile_slot<MODE>(R, tm, J + 1, 0) * TILE), &full[1]);
+      tma_load_2d(st + 64 * KC, &kmap, 0, (int)(krow0 + (long)tile_slot<MODE>(R, tm, J, 0) * TILE), &full[1]);
+    }
     // ---------- blocked Cholesky + inverse of the diagonal tile ----------
-    if (!factor_invert_diag(sT, sStage, sFail, J, tid)) break;
+    if (!factor_invert_diag(sT, sStage, sFail, J, tid)) {
+      if (pre_o) wait_stage(1);  // no TMA left in flight into this CTA's shared memory
+      break;
+    }
     TMARK(2);
     // ---------- Y_J = G_JJ^-1 (Kfe_J - sum) ; S += Y_J^T Y_J ; store G_JJ^-1 ----------
     {
@@ -670,6 +683,8 @@ k_condense(RveDev R, const __grid_constant__ TileMask tm, const __grid_constant_
           for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
       }
       int K = next_pair<MODE>(R, tm, I, J, 0), kc = 0, par = 0;
+      const bool prefetched = pre_o && I == J + 1;  // chunk (K = 0, kc = 0) already in stage 1
+      if (prefetched) par = 1;
       auto issue_o = [&](int stg, int KK, int kcc) {  // G_IK and G_JK chunks kcc, one thread
         double* st = sStage + stg * STAGE_DBL;
         fence_proxy_async();
@@ -684,7 +699,7 @@ k_condense(RveDev R, const __grid_constant__ TileMask tm, const __grid_constant_
         stage_chunk(st + 64 * KC, tile_ptr<MODE>(Kb, R, tm, J, KK), kcc, tid);
         cp_async_commit();
       };
-      if (K < J) {
+      if (K < J && !prefetched) {
         if (TMA_STAGING) { if (tid == 0) issue_o(0, K, 0); }
         else stage_o(0, K, 0);
       }
