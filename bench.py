@@ -115,16 +115,16 @@ def oracle_step_time(wl, target_s: float = 10.0):
     nthreads = oracle.default_threads()
     per = 1 if wl.phase.shape[0] == 1 else None
 
-    def sample(n):
+    def sample(n, threads=None):
         ids = np.arange(n) % wl.n_rve
         ph = np.repeat(wl.phase, n, 0) if per else wl.phase[ids]
         mt = np.repeat(wl.mat, n, 0) if wl.mat.shape[0] == 1 else wl.mat[ids]
         t0 = time.perf_counter()
         if wl.kind == "linear":
-            C = oracle.condense_batch_linear(wl.dim, wl.r, ph, mt, n, want_W=True, nthreads=nthreads)[0]
+            C = oracle.condense_batch_linear(wl.dim, wl.r, ph, mt, n, want_W=True, nthreads=threads or nthreads)[0]
         else:
             F = np.tile([1.0, 0.0, 0.0, 1.0], (n, 1))
-            C = oracle.condense_batch_nh(wl.r, ph, mt, F, nthreads=nthreads)["A_eff"]
+            C = oracle.condense_batch_nh(wl.r, ph, mt, F, nthreads=threads or nthreads)["A_eff"]
         return time.perf_counter() - t0, C
 
     n = max(nthreads, 8)
@@ -134,6 +134,9 @@ def oracle_step_time(wl, target_s: float = 10.0):
         n = min(256 * wl.n_rve, max(n * 2, int(n * 0.8 * target_s / max(t, 1e-3))))
         t, C = sample(n)
     t_rve = t / n
+    # per-core rate: one thread on a fixed 64-RVE slice
+    n1 = min(64, wl.n_rve)
+    t1, _ = sample(n1, threads=1)
     # macro direct solve at full size with representative tangents
     Cm = np.broadcast_to(C[:1], (wl.n_rve,) + C.shape[1:]).copy()
     t0 = time.perf_counter()
@@ -149,7 +152,8 @@ def oracle_step_time(wl, target_s: float = 10.0):
             f"{n} RVE condensations (the {wl.n_rve} RVEs of the step, cyclically)")
     detail = {"cores": nthreads, "sample": f"{what} condensed (skyline Cholesky, unit-strain route, "
                                              f"{t:.1f} s) + 1 full-size direct macro solve ({t_macro:.2f} s); "
-                                             f"scaled to a full step", "t_rve_s": t_rve, "t_macro_s": t_macro}
+                                             f"scaled to a full step", "t_rve_s": t_rve, "t_macro_s": t_macro,
+              "per_core_tangents_s": n1 / t1, "per_core_sample": f"{n1} RVEs on 1 thread ({t1:.2f} s)"}
     return step, detail
 
 
@@ -299,7 +303,8 @@ def main():
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
                 "cpu_baseline": {"value": val, "unit": "tangents/s", "cores": detail["cores"], "kind": "oracle",
-                                 "sample": detail["sample"], "cpu": cpu_model()},
+                                 "sample": detail["sample"], "cpu": cpu_model(),
+                                 "per_core_value": detail["per_core_tangents_s"]},
                 "e2e": {"value": val, "unit": "tangents/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -526,7 +531,9 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         st, detail = oracle_step_time(wl)
         line["cpu_baseline"] = {"value": wl.n_rve / st, "unit": "tangents/s", "cores": detail["cores"],
-                                "kind": "oracle", "sample": detail["sample"], "cpu": cpu_model()}
+                                "kind": "oracle", "sample": detail["sample"], "cpu": cpu_model(),
+                                "per_core_value": detail["per_core_tangents_s"],
+                                "per_core_sample": detail["per_core_sample"]}
     print(json.dumps(line))
     if world > 1:
         torch.distributed.destroy_process_group()
