@@ -280,11 +280,12 @@ def main():
     if world > 1:  # weak scaling: one macro problem, its RVEs sharded; ~the same RVE count per GPU
         nel1 = wl.nel
         wl = W.make(args.config, nel=int(round(nel1 * world ** (1.0 / wl.dim))))
+    n_rve_run = wl.n_rve // wl.n_qp if args.macro_basis == "constant" else wl.n_rve  # one RVE per element
     config = {"workload": f"{wl.name}: {wl.description}", "config_index": args.config,
-              "n_rve": wl.n_rve, "rve_dofs": wl.n_pad, "n_f": wl.n_f, "macro_dof": wl.n_dof,
+              "n_rve": n_rve_run, "rve_dofs": wl.n_pad, "n_f": wl.n_f, "macro_dof": wl.n_dof,
               "flop_per_rve": wl.flop_per_rve(),
               "parallelism": f"rve-sharded x{world} (C_eff all-gather, replicated macro CG)" if world > 1 else "single",
-              "macro_nel": wl.nel, "rve_per_gpu": wl.n_rve / world,
+              "macro_nel": wl.nel, "rve_per_gpu": n_rve_run / world,
               "factorization": "tile-sparse" if args.tile_sparse else "dense", "macro_basis": args.macro_basis,
               "rve_ordering": args.rve_ordering}
 
