@@ -90,8 +90,11 @@ __global__ void __launch_bounds__(NH_THR) k_rve_element_nh(RveDev R, int b0, int
                                                           const double* __restrict__ w, double* __restrict__ EL,
                                                           int* __restrict__ jflag) {
   extern __shared__ double nh_smem[];
-  double (*sQ)[20] = reinterpret_cast<double (*)[20]>(nh_smem);  // [NH_ELB * 4][20]: A [16], P [4] per qp
-  double* sOut = nh_smem + NH_ELB * 4 * 20;                      // [NH_ELB][EL_STRIDE]
+  // per (element, qp): A [16], P [4], the shape gradients G [8] and the weight eta~ j (phase 2 reads them
+  // from here instead of re-loading the mesh tables)
+  constexpr int QW = 29;
+  double (*sQ)[QW] = reinterpret_cast<double (*)[QW]>(nh_smem);  // [NH_ELB * 4][QW]
+  double* sOut = nh_smem + NH_ELB * 4 * QW;                      // [NH_ELB][EL_STRIDE]
   __shared__ int sOk[NH_ELB];
   const int ne = R.ne, nq = R.nq, tid = threadIdx.x;
   const long ge0 = (long)blockIdx.x * NH_ELB, n_el = (long)nb * ne;
@@ -118,6 +121,9 @@ __global__ void __launch_bounds__(NH_THR) k_rve_element_nh(RveDev R, int b0, int
         F[2] += w1 * G[2 * aa]; F[3] += w1 * G[2 * aa + 1];
       }
       double* Q = sQ[tid];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) Q[20 + k] = G[k];
+      Q[28] = R.wdet[e * nq + q];
       if (!cook_material(F, alpha, beta, kappa, Q + 16, Q)) {
         atomicMin(&jflag[b], e * nq + q);  // first failing qp of this RVE (init INT_MAX)
         sOk[le] = 0;
@@ -131,14 +137,13 @@ __global__ void __launch_bounds__(NH_THR) k_rve_element_nh(RveDev R, int b0, int
     const long ge = ge0 + le;
     double* out = sOut + le * EL_STRIDE;
     if (ge < n_el) {
-      const int e = (int)(ge % ne);
       const bool ok = sOk[le];
       double ke[8] = {}, fe[4] = {}, re = 0.0;
       for (int q = 0; q < nq; ++q) {
-        const double* G = R.grad + (long)(e * nq + q) * 4 * 2;
         const double* A = sQ[le * 4 + q];
         const double* P = A + 16;
-        const double wq = R.wdet[e * nq + q];
+        const double* G = A + 20;
+        const double wq = A[28];
         const double ga0 = G[2 * a], ga1 = G[2 * a + 1];
         double t[4];  // row (a, i): t[k] = sum_J g_a[J] A[(i,J), k]
         for (int k = 0; k < 4; ++k) t[k] = ga0 * A[(2 * i) * 4 + k] + ga1 * A[(2 * i + 1) * 4 + k];
@@ -154,7 +159,7 @@ __global__ void __launch_bounds__(NH_THR) k_rve_element_nh(RveDev R, int b0, int
       if (row < 5) {  // qp sums of A (rows 0-3: 4 entries each) and P (row 4)
         double sv[4] = {};
         for (int q = 0; q < nq; ++q) {
-          const double wq = R.wdet[e * nq + q];
+          const double wq = sQ[le * 4 + q][28];
           for (int k = 0; k < 4; ++k) sv[k] += wq * sQ[le * 4 + q][row * 4 + k];
         }
         for (int k = 0; k < 4; ++k) out[EL_A + row * 4 + k] = ok ? sv[k] : 0.0;
@@ -171,7 +176,7 @@ __global__ void __launch_bounds__(NH_THR) k_rve_element_nh(RveDev R, int b0, int
 void launch_rve_material_nh(const RveDev& R, int b0, int nb, const double* F, const double* w,
                             double* EL, double* /*unused*/, int* jflag, cudaStream_t s) {
   const long n = (long)nb * R.ne;
-  const size_t sm = (size_t)NH_ELB * (4 * 20 + EL_STRIDE) * sizeof(double);
+  const size_t sm = (size_t)NH_ELB * (4 * 29 + EL_STRIDE) * sizeof(double);
   cudaFuncSetAttribute(k_rve_element_nh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   k_rve_element_nh<<<(unsigned)((n + NH_ELB - 1) / NH_ELB), NH_THR, sm, s>>>(R, b0, nb, F, w, EL, jflag);
 }
