@@ -554,7 +554,8 @@ k_condense(RveDev R, const __grid_constant__ TileMask tm, const __grid_constant_
   constexpr bool TMA_STAGING = MODE == 0;
   const long krow0 = (long)bl * R.nslot * TILE;  // first pool row of this RVE (kmap rows)
   const long yrow0 = (long)bl * NT;              // first Y row of this RVE (ymap rows)
-  double Sacc = 0.0;  // thread (i,j) = (tid>>3, tid&7), tid < 64: sum_r Y[r][i] Y[r][j]
+  // Schur sum S = sum_J Y_J^T Y_J (8x8) on DMMA by warp 0: lane (lr, lc) holds S[lr][2lc], S[lr][2lc+1]
+  double Sacc0 = 0.0, Sacc1 = 0.0;
 
   // ======================= forward: factor + Y ==============================
   for (int J = 0; J < nt; ++J) {
@@ -661,11 +662,10 @@ k_condense(RveDev R, const __grid_constant__ TileMask tm, const __grid_constant_
       }
     }
     __syncthreads();
-    if (tid < 64) {
-      const int i = tid >> 3, j = tid & 7;
-      double s = 0.0;
-      for (int r = 0; r < TILE; ++r) s = fma(sY2[swy(r, i)], sY2[swy(r, j)], s);
-      Sacc += s;
+    if (warp == 0) {
+#pragma unroll
+      for (int k0 = 0; k0 < TILE; k0 += 4)  // A = Y_J^T (8 x 64), B' = Y_J^T (rows j, k = r)
+        dmma(Sacc0, Sacc1, sY2[swy(k0 + lc, lr)], sY2[swy(k0 + lc, lr)]);
     }
     __syncthreads();  // sY2 (stage area) free again
     TMARK(3);
@@ -772,7 +772,10 @@ k_condense(RveDev R, const __grid_constant__ TileMask tm, const __grid_constant_
   {
     double* sSum = sStage;  // reuse: 8x8 plain
     __syncthreads();
-    if (tid < 64) sSum[tid] = Sacc;
+    if (warp == 0) {
+      sSum[lr * 8 + 2 * lc] = Sacc0;
+      sSum[lr * 8 + 2 * lc + 1] = Sacc1;
+    }
     __syncthreads();
     const int m = R.m;
     const double* Ca = Cavg + (long)bl * 64;
