@@ -76,6 +76,6 @@ if __name__ == "__main__":
     rng = np.random.default_rng(0)
     wl3 = W.config3()
     linear("cfg3 random (full, sampled)", wl3, np.sort(np.unique(np.concatenate(
-        [rng.choice(wl3.n_rve, 30, replace=False), [0, wl3.n_rve - 1]]))))
+        [rng.choice(wl3.n_rve, 254, replace=False), [0, wl3.n_rve - 1]]))))
     linear("cfg4 sphere (full)", W.config4())
     finite_per_state("cfg5 neo-hooke (full)", W.config5())
