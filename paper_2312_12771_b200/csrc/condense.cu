@@ -205,15 +205,29 @@ __device__ __forceinline__ int chol16_inv_inplace(double* sD, int k0, int lane) 
 #pragma unroll
     for (int q = 0; q < 4; ++q) a[q] = (r >= c0 + q) ? sD[sd(k0 + r, k0 + c0 + q)] : 0.0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const double dkk = __shfl_sync(FULL, a[k], c0 + k);
-      if (!(dkk > 0.0) && fail == 16) fail = c0 + k;
-      ip[c0 + k] = rsqrt(dkk);
-      a[k] = (r == c0 + k) ? dkk * ip[c0 + k] : a[k] * ip[c0 + k];
+    for (int k = 0; k < 4; k += 2) {
+      // two pivots at a time: the 2x2 pivot block [A B; B C] gives L_kk = sqrt(A) and
+      // L_k+1,k+1 = sqrt(det / A), det = AC - B^2 -- the two rsqrt are independent, so the chain
+      // has one rsqrt level per two columns
+      const double A = __shfl_sync(FULL, a[k], c0 + k);
+      const double Bv = __shfl_sync(FULL, a[k], c0 + k + 1);
+      const double Cv = __shfl_sync(FULL, a[k + 1], c0 + k + 1);
+      const double det = fma(A, Cv, -(Bv * Bv));
+      if (!(A > 0.0) && fail == 16) fail = c0 + k;
+      if (!(det > 0.0) && fail == 16) fail = c0 + k + 1;
+      const double ia = rsqrt(A), id = rsqrt(det);
+      const double ip1 = (A * ia) * id;  // 1 / L_k+1,k+1 = sqrt(A) / sqrt(det)
+      ip[c0 + k] = ia;
+      ip[c0 + k + 1] = ip1;
+      const double l10 = Bv * ia;  // L_k+1,k
+      const double lk = a[k] * ia;  // column k of row r (row k: sqrt(A); row k+1: l10)
+      const double lk1 = fma(-lk, l10, a[k + 1]) * ip1;  // column k+1 (row k+1: sqrt(det / A))
+      a[k] = lk;
+      if (r >= c0 + k + 1) a[k + 1] = lk1;
 #pragma unroll
-      for (int j = k + 1; j < 4; ++j) {
-        const double ljk = __shfl_sync(FULL, a[k], c0 + j);
-        if (r >= c0 + j) a[j] = fma(-a[k], ljk, a[j]);
+      for (int j = k + 2; j < 4; ++j) {
+        const double ljk = __shfl_sync(FULL, a[k], c0 + j), ljk1 = __shfl_sync(FULL, a[k + 1], c0 + j);
+        if (r >= c0 + j) a[j] = fma(-a[k], ljk, fma(-a[k + 1], ljk1, a[j]));
       }
     }
     if (lane < 16 && r >= c0) {
