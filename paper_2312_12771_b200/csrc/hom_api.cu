@@ -298,8 +298,18 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
       int a = (int)((long)M.ndof * g / G), b = (int)((long)M.ndof * (g + 1) / G);
       c->max_slice_nnz = std::max(c->max_slice_nnz, rowptr[b] - rowptr[a]);
     }
+  M.cg_ellw = 0;
+  for (int i = 0; i < M.ndof; ++i) M.cg_ellw = std::max(M.cg_ellw, rowptr[i + 1] - rowptr[i]);
   hom::cg2_slice_sizes(M, rowptr.data(), 16, &c->cg2_slice[0][0], &c->cg2_slice[0][1]);
   hom::cg2_slice_sizes(M, rowptr.data(), 8, &c->cg2_slice[1][0], &c->cg2_slice[1][1]);
+  {
+    std::vector<int> win(2 * 16 * 2, 0);
+    hom::cg2_windows(M, rowptr.data(), col.data(), 16, win.data(), &M.cg_wmax[0], &M.cg_wok[0]);
+    hom::cg2_windows(M, rowptr.data(), col.data(), 8, win.data() + 32, &M.cg_wmax[1], &M.cg_wok[1]);
+    M.cg_win = upload(c, win, s, &rc);
+  }
+  M.cg_gval = dalloc<double>(c, (size_t)M.ndof * M.cg_ellw, &rc);
+  M.cg_gcol = dalloc<int>(c, (size_t)M.ndof * M.cg_ellw, &rc);
   std::vector<uint8_t> dmask(M.ndof, 0);
   std::vector<double> dval(M.ndof, 0.0), fbody(M.ndof, 0.0);
   if (mac->n_dirichlet > 0 && (!mac->dirichlet_dof || !mac->dirichlet_value))

@@ -92,7 +92,17 @@ struct MacroDev {
   int constant_basis;             // 1: one RVE per element (eq:constSolution1/2), D = C_eff per element
   const double* Cavg_e;           // [ne][m][m] <C> per element (constant basis)
   const double* evol;             // [ne] element volume |B_e|
+  // cluster PCG with z windows (meshes whose full z copy does not fit a CTA): for cluster size
+  // G = 16 (index 0) and 8 (index 1), CTA g reads z only on its CSR slice's column range
+  // cg_win[(idx*16 + g)*2 + 0..1] = [lo, hi); cg_wmax = largest window; cg_wok = every CTA's rows
+  // fall in at most CG_WDEST other windows
+  const int* cg_win;
+  int cg_wmax[2], cg_wok[2];
+  int cg_ellw;  // k_macro_cg_cluster2: ELL width (longest CSR row)
+  double* cg_gval;  // [cg_ellw][ndof] ELL slots that do not fit shared memory (L2-resident spill)
+  int* cg_gcol;
 };
+constexpr int CG_WDEST = 4;
 
 // Tile structure of a tile-sparse factor with nt <= 64, passed to k_condense by value (kernel
 // parameter space = constant bank: warp-uniform lookups without global loads): bit J of row[I] /
@@ -141,6 +151,9 @@ void launch_spmv(const MacroDev& M, const double* val, const double* x, double* 
 void launch_macro_cg_large(const MacroDev& M, const double* val, const double* diag, const double* rhs,
                            double scale, double rtol, int max_iter, double* xout, double* work, double* sc,
                            double* part, CgState* st, cudaStream_t s);
+// column windows of the node-aligned CSR slices for cluster size G (see MacroDev::cg_win)
+void cg2_windows(const MacroDev& M, const int* host_rowptr, const int* host_col, int G, int* win, int* wmax,
+                 int* wok);
 void cg2_slice_sizes(const MacroDev& M, const int* host_rowptr, int G, int* max_nr, int* max_nnz);
 bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const double* val, const double* rhs,
                               double scale, double rtol, int max_iter, double* x, CgState* st, cudaStream_t s);

@@ -539,8 +539,8 @@ bool launch_macro_cg_cluster(const MacroDev& M, int max_slice_nnz, const double*
 //   loop: x += a p; r -= a s; z = M^-1 r; [z slices + (r.z, r.r) partials -> all CTAs; sync]
 //         w = A z; [(z.w) partials -> all CTAs; sync]
 //         b = g'/g; a = g'/(d - b g'/a); p = z + b p; s = w + b s
-constexpr int CG2_THR = 256;
 
+template <int CG2_THR>
 __device__ __forceinline__ void cg2_publish(cgx::cluster_group& cl, double* slots, int nv, double* v, double* wred) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int j = 0; j < nv; ++j) {
@@ -565,10 +565,11 @@ __device__ __forceinline__ double cg2_sum(const double* slots, int j, int G) {
   return a;
 }
 
+template <bool WIN, int CG2_THR>  // CG2_THR: 256, or 512 for long slices (more rows in flight)
 __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const double* __restrict__ val,
                                                                const double* __restrict__ b, double scale,
                                                                double rtol, int max_iter, double* __restrict__ xout,
-                                                               CgState* st) {
+                                                               CgState* st, int js) {
   cgx::cluster_group cl = cgx::this_cluster();
   const int G = cl.num_blocks(), g = cl.block_rank();
   const int n = M.ndof, dim = M.dim, tid = threadIdx.x;
@@ -578,24 +579,80 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
   double* slotsA = sm;                       // [3][CGC_MAXG]: (r.z, r.r)
   double* slotsB = slotsA + 3 * CGC_MAXG;    // [3][CGC_MAXG]: (z.w)
   double* wred = slotsB + 3 * CGC_MAXG;      // [3][32]
-  double* zf = wred + 96;                    // [n] full copy of z
-  double* x = zf + n;
+  // z: a full copy (WIN = false) or this CTA's column window [wlo, whi) (WIN = true; indices into zf
+  // are then offset by wlo, the CSR columns in shared memory pre-offset)
+  const int* wtab = M.cg_win + (G == 16 ? 0 : 2 * CGC_MAXG);
+  const int wlo = WIN ? __ldg(wtab + 2 * g) : 0;
+  const int zlen = WIN ? M.cg_wmax[G == 16 ? 0 : 1] : n;
+  double* zf = wred + 96;                    // [zlen]
+  double* x = zf + zlen;
   double* r = x + nr;
   double* p = r + nr;
   double* sv = p + nr;
   double* w = sv + nr;
   double* mi = w + nr;                       // [nr][dim] block-Jacobi inverse rows
-  const int nz0 = M.rowptr[r0], nnz = M.rowptr[r1] - nz0;
+  // the CSR slice as column-major ELL (slot j of local row i at j * nr + i: consecutive threads read
+  // consecutive words), padded to the longest row with zero values pointing at the row's own z.
+  // Slots j < js live in shared memory, the rest (large meshes) in global memory at [j][n], read
+  // back from L2 every SpMV
+  const int nz0 = M.rowptr[r0], ew = M.cg_ellw, nell = js * nr;
   double* sval = mi + nr * dim;
-  int* scol = reinterpret_cast<int*>(sval + nnz);
-  int* srow = scol + nnz;
-  for (int k = tid; k < nnz; k += CG2_THR) { sval[k] = val[nz0 + k]; scol[k] = M.col[nz0 + k]; }
+  int* scol = reinterpret_cast<int*>(sval + nell);
+  int* srow = scol + nell;
+  double* gval = M.cg_gval + r0;
+  int* gcol = M.cg_gcol + r0;
   for (int i = tid; i <= nr; i += CG2_THR) srow[i] = M.rowptr[r0 + i] - nz0;
   __syncthreads();
-  // remote copies of z: this CTA's slice in every CTA of the cluster (addresses mapped once)
-  double* zrem[CGC_MAXG];
+  for (int e = tid; e < ew * nr; e += CG2_THR) {
+    const int j = e / nr, i = e - j * nr, k = srow[i] + j;
+    const bool in = k < srow[i + 1];
+    const double vv = in ? val[nz0 + k] : 0.0;
+    const int cc = in ? M.col[nz0 + k] - wlo : r0 + i - wlo;
+    if (j < js) {
+      sval[e] = vv;
+      scol[e] = cc;
+    } else {
+      gval[(size_t)j * n + i] = vv;
+      gcol[(size_t)j * n + i] = cc;
+    }
+  }
+  __syncthreads();  // also orders this CTA's global ELL writes before its own reads
+  // remote copies of z: this CTA's slice in every CTA of the cluster (addresses mapped once);
+  // WIN: only the CTAs whose window meets these rows, local rows [dlo, dhi) of each
+  double* zrem[WIN ? CG_WDEST + 1 : CGC_MAXG];
+  int dlo[WIN ? CG_WDEST + 1 : 1], dhi[WIN ? CG_WDEST + 1 : 1];
+  int ndst = 0;
+  if (WIN) {
 #pragma unroll
-  for (int t = 0; t < CGC_MAXG; ++t) zrem[t] = t < G ? cl.map_shared_rank(zf, t) + r0 : nullptr;
+    for (int q = 0; q < CG_WDEST + 1; ++q) { zrem[q] = nullptr; dlo[q] = 0; dhi[q] = 0; }
+    for (int t = 0; t < G; ++t) {
+      const int lo = max(r0, __ldg(wtab + 2 * t)), hi = min(r1, __ldg(wtab + 2 * t + 1));
+      if (lo >= hi || ndst > CG_WDEST) continue;
+#pragma unroll
+      for (int q = 0; q < CG_WDEST + 1; ++q)
+        if (q == ndst) {
+          zrem[q] = cl.map_shared_rank(zf, t) + (r0 - __ldg(wtab + 2 * t));
+          dlo[q] = lo - r0;
+          dhi[q] = hi - r0;
+        }
+      ++ndst;
+    }
+  } else {
+#pragma unroll
+    for (int t = 0; t < CGC_MAXG; ++t) zrem[t] = t < G ? cl.map_shared_rank(zf, t) + r0 : nullptr;
+  }
+  auto put_z = [&](int i, double z) {  // local row i of this CTA -> every copy that reads it
+    if (WIN) {
+#pragma unroll
+      for (int q = 0; q < CG_WDEST + 1; ++q)
+        if (q < ndst && i >= dlo[q] && i < dhi[q]) zrem[q][i] = z;
+    } else {
+#pragma unroll
+      for (int t = 0; t < CGC_MAXG; ++t)
+        if (t < G) zrem[t][i] = z;
+    }
+  };
+  const int zown = r0 - wlo;  // zf index of local row 0
   // node-block Jacobi: invert the free part of each dim x dim diagonal block
   for (int nd = nd0 + tid; nd < nd1; nd += CG2_THR) {
     double a[3][3] = {}, inv[3][3] = {};
@@ -603,9 +660,10 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
     for (int ci = 0; ci < dim; ++ci) {
       const int row = nd * dim + ci;
       fr[ci] = !M.dmask[row];
-      for (int k = srow[row - r0]; k < srow[row - r0 + 1]; ++k) {
-        const int cc = scol[k] - nd * dim;
-        if (cc >= 0 && cc < dim) a[ci][cc] = sval[k];
+      const int li = row - r0, len = srow[li + 1] - srow[li];
+      for (int j = 0; j < len; ++j) {
+        const int cc = (j < js ? scol[j * nr + li] : gcol[(size_t)j * n + li]) + wlo - nd * dim;
+        if (cc >= 0 && cc < dim) a[ci][cc] = j < js ? sval[j * nr + li] : gval[(size_t)j * n + li];
       }
     }
     for (int ci = 0; ci < 3; ++ci)
@@ -633,7 +691,10 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
     x[i] = 0.0;
     r[i] = M.dmask[gi] ? 0.0 : b[gi];
     if (M.dmask[gi])  // Dirichlet row: w_i = 0 without a mask test in the SpMV
-      for (int k = srow[i]; k < srow[i + 1]; ++k) sval[k] = 0.0;
+      for (int j = 0; j < ew; ++j) {
+        if (j < js) sval[j * nr + i] = 0.0;
+        else gval[(size_t)j * n + i] = 0.0;
+      }
   }
   cl.sync();  // every CTA of the cluster is running before the first DSMEM store
 
@@ -646,9 +707,7 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
       for (int cj = 0; cj < dim; ++cj) z += mi[i * dim + cj] * r[nl * dim + cj];
       rz += r[i] * z;
       rr += r[i] * r[i];
-#pragma unroll
-      for (int t = 0; t < CGC_MAXG; ++t)
-        if (t < G) zrem[t][i] = z;
+      put_z(i, z);
       (void)ci;
     }
     part[0] = rz;
@@ -660,36 +719,49 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
     for (int i = tid; i < nr; i += CG2_THR) {
       double s0 = 0.0, s1 = 0.0;
       {  // Dirichlet rows have zero values (set up above)
-        int k = srow[i];
-        const int ke = srow[i + 1];
-        for (; k + 1 < ke; k += 2) {
-          s0 += sval[k] * zf[scol[k]];
-          s1 += sval[k + 1] * zf[scol[k + 1]];
+        const double* vv = sval + i;
+        const int* cc = scol + i;
+        int j = 0;
+        for (; j + 1 < js; j += 2) {  // js is even unless js == ew
+          s0 += vv[j * nr] * zf[cc[j * nr]];
+          s1 += vv[(j + 1) * nr] * zf[cc[(j + 1) * nr]];
         }
-        if (k < ke) s0 += sval[k] * zf[scol[k]];
+        if (j < js) {
+          s0 += vv[j * nr] * zf[cc[j * nr]];
+        } else if (j < ew) {  // spilled slots, from L2
+          const double* gv = gval + i;
+          const int* gc = gcol + i;
+          for (; j + 1 < ew; j += 2) {
+            const double v0 = __ldcg(gv + (size_t)j * n), v1 = __ldcg(gv + (size_t)(j + 1) * n);
+            const int c0 = __ldcg(gc + (size_t)j * n), c1 = __ldcg(gc + (size_t)(j + 1) * n);
+            s0 += v0 * zf[c0];
+            s1 += v1 * zf[c1];
+          }
+          if (j < ew) s0 += __ldcg(gv + (size_t)j * n) * zf[__ldcg(gc + (size_t)j * n)];
+        }
       }
       const double wi = s0 + s1;
       w[i] = wi;
-      zw += zf[r0 + i] * wi;
+      zw += zf[zown + i] * wi;
     }
     return zw;
   };
 
   double v[3];
   precond_publish(v);
-  cg2_publish(cl, slotsA, 2, v, wred);
+  cg2_publish<CG2_THR>(cl, slotsA, 2, v, wred);
   cl.sync();
   double gam = cg2_sum(slotsA, 0, G), rr = cg2_sum(slotsA, 1, G);
   const double bnorm = sqrt(rr);
   int it = 0, status = 0;
   if (bnorm > 0.0) {
     v[0] = spmv();
-    cg2_publish(cl, slotsB, 1, v, wred);
+    cg2_publish<CG2_THR>(cl, slotsB, 1, v, wred);
     cl.sync();
     double del = cg2_sum(slotsB, 0, G);
     if (!(del > 0.0)) status = 6;
     double alpha = gam / del;
-    for (int i = tid; i < nr; i += CG2_THR) { p[i] = zf[r0 + i]; sv[i] = w[i]; }
+    for (int i = tid; i < nr; i += CG2_THR) { p[i] = zf[zown + i]; sv[i] = w[i]; }
     // 2-D: the direction update of the previous iteration, the x / r update and z = M^-1 r in one
     // pass -- threads i and i^1 hold the two rows of a node (node-aligned slices), the 2x2 block
     // preconditioner takes the sibling residual by a shuffle: no CTA barrier (same arithmetic)
@@ -703,7 +775,7 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
         if (act) {
           double pi = p[i], si = sv[i];
           if (!first) {
-            pi = zf[r0 + i] + beta * pi;
+            pi = zf[zown + i] + beta * pi;
             si = w[i] + beta * si;
             p[i] = pi;
             sv[i] = si;
@@ -720,9 +792,7 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
           z += mi[i * 2 + 1] * ro;
           rz += ri * z;
           rr2 += ri * ri;
-#pragma unroll
-          for (int t = 0; t < CGC_MAXG; ++t)
-            if (t < G) zrem[t][i] = z;
+          put_z(i, z);
         }
       }
       part[0] = rz;
@@ -739,13 +809,13 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
         __syncthreads();  // r complete before the block preconditioner mixes components
         precond_publish(v);
       }
-      cg2_publish(cl, slotsA, 2, v, wred);
+      cg2_publish<CG2_THR>(cl, slotsA, 2, v, wred);
       cl.sync();
       const double gn = cg2_sum(slotsA, 0, G);
       rr = cg2_sum(slotsA, 1, G);
       if (sqrt(rr) <= rtol * bnorm) break;
       v[0] = spmv();
-      cg2_publish(cl, slotsB, 1, v, wred);
+      cg2_publish<CG2_THR>(cl, slotsB, 1, v, wred);
       cl.sync();
       del = cg2_sum(slotsB, 0, G);
       beta = gn / gam;
@@ -755,7 +825,7 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
       gam = gn;
       if (dim != 2)
         for (int i = tid; i < nr; i += CG2_THR) {
-          p[i] = zf[r0 + i] + beta * p[i];
+          p[i] = zf[zown + i] + beta * p[i];
           sv[i] = w[i] + beta * sv[i];
         }
     }
@@ -774,56 +844,95 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
   cl.sync();  // no CTA exits while others may still write its shared memory
 }
 
+void cg2_windows(const MacroDev& M, const int* host_rowptr, const int* host_col, int G, int* win, int* wmax,
+                 int* wok) {
+  *wmax = 0;
+  for (int g = 0; g < G; ++g) {  // node-aligned partition, as in k_macro_cg_cluster2
+    const int r0 = (int)((long)M.n_nodes * g / G) * M.dim, r1 = (int)((long)M.n_nodes * (g + 1) / G) * M.dim;
+    int lo = r0, hi = r1;
+    for (int k = host_rowptr[r0]; k < host_rowptr[r1]; ++k) {
+      lo = std::min(lo, host_col[k]);
+      hi = std::max(hi, host_col[k] + 1);
+    }
+    win[2 * g] = lo;
+    win[2 * g + 1] = hi;
+    *wmax = std::max(*wmax, hi - lo);
+  }
+  *wok = 1;
+  for (int g = 0; g < G; ++g) {  // windows (other than its own) that CTA g's rows reach
+    const int r0 = (int)((long)M.n_nodes * g / G) * M.dim, r1 = (int)((long)M.n_nodes * (g + 1) / G) * M.dim;
+    int nd = 0;
+    for (int t = 0; t < G; ++t)
+      if (t != g && std::max(r0, win[2 * t]) < std::min(r1, win[2 * t + 1])) ++nd;
+    if (nd > CG_WDEST) *wok = 0;
+  }
+}
+
 void cg2_slice_sizes(const MacroDev& M, const int* host_rowptr, int G, int* max_nr, int* max_nnz) {
   *max_nr = *max_nnz = 0;
   for (int g = 0; g < G; ++g) {  // node-aligned partition, as in k_macro_cg_cluster2
     const int nd0 = (int)((long)M.n_nodes * g / G), nd1 = (int)((long)M.n_nodes * (g + 1) / G);
     *max_nr = std::max(*max_nr, (nd1 - nd0) * M.dim);
-    *max_nnz = std::max(*max_nnz, host_rowptr[nd1 * M.dim] - host_rowptr[nd0 * M.dim]);
+    *max_nnz = std::max(*max_nnz, (nd1 - nd0) * M.dim * M.cg_ellw);  // ELL slice (k_macro_cg_cluster2)
   }
 }
 
 bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const double* val, const double* rhs,
                               double scale, double rtol, int max_iter, double* x, CgState* st, cudaStream_t s) {
-  static int cached_G = -1;
   static const int force_G = [] {
     const char* e = getenv("HOM_CG_CLUSTER");  // experiment knob: 8 or 16
     return e ? atoi(e) : 0;
   }();
-  for (int gi = 0; gi < 2; ++gi) {
-    const int G = gi == 0 ? 16 : 8;
-    if (force_G && G != force_G) continue;
-    if (cached_G > 0 && G != cached_G) continue;
-    const int max_nr = slice[gi][0], max_nnz = slice[gi][1];
-    const size_t sm = (size_t)(6 * CGC_MAXG + 96 + M.ndof + 5 * max_nr + max_nr * M.dim) * 8 +
-                      (size_t)max_nnz * 12 + (size_t)(max_nr + 1) * 4 + 64;
-    if (sm > 220 * 1024) continue;
-    cudaFuncSetAttribute(k_macro_cg_cluster2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (G > 8) cudaFuncSetAttribute(k_macro_cg_cluster2, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(G, 1, 1);
-    cfg.blockDim = dim3(CG2_THR, 1, 1);
-    cfg.dynamicSmemBytes = sm;
-    cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = G;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int ncl = 0;
-    if (cudaOccupancyMaxActiveClusters(&ncl, k_macro_cg_cluster2, &cfg) != cudaSuccess || ncl < 1) {
+  static const int prefer_full = [] {
+    const char* e = getenv("HOM_CG_FULLZ");  // experiment knob: 1 = try the full z copy first
+    return e ? atoi(e) : 0;
+  }();
+  // preference: the whole ELL slice in shared memory, z windows (fewer DSMEM stores), 16 CTAs
+  for (int c = 0; c < 8; ++c) {
+      const int spill = c >> 2, gi = c & 1, win = ((c >> 1) & 1) ^ (prefer_full ? 0 : 1);
+      const int G = gi == 0 ? 16 : 8;
+      if (force_G && G != force_G) continue;
+      if (win && !M.cg_wok[gi]) continue;
+      const int max_nr = slice[gi][0];
+      const int zlen = win ? M.cg_wmax[gi] : M.ndof;
+      const size_t base = (size_t)(6 * CGC_MAXG + 96 + zlen + 5 * max_nr + max_nr * M.dim) * 8 +
+                          (size_t)(max_nr + 1) * 4 + 64;
+      const size_t cap = 220 * 1024;
+      if (base > cap) continue;
+      int js = (int)std::min<size_t>(M.cg_ellw, (cap - base) / ((size_t)max_nr * 12));
+      if (js < M.cg_ellw) {
+        if (!spill) continue;
+        js &= ~1;
+      } else if (spill) {
+        continue;  // already tried without
+      }
+      const size_t sm = base + (size_t)max_nr * js * 12;
+      const bool wide = max_nr > 768;
+      auto k = win ? (wide ? k_macro_cg_cluster2<true, 512> : k_macro_cg_cluster2<true, 256>)
+                   : (wide ? k_macro_cg_cluster2<false, 512> : k_macro_cg_cluster2<false, 256>);
+      cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+      if (G > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(G, 1, 1);
+      cfg.blockDim = dim3(wide ? 512 : 256, 1, 1);
+      cfg.dynamicSmemBytes = sm;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = G;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, k, &cfg) != cudaSuccess || ncl < 1) {
+        cudaGetLastError();
+        continue;
+      }
+      cudaError_t e = cudaLaunchKernelEx(&cfg, k, M, val, rhs, scale, rtol, max_iter, x, st, js);
+      if (e == cudaSuccess) return true;
       cudaGetLastError();
-      continue;
     }
-    cudaError_t e = cudaLaunchKernelEx(&cfg, k_macro_cg_cluster2, M, val, rhs, scale, rtol, max_iter, x, st);
-    if (e == cudaSuccess) {
-      cached_G = G;
-      return true;
-    }
-    cudaGetLastError();
-  }
   return false;
 }
 

@@ -467,6 +467,23 @@ def test_large_macro_grid_pcg_matches_direct_solve(torch_cuda):
     assert np.array_equal(u.cpu().numpy(), u2.cpu().numpy())  # deterministic reductions
 
 
+@pytest.mark.parametrize("nel", [64, 91])
+def test_cluster_pcg_z_windows_match_direct_solve(torch_cuda, nel):
+    """Macro meshes whose full z copy no longer fits one CTA's shared memory (nel = 91, the N = 8
+    weak-scaling mesh) run the cluster PCG on per-CTA column windows of z; nel = 64 still fits the
+    full copy.  Both must agree with the direct solve and be deterministic."""
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = W.config2(nel=nel, r=2)
+    h = Homogenizer.from_workload(wl)
+    C = h.condense()
+    u, info = h.macro_solve(C)
+    assert info.rel_residual <= 1e-13
+    u_direct = oracle.macro_solve(2, wl.nel, C.cpu().numpy(), wl.dir_dof, wl.dir_val, body=wl.body)
+    assert rel(u.cpu().numpy(), u_direct) <= TOL_U
+    u2, _ = h.macro_solve(C)
+    assert np.array_equal(u.cpu().numpy(), u2.cpu().numpy())
+
+
 # ------------------------------------------------------------------ Cook's membrane (SURVEY §8(f) 1, PAPER.md §4.2)
 def _cook_small(n_steps=2):
     return W.cook(nel=3, r=6, n_steps=n_steps)
