@@ -80,6 +80,60 @@ def test_ragged_3d(torch_cuda):
     check_linear_against_oracle(wl)
 
 
+# ------------------------------------------------------------------ degenerate sizes
+@pytest.mark.parametrize("tile_sparse", [False, True])
+@pytest.mark.parametrize("dim,r", [(2, 1), (2, 2), (3, 1), (3, 2)])
+def test_degenerate_rves_and_single_macro_element(torch_cuda, dim, r, tile_sparse):
+    """r = 1: every RVE node is one periodic image of the pinned corner, so n_f = 0 (empty K_ff)
+    and C_eff = <C> = the single element's C; r = 2: n_f = dim (2^dim - 1) < one tile.  One macro
+    element (nel = 1).  Both through the full path against the oracle."""
+    wl = W.config3(nel=1, r=r, seed=5) if dim == 2 else W.config4(nel=1, r=r)
+    if dim == 3:
+        wl.phase = (np.arange(r ** 3) % 2).astype(np.uint8)[None]
+    g, o = check_linear_against_oracle(wl, tile_sparse=tile_sparse)
+    if r == 1:  # no fluctuation DOFs: C_eff is the isotropic tangent of the RVE's one element
+        m = 3 if dim == 2 else 6
+        for b in range(wl.n_rve):
+            mat = wl.mat[b if wl.mat.shape[0] > 1 else 0]
+            E, nu = mat[wl.phase[b if wl.phase.shape[0] > 1 else 0][0]]
+            lam, mu = E * nu / ((1 + nu) * (1 - 2 * nu)), E / (2 * (1 + nu))
+            C = np.diag([lam + 2 * mu] * dim + [mu] * (m - dim))
+            C[:dim, :dim] += lam * (np.ones((dim, dim)) - np.eye(dim))
+            assert rel(g["C"][b], C) <= TOL_C
+
+
+@pytest.mark.parametrize("r", [1, 2])
+def test_degenerate_rve_finite_strain(torch_cuda, r):
+    """Neo-Hooke with r = 1 (n_f = 0) and r = 2 (n_f = 6, one ragged tile) RVEs through the
+    per-state condensation at a random macro deformation gradient."""
+    import torch
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = W.config5(nel=1, r=r, n_steps=1)
+    rng = np.random.default_rng(11)
+    Fb = np.tile(np.array([1.0, 0, 0, 1.0]), (wl.n_rve, 1)) + 0.05 * rng.standard_normal((wl.n_rve, 4))
+    c = oracle.condense_batch_nh(wl.r, wl.phase, wl.mat, Fb)
+    h = Homogenizer.from_workload(wl)
+    A, Pe, Pa = h.condense(torch.tensor(Fb, device="cuda"))
+    assert rel(A.cpu().numpy(), c["A_eff"]) <= TOL_C
+    assert rel(Pe.cpu().numpy(), c["P_eff"]) <= TOL_C
+    assert rel(Pa.cpu().numpy(), c["P_avg"]) <= TOL_C
+    if r == 1:
+        np.testing.assert_array_equal(Pe.cpu().numpy(), Pa.cpu().numpy())
+
+
+def test_zero_load_gives_zero_solution(torch_cuda):
+    """No body force, no prescribed displacement: the PCG returns u = 0 with 0 iterations (b = 0
+    branch) and the recovered fluctuations are exactly zero."""
+    wl = W.config2(nel=2, r=4)
+    wl.dir_val = np.zeros_like(wl.dir_val)
+    wl.body = None
+    g = gpu_linear(wl)
+    assert g["info"].iterations == 0
+    assert np.all(g["u"] == 0.0) and np.all(g["w"] == 0.0)
+    o = oracle.solve_linear(wl)
+    assert rel(g["C"], o["C_eff"]) <= TOL_C
+
+
 # ------------------------------------------------------------------ config 3
 def test_config3_reduced_macro_full_rve(torch_cuda):
     """Config 3's 32x32 RVEs with per-RVE random phases and moduli (every RVE different)."""
