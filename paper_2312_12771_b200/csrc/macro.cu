@@ -488,9 +488,7 @@ __global__ void __launch_bounds__(CGC_THR) k_macro_cg_cluster(MacroDev M, const 
 bool launch_macro_cg_cluster(const MacroDev& M, int max_slice_nnz, const double* val, const double* diag,
                              const double* rhs, double scale, double rtol, int max_iter, double* x, double* p,
                              CgState* st, cudaStream_t s) {
-  static int cached_G = -1;
   for (int G : {16, 8}) {
-    if (cached_G > 0 && G != cached_G) continue;
     int max_rows = (M.ndof + G - 1) / G + 1;
     size_t base = (size_t)(4 * CGC_MAXG + 64 + 5 * max_rows) * 8;
     size_t with_csr = base + (size_t)max_slice_nnz * 12 + (size_t)(max_rows + 1) * 4 + 64;
@@ -518,10 +516,7 @@ bool launch_macro_cg_cluster(const MacroDev& M, int max_slice_nnz, const double*
     }
     cudaError_t e = cudaLaunchKernelEx(&cfg, k_macro_cg_cluster, M, val, diag, rhs, scale, rtol, max_iter, x, p,
                                        st, csr);
-    if (e == cudaSuccess) {
-      cached_G = G;
-      return true;
-    }
+    if (e == cudaSuccess) return true;
     cudaGetLastError();
   }
   return false;
