@@ -217,6 +217,36 @@ def test_config5_condense_per_state(torch_cuda):
     assert rel(ut.cpu().numpy(), u + du_o) <= TOL_U
 
 
+def test_config5_full_size_sampled(torch_cuda):
+    """Full config 5 (32x32 macro, 4096 RVEs of 16x16, the bench's launch configuration) at a
+    non-trivial state: A_eff / P_eff / <P> of sampled RVEs against the oracle, and the Newton
+    correction of the macro DOFs against the oracle's direct solve with the GPU tangents."""
+    import torch
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = W.config5()
+    rng = np.random.default_rng(5)
+    nn = wl.nel + 1
+    xy = np.stack(np.meshgrid(np.arange(nn), np.arange(nn)), -1).reshape(-1, 2) / wl.nel
+    # smooth state, zero on the clamped edge x = 0 (no jump at the Dirichlet nodes)
+    u = np.stack([xy[:, 0] * (0.01 + 1e-3 * np.sin(3 * xy[:, 1])), -2e-3 * xy[:, 0] ** 2], -1).reshape(-1)
+    w = 1e-3 * rng.standard_normal((wl.n_rve, wl.n_pad))
+    w[:, :2] = 0.0
+    h = Homogenizer.from_workload(wl)
+    h.set_fluctuations(torch.tensor(w, device="cuda"))
+    F = h.macro_kinematics(torch.tensor(u, device="cuda"))
+    A, Pe, Pa = h.condense(F)
+    Fb = oracle.macro_kin(2, wl.nel, u, kind=1) + np.array([1.0, 0, 0, 1.0])
+    ids = np.unique(np.concatenate([rng.choice(wl.n_rve, 24, replace=False), [0, wl.n_rve - 1]]))
+    c = oracle.condense_batch_nh(wl.r, wl.phase, wl.mat, Fb[ids], w[ids])
+    assert rel(A.cpu().numpy()[ids], c["A_eff"]) <= TOL_C
+    assert rel(Pe.cpu().numpy()[ids], c["P_eff"]) <= TOL_C
+    assert rel(Pa.cpu().numpy()[ids], c["P_avg"]) <= TOL_C
+    du, info = h.macro_solve(A, Pe, scale=0.0)
+    du_o = oracle.macro_solve(2, wl.nel, A.cpu().numpy(), wl.dir_dof, np.zeros(len(wl.dir_dof)),
+                              S=Pe.cpu().numpy(), kind=1)
+    assert rel(du.cpu().numpy(), du_o) <= TOL_U
+
+
 def test_config5_newton_load_steps(torch_cuda):
     """Full load-stepping Newton (reduced macro): u per converged step <= 1e-8 vs the oracle,
     and quadratic decay of the macro residual (S:414 reading)."""
