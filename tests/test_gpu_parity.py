@@ -350,6 +350,8 @@ def test_tile_sparse_table_path_large_rve(torch_cuda):
     assert t["h"].sizes.n_tiles > 64
     assert np.array_equal(t["C"], d["C"]) and np.array_equal(t["u"], d["u"]) and np.array_equal(t["w"], d["w"])
     assert t["h"].work.g_tiles < d["h"].work.g_tiles
+    o = oracle.solve_linear(wl)  # the largest RVE of the suite against the oracle
+    assert rel(d["C"], o["C_eff"]) <= TOL_C and rel(d["u"], o["u"]) <= TOL_U
 
 
 def test_tile_sparse_finite_strain_per_state(torch_cuda):
