@@ -214,7 +214,9 @@ int hom_macro_kinematics(hom_ctx* ctx, const double* d_u, double* d_kin, void* s
 int hom_condense(hom_ctx* ctx, const double* d_kin, double* d_C_eff, double* d_P_eff,
                  double* d_P_avg, void* stream);
 
-/* Solve the condensed macro system by Jacobi-preconditioned CG on the free DOFs:
+/* Solve the condensed macro system by CG on the free DOFs, preconditioned by the inverses of the
+ * dim x dim diagonal node blocks (Dirichlet components removed; one thread-block cluster holds the
+ * whole solve for meshes up to ~17k DOFs in 2-D, grid-wide kernels beyond; deterministic sums):
  *   K_FF x_F = -R_F - K_FD x_D,   K = sum_qp eta B^T D_b B,  R = sum_qp eta B^T S_b - f_body,
  * with x_D = dirichlet_scale * dirichlet_value.  d_D = C_eff/A_eff [B][m][m]; d_S [B][m] or NULL.
  * Linear: d_S = NULL, scale = 1 -> x = u.  Newton: d_S = P_eff, scale = increment -> x = du.
