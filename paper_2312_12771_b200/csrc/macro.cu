@@ -555,9 +555,15 @@ __device__ __forceinline__ void cg2_publish(cgx::cluster_group& cl, double* slot
   }
 }
 __device__ __forceinline__ double cg2_sum(const double* slots, int j, int G) {
-  double a = 0.0;
-  for (int k = 0; k < G; ++k) a += slots[j * CGC_MAXG + k];
-  return a;
+  // fixed-order pairwise tree over the G partials (G = 8 or 16; unused slots of G = 8 skipped):
+  // the same order in every CTA, 4 dependent adds instead of G
+  const double* s = slots + j * CGC_MAXG;
+  double t[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) t[k] = G > 8 ? s[2 * k] + s[2 * k + 1] : s[k];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) t[k] = t[2 * k] + t[2 * k + 1];
+  return (t[0] + t[1]) + (t[2] + t[3]);
 }
 
 template <bool WIN, int CG2_THR>  // CG2_THR: 256, or 512 for long slices (more rows in flight)
