@@ -767,6 +767,10 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
     // pass -- threads i and i^1 hold the two rows of a node (node-aligned slices), the 2x2 block
     // preconditioner takes the sibling residual by a shuffle: no CTA barrier (same arithmetic)
     double beta = 0.0;
+    // OVL (256-thread CTAs): the direction update p = z + beta p, s = w + beta s runs between the
+    // arrive and the wait of the (z.w) cluster barrier; the 512-thread variant (long, L2-spilled
+    // slices) measured faster with it fused into the x / r pass.  Same arithmetic either way.
+    constexpr bool OVL = CG2_THR == 256;
     auto fused2 = [&](bool first, double* part) {
       double rz = 0.0, rr2 = 0.0;
       for (int base = 0; base < nr; base += CG2_THR) {
@@ -775,7 +779,7 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
         double ri = 0.0;
         if (act) {
           double pi = p[i], si = sv[i];
-          if (!first) {
+          if (!OVL && !first) {
             pi = zf[zown + i] + beta * pi;
             si = w[i] + beta * si;
             p[i] = pi;
@@ -816,19 +820,22 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
       rr = cg2_sum(slotsA, 1, G);
       if (sqrt(rr) <= rtol * bnorm) break;
       v[0] = spmv();
-      cg2_publish<CG2_THR>(cl, slotsB, 1, v, wred);
-      cl.sync();
-      del = cg2_sum(slotsB, 0, G);
       beta = gn / gam;
-      const double den = del - beta * gn / alpha;
-      if (!(den > 0.0)) { status = 6; break; }
-      alpha = gn / den;
-      gam = gn;
-      if (dim != 2)
+      cg2_publish<CG2_THR>(cl, slotsB, 1, v, wred);
+      cl.barrier_arrive();
+      // the direction updates need beta (known) and local rows only: they run while the cluster
+      // barrier of the (z.w) exchange completes
+      if (OVL || dim != 2)
         for (int i = tid; i < nr; i += CG2_THR) {
           p[i] = zf[zown + i] + beta * p[i];
           sv[i] = w[i] + beta * sv[i];
         }
+      cl.barrier_wait();
+      del = cg2_sum(slotsB, 0, G);
+      const double den = del - beta * gn / alpha;
+      if (!(den > 0.0)) { status = 6; break; }
+      alpha = gn / den;
+      gam = gn;
     }
     if (status == 0 && it > max_iter) { status = 5; it = max_iter; }
   }
