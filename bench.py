@@ -300,7 +300,8 @@ def main():
                 steps.append(st)
         t = statistics.median(steps)
         val = wl.n_rve / t
-        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tangents/s", "n_gpus": 0,
+        line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tangents/s", "n_gpus": world,
+                "device": "host CPU (the oracle on rank 0; other ranks idle)",
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
                 "cpu_baseline": {"value": val, "unit": "tangents/s", "cores": detail["cores"], "kind": "oracle",
