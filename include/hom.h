@@ -258,8 +258,15 @@ int hom_newton_update(hom_ctx* ctx, double* d_u, const double* d_du, void* strea
 int hom_set_fluctuations(hom_ctx* ctx, const double* d_w, void* stream);
 int hom_get_fluctuations(hom_ctx* ctx, double* d_w, void* stream);
 
-/* max_b ||r_f,b||_2 of the last finite-strain hom_condense (R_micro); synchronises. */
+/* max_b ||r_f,b||_2 / |Omega| of the last finite-strain hom_condense: the micro residual R_micro of
+ * eq:constSolution2 / P:313-315, which carries the 1/|Omega| of eq:discreteSys_L (with the
+ * Dirac basis the macro integral reduces to the value at the Gauss point by the shifting property,
+ * P:248-250), i.e. the RVE-averaged residual (R21).  Synchronises. */
 int hom_micro_residual_max(hom_ctx* ctx, double* out, void* stream);
+
+/* Macro-only update d_u += d_du [n_macro_dof] (the q <- q + dq of P:342 without the fluctuation
+ * update; used by the classical staggered scheme's no-predictor variant).  Enqueue only. */
+int hom_macro_update(hom_ctx* ctx, double* d_u, const double* d_du, void* stream);
 
 /* Replace the phase field and/or material table (same shapes and per_rve flags as at
  * setup) from HOST memory (pinned recommended) with asynchronous copies on `stream`;

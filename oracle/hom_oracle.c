@@ -190,24 +190,19 @@ int orc_linear_C(int dim, double E, double nu, double* C) {
  *   A = dP/dF,  both row-major (i,J).  beta = 0 is the config-5 reading R11. */
 int orc_mr_material(const double* F, double alpha, double beta, double kappa, double* psi, double* P,
                     double* A) {
-  /* J - 1 from the displacement gradient F - I (no cancellation near the reference) */
-  double Jm1 = (F[0] - 1.0) + (F[3] - 1.0) + (F[0] - 1.0) * (F[3] - 1.0) - F[1] * F[2];
-  double J = 1.0 + Jm1;
+  double J = F[0] * F[3] - F[1] * F[2];
   if (!(J > 0.0)) return ORC_ERR_JACOBIAN;
   /* cofactor H = dJ/dF, 2-D specialisation of (1/2) F xx F */
   double H[4] = {F[3], -F[2], -F[1], F[0]};
   double FF = F[0] * F[0] + F[1] * F[1] + F[2] * F[2] + F[3] * F[3];
   if (psi)
-    *psi = alpha * (FF - 2.0) + beta * (FF + J * J - 3.0) + 0.5 * kappa * Jm1 * Jm1 -
-           2.0 * (alpha + 2.0 * beta) * log1p(Jm1);
-  /* dPsi/dJ of the J-dependent terms: 2 beta J + kappa (J-1) - 2 (alpha + 2 beta)/J */
-  double s = 2.0 * beta * J + kappa * Jm1 - 2.0 * (alpha + 2.0 * beta) / J;
-  /* P = 2 (alpha + beta) F + s H, evaluated as 2 (alpha + beta) (F - H) + (s + 2 (alpha + beta)) H
-   * with s + 2 (alpha + beta) = (J - 1) (2 beta + kappa + 2 (alpha + 2 beta) / J) (same value; both
-   * terms vanish at F = I instead of cancelling) */
-  double c1 = Jm1 * (2.0 * beta + kappa + 2.0 * (alpha + 2.0 * beta) / J);
-  double FmH[4] = {F[0] - F[3], F[1] + F[2], F[2] + F[1], F[3] - F[0]};
-  for (int i = 0; i < 4; ++i) P[i] = 2.0 * (alpha + beta) * FmH[i] + c1 * H[i];
+    *psi = alpha * (FF - 2.0) + beta * (FF + J * J - 3.0) + 0.5 * kappa * (J - 1.0) * (J - 1.0) -
+           2.0 * (alpha + 2.0 * beta) * log(J);
+  /* s = dPsi/dJ of the J-dependent terms: 2 beta J + kappa (J-1) - 2 (alpha + 2 beta)/J */
+  double s = 2.0 * beta * J + kappa * (J - 1.0) - 2.0 * (alpha + 2.0 * beta) / J;
+  /* P = dPsi/dF = 2 alpha F + 2 beta F + s H, term by term as differentiated above (plain form;
+   * at F = I the terms cancel to round-off, which the parity tests allow for, R23) */
+  for (int i = 0; i < 4; ++i) P[i] = 2.0 * alpha * F[i] + 2.0 * beta * F[i] + s * H[i];
   if (A) {
     double t = 2.0 * beta + kappa + 2.0 * (alpha + 2.0 * beta) / (J * J); /* d2Psi/dJ2 */
     /* dH/dF: H11=F22, H12=-F21, H21=-F12, H22=F11 */

@@ -341,7 +341,9 @@ def newton_step_nh(wl, u, w, x_dir, nthreads: int | None = None, load_factor: fl
     R = macro_residual(dim, nel, c["P_avg"], wl.body, kind=1, mesh=mesh, fext=fext)
     free = np.ones(len(u), bool)
     free[wl.dir_dof] = False
-    info = {"R_norm": float(np.linalg.norm(R[free])), "rf_max": float(c["rf_norm"].max()), "cond": c}
+    # R_micro per RVE = r_f / |Omega| (eq:constSolution2 with the Dirac shifting property, P:248-250,
+    # P:305-315; R21), |Omega| = L^2
+    info = {"R_norm": float(np.linalg.norm(R[free])), "rf_max": float(c["rf_norm"].max()) / L ** 2, "cond": c}
     du = macro_solve(dim, nel, c["A_eff"], wl.dir_dof, x_dir, S=c["P_eff"], body=wl.body, kind=1, mesh=mesh,
                      fext=fext)
     dF = macro_kin(dim, nel, du, kind=1, mesh=mesh)
@@ -392,13 +394,6 @@ def newton_nh(wl, tol: float = 1e-11, max_iter: int = 25, steps=None, nthreads: 
     return out
 
 
-def _inner_done(inner, micro_tol):
-    """Inner RVE Newton converged: max ||r_f|| < micro_tol, or the round-off floor of the r_f sums
-    reached after quadratic convergence (below 1e-9, no longer halving) -- DESIGN.md reading R21."""
-    rf = inner[-1]
-    return rf < micro_tol or (len(inner) >= 2 and rf < 1e-9 and rf > 0.5 * inner[-2])
-
-
 def newton_classical(wl, tol: float = 1e-9, micro_tol: float = 1e-13, max_iter: int = 25, max_inner: int = 30,
                      steps=None, nthreads: int | None = None, divergence: float = 1e10):
     """Classical staggered FE^2: per macro iteration, equilibrate every RVE at the
@@ -423,9 +418,9 @@ def newton_classical(wl, tol: float = 1e-9, micro_tol: float = 1e-13, max_iter: 
             try:
                 for _ in range(max_inner + 1):
                     c = condense_batch_nh(r, wl.phase, wl.mat, Fbar, w, nthreads=nthreads, L=L)
-                    rf = float(c["rf_norm"].max())
+                    rf = float(c["rf_norm"].max()) / L ** 2  # max_b ||R_micro,b|| (R21)
                     inner.append(rf)
-                    if _inner_done(inner, micro_tol) or not (rf <= divergence):
+                    if rf < micro_tol or not (rf <= divergence):
                         break
                     w = w + c["Z"]
             except OracleError as e:
@@ -436,7 +431,7 @@ def newton_classical(wl, tol: float = 1e-9, micro_tol: float = 1e-13, max_iter: 
             R = macro_residual(dim, nel, c["P_avg"], wl.body, kind=1, mesh=mesh, fext=fext)
             rn = float(np.linalg.norm(R[free]))
             hist.append((rn, inner))
-            if not _inner_done(inner, micro_tol):
+            if not inner[-1] < micro_tol:  # inner loop exhausted max_inner
                 break
             if it > 0 and rn <= tol:
                 converged = True

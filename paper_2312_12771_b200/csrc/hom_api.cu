@@ -980,8 +980,18 @@ int hom_micro_residual_max(hom_ctx* c, double* out, void* stream) {
   if (!c || !out) return set_err(c, HOM_ERR_INVALID_ARG, "hom_micro_residual_max: NULL");
   cudaStream_t s = (cudaStream_t)stream;
   run(c, HOM_PROF_OTHER, s, [&] { hom::launch_max_reduce(c->rfn + c->b_lo, c->b_hi - c->b_lo, c->scal + 1, s); });
-  cudaMemcpyAsync(out, c->scal + 1, sizeof(double), cudaMemcpyDeviceToHost, s);
-  return check_cuda(c, cudaStreamSynchronize(s), "hom_micro_residual_max");
+  double v = 0.0;
+  cudaMemcpyAsync(&v, c->scal + 1, sizeof(double), cudaMemcpyDeviceToHost, s);
+  int rc = check_cuda(c, cudaStreamSynchronize(s), "hom_micro_residual_max");
+  *out = v / c->R.vol;  // R_micro of eq:constSolution2 carries 1/|Omega| (R21)
+  return rc;
+}
+
+int hom_macro_update(hom_ctx* c, double* d_u, const double* d_du, void* stream) {
+  if (!c || !d_u || !d_du) return set_err(c, HOM_ERR_INVALID_ARG, "hom_macro_update: NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  run(c, HOM_PROF_OTHER, s, [&] { hom::launch_axpy(d_u, d_du, 1.0, c->M.ndof, s); });
+  return check_cuda(c, cudaGetLastError(), "hom_macro_update");
 }
 
 int hom_set_phases(hom_ctx* c, const uint8_t* h_phase, const double* h_params, void* stream) {

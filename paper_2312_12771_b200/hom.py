@@ -24,7 +24,7 @@ STATUS = {0: "HOM_OK", 1: "HOM_ERR_INVALID_ARG", 2: "HOM_ERR_MESH", 3: "HOM_ERR_
 
 # every symbol include/hom.h declares (checked by tests/test_abi.py)
 EXPORTS = ["hom_setup", "hom_get_sizes", "hom_get_work", "hom_debug_rve_kff", "hom_set_load_factor", "hom_macro_assemble", "hom_macro_spmv", "hom_macro_kinematics", "hom_condense", "hom_macro_solve",
-           "hom_macro_residual_norm", "hom_recover_fluctuations", "hom_newton_update", "hom_set_fluctuations",
+           "hom_macro_residual_norm", "hom_recover_fluctuations", "hom_newton_update", "hom_macro_update", "hom_set_fluctuations",
            "hom_get_fluctuations", "hom_micro_residual_max", "hom_set_phases", "hom_launch_count",
            "hom_profile_enable", "hom_profile_read", "hom_last_error", "hom_destroy"]
 PROF_CLASSES = ["rve_assemble", "condense", "macro_assemble", "cg", "recover", "other"]
@@ -119,6 +119,7 @@ def lib(build_if_missing: bool = True):
         L.hom_debug_rve_kff.argtypes = [P, I, P, P]
         L.hom_recover_fluctuations.argtypes = [P, P, P, P]
         L.hom_newton_update.argtypes = [P, P, P, P]
+        L.hom_macro_update.argtypes = [P, P, P, P]
         L.hom_set_fluctuations.argtypes = [P, P, P]
         L.hom_get_fluctuations.argtypes = [P, P, P]
         L.hom_micro_residual_max.argtypes = [P, ctypes.POINTER(ctypes.c_double), P]
@@ -138,16 +139,6 @@ def lib(build_if_missing: bool = True):
 
 def _np_ptr(a):
     return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
-
-
-def _inner_done(inner, micro_tol):
-    """Classical-scheme inner RVE Newton converged (reading R21): max ||r_f|| < micro_tol,
-    or quadratic convergence has reached the round-off floor of the r_f sums (below 1e-9 and no
-    longer halving) -- the paper's 1e-13 is below that floor at Cook's stress levels."""
-    rf = inner[-1]
-    if rf < micro_tol:
-        return True
-    return len(inner) >= 2 and rf < 1e-9 and rf > 0.5 * inner[-2]
 
 
 class Homogenizer:
@@ -315,6 +306,9 @@ class Homogenizer:
         self._check(lib().hom_newton_update(self.h, self._ptr(u), self._ptr(du), self._stream()),
                     "hom_newton_update")
 
+    def macro_update(self, u, du):
+        self._check(lib().hom_macro_update(self.h, self._ptr(u), self._ptr(du), self._stream()), "hom_macro_update")
+
     def set_fluctuations(self, w):
         self._check(lib().hom_set_fluctuations(self.h, self._ptr(w), self._stream()), "hom_set_fluctuations")
 
@@ -370,17 +364,18 @@ class Homogenizer:
         return C, u, w, info
 
     def newton(self, n_steps, tol=1e-11, max_iter=25, history=None, force_load=False, micro_tol=None,
-               divergence=1e10, raise_on_fail=True):
+               divergence=1e10, raise_on_fail=True, on_step=None):
         """Finite-strain load stepping with the monolithic null-space Newton (generalized scheme,
         P:325-342, P:398-428).
 
         Per iteration: F = I + grad u; condense -> (A_eff, P_eff, <P>); check ||R_macro|| (with <P>)
-        and max ||r_f|| (reading R3; micro_tol=None uses tol, micro_tol=inf checks the macro
+        and max ||r_f|| / |Omega| (reading R3; micro_tol=None uses tol, micro_tol=inf checks the macro
         residual only, as the paper's Cook study); solve the condensed system for du
         (eq:solution2); update u and w.  Load steps: the Dirichlet values (default) or,
         with force_load, the external load factor k/n_steps (T_k = k T / n_l).  Failure:
         ||R_macro|| > divergence, a micro J <= 0, or max_iter.  Returns u (device) and the
-        per-step residual histories [(||R_macro||, max ||r_f||), ...]."""
+        per-step residual histories [(||R_macro||, max ||r_f||), ...]; on_step(k, u) is called after
+        every converged load step k (u on the device)."""
         u = self.torch.zeros(self.n_dof, dtype=self.torch.float64, device="cuda")
         du = self.empty(self.n_dof)
         mtol = tol if micro_tol is None else micro_tol
@@ -413,6 +408,8 @@ class Homogenizer:
             hist_all.append(hist)
             if history is not None:
                 history.append(hist)
+            if on_step is not None and converged:
+                on_step(k, u)
             if not converged:
                 if raise_on_fail:
                     raise HomError(5, None, f"Newton did not converge in load step {k}: {hist[-1]}")
@@ -423,7 +420,8 @@ class Homogenizer:
                          force_load=True, predictor=True):
         """Classical staggered FE^2 scheme for comparison with the generalized one:
         every macro iteration first equilibrates all RVEs at the fixed macro deformation
-        (batched inner Newton on R_micro: w <- w - K_ff^-1 r_f until max ||r_f|| < micro_tol),
+        (batched inner Newton on R_micro: w <- w - K_ff^-1 r_f until max ||r_f|| / |Omega| < micro_tol,
+        the paper's 1e-13; R_micro normalisation: DESIGN.md R21),
         then solves [K - D L^-1 E] dq = -R_macro (eq:solution1, no -D L^-1 R_micro term),
         updates q and w with eq:reduction (dw = -L^-1 E dq) and restarts until
         ||R_macro|| < tol; failure if ||R_macro|| > divergence, J <= 0 or no convergence.
@@ -445,7 +443,7 @@ class Homogenizer:
                         A, Pe, Pa = self.condense(F)
                         rf = self.micro_residual_max()
                         inner.append(rf)
-                        if _inner_done(inner, micro_tol) or not (rf <= divergence):
+                        if rf < micro_tol or not (rf <= divergence):
                             break
                         self.newton_update(u, zero)  # w -= K_ff^-1 r_f at fixed F
                 except HomError as e:
@@ -455,7 +453,7 @@ class Homogenizer:
                     break
                 rn = self.macro_residual_norm(Pa)
                 hist.append((rn, inner))
-                if not _inner_done(inner, micro_tol):
+                if not inner[-1] < micro_tol:
                     break
                 if it > 0 and rn <= tol:
                     converged = True
@@ -466,7 +464,7 @@ class Homogenizer:
                 if predictor:
                     self.newton_update(u, du)  # q += dq; w += -L^-1 E dq (r_f ~ 0 after the inner loop)
                 else:  # variant without the eq:reduction predictor: q += dq only
-                    u.add_(du)
+                    self.macro_update(u, du)
             hist_all.append(hist)
             if not converged:
                 return u, hist_all, False

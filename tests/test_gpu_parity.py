@@ -39,10 +39,20 @@ def gpu_linear(wl, **kw):
     return out
 
 
+def rel_max(a, b):
+    """Largest per-RVE relative Frobenius error max_b ||a_b - b_b|| / ||b_b|| (rows = RVEs), so that
+    a soft RVE's error cannot hide under a stiff one's norm."""
+    a = np.asarray(a, dtype=np.float64).reshape(len(a), -1)
+    b = np.asarray(b, dtype=np.float64).reshape(len(b), -1)
+    nb = np.linalg.norm(b, axis=1)
+    return float(np.max(np.linalg.norm(a - b, axis=1) / np.where(nb > 0, nb, 1.0)))
+
+
 def check_linear_against_oracle(wl, **kw):
     g = gpu_linear(wl, **kw)
     o = oracle.solve_linear(wl)
     assert rel(g["C"], o["C_eff"]) <= TOL_C, rel(g["C"], o["C_eff"])
+    assert rel_max(g["C"], o["C_eff"]) <= TOL_C, rel_max(g["C"], o["C_eff"])
     assert rel(g["u"], o["u"]) <= TOL_U, rel(g["u"], o["u"])
     w_o = oracle.recover_linear(o["W"], o["eps"])
     assert rel(g["w"], w_o) <= TOL_U, rel(g["w"], w_o)
@@ -140,29 +150,20 @@ def test_config3_reduced_macro_full_rve(torch_cuda):
     check_linear_against_oracle(W.config3(nel=4))
 
 
-def test_config3_full_size_sampled(torch_cuda):
-    """Full config 3 (16384 RVEs, launch configuration of the bench's chunked path): C_eff of
-    sampled RVEs against the oracle, and the macro solution checked by the oracle's residual."""
+def test_config3_full_size_all_rves(torch_cuda):
+    """Full config 3 (16384 RVEs of 32x32, every RVE different; the bench's chunked launch
+    configuration) against the oracle's own answers: every RVE's C_eff (batch Frobenius and per-RVE
+    max relative error <= 1e-10), the oracle's own macro solution u (its C_eff, direct solve) <= 1e-8,
+    and every RVE's recovered fluctuation field <= 1e-8."""
     wl = W.config3()
     g = gpu_linear(wl)
-    rng = np.random.default_rng(0)
-    ids = np.sort(rng.choice(wl.n_rve, 24, replace=False))
-    ids = np.unique(np.concatenate([ids, [0, wl.n_rve - 1]]))
-    o = oracle.solve_linear(wl, rve_ids=ids)
-    assert rel(g["C"][ids], o["C_eff_subset"]) <= TOL_C
-    # macro equilibrium with the GPU tangents (property valid at any size)
-    eps = oracle.macro_kin(2, wl.nel, g["u"])
-    S = np.einsum("bij,bj->bi", g["C"], eps)
-    R = oracle.macro_residual(2, wl.nel, S, wl.body)
-    free = np.ones(wl.n_dof, bool)
-    free[wl.dir_dof] = False
-    f = -oracle.macro_residual(2, wl.nel, None, wl.body)
-    assert np.linalg.norm(R[free]) <= 1e-10 * np.linalg.norm(f[free])
-    # the oracle's direct macro solve with the GPU tangents: the CG solution to 1e-8
-    u_direct = oracle.macro_solve(2, wl.nel, g["C"], wl.dir_dof, wl.dir_val, body=wl.body)
-    assert rel(g["u"], u_direct) <= TOL_U
-    w_o = oracle.recover_linear(o["W_subset"], eps[ids])
-    assert rel(g["w"][ids], w_o) <= TOL_U
+    o = oracle.solve_linear(wl)
+    assert rel(g["C"], o["C_eff"]) <= TOL_C, rel(g["C"], o["C_eff"])
+    assert rel_max(g["C"], o["C_eff"]) <= TOL_C, rel_max(g["C"], o["C_eff"])
+    assert rel(g["u"], o["u"]) <= TOL_U, rel(g["u"], o["u"])
+    w_o = oracle.recover_linear(o["W"], o["eps"])
+    assert rel(g["w"], w_o) <= TOL_U, rel(g["w"], w_o)
+    assert rel_max(g["w"], w_o) <= TOL_U, rel_max(g["w"], w_o)
 
 
 def test_chunking_is_bitwise_invariant(torch_cuda):
@@ -262,6 +263,29 @@ def test_config5_newton_load_steps(torch_cuda):
         for i in range(1, len(r) - 1):
             if r[i] < 1e-2 * r[0] and r[i + 1] > 1e-13:
                 assert np.log(r[i + 1]) / np.log(r[i]) >= 1.7 or r[i + 1] < 1e-12
+
+
+def test_config5_full_size_newton_all_load_steps(torch_cuda):
+    """Full config 5 (32x32 macro, 4096 RVEs of 16x16, 10 load steps to a stretch of 1.1, reading
+    R10): the GPU's monolithic Newton (eq:solution2 + P:424-427, load stepping P:613-617) against the
+    oracle's, both to the parity tolerance 1e-11 (R3/R13): converged u after EVERY load step <= 1e-8,
+    the final fluctuation state <= 1e-8 (batch and per RVE), and the same Newton iteration counts."""
+    import torch
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = W.config5()
+    o = oracle.newton_nh(wl, tol=1e-11)
+    assert len(o) == wl.n_steps and all(s["converged"] for s in o)
+    h = Homogenizer.from_workload(wl)
+    us = {}
+    _, hist = h.newton(wl.n_steps, tol=1e-11, on_step=lambda k, u: us.__setitem__(k, u.cpu().numpy()))
+    assert sorted(us) == list(range(1, wl.n_steps + 1))
+    for k in range(1, wl.n_steps + 1):
+        assert rel(us[k], o[k - 1]["u"]) <= TOL_U, (k, rel(us[k], o[k - 1]["u"]))
+    w = h.get_fluctuations().cpu().numpy()
+    assert rel(w, o[-1]["w"]) <= TOL_U and rel_max(w, o[-1]["w"]) <= TOL_U
+    its_g = [len(s) for s in hist]
+    its_o = [len(s["history"]) for s in o]
+    assert its_g == its_o, (its_g, its_o)
 
 
 # ------------------------------------------------------------------ failure reporting
@@ -623,10 +647,11 @@ def test_cook_generalized_newton_matches_oracle(torch_cuda):
 def test_cook_classical_newton_matches_oracle(torch_cuda):
     from paper_2312_12771_b200.hom import Homogenizer
     wl = _cook_small(n_steps=3)
-    o = oracle.newton_classical(wl, tol=1e-9, micro_tol=1e-11)
+    # the paper's criteria: inner RVE Newton to 1e-13 (R_micro = r_f / |Omega|, R21), macro 1e-9
+    o = oracle.newton_classical(wl, tol=1e-9, micro_tol=1e-13)
     assert all(s["converged"] for s in o)
     h = Homogenizer.from_workload(wl, tile_sparse=True)
-    u, hist, ok = h.newton_classical(wl.n_steps, tol=1e-9, micro_tol=1e-11)
+    u, hist, ok = h.newton_classical(wl.n_steps, tol=1e-9, micro_tol=1e-13)
     assert ok
     assert rel(u.cpu().numpy(), o[-1]["u"]) <= TOL_U
     assert [len(s) for s in hist] == [len(s["history"]) for s in o]
@@ -647,7 +672,34 @@ def test_cook_table1_generalized_iteration_counts(torch_cuda):
         _, hist = h.newton(n_l, tol=1e-9, micro_tol=float("inf"), max_iter=30, force_load=True)
         assert [len(s) - 1 for s in hist] == [want[n_l]] * n_l
         r = [x[0] for x in hist[0]]
-        assert r[-1] <= 1e-9 and r[-2] <= 1e-2 and r[-2] ** 1.7 >= r[-1]  # quadratic tail
+        # quadratic decay (the SPEC's reading of Table 2): once r_i < 1e-2 r_0,
+        # log r_{i+1} / log r_i >= 1.7
+        assert r[-1] <= 1e-9
+        tail = [i for i in range(1, len(r) - 1) if r[i] < 1e-2 * r[0]]
+        assert tail, r
+        for i in tail:
+            assert np.log(r[i + 1]) / np.log(r[i]) >= 1.7, r
+
+
+def test_cook_table1_classical_iteration_counts(torch_cuda):
+    """PAPER.md Table 1 classical column where the paper's scheme converges: 4 macro
+    iterations per load step at n_l = 22, with the paper's criteria (inner RVE Newton to 1e-13 on
+    R_micro = r_f / |Omega|, reading R21; macro 1e-9), and every inner loop within the 8
+    iterations of S:417 (Table 2 shows <= 7).  The paper's failures at n_l = 2 and 12 are not
+    reproduced."""
+    import json
+    import os
+    from paper_2312_12771_b200.hom import Homogenizer
+    gold = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "table1_newton.json")))
+    want = dict(zip(gold["n_l"], gold["classical_iterations"]))[22]
+    wl = W.cook(n_steps=22)
+    h = Homogenizer.from_workload(wl, tile_sparse=True)
+    _, hist, ok = h.newton_classical(22, tol=1e-9, micro_tol=1e-13, max_iter=30, max_inner=30)
+    assert ok
+    assert [len(s) - 1 for s in hist] == [want] * 22
+    for s in hist:
+        for rn, inner in s:
+            assert inner[-1] < 1e-13 and len(inner) <= 8, inner
 
 
 def test_cook_classical_and_generalized_reach_the_same_state(torch_cuda):

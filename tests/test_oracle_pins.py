@@ -347,6 +347,90 @@ def test_macro_solution_satisfies_equilibrium():
     assert abs(u @ internal - f @ u) < 1e-12 * abs(f @ u)
 
 
+def _cook_boundary_loop(nel):
+    """Counter-clockwise boundary node loop of the mapped nel x nel grid (x fastest numbering)."""
+    idx = lambda i, j: j * (nel + 1) + i  # noqa: E731
+    loop = [idx(i, 0) for i in range(nel)] + [idx(nel, j) for j in range(nel)]
+    loop += [idx(i, nel) for i in range(nel, 0, -1)] + [idx(0, j) for j in range(nel, 0, -1)]
+    return loop
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_mapped_mesh_macro_patch_test_cook_trapezoid(kind):
+    """Pins orc_mesh_macro_kin / _residual / _solve on the distorted Cook trapezoid (eq:refcon,
+    P:544-552): (1) an affine field u = A X + b has the constant gradient A at every macro qp;
+    (2) a constant stress S gives the internal force int grad N_A . S dV = sum over the boundary
+    edges of N_A S n ds (divergence theorem; 2x2 Gauss is exact for bilinear maps), i.e. zero at
+    interior nodes and (len/2) S n per adjacent edge at boundary nodes, computed here from the
+    edge geometry alone; (3) the patch test: with a constant isotropic tangent and the affine field
+    prescribed on every boundary node, the direct solve reproduces it at the interior nodes."""
+    nel = 5
+    X, conn = W.cook(nel=nel, r=2, n_steps=1).macro_mesh()
+    rng = np.random.default_rng(3 + kind)
+    A = 1e-2 * rng.standard_normal((2, 2))
+    b = rng.standard_normal(2)
+    u = (X @ A.T + b).reshape(-1)
+    kin = oracle.macro_kin(2, nel, u, kind=kind, mesh=(X, conn))
+    want = np.array([A[0, 0], A[1, 1], A[0, 1] + A[1, 0]]) if kind == 0 else A.reshape(4)
+    np.testing.assert_allclose(kin, np.broadcast_to(want, kin.shape), rtol=0, atol=1e-15)
+    # (2) constant stress -> boundary tractions
+    Sm = rng.standard_normal((2, 2))
+    if kind == 0:
+        Sm = 0.5 * (Sm + Sm.T)
+        Sv = np.array([Sm[0, 0], Sm[1, 1], Sm[0, 1]])
+    else:
+        Sv = Sm.reshape(4)
+    nq = conn.shape[0] * 4
+    R = oracle.macro_residual(2, nel, np.tile(Sv, (nq, 1)), None, kind=kind, mesh=(X, conn))
+    expect = np.zeros_like(R)
+    loop = _cook_boundary_loop(nel)
+    for p, q in zip(loop, loop[1:] + loop[:1]):
+        t = X[q] - X[p]
+        nlen = np.array([t[1], -t[0]])  # outward normal x edge length (CCW loop)
+        f = 0.5 * Sm @ nlen
+        expect[2 * p:2 * p + 2] += f
+        expect[2 * q:2 * q + 2] += f
+    np.testing.assert_allclose(R, expect, rtol=0, atol=1e-12 * np.abs(expect).max())
+    # (3) patch test
+    E, nu = 2.5, 0.3
+    if kind == 0:
+        lam, mu = E * nu / ((1 + nu) * (1 - 2 * nu)), E / (2 * (1 + nu))
+        D = np.array([[lam + 2 * mu, lam, 0], [lam, lam + 2 * mu, 0], [0, 0, mu]])
+    else:
+        D = bf.iso_tangent_full(2, E, nu)
+    bnd = np.array(loop)
+    dd = np.sort(np.concatenate([2 * bnd, 2 * bnd + 1])).astype(np.int32)
+    x = oracle.macro_solve(2, nel, np.tile(D, (nq, 1, 1)), dd, u[dd], kind=kind, mesh=(X, conn))
+    np.testing.assert_allclose(x, u, rtol=0, atol=1e-12 * np.abs(u).max())
+
+
+@pytest.mark.parametrize("dim,nel", [(2, 3), (3, 2)])
+def test_mesh_macro_routines_equal_structured_on_uniform_grid(dim, nel):
+    """The explicit-mesh branch (grid_elem with conn, orc_mesh_macro_*) on the uniform grid passed as an
+    explicit mesh equals the structured-grid routines (orc_macro_*): kinematics, residual, solve."""
+    X, conn = W.grid_mesh(dim, nel)
+    rng = np.random.default_rng(dim)
+    m = 3 if dim == 2 else 6
+    nq = conn.shape[0] * 2 ** dim
+    u = rng.standard_normal(X.shape[0] * dim)
+    for kind in ((0, 1) if dim == 2 else (0,)):
+        mk = m if kind == 0 else dim * dim
+        np.testing.assert_allclose(oracle.macro_kin(dim, nel, u, kind=kind, mesh=(X, conn)),
+                                   oracle.macro_kin(dim, nel, u, kind=kind), rtol=0, atol=1e-13)
+        S = rng.standard_normal((nq, mk))
+        body = rng.standard_normal(dim)
+        np.testing.assert_allclose(oracle.macro_residual(dim, nel, S, body, kind=kind, mesh=(X, conn)),
+                                   oracle.macro_residual(dim, nel, S, body, kind=kind), rtol=0, atol=1e-13)
+        G = rng.standard_normal((nq, mk, mk))
+        D = np.einsum("qij,qkj->qik", G, G) + mk * np.eye(mk)
+        left = W.face_nodes(dim, nel, 0, 0)
+        dd = np.sort(np.concatenate([dim * left + c for c in range(dim)])).astype(np.int32)
+        xd = rng.standard_normal(len(dd))
+        a = oracle.macro_solve(dim, nel, D, dd, xd, S=S, body=body, kind=kind, mesh=(X, conn))
+        b = oracle.macro_solve(dim, nel, D, dd, xd, S=S, body=body, kind=kind)
+        np.testing.assert_allclose(a, b, rtol=1e-12, atol=1e-12 * np.abs(b).max())
+
+
 # ---------------------------------------------------------------- 1-D benchmark (a)
 def _bench1d(k):
     g = json.load(open(os.path.join(GOLD, "bench1d.json")))
