@@ -7,8 +7,13 @@ Schur epilogue, all RVEs), hom_macro_solve (K5 assembly + K6/K7 PCG) and
 hom_recover_fluctuations (K8).  For config 5 a step is one monolithic Newton
 iteration (kinematics, condensation, residual norms, macro solve, update).
 
-Default workload: BASELINE.json configs[1] (config 2: 32x32 macro Q1, 4096 RVEs
-of 16x16 Q1 with a centred disc).  Prints ONE JSON line on rank 0.
+Default workload: BASELINE.json configs[2] (config 3: 64x64 macro Q1, 16384 RVEs of
+32x32 Q1 with per-RVE random phases and moduli) -- the largest configuration that fits one
+GPU, which is the headline when BASELINE's metric names no configuration; dense blocked
+factorisation through the chunked path (six passes of <= 2774 RVEs over a 48 GB K_ff pool).
+Companion keys: config 2 and config 5 (the configs whose k_condense sits furthest below
+the FP64 roofline), the tile-sparse factorisation of the same workload, and the K6 SpMV
+roofline on a scaled macro mesh.  Prints ONE JSON line on rank 0.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
@@ -50,6 +55,28 @@ def fp64_peak():
     if "fp64_dmma_tflops_microbench" in f:
         return float(f["fp64_dmma_tflops_microbench"]), "MEASURED_FP64.json (DMMA microbenchmark, this pool's B200)"
     return FP64_PEAK_TFLOPS, "measured DMMA microbenchmark (profiles/r01_fp64_peaks.txt)"
+
+
+def dgemm_live_tflops(n: int = 8192, reps: int = 10):
+    """cuBLAS DGEMM n^3 on this GPU in this run (best of `reps`, CUDA events): the second FP64
+    denominator next to the DMMA microbenchmark peak."""
+    import torch
+    a = torch.rand(n, n, dtype=torch.float64, device="cuda")
+    b = torch.rand(n, n, dtype=torch.float64, device="cuda")
+    c = torch.empty_like(a)
+    for _ in range(2):
+        torch.matmul(a, b, out=c)
+    best = float("inf")
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b, out=c)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b, c
+    torch.cuda.empty_cache()
+    return 2.0 * n ** 3 / (best * 1e-3) / 1e12
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -157,6 +184,28 @@ def oracle_step_time(wl, target_s: float = 10.0):
     return step, detail
 
 
+def oracle_full_steps(wl, steps: int, budget_s: float = 150.0):
+    """The reference arm: full oracle steps (every RVE condensed, direct macro solve, recovery of
+    every RVE), as it stands, on all host threads; stops early once `budget_s` is spent (at least one
+    full step).  Returns (list of per-step seconds, cores)."""
+    import numpy as np
+
+    import oracle
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        if wl.kind == "linear":
+            o = oracle.solve_linear(wl)
+            oracle.recover_linear(o["W"], o["eps"])
+        else:  # one monolithic Newton iteration at the reference state (the per-iteration work)
+            oracle.newton_step_nh(wl, np.zeros(wl.n_dof), np.zeros((wl.n_rve, wl.n_pad)),
+                                  wl.dir_val / wl.n_steps)
+        times.append(time.perf_counter() - t0)
+        if sum(times) > budget_s:
+            break
+    return times, oracle.default_threads()
+
+
 def cpu_model():
     try:
         for ln in open("/proc/cpuinfo"):
@@ -253,15 +302,75 @@ def tile_sparse_line(wl, C_dense, steps: int, warmup: int, ordering="folded"):
     return out
 
 
+# ----------------------------------------------------------------------------- companion configs
+def companion_line(cfg: int, steps: int, warmup: int):
+    """Config `cfg` on its own context in the same run: tangents/s of the step and the k_condense
+    roofline (dense algorithmic flops / the kernel's CUDA-event time)."""
+    import torch
+
+    from paper_2312_12771_b200 import workloads as W
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = W.make(cfg)
+    h = Homogenizer.from_workload(wl)
+    B, m = h.n_rve, h.m
+    C, u, w = h.empty(B, m, m), h.empty(h.n_dof), h.empty(B, h.n_pad)
+    if h.finite:
+        F, Pe, Pa, du = h.empty(B, m), h.empty(B, m), h.empty(B, m), h.empty(h.n_dof)
+        u0, _ = h.newton(1, tol=1e-9)  # a mid-load state
+        u.copy_(u0)
+
+    def step():
+        if h.finite:
+            h.macro_kinematics(u, F)
+            h.condense(F, C, Pe, Pa)
+            h.macro_residual_norm(Pa)
+            h.micro_residual_max()
+            h.macro_solve(C, Pe, scale=0.0, x=du)
+            h.newton_update(u, du)
+        else:
+            h.condense(None, C)
+            h.macro_solve(C, None, 1.0, u)
+            h.recover(u, w)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    h.profile(True)
+    stream = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    prof = h.profile_read()
+    h.profile(False)
+    cond_ms = prof["condense"][0]
+    achieved = wl.flop_per_rve() * B * steps / (cond_ms * 1e-3) / 1e12
+    peak, _ = fp64_peak()
+    out = {"workload": f"{wl.name}: {wl.description}", "step": "one Newton iteration" if h.finite else
+           "condense + macro solve + recovery", "value": B * steps / (ms * 1e-3), "unit": "tangents/s",
+           "ms_per_step": ms / steps, "condense_ms_per_step": cond_ms / steps,
+           "roofline": {"bound": "tensor", "kernel": "k_condense", "achieved": achieved, "peak": peak,
+                        "unit": "TFLOP/s", "frac": achieved / peak,
+                        "algorithmic": f"{wl.flop_per_rve():.4g} flop/RVE x {B} RVEs per step"},
+           "assembly_ms_per_step": prof["rve_assemble"][0] / steps,
+           "macro_solve_ms_per_step": (prof["macro_assemble"][0] + prof["cg"][0]) / steps}
+    h.close()
+    return out
+
+
 # ----------------------------------------------------------------------------- main
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-companions", action="store_true", help="skip the config-2 / config-5 companion keys")
     ap.add_argument("--spmv-nel", type=int, default=2048, help="scaled macro mesh of the K6 SpMV roofline (0: skip)")
     ap.add_argument("--macro-basis", default="dirac", choices=["dirac", "constant"],
                     help="constant: one RVE per macro element (SURVEY §8(f) 2, small strain)")
@@ -292,21 +401,22 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        steps = []
-        detail = None
-        for i in range(args.warmup + args.steps):
-            st, detail = oracle_step_time(wl, target_s=2.0)
-            if i >= args.warmup:
-                steps.append(st)
-        t = statistics.median(steps)
+        times, cores = oracle_full_steps(wl, args.warmup + args.steps)
+        timed = times[min(args.warmup, len(times) - 1):] if len(times) > 1 else times
+        t = statistics.median(timed)
         val = wl.n_rve / t
+        what = ("full steps: every RVE condensed (skyline Cholesky, unit-strain route), direct macro solve, "
+                "recovery of every RVE" if wl.kind == "linear" else
+                "full Newton iterations: every RVE condensed at the reference state, direct macro solve")
+        sample = (f"{len(timed)} timed of {len(times)} run ({args.warmup} warm-up requested, {args.steps} timed "
+                  f"requested; the arm stops after 150 s of oracle work) -- {what}")
         line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "tangents/s", "n_gpus": world,
                 "device": "host CPU (the oracle on rank 0; other ranks idle)",
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+                "steps": len(timed), "steps_requested": args.steps, "warmup": len(times) - len(timed),
+                "ms_per_step": t * 1e3, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": config,
-                "cpu_baseline": {"value": val, "unit": "tangents/s", "cores": detail["cores"], "kind": "oracle",
-                                 "sample": detail["sample"], "cpu": cpu_model(),
-                                 "per_core_value": detail["per_core_tangents_s"]},
+                "cpu_baseline": {"value": val, "unit": "tangents/s", "cores": cores, "kind": "oracle",
+                                 "sample": sample, "cpu": cpu_model()},
                 "e2e": {"value": val, "unit": "tangents/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
         return
@@ -408,8 +518,13 @@ def main():
     value = B * args.steps / (ms * 1e-3)  # B = all RVEs of the (sharded) problem when world > 1
 
     # ---------------- end to end: host inputs (pinned) -> C-ABI -> host results, every step
-    ph_host = torch.from_numpy(np.ascontiguousarray(wl.phase if wl.phase.shape[0] > 1 else wl.phase[0])).pin_memory()
-    mt_host = torch.from_numpy(np.ascontiguousarray(wl.mat if wl.mat.shape[0] > 1 else wl.mat[0])).pin_memory()
+    # the same rows the context was built from (Homogenizer.from_workload: one RVE per element with the
+    # constant basis takes the rows of the element's first Gauss-point RVE)
+    stride = wl.n_qp if args.macro_basis == "constant" else 1
+    ph_rows = wl.phase[::stride] if wl.phase.shape[0] > 1 else wl.phase[0]
+    mt_rows = wl.mat[::stride] if wl.mat.shape[0] > 1 else wl.mat[0]
+    ph_host = torch.from_numpy(np.ascontiguousarray(ph_rows)).pin_memory()
+    mt_host = torch.from_numpy(np.ascontiguousarray(mt_rows)).pin_memory()
     C_host = torch.empty((B, m, m), dtype=torch.float64).pin_memory()
     u_host = torch.empty(h.n_dof, dtype=torch.float64).pin_memory()
     w_host = torch.empty((B, h.n_pad), dtype=torch.float64).pin_memory()
@@ -482,6 +597,7 @@ def main():
     n_local = h.sizes.rve_count  # RVEs this rank condenses per step (all chunks)
     achieved = flop_rve * n_local * args.steps / (cond_ms * 1e-3) / 1e12 if cond_ms > 0 else None
     peak, peak_src = fp64_peak()
+    dgemm = dgemm_live_tflops()
     step_ms_total = sum(v[0] for v in prof.values())
     breakdown = {k: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps,
                      "share": (v[0] / step_ms_total if step_ms_total else None)} for k, v in prof.items()}
@@ -504,6 +620,8 @@ def main():
                      "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                      "peak_source": peak_src,
+                     "peak_dgemm_live": dgemm, "frac_dgemm_live": (achieved / dgemm) if achieved else None,
+                     "peak_dgemm_live_source": "cuBLAS DGEMM 8192^3 (torch.matmul f64), best of 10, this GPU, this run",
                      "algorithmic": f"{algo} x {n_local} RVEs per step ({max(cond_n, 1) // args.steps} launch(es) of "
                                     f"<= {per_launch} RVEs)"},
         "fp64_tflops_condense": achieved,
@@ -522,6 +640,10 @@ def main():
     }
     if world == 1 and not args.tile_sparse and not h.finite and args.macro_basis == "dirac":
         line["tile_sparse"] = tile_sparse_line(wl, C, args.steps, args.warmup, args.rve_ordering)
+    if world == 1 and not args.no_companions and args.config == 3 and not args.tile_sparse:
+        h.close()  # free the 48 GB K_ff pool before the companion contexts
+        torch.cuda.empty_cache()
+        line["companions"] = {f"cfg{c}": companion_line(c, max(args.steps, 20), args.warmup) for c in (2, 5)}
     if world == 1 and args.spmv_nel > 0:
         if m == 3:
             C_tile = C

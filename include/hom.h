@@ -271,8 +271,18 @@ int hom_macro_update(hom_ctx* ctx, double* d_u, const double* d_du, void* stream
 /* Replace the phase field and/or material table (same shapes and per_rve flags as at
  * setup) from HOST memory (pinned recommended) with asynchronous copies on `stream`;
  * either pointer may be NULL to keep the current data.  This is the per-step input
- * of an end-to-end run. */
+ * of an end-to-end run.  Phase ids are validated on the host first (HOM_ERR_INVALID_ARG
+ * if any id >= n_phases; nothing is copied then). */
 int hom_set_phases(hom_ctx* ctx, const uint8_t* h_phase, const double* h_params, void* stream);
+
+/* Constant macro basis (options.macro_basis = 1) only: the per-element volume average <C>_e
+ * [B][m][m] that hom_condense keeps for the macro stiffness (eq:constSolution1/2).
+ * With RVE sharding a context holds only its local rows, so the caller all-gathers them next to
+ * C_eff: get copies the local rows [rve_begin, rve_begin + rve_count) into d_cavg (other rows
+ * untouched), set replaces all B rows from d_cavg.  Enqueue only; HOM_ERR_INVALID_ARG for the
+ * Dirac basis. */
+int hom_get_element_cavg(hom_ctx* ctx, double* d_cavg, void* stream);
+int hom_set_element_cavg(hom_ctx* ctx, const double* d_cavg, void* stream);
 
 /* Kernel launches enqueued by this context since creation (for launch accounting). */
 int64_t hom_launch_count(const hom_ctx* ctx);

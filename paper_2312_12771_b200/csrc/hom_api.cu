@@ -276,6 +276,8 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
     if (!element_tables(dim, x, &mgrad[(size_t)e * nq * nen * dim], &mw[(size_t)e * nq], e == 0 ? shp.data() : nullptr))
       return fail(HOM_ERR_MESH, "macro element with det J <= 0");
   }
+  // shared-element records pack (e << 8 | a << 4 | b) into an int (build_pairs, k_macro_assemble)
+  if (M.ne >= (1 << 23)) return fail(HOM_ERR_INVALID_ARG, "macro mesh too large (>= 2^23 elements)");
   PairTables MP = build_pairs(M.n_nodes, M.ne, nen, mconn);
   // scalar CSR over all DOFs, node-block structure
   std::vector<int> rowptr(M.ndof + 1, 0), col, nzblk;
@@ -715,6 +717,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   M.constant_basis = c->opt.macro_basis == 1;
   if (M.constant_basis) {
     c->Cavg_e = dalloc<double>(c, (size_t)c->B * c->m * c->m, &rc);
+    if (c->Cavg_e) cudaMemsetAsync(c->Cavg_e, 0, sizeof(double) * c->B * c->m * c->m, s);
     M.Cavg_e = c->Cavg_e;
   }
   M.rowptr = upload(c, rowptr, s, &rc);
@@ -997,11 +1000,32 @@ int hom_macro_update(hom_ctx* c, double* d_u, const double* d_du, void* stream) 
 int hom_set_phases(hom_ctx* c, const uint8_t* h_phase, const double* h_params, void* stream) {
   if (!c) return HOM_ERR_INVALID_ARG;
   cudaStream_t s = (cudaStream_t)stream;
-  if (h_phase)
+  if (h_phase) {
+    // K1 indexes the material tables with the id: validate on the host before the copy
+    // (one pass over the bytes; ~2 ms for config 3's 16.8 MB against a ~1.5 s step)
+    uint8_t mx = 0;
+    for (size_t i = 0; i < c->phase_bytes; ++i) mx = h_phase[i] > mx ? h_phase[i] : mx;
+    if (mx >= c->R.n_phase) return set_err(c, HOM_ERR_INVALID_ARG, "hom_set_phases: phase id >= n_phases");
     cudaMemcpyAsync(const_cast<uint8_t*>(c->R.phase), h_phase, c->phase_bytes, cudaMemcpyHostToDevice, s);
+  }
   if (h_params)
     cudaMemcpyAsync(const_cast<double*>(c->R.mat), h_params, c->mat_bytes, cudaMemcpyHostToDevice, s);
   return check_cuda(c, cudaGetLastError(), "hom_set_phases");
+}
+
+int hom_get_element_cavg(hom_ctx* c, double* d_cavg, void* stream) {
+  if (!c || !d_cavg || !c->Cavg_e) return set_err(c, HOM_ERR_INVALID_ARG, "hom_get_element_cavg (constant basis only)");
+  const size_t row = sizeof(double) * c->m * c->m;
+  cudaMemcpyAsync(d_cavg + (size_t)c->b_lo * c->m * c->m, c->Cavg_e + (size_t)c->b_lo * c->m * c->m,
+                  row * (c->b_hi - c->b_lo), cudaMemcpyDeviceToDevice, (cudaStream_t)stream);
+  return check_cuda(c, cudaGetLastError(), "hom_get_element_cavg");
+}
+
+int hom_set_element_cavg(hom_ctx* c, const double* d_cavg, void* stream) {
+  if (!c || !d_cavg || !c->Cavg_e) return set_err(c, HOM_ERR_INVALID_ARG, "hom_set_element_cavg (constant basis only)");
+  cudaMemcpyAsync(c->Cavg_e, d_cavg, sizeof(double) * c->B * c->m * c->m, cudaMemcpyDeviceToDevice,
+                  (cudaStream_t)stream);
+  return check_cuda(c, cudaGetLastError(), "hom_set_element_cavg");
 }
 
 int hom_profile_enable(hom_ctx* c, int enable) {

@@ -25,7 +25,8 @@ STATUS = {0: "HOM_OK", 1: "HOM_ERR_INVALID_ARG", 2: "HOM_ERR_MESH", 3: "HOM_ERR_
 # every symbol include/hom.h declares (checked by tests/test_abi.py)
 EXPORTS = ["hom_setup", "hom_get_sizes", "hom_get_work", "hom_debug_rve_kff", "hom_set_load_factor", "hom_macro_assemble", "hom_macro_spmv", "hom_macro_kinematics", "hom_condense", "hom_macro_solve",
            "hom_macro_residual_norm", "hom_recover_fluctuations", "hom_newton_update", "hom_macro_update", "hom_set_fluctuations",
-           "hom_get_fluctuations", "hom_micro_residual_max", "hom_set_phases", "hom_launch_count",
+           "hom_get_fluctuations", "hom_micro_residual_max", "hom_set_phases", "hom_get_element_cavg",
+           "hom_set_element_cavg", "hom_launch_count",
            "hom_profile_enable", "hom_profile_read", "hom_last_error", "hom_destroy"]
 PROF_CLASSES = ["rve_assemble", "condense", "macro_assemble", "cg", "recover", "other"]
 
@@ -124,6 +125,8 @@ def lib(build_if_missing: bool = True):
         L.hom_get_fluctuations.argtypes = [P, P, P]
         L.hom_micro_residual_max.argtypes = [P, ctypes.POINTER(ctypes.c_double), P]
         L.hom_set_phases.argtypes = [P, P, P, P]
+        L.hom_get_element_cavg.argtypes = [P, P, P]
+        L.hom_set_element_cavg.argtypes = [P, P, P]
         L.hom_profile_enable.argtypes = [P, I]
         L.hom_profile_read.argtypes = [P, P, P]
         L.hom_launch_count.argtypes = [P]
@@ -331,6 +334,15 @@ class Homogenizer:
                 return ctypes.c_void_p(x.data_ptr())
             return x.ctypes.data_as(ctypes.c_void_p)
         self._check(lib().hom_set_phases(self.h, hp(phase), hp(params), self._stream()), "hom_set_phases")
+
+    def get_element_cavg(self, out=None):
+        """Constant basis: the local rows of the per-element <C> [B][m][m] (other rows untouched)."""
+        out = self.empty(self.n_rve, self.m, self.m) if out is None else out
+        self._check(lib().hom_get_element_cavg(self.h, self._ptr(out), self._stream()), "hom_get_element_cavg")
+        return out
+
+    def set_element_cavg(self, cavg):
+        self._check(lib().hom_set_element_cavg(self.h, self._ptr(cavg), self._stream()), "hom_set_element_cavg")
 
     def profile(self, enable=True):
         self._check(lib().hom_profile_enable(self.h, int(enable)), "hom_profile_enable")

@@ -82,3 +82,38 @@ def test_sharded_linear_solve_world2_matches_single_process():
         assert np.array_equal(r["u"], o["u"])
         assert np.array_equal(r["w"], w_o[int(r["lo"]):int(r["hi"])])
     assert int(res[0]["hi"]) == int(res[1]["lo"])
+
+
+def _packed_worker(rank, world, port, out_dir):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2312_12771_b200.dist import allgather_packed
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    parts = rve_partition(9, 4, world)  # uneven 5/4 element split
+    B = 36
+    lo, hi = parts[rank]
+    A = torch.full((B, 4, 4), float("nan"), dtype=torch.float64)
+    P = torch.full((B, 4), float("nan"), dtype=torch.float64)
+    b = torch.arange(B, dtype=torch.float64)
+    A[lo:hi] = b[lo:hi, None, None] * 100 + torch.arange(16, dtype=torch.float64).reshape(4, 4)
+    P[lo:hi] = -b[lo:hi, None] - torch.arange(4, dtype=torch.float64) / 10
+    sc = allgather_packed([A, P], parts, rank, scalars=(float(rank + 1) * 1.5, -rank))
+    np.savez(os.path.join(out_dir, f"p{rank}.npz"), A=A.numpy(), P=P.numpy(), sc=np.array(sc))
+    dist.destroy_process_group()
+
+
+def test_allgather_packed_world2_one_collective_for_all_tensors_and_scalars():
+    """The packed exchange (one all-gather per Newton iteration: A_eff, P_eff, <P> and each rank's
+    max ||R_micro||) delivers every row of every tensor and every rank's scalars to every rank."""
+    import torch.multiprocessing as mp
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_packed_worker, args=(2, _free_port(), d), nprocs=2, join=True)
+        res = [np.load(os.path.join(d, f"p{r}.npz")) for r in range(2)]
+    b = np.arange(36, dtype=np.float64)
+    A = b[:, None, None] * 100 + np.arange(16).reshape(4, 4)
+    P = -b[:, None] - np.arange(4) / 10
+    for r in res:
+        assert np.array_equal(r["A"], A) and np.array_equal(r["P"], P)
+        assert r["sc"].tolist() == [[1.5, 0.0], [3.0, -1.0]]

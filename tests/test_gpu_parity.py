@@ -543,6 +543,49 @@ def test_rve_range_shards_reassemble_bitwise(torch_cuda):
         assert h.sizes.rve_begin == lo and h.sizes.rve_count == hi - lo
 
 
+def test_rve_range_shards_constant_basis_need_element_cavg(torch_cuda):
+    """Constant macro basis + sharding: the macro stiffness also reads <C>_e of every
+    element, which a context only holds for its own range.  Exchanging C_eff AND <C>_e
+    (hom_get/set_element_cavg) reproduces the single-context path bit for bit."""
+    from paper_2312_12771_b200.dist import rve_partition
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = W.config3(nel=3, r=8, seed=31)
+    full = gpu_linear(wl, macro_basis="constant")
+    parts = rve_partition(wl.nel ** 2, 1, 2)
+    hs = [Homogenizer.from_workload(wl, rve_range=p, macro_basis="constant") for p in parts]
+    B = wl.nel ** 2
+    C, Ca = hs[0].empty(B, 3, 3), hs[0].empty(B, 3, 3)
+    for h, (lo, hi) in zip(hs, parts):
+        Cl, Cal = h.empty(B, 3, 3), h.empty(B, 3, 3)
+        h.condense(None, Cl)
+        h.get_element_cavg(Cal)
+        C[lo:hi], Ca[lo:hi] = Cl[lo:hi], Cal[lo:hi]
+    assert np.array_equal(C.cpu().numpy(), full["C"])
+    for h, (lo, hi) in zip(hs, parts):
+        h.set_element_cavg(Ca)
+        u, _ = h.macro_solve(C)
+        assert np.array_equal(u.cpu().numpy(), full["u"])
+        w = h.recover(u)
+        assert np.array_equal(w[lo:hi].cpu().numpy(), full["w"][lo:hi])
+    with pytest.raises(Exception):
+        Homogenizer.from_workload(wl).get_element_cavg()  # Dirac basis: no per-element <C>
+
+
+def test_set_phases_rejects_bad_phase_ids(torch_cuda):
+    """hom_set_phases validates the ids before the copy: an id >= n_phases returns
+    HOM_ERR_INVALID_ARG and leaves the device phase field unchanged."""
+    from paper_2312_12771_b200.hom import Homogenizer, HomError
+    wl = W.config3(nel=2, r=6, seed=3)
+    h = Homogenizer.from_workload(wl)
+    C0 = h.condense().cpu().numpy()
+    bad = np.ascontiguousarray(wl.phase.copy())
+    bad[1, 5] = 2
+    with pytest.raises(HomError) as e:
+        h.set_phases(bad, None)
+    assert e.value.code == 1
+    assert np.array_equal(h.condense().cpu().numpy(), C0)
+
+
 # ------------------------------------------------------------------ K6 SpMV and the grid-wide PCG (scaled meshes)
 def test_macro_spmv_matches_oracle_operator(torch_cuda):
     from paper_2312_12771_b200.hom import Homogenizer
