@@ -15,6 +15,7 @@
 // DMMA fragment reads bank-conflict free; diagonal tiles are stored inverted
 // (G_JJ^-1) so that the triangular solves are DMMA GEMMs too.
 #include <cuda.h>
+#include <cstdlib>
 #include <cudaTypedefs.h>
 
 #include "hom_internal.cuh"
@@ -155,8 +156,13 @@ __device__ __forceinline__ long long clk_ordered() {
   do {                                                                                \
     if (blockIdx.x < 64 && J < 40 && threadIdx.x == 0) g_tm[blockIdx.x][J][slot] = clk_ordered(); \
   } while (0)
+#define TMARK_T(slot, t)                                                                    \
+  do {                                                                                      \
+    if (blockIdx.x < 64 && J < 40 && threadIdx.x == (t)) g_tm[blockIdx.x][J][slot] = clk_ordered(); \
+  } while (0)
 #else
 #define TMARK(slot) do {} while (0)
+#define TMARK_T(slot, t) do {} while (0)
 #endif
 
 // Stage the [64][KC] k-chunk kc (columns kc*KC..) of a row-major 64x64 global tile into swizzled smem.
@@ -306,13 +312,17 @@ __device__ __forceinline__ int chol16_inv_inplace(double* sD, int k0, int lane) 
 
 
 // Blocked (16-wide) Cholesky of the SPD 64x64 tile in sD followed by the blocked
-// triangular inverse, in place, by the 4 warps of the CTA: the 16x16 pivot blocks on
-// warp 0 (registers + shuffles), panels, trailing updates and the off-diagonal
-// inverse blocks on DMMA over all warps.  On return sD = G_JJ^-1 (lower, exact zeros
-// above the diagonal: the caller zeroes the strict upper part).  sScr: 3 x 16x20.
-// Returns false (sFail set to the 1-based failing row of the RVE) on a non-positive pivot.
-__device__ __forceinline__ bool factor_invert_diag(double* sD, double* sScr, int* sFail, int J, int tid) {
-  const int lane = tid & 31, warp = tid >> 5;
+// triangular inverse, in place, by NW warps (warp index `warp` < NW; `sync` is their
+// barrier): the 16x16 pivot blocks on warp 0 (registers + shuffles), panels, trailing
+// updates and the off-diagonal inverse blocks on DMMA over the NW warps.  On return
+// sD = G_JJ^-1 (lower, exact zeros above the diagonal: the caller zeroes the strict upper
+// part).  sScr: 3 x 16x20.  Returns false (sFail set to the 1-based failing row of the RVE)
+// on a non-positive pivot.  NW = 4: k_condense (all warps of the CTA); NW = 1: the factor
+// warp of k_condense_ws, which runs this while the MMA warps accumulate the column's
+// off-diagonal tiles.
+template <int NW, typename Sync>
+__device__ __forceinline__ bool factor_invert_diag(double* sD, double* sScr, int* sFail, int J, int warp,
+                                                   int lane, Sync sync) {
   const int lr = lane >> 2, lc = lane & 3;
 #pragma unroll 1
   for (int kb = 0; kb < 4; ++kb) {
@@ -321,44 +331,64 @@ __device__ __forceinline__ bool factor_invert_diag(double* sD, double* sScr, int
       const int f = chol16_inv_inplace(sD, k0, lane);  // block (kb,kb) := L_kk^-1
       if (f < 16 && lane == 0) sFail[0] = J * TILE + k0 + f + 1;
     }
-    __syncthreads();
+    sync();
     if (kb == 0) TMARK(5);
     if (sFail[0]) return false;
     if (kb == 3) break;
     const int rb0 = k0 + 16, nrt = (TILE - rb0) / 8;
     // panel: L_ik = A_ik X_kk^T (X_kk lower: col tile 0 needs k < 8 only); row tiles over warps
-    double p[2][4];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int ti = warp + 4 * u;
-      if (ti < nrt) {
+    if constexpr (NW == 1) {  // one warp: each row tile reads and then overwrites only its own rows
+#pragma unroll 1
+      for (int ti = 0; ti < nrt; ++ti) {
         const int r = rb0 + 8 * ti + lr;
-        p[u][0] = p[u][1] = p[u][2] = p[u][3] = 0.0;
+        double q[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
         for (int kk = 0; kk < 16; kk += 4) {
           const double a = sD[sd(r, k0 + kk + lc)];
-          if (kk < 8) dmma(p[u][0], p[u][1], a, sD[sd(k0 + lr, k0 + kk + lc)]);
-          dmma(p[u][2], p[u][3], a, sD[sd(k0 + 8 + lr, k0 + kk + lc)]);
+          if (kk < 8) dmma(q[0], q[1], a, sD[sd(k0 + lr, k0 + kk + lc)]);
+          dmma(q[2], q[3], a, sD[sd(k0 + 8 + lr, k0 + kk + lc)]);
+        }
+        __syncwarp();
+        sD[sd(r, k0 + 2 * lc)] = q[0];
+        sD[sd(r, k0 + 2 * lc + 1)] = q[1];
+        sD[sd(r, k0 + 8 + 2 * lc)] = q[2];
+        sD[sd(r, k0 + 8 + 2 * lc + 1)] = q[3];
+        __syncwarp();
+      }
+    } else {
+      double p[2][4];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int ti = warp + NW * u;
+        if (ti < nrt) {
+          const int r = rb0 + 8 * ti + lr;
+          p[u][0] = p[u][1] = p[u][2] = p[u][3] = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < 16; kk += 4) {
+            const double a = sD[sd(r, k0 + kk + lc)];
+            if (kk < 8) dmma(p[u][0], p[u][1], a, sD[sd(k0 + lr, k0 + kk + lc)]);
+            dmma(p[u][2], p[u][3], a, sD[sd(k0 + 8 + lr, k0 + kk + lc)]);
+          }
         }
       }
-    }
-    __syncthreads();
+      sync();
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int ti = warp + 4 * u;
-      if (ti < nrt) {
-        const int r = rb0 + 8 * ti + lr;
-        sD[sd(r, k0 + 2 * lc)] = p[u][0];
-        sD[sd(r, k0 + 2 * lc + 1)] = p[u][1];
-        sD[sd(r, k0 + 8 + 2 * lc)] = p[u][2];
-        sD[sd(r, k0 + 8 + 2 * lc + 1)] = p[u][3];
+      for (int u = 0; u < 2; ++u) {
+        const int ti = warp + NW * u;
+        if (ti < nrt) {
+          const int r = rb0 + 8 * ti + lr;
+          sD[sd(r, k0 + 2 * lc)] = p[u][0];
+          sD[sd(r, k0 + 2 * lc + 1)] = p[u][1];
+          sD[sd(r, k0 + 8 + 2 * lc)] = p[u][2];
+          sD[sd(r, k0 + 8 + 2 * lc + 1)] = p[u][3];
+        }
       }
+      sync();
     }
-    __syncthreads();
     // trailing: A_ij -= L_ik L_jk^T on the lower 8x8 tiles of rows/cols rb0..63 (reads the
     // panel columns, writes disjoint columns: no hazard between warps)
     const int ntr = nrt * (nrt + 1) / 2;
-    for (int t = warp; t < ntr; t += 4) {
+    for (int t = warp; t < ntr; t += NW) {
       int ti = 0;
       while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
       const int tj = t - ti * (ti + 1) / 2;
@@ -370,7 +400,7 @@ __device__ __forceinline__ bool factor_invert_diag(double* sD, double* sScr, int
       sD[sd(r + lr, cb + 2 * lc)] = acc0;
       sD[sd(r + lr, cb + 2 * lc + 1)] = acc1;
     }
-    __syncthreads();
+    sync();
   }
   TMARK(6);
   // off-diagonal blocks of the inverse, in place, block rows i ascending:
@@ -379,7 +409,7 @@ __device__ __forceinline__ bool factor_invert_diag(double* sD, double* sScr, int
 #pragma unroll 1
   for (int i = 1; i < 4; ++i) {
     const int ntile = 4 * i;  // (k, tr, tc)
-    for (int t = warp; t < ntile; t += 4) {
+    for (int t = warp; t < ntile; t += NW) {
       const int k = t >> 2, tr = (t >> 1) & 1, tc = t & 1;
       double t0 = 0.0, t1 = 0.0;
       for (int j = k; j < i; ++j) {
@@ -394,8 +424,8 @@ __device__ __forceinline__ bool factor_invert_diag(double* sD, double* sScr, int
       W[(8 * tr + lr) * 20 + 8 * tc + 2 * lc] = t0;
       W[(8 * tr + lr) * 20 + 8 * tc + 2 * lc + 1] = t1;
     }
-    __syncthreads();
-    for (int t = warp; t < ntile; t += 4) {
+    sync();
+    for (int t = warp; t < ntile; t += NW) {
       const int k = t >> 2, tr = (t >> 1) & 1, tc = t & 1;
       const double* W = sScr + k * 320;
       double o0 = 0.0, o1 = 0.0;
@@ -408,7 +438,7 @@ __device__ __forceinline__ bool factor_invert_diag(double* sD, double* sScr, int
       sD[sd(r, cc)] = o0;  // only X_ii and sScr are read in this phase: in-place write is safe
       sD[sd(r, cc + 1)] = o1;
     }
-    __syncthreads();
+    sync();
   }
   return true;
 }
@@ -650,7 +680,7 @@ k_condense(RveDev R, const __grid_constant__ TileMask tm, const __grid_constant_
       tma_load_2d(st + 64 * KC, &kmap, 0, (int)(krow0 + (long)tile_slot<MODE>(R, tm, J, 0) * TILE), &full[1]);
     }
     // ---------- blocked Cholesky + inverse of the diagonal tile ----------
-    if (!factor_invert_diag(sT, sStage, sFail, J, tid)) {
+    if (!factor_invert_diag<4>(sT, sStage, sFail, J, warp, lane, [] { __syncthreads(); })) {
       if (pre_o) wait_stage(1);  // no TMA left in flight into this CTA's shared memory
       break;
     }
@@ -888,7 +918,392 @@ k_condense(RveDev R, const __grid_constant__ TileMask tm, const __grid_constant_
 #endif
 }
 
+// ====================================================================================
+// k_condense_ws: the same factorisation with a dedicated factor warp (dense structure).
+//
+// k_condense runs the 64x64 diagonal factor + inverse (a serial pivot chain on one warp, ~30% of
+// a CTA's time at config 2, profiles/r02/) while its other three warps wait at a barrier.  Here a
+// fifth warp owns that chain and the four MMA warps keep the FP64 tensor pipe busy meanwhile: for
+// column J they accumulate S_IJ = A_IJ - sum_{K<J} G_IK G_JK^T of every off-diagonal tile (which
+// does not depend on G_JJ) and park S_IJ in the tile's pool slot; once the factor warp has
+// published G_JJ^-1 they stream the parked tiles back in 16-row chunks and form
+// G_IJ = S_IJ (G_JJ^-1)^T.  The factor warp also forms Y_J = G_JJ^-1 (K_fe,J - sum_K G_JK Y_K), the
+// Schur sum Y^T Y and the C_eff / P_eff epilogue.  Hand-offs are named barriers:
+//   BAR_S: MMA warps arrive after writing S_JJ (sT) and K_fe,J - yacc (sY); the factor warp syncs.
+//   BAR_G: the factor warp arrives after G_JJ^-1 (sT, pool), Y_J (pool); the MMA warps sync.
+// The backward pass X = G^-T Y (MMA warps) is the one of k_condense.
+// ====================================================================================
+constexpr int NTC_WS = NTC + 32;
+constexpr int BAR_MMA = 1, BAR_S = 2, BAR_G = 3;
+__device__ __forceinline__ void nbar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nbar_arrive(int id, int n) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+// generic-proxy global writes of this thread before later async-proxy (TMA) reads of them
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// smem (doubles): stages[2] (TMA k-chunks; the TRSM / backward row-chunk ring) | factor scratch |
+// sY (K_fe,J - yacc; backward: Y_J - xacc) | sY2 (Y_J) | sT (packed diagonal tile) | misc
+constexpr int WS_STAGES = 2 * STAGE_DBL;
+constexpr int WS_SCR = WS_STAGES, WS_SY = WS_SCR + 3 * 320, WS_SY2 = WS_SY + 64 * RHSW, WS_ST = WS_SY2 + 64 * RHSW;
+constexpr int WS_MISC = WS_ST + SD_DBL, WS_SMEM_DBL = WS_MISC + 64;
+constexpr int WS_RC = 16, WS_NCH = 4, WS_CH = WS_RC * TILE;  // TRSM row chunks: 16 rows, 4-deep ring
+static_assert(WS_NCH * WS_CH <= WS_STAGES, "TRSM chunk ring fits the stage area");
+static_assert(4 * (16 * TILE + 16 * RHSW) <= WS_SY, "backward ring fits stages + scratch");
+static_assert(WS_SMEM_DBL * 8 + 1024 <= 76 * 1024, "three CTAs per SM");
+
+__global__ void __launch_bounds__(NTC_WS, 3)
+k_condense_ws(RveDev R, const __grid_constant__ CUtensorMap kmap, const __grid_constant__ CUtensorMap ymap, int b0,
+              double* __restrict__ Kt, double* __restrict__ Y, const double* __restrict__ Cavg,
+              const double* __restrict__ Pavg, double* __restrict__ Ceff, double* __restrict__ Peff,
+              double* __restrict__ PavgOut, double* __restrict__ X, int* __restrict__ info) {
+  extern __shared__ __align__(1024) double smem[];
+  double* sStage = smem;
+  double* sScr = smem + WS_SCR;
+  double* sY = smem + WS_SY;
+  double* sY2 = smem + WS_SY2;
+  double* sT = smem + WS_ST;
+  int* sFail = reinterpret_cast<int*>(smem + WS_MISC);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + WS_MISC + 8);
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int lr = lane >> 2, lc = lane & 3;
+  const int bl = blockIdx.x, b = b0 + bl;
+  const int nt = R.nt, NT = R.NT;
+  double* Kb = Kt + (long)bl * R.nslot * TILE_ELEMS;
+  double* Yb = Y + (long)bl * NT * RHSW;
+  double* Xb = X + (long)(b - R.xb0) * NT * RHSW;
+  const TileMask tm{};  // unused (dense structure)
+  if (tid == 0) {
+    sFail[0] = 0;
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 4) {
+    // ============================ factor warp ============================
+    double Sacc0 = 0.0, Sacc1 = 0.0;  // Schur sum Y^T Y (8x8 DMMA fragment)
+    for (int J = 0; J < nt; ++J) {
+      nbar_sync(BAR_S, NTC_WS);
+      TMARK_T(5, 128);
+#ifdef HOM_WS_FAKE  // timing experiment only: identity instead of the factor (wrong results)
+      for (int idx = lane; idx < SD_DBL; idx += 32) sT[idx] = 0.0;
+      __syncwarp();
+      for (int r = lane; r < TILE; r += 32) sT[sd(r, r)] = 1.0;
+      __syncwarp();
+      const bool ok = true;
+#else
+      const bool ok = factor_invert_diag<1>(sT, sScr, sFail, J, 0, lane, [] { __syncwarp(); });
+#endif
+      TMARK_T(6, 128);
+      if (ok) {
+        // Y_J = G_JJ^-1 (K_fe,J - sum_K G_JK Y_K): 8 row blocks, G_JJ^-1 lower (k < 8 (rb + 1))
+#pragma unroll 1
+        for (int rb = 0; rb < 8; ++rb) {
+          double y0 = 0.0, y1 = 0.0;
+          for (int k0 = 0; k0 < 8 * rb + 8; k0 += 4) dmma(y0, y1, sT[sd(8 * rb + lr, k0 + lc)], sY[swy(k0 + lc, lr)]);
+          const int rr = 8 * rb + lr, cc = 2 * lc;
+          sY2[swy(rr, cc)] = y0;
+          sY2[swy(rr, cc + 1)] = y1;
+          *reinterpret_cast<double2*>(Yb + (long)(J * TILE + rr) * RHSW + cc) = make_double2(y0, y1);
+        }
+        __syncwarp();
+#pragma unroll
+        for (int k0 = 0; k0 < TILE; k0 += 4)  // S += Y_J^T Y_J
+          dmma(Sacc0, Sacc1, sY2[swy(k0 + lc, lr)], sY2[swy(k0 + lc, lr)]);
+        double* Gjj = tile_ptr<0>(Kb, R, tm, J, J);
+        for (int idx = lane; idx < TILE_ELEMS / 2; idx += 32) {
+          const int r = idx >> 5, cc = 2 * (idx & 31);
+          *reinterpret_cast<double2*>(Gjj + r * TILE + cc) =
+              sd_upper(r, cc) ? make_double2(0.0, 0.0) : make_double2(sT[sd(r, cc)], sT[sd(r, cc + 1)]);
+        }
+        fence_proxy_async_global();  // Y_J is read by TMA in later columns
+      }
+      __syncwarp();
+      TMARK_T(7, 128);
+      nbar_arrive(BAR_G, NTC_WS);
+      if (!ok) return;
+    }
+    // K4 epilogue: C_eff = <C> - Y_e^T Y_e / |Omega|, P_eff = <P> - Y_e^T Y_r / |Omega|
+    // (sY2: the MMA warps' backward ring may already cover the scratch area)
+    double* sSum = sY2;
+    sSum[lr * 8 + 2 * lc] = Sacc0;
+    sSum[lr * 8 + 2 * lc + 1] = Sacc1;
+    __syncwarp();
+    const int m = R.m;
+    const double* Ca = Cavg + (long)bl * 64;
+    for (int t = lane; t < m * m; t += 32) {
+      const int i = t / m, j = t % m;
+      Ceff[(long)b * m * m + t] = Ca[i * m + j] - sSum[i * 8 + j] / R.vol;
+    }
+    if (R.finite && lane < m) {
+      const double pa = Pavg[(long)bl * 8 + lane];
+      if (Peff) Peff[(long)b * m + lane] = pa - sSum[lane * 8 + m] / R.vol;
+      if (PavgOut) PavgOut[(long)b * m + lane] = pa;
+    }
+    return;
+  }
+
+  // ============================ MMA warps (tid < 128) ============================
+  auto gsync = [] { nbar_sync(BAR_MMA, NTC); };
+  const int R0 = (warp >> 1) * 32, C0 = (warp & 1) * 32;  // accumulation quadrant
+  const int cLo = warp, cHi = 7 - warp;                    // TRSM column-block pair (balanced)
+  uint32_t ph0 = 0, ph1 = 0;
+  auto wait_stage = [&](int st) {
+    if (st == 0) { mbar_wait(&full[0], ph0); ph0 ^= 1u; }
+    else { mbar_wait(&full[1], ph1); ph1 ^= 1u; }
+  };
+  const long krow0 = (long)bl * R.nslot * TILE;
+  const long yrow0 = (long)bl * NT;
+  bool failed = false;
+
+  for (int J = 0; J < nt; ++J) {
+    TMARK(0);
+    // ---------- S_JJ = A_JJ - sum_K G_JK G_JK^T ; yacc = sum_K G_JK Y_K (as k_condense) ----------
+    {
+      double dacc[9][2];
+      double yacc[2][2] = {};
+      DIAG_DISPATCH(diag_load, dacc, tile_ptr<0>(Kb, R, tm, J, J), lane);
+      int K = 0, kc = 0, par = 0;
+      auto issue_d = [&](int stg, int KK, int kcc) {
+        double* st = sStage + stg * STAGE_DBL;
+        fence_proxy_async();
+        mbar_expect(&full[stg], (64 * KC + KC * RHSW) * 8);
+        tma_load_2d(st, &kmap, kcc * KC, (int)(krow0 + (long)tile_slot<0>(R, tm, J, KK) * TILE), &full[stg]);
+        tma_load_2d(st + 2 * 64 * KC, &ymap, 0, (int)(yrow0 + KK * TILE + kcc * KC), &full[stg]);
+      };
+      if (K < J && tid == 0) issue_d(0, K, 0);
+      while (K < J) {
+        int K2 = K, kc2 = kc + 1;
+        if (kc2 == CPT) { kc2 = 0; K2 = K + 1; }
+        if (K2 < J && tid == 0) issue_d(par ^ 1, K2, kc2);
+        wait_stage(par);
+        const double* st = sStage + par * STAGE_DBL;
+        switch (warp) {
+          case 0: diag_chunk<0, true>(dacc, st, lane); break;
+          case 1: diag_chunk<1, true>(dacc, st, lane); break;
+          case 2: diag_chunk<2, true>(dacc, st, lane); break;
+          default: diag_chunk<3, true>(dacc, st, lane); break;
+        }
+        const double* sYc = st + 2 * 64 * KC;
+#pragma unroll
+        for (int k0 = 0; k0 < KC; k0 += 4) {
+          const double bb = sYc[(k0 + lc) * RHSW + lr];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) dmma(yacc[u][0], yacc[u][1], st[swt(16 * warp + 8 * u + lr, k0 + lc)], bb);
+        }
+        gsync();
+        K = K2; kc = kc2; par ^= 1;
+      }
+      DIAG_DISPATCH(diag_store, dacc, sT, lane);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int r = 16 * warp + 8 * u + lr, cc = 2 * lc;
+        const double2 y = __ldcg(reinterpret_cast<const double2*>(Yb + (long)(J * TILE + r) * RHSW + cc));
+        sY[swy(r, cc)] = y.x - yacc[u][0];
+        sY[swy(r, cc + 1)] = y.y - yacc[u][1];
+      }
+    }
+    nbar_arrive(BAR_S, NTC_WS);  // sT, sY ready: the factor warp starts the pivot chain
+    TMARK(1);
+    // ---------- off-diagonal accumulation of column J under the chain; park S_IJ in its slot ----------
+    if (J > 0) {
+      for (int I = J + 1; I < nt; ++I) {
+        double acc[4][4][2];
+        double* Aij = tile_ptr<0>(Kb, R, tm, I, J);
+        if (__ldg(R.tile_nz + I * nt + J)) {
+          load_frag(acc, Aij, R0, C0, lane);
+        } else {  // fill tile: A_IJ = 0 (never written by K1)
+#pragma unroll
+          for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+            for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
+        }
+        int K = 0, kc = 0, par = 0;
+        auto issue_o = [&](int stg, int KK, int kcc) {
+          double* st = sStage + stg * STAGE_DBL;
+          fence_proxy_async();
+          mbar_expect(&full[stg], 2 * 64 * KC * 8);
+          tma_load_2d(st, &kmap, kcc * KC, (int)(krow0 + (long)tile_slot<0>(R, tm, I, KK) * TILE), &full[stg]);
+          tma_load_2d(st + 64 * KC, &kmap, kcc * KC, (int)(krow0 + (long)tile_slot<0>(R, tm, J, KK) * TILE),
+                      &full[stg]);
+        };
+        if (tid == 0) issue_o(0, 0, 0);
+        while (K < J) {
+          int K2 = K, kc2 = kc + 1;
+          if (kc2 == CPT) { kc2 = 0; K2 = K + 1; }
+          if (K2 < J && tid == 0) issue_o(par ^ 1, K2, kc2);
+          wait_stage(par);
+          const double* st = sStage + par * STAGE_DBL;
+          mma_chunk<false, true>(acc, st, st + 64 * KC, R0, C0, lane);
+          gsync();
+          K = K2; kc = kc2; par ^= 1;
+        }
+#pragma unroll
+        for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+          for (int ni = 0; ni < 4; ++ni)
+            *reinterpret_cast<double2*>(Aij + (R0 + 8 * mi + lr) * TILE + C0 + 8 * ni + 2 * lc) =
+                make_double2(acc[mi][ni][0], acc[mi][ni][1]);
+      }
+    } else {  // J = 0: S_I0 = A_I0 is already in place; fill tiles need explicit zeros
+      for (int I = 1; I < nt; ++I) {
+        if (__ldg(R.tile_nz + I * nt)) continue;
+        double* Ai0 = tile_ptr<0>(Kb, R, tm, I, 0);
+        for (int idx = tid; idx < TILE_ELEMS / 2; idx += NTC)
+          reinterpret_cast<double2*>(Ai0)[idx] = make_double2(0.0, 0.0);
+      }
+    }
+    gsync();  // every parked S_IJ written before any warp streams it back
+    TMARK(2);
+    nbar_sync(BAR_G, NTC_WS);
+    TMARK(3);
+    if (sFail[0]) { failed = true; break; }
+    // ---------- G_IJ = S_IJ (G_JJ^-1)^T, streamed in 16-row chunks of the parked tiles ----------
+    {
+      const int nch = (nt - 1 - J) * (TILE / WS_RC);
+      int nis = 0;
+      auto issue_c = [&]() {  // chunk nis: tile I = J + 1 + nis / 4, rows 16 (nis % 4)
+        const int I = J + 1 + nis / (TILE / WS_RC), rq = nis % (TILE / WS_RC);
+        stage_rows(sStage + (nis % WS_NCH) * WS_CH, tile_ptr<0>(Kb, R, tm, I, J), rq * WS_RC, WS_RC, tid);
+        cp_async_commit();
+        ++nis;
+      };
+      while (nis < WS_NCH - 1 && nis < nch) issue_c();
+      for (int c = 0; c < nch; ++c) {
+        if (nis < nch) {
+          issue_c();
+          cp_async_wait<WS_NCH - 1>();
+        } else {
+          const int ahead = nis - c - 1;
+          if (ahead >= 2) cp_async_wait<2>();
+          else if (ahead == 1) cp_async_wait<1>();
+          else cp_async_wait<0>();
+        }
+        gsync();
+        const double* sS = sStage + (c % WS_NCH) * WS_CH;
+        // warp: column blocks cLo, cHi (all 16 rows = 2 row blocks); G_JJ^-1 lower: block c needs k < 8(c+1)
+        double g[2][2][2] = {};
+        int k0 = 0;
+        for (; k0 < 8 * (cLo + 1); k0 += 4) {
+          const double bl0 = sT[sd(8 * cLo + lr, k0 + lc)], bh0 = sT[sd(8 * cHi + lr, k0 + lc)];
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) {
+            const double a = sS[sw64(8 * mi + lr, k0 + lc)];
+            dmma(g[mi][0][0], g[mi][0][1], a, bl0);
+            dmma(g[mi][1][0], g[mi][1][1], a, bh0);
+          }
+        }
+        for (; k0 < 8 * (cHi + 1); k0 += 4) {
+          const double bh0 = sT[sd(8 * cHi + lr, k0 + lc)];
+#pragma unroll
+          for (int mi = 0; mi < 2; ++mi) dmma(g[mi][1][0], g[mi][1][1], sS[sw64(8 * mi + lr, k0 + lc)], bh0);
+        }
+        const int I = J + 1 + c / (TILE / WS_RC), rq = c % (TILE / WS_RC);
+        double* Gij = tile_ptr<0>(Kb, R, tm, I, J) + (long)rq * WS_RC * TILE;
+#pragma unroll
+        for (int mi = 0; mi < 2; ++mi) {
+          const int r = 8 * mi + lr;
+          *reinterpret_cast<double2*>(Gij + r * TILE + 8 * cLo + 2 * lc) = make_double2(g[mi][0][0], g[mi][0][1]);
+          *reinterpret_cast<double2*>(Gij + r * TILE + 8 * cHi + 2 * lc) = make_double2(g[mi][1][0], g[mi][1][1]);
+        }
+        gsync();  // ring slot c % 4 free before it is refilled
+      }
+      fence_proxy_async_global();  // G_IJ is read by TMA in later columns
+    }
+    gsync();
+    TMARK(4);
+  }
+
+  if (failed) {  // report and poison the outputs of this RVE (the factor warp has returned)
+    if (tid == 0) info[b] = sFail[0];
+    const double nan = __longlong_as_double(0x7ff8000000000000LL);
+    if (tid < R.m * R.m) Ceff[(long)b * R.m * R.m + tid] = nan;
+    if (Peff && tid < R.m) Peff[(long)b * R.m + tid] = nan;
+    return;
+  }
+
+  // ======================= backward: X = G^-T Y (as k_condense, MMA warps) ===================
+  constexpr int RC = 16, RPT = TILE / RC;
+  constexpr int NSTB = 4, BST = RC * TILE + RC * RHSW;
+  for (int J = nt - 1; J >= 0; --J) {
+    double xacc[2][2] = {};
+    int I = J + 1, rq = 0;
+    int nis = 0, ncon = 0;
+    auto issue_b = [&]() {
+      double* nb = smem + (nis % NSTB) * BST;
+      stage_rows(nb, tile_ptr<0>(Kb, R, tm, I, J), rq * RC, RC, tid);
+      stage_rhs(nb + RC * TILE, Xb + (long)(I * TILE + rq * RC) * RHSW, RC, tid);
+      cp_async_commit();
+      ++nis;
+      if (++rq == RPT) { rq = 0; ++I; }
+    };
+    {  // G_JJ^-1 (lower 16x16 blocks) into the packed buffer: the oldest cp.async group, so every
+       // wait of the chunk ring below also covers it
+      const double* src = tile_ptr<0>(Kb, R, tm, J, J);
+      for (int idx = tid; idx < TILE * 32; idx += NTC) {
+        const int r = idx >> 5, c2 = 2 * (idx & 31);
+        if (!sd_upper(r, c2)) cp_async16(sT + sd(r, c2), src + r * TILE + c2);
+      }
+      cp_async_commit();
+    }
+    while (nis < NSTB - 1 && I < nt) issue_b();
+    while (ncon < nis) {
+      if (I < nt) {
+        issue_b();
+        cp_async_wait<NSTB - 1>();
+      } else {
+        const int ahead = nis - ncon - 1;
+        if (ahead >= 2) cp_async_wait<2>();
+        else if (ahead == 1) cp_async_wait<1>();
+        else cp_async_wait<0>();
+      }
+      gsync();
+      const double* tl = smem + (ncon % NSTB) * BST;
+      const double* xi = tl + RC * TILE;
+#pragma unroll
+      for (int k0 = 0; k0 < RC; k0 += 4) {
+        const double bb = xi[swy(k0 + lc, lr)];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) dmma(xacc[u][0], xacc[u][1], tl[sw64(k0 + lc, 16 * warp + 8 * u + lr)], bb);
+      }
+      gsync();
+      ++ncon;
+    }
+    cp_async_wait<0>();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int r = 16 * warp + 8 * u + lr, cc = 2 * lc;
+      const double2 y = __ldcg(reinterpret_cast<const double2*>(Yb + (long)(J * TILE + r) * RHSW + cc));
+      sY[swy(r, cc)] = y.x - xacc[u][0];
+      sY[swy(r, cc + 1)] = y.y - xacc[u][1];
+    }
+    gsync();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int r = 16 * warp + 8 * u;
+      double x0 = 0.0, x1 = 0.0;
+      for (int k0 = r; k0 < TILE; k0 += 4) dmma(x0, x1, sT[sd(k0 + lc, r + lr)], sY[swy(k0 + lc, lr)]);
+      const int rr = r + lr, cc = 2 * lc;
+      *reinterpret_cast<double2*>(Xb + (long)(J * TILE + rr) * RHSW + cc) = make_double2(x0, x1);
+    }
+    gsync();
+  }
+}
+
 __global__ void k_first_fail(const int* __restrict__ f, int n, int sentinel, int* out);
+
+// Dense-structure kernel: 0 = k_condense (default), 1 = k_condense_ws (factor warp + 4 MMA warps;
+// HOM_CONDENSE=ws selects it, for A/B measurements -- slower on this B200).
+static int condense_variant() {
+  static const int v = [] {
+    const char* e = getenv("HOM_CONDENSE");
+    return (e && e[0] == 'w') ? 1 : 0;
+  }();
+  return v;
+}
 
 void launch_condense(const RveDev& R, int b0, int nb, double* Kt, double* Y, const double* Cavg,
                      const double* Pavg, double* Ceff, double* Peff, double* PavgOut, double* X,
@@ -921,6 +1336,12 @@ void launch_condense(const RveDev& R, int b0, int nb, double* Kt, double* Y, con
     const cuuint32_t ybox[2] = {(cuuint32_t)RHSW, (cuuint32_t)KC};
     encode(&ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, Y, ydim, ystr, ybox, one, CU_TENSOR_MAP_INTERLEAVE_NONE,
            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  }
+  if (R.dense_tiles && condense_variant() == 1) {
+    const size_t smw = (size_t)WS_SMEM_DBL * sizeof(double);
+    cudaFuncSetAttribute(k_condense_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
+    k_condense_ws<<<nb, NTC_WS, smw, s>>>(R, kmap, ymap, b0, Kt, Y, Cavg, Pavg, Ceff, Peff, PavgOut, X, info);
+    return;
   }
   auto k = R.dense_tiles ? k_condense<0> : (tm ? k_condense<1> : k_condense<2>);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

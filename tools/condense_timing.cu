@@ -62,6 +62,25 @@ int main(int argc, char** argv) {
   printf("nt=%d nb=%d  kernel %.3f ms  err=%s\n", nt, nb, ms, cudaGetErrorString(cudaGetLastError()));
   static long long tm[64][40][8];
   cudaMemcpyFromSymbol(tm, hom::g_tm, sizeof(tm));
+  const char* var = getenv("HOM_CONDENSE");
+  if (var && var[0] == 'w') {  // k_condense_ws marks: MMA 0..4, factor warp 5..7
+    printf("  J |  syrk | accum+park | waitG | trsm | total || factor: waitS chain  Y+store (k-cycles)\n");
+    double t[8] = {};
+    for (int J = 0; J < nt && J < 40; ++J) {
+      double v[8] = {};
+      for (int b = 0; b < 64; ++b) {
+        long long* m = tm[b][J];
+        v[0] += m[1] - m[0]; v[1] += m[2] - m[1]; v[2] += m[3] - m[2]; v[3] += m[4] - m[3]; v[4] += m[4] - m[0];
+        v[5] += m[5] - (J ? tm[b][J - 1][7] : m[0]); v[6] += m[6] - m[5]; v[7] += m[7] - m[6];
+      }
+      printf("%3d | %5.1f | %10.1f | %5.1f | %4.1f | %5.1f || %5.1f %6.1f %6.1f\n", J, v[0] / 64e3, v[1] / 64e3,
+             v[2] / 64e3, v[3] / 64e3, v[4] / 64e3, v[5] / 64e3, v[6] / 64e3, v[7] / 64e3);
+      for (int k = 0; k < 8; ++k) t[k] += v[k];
+    }
+    printf("sum | %5.1f | %10.1f | %5.1f | %4.1f | %5.1f || %5.1f %6.1f %6.1f\n", t[0] / 64e3, t[1] / 64e3, t[2] / 64e3,
+           t[3] / 64e3, t[4] / 64e3, t[5] / 64e3, t[6] / 64e3, t[7] / 64e3);
+    return 0;
+  }
   printf("  J |  diagS | factor |   Y+Sacc | offdiag | total | (k-cycles, mean over 64 CTAs)\n");
   double tot[5] = {};
   for (int J = 0; J < nt && J < 40; ++J) {
