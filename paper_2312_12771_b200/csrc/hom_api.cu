@@ -30,6 +30,7 @@ struct hom_ctx {
   std::vector<void*> allocs;
   // chunk-local scratch
   double *Kt = nullptr, *Y = nullptr, *Cavg = nullptr, *Pavg = nullptr, *Aq = nullptr, *Pq = nullptr;
+  int fs_slots = 0;                                // persistent CTAs of the fused finite-strain K1
   // whole-batch state
   double *X = nullptr, *rfn = nullptr, *w = nullptr, *kin = nullptr;
   int *info = nullptr, *jflag = nullptr, *first_fail = nullptr;
@@ -566,8 +567,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
 
   // ------------------------------------------------------------ chunking + allocation
   const size_t tiles = (size_t)R.nslot;
-  const size_t per_rve = tiles * hom::TILE_ELEMS * 8 + (size_t)R.NT * hom::RHSW * 8 + 64 * 8 * 2 +
-                         (c->finite ? (size_t)R.ne * 124 * 8 : 0);
+  const size_t per_rve = tiles * hom::TILE_ELEMS * 8 + (size_t)R.NT * hom::RHSW * 8 + 64 * 8 * 2;
   if (c->opt.rve_count > 0 && (c->opt.rve_begin < 0 || c->opt.rve_begin + c->opt.rve_count > c->B))
     return fail(HOM_ERR_INVALID_ARG, "rve_begin / rve_count outside [0, B)");
   c->b_lo = c->opt.rve_count > 0 ? c->opt.rve_begin : 0;
@@ -737,7 +737,8 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   c->Cavg = dalloc<double>(c, (size_t)64 * chunk, &rc);
   c->Pavg = dalloc<double>(c, (size_t)8 * chunk, &rc);
   if (c->finite) {
-    c->Aq = dalloc<double>(c, (size_t)chunk * R.ne * 124, &rc);  // element table of k_rve_element_nh
+    c->fs_slots = hom::rve_assemble_fs_slots(R);  // persistent CTAs of the fused finite-strain K1
+    c->Aq = dalloc<double>(c, (size_t)c->fs_slots * R.ne * hom::FS_RECORD, &rc);  // their element-record scratch
     c->Pq = nullptr;
     c->w = dalloc<double>(c, (size_t)c->B * R.npad, &rc);
   }
@@ -822,10 +823,13 @@ int hom_condense(hom_ctx* c, const double* d_kin, double* d_C_eff, double* d_P_e
   for (int b0 = c->b_lo; b0 < c->b_hi; b0 += c->chunk) {
     int nb = std::min(c->chunk, c->b_hi - b0);
     if (c->finite)
+      run(c, HOM_PROF_RVE_ASSEMBLE, s, [&] {
+        hom::launch_rve_assemble_fs(R, b0, nb, d_kin, c->w, c->Kt, c->Y, c->Cavg, c->Pavg, c->rfn, c->Aq,
+                                    c->fs_slots, c->jflag, s);
+      });
+    else
       run(c, HOM_PROF_RVE_ASSEMBLE, s,
-          [&] { hom::launch_rve_material_nh(R, b0, nb, d_kin, c->w, c->Aq, c->Pq, c->jflag, s); });
-    run(c, HOM_PROF_RVE_ASSEMBLE, s,
-        [&] { hom::launch_rve_assemble(R, b0, nb, c->Kt, c->Y, c->Cavg, c->Pavg, c->rfn, c->Aq, c->Pq, s); });
+          [&] { hom::launch_rve_assemble(R, b0, nb, c->Kt, c->Y, c->Cavg, c->Pavg, c->rfn, s); });
     run(c, HOM_PROF_CONDENSE, s, [&] {
       hom::launch_condense(R, b0, nb, c->Kt, c->Y, c->Cavg, c->Pavg, d_C_eff, d_P_eff, d_P_avg, c->X, c->info, s,
                            c->has_tmask ? &c->tmask : nullptr);
@@ -889,7 +893,7 @@ int hom_debug_rve_kff(hom_ctx* c, int rve, double* d_Kff, void* stream) {
   if (c->finite) return set_err(c, HOM_ERR_INVALID_ARG, "hom_debug_rve_kff: small strain only");
   if (rve < c->b_lo || rve >= c->b_hi) return set_err(c, HOM_ERR_INVALID_ARG, "hom_debug_rve_kff: RVE out of range");
   cudaStream_t s = (cudaStream_t)stream;
-  hom::launch_rve_assemble(c->R, rve, 1, c->Kt, c->Y, c->Cavg, c->Pavg, c->rfn, c->Aq, c->Pq, s);
+  hom::launch_rve_assemble(c->R, rve, 1, c->Kt, c->Y, c->Cavg, c->Pavg, c->rfn, s);
   hom::launch_expand_kff(c->R, c->Kt, d_Kff, s);
   return check_cuda(c, cudaStreamSynchronize(s), "hom_debug_rve_kff");
 }

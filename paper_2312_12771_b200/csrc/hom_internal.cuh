@@ -120,13 +120,18 @@ struct CgState {
 };
 
 // ---- kernels (launch wrappers; all enqueue on `s`) ----
-void launch_rve_material_nh(const RveDev& R, int b0, int nb, const double* F, const double* w,
-                            double* Aq, double* Pq, int* jflag, cudaStream_t s);
 size_t rve_assemble_smem(const RveDev& R, int npw);  // K1 dynamic shared memory
 int rve_assemble_npw(const RveDev& R);              // K1 row-buffer nodes per warp
+// small strain (and dim 1): one CTA per RVE of [b0, b0 + nb)
 void launch_rve_assemble(const RveDev& R, int b0, int nb, double* Kt, double* Y, double* Cavg,
-                         double* Pavg, double* rfn, const double* Aq, const double* Pq,
-                         cudaStream_t s);
+                         double* Pavg, double* rfn, cudaStream_t s);
+// finite strain, fused material pass + tile writer: `slots` persistent CTAs, each with a scratch
+// slice of ne * FS_RECORD doubles (rve_assemble_fs_slots() = resident CTAs on the device)
+constexpr int FS_RECORD = 76;  // element record (rve_assembly.cu EL_STRIDE)
+int rve_assemble_fs_slots(const RveDev& R);
+void launch_rve_assemble_fs(const RveDev& R, int b0, int nb, const double* F, const double* w, double* Kt,
+                            double* Y, double* Cavg, double* Pavg, double* rfn, double* scratch, int slots,
+                            int* jflag, cudaStream_t s);
 void launch_condense(const RveDev& R, int b0, int nb, double* Kt, double* Y, const double* Cavg,
                      const double* Pavg, double* Ceff, double* Peff, double* PavgOut, double* X,
                      int* info, cudaStream_t s,

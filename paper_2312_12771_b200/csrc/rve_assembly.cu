@@ -13,6 +13,8 @@
 // One CTA per RVE; each warp gathers one node row-block of a tile at a time
 // and streams it out with coalesced 16-byte stores -- the kernel is HBM-write
 // bound (K1).
+#include <algorithm>
+
 #include "hom_internal.cuh"
 
 namespace hom {
@@ -46,11 +48,12 @@ __device__ __forceinline__ double unit_stress(int k, int c, int J, double lam, d
 // with H = cof F (the 2-D specialisation of 1/2 F xx F).  kind 1 = beta 0 (R11).
 // F~ = F + grad w (eq:microGrad).
 // ---------------------------------------------------------------------------
-// Element quantities per (RVE, element), 124 doubles (EL_STRIDE): K_e [8][8] = sum_q eta G_q^T A_q G_q,
-// F_e [8][4] = sum_q eta G_q^T A_q, r_e [8] = sum_q eta G_q^T P_q (the element parts of K_ff, K_fF and
-// r_f, eq:discreteSys_D/L), and the qp sums sum_q eta A_q [16], sum_q eta P_q [4] for <A>, <P>.
-// One thread per element row (a, i): the material point is re-evaluated by the 8 row threads.
-constexpr int EL_STRIDE = 124, EL_F = 64, EL_R = 96, EL_A = 104, EL_P = 120;
+// Element record per (RVE, element), 76 doubles (EL_STRIDE): K_e = sum_q eta G_q^T A_q G_q packed
+// lower-triangular ([8][8] symmetric, 36 entries, EL_K), F_e [8][4] = sum_q eta G_q^T A_q (EL_F) and
+// r_e [8] = sum_q eta G_q^T P_q (EL_R) -- the element parts of K_ff, K_fF and r_f (eq:discreteSys_D/L).
+// The volume sums of A and P for <A>, <P> are reduced on chip, not stored.
+constexpr int EL_STRIDE = FS_RECORD, EL_K = 0, EL_F = 36, EL_R = 68;
+__device__ __forceinline__ int pk8(int r, int c) { return r >= c ? ((r * (r + 1)) >> 1) + c : ((c * (c + 1)) >> 1) + r; }
 
 __device__ __forceinline__ bool cook_material(const double* F, double alpha, double beta, double kappa, double* P,
                                               double* A) {
@@ -80,32 +83,35 @@ __device__ __forceinline__ bool cook_material(const double* F, double alpha, dou
   return true;
 }
 
-// Block of NH_ELB consecutive (RVE, element) pairs, NH_THR threads: phase 1, one thread per
-// (element, qp) evaluates F~, P, A once (shared memory); phase 2, one thread per element row (a, i)
-// forms its rows of K_e, F_e, r_e from them; the block's NH_ELB x EL_STRIDE outputs are staged in
-// shared memory and written back as one contiguous, coalesced range.
-constexpr int NH_ELB = 32, NH_THR = 256;
-
-__global__ void __launch_bounds__(NH_THR) k_rve_element_nh(RveDev R, int b0, int nb, const double* __restrict__ Fbar,
-                                                          const double* __restrict__ w, double* __restrict__ EL,
-                                                          int* __restrict__ jflag) {
-  extern __shared__ double nh_smem[];
-  // per (element, qp): A [16], P [4], the shape gradients G [8] and the weight eta~ j (phase 2 reads them
-  // from here instead of re-loading the mesh tables)
-  constexpr int QW = 29;
-  double (*sQ)[QW] = reinterpret_cast<double (*)[QW]>(nh_smem);  // [NH_ELB * 4][QW]
-  double* sOut = nh_smem + NH_ELB * 4 * QW;                      // [NH_ELB][EL_STRIDE]
-  __shared__ int sOk[NH_ELB];
+// Element records of elements [e0, e0 + cnt) (cnt <= FS_ELB) of RVE b by the CTA's NTHR threads:
+// phase 1, one thread per (element, qp) evaluates F~, P, A once (shared memory); phase 2, one
+// thread per element row (a, i) forms its rows of K_e, F_e, r_e and the qp sums of A and P;
+// the records are staged in shared memory and written as one contiguous, coalesced range to
+// `out` (the CTA's L2-resident scratch, read back by the tile writer of the same CTA).
+constexpr int FS_ELB = 32, FS_QW = 29;
+constexpr int FS_SMEM_DBL = FS_ELB * 4 * FS_QW;
+// L2 residency hints: the element records are re-read by the same CTA moments later (evict_last),
+// the K_ff tiles stream out once (evict_first) so they do not push the records out of L2
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void st_hint(double* a, double v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void nh_elements(const RveDev& R, int b, int e0, int cnt, const double* __restrict__ Fbar,
+                                            const double* __restrict__ w, double* __restrict__ out,
+                                            int* __restrict__ jflag, double* sm, int* sOk, double (&avg)[4]) {
+  double (*sQ)[FS_QW] = reinterpret_cast<double (*)[FS_QW]>(sm);  // [FS_ELB * 4][FS_QW]
   const int ne = R.ne, nq = R.nq, tid = threadIdx.x;
-  const long ge0 = (long)blockIdx.x * NH_ELB, n_el = (long)nb * ne;
-  if (tid < NH_ELB) sOk[tid] = 1;
+  if (tid < FS_ELB) sOk[tid] = 1;
   __syncthreads();
   // ---- phase 1: material point per (element, qp) ----
-  if (tid < NH_ELB * 4) {
+  if (tid < FS_ELB * 4) {
     const int le = tid >> 2, q = tid & 3;
-    const long ge = ge0 + le;
-    if (ge < n_el && q < nq) {
-      const int bl = (int)(ge / ne), e = (int)(ge % ne), b = b0 + bl;
+    if (le < cnt && q < nq) {
+      const int e = e0 + le;
       const double* Fb = Fbar + (long)b * 4;
       const double* wb = w + (long)b * R.npad;
       const int ph = R.phase[(R.phase_per_rve ? (long)b * ne : 0) + e];
@@ -131,12 +137,12 @@ __global__ void __launch_bounds__(NH_THR) k_rve_element_nh(RveDev R, int b0, int
     }
   }
   __syncthreads();
-  // ---- phase 2: element rows (a, i) ----
+  // ---- phase 2: element rows (a, i), written straight to the L2-resident scratch ----
   {
     const int le = tid >> 3, row = tid & 7, a = row >> 1, i = row & 1;
-    const long ge = ge0 + le;
-    double* out = sOut + le * EL_STRIDE;
-    if (ge < n_el) {
+    double* o = out + (long)le * EL_STRIDE;
+    const uint64_t pol = l2_policy_evict_last();
+    if (le < cnt) {
       const bool ok = sOk[le];
       double ke[8] = {}, fe[4] = {}, re = 0.0;
       for (int q = 0; q < nq; ++q) {
@@ -153,60 +159,31 @@ __global__ void __launch_bounds__(NH_THR) k_rve_element_nh(RveDev R, int b0, int
           for (int j = 0; j < 2; ++j)  // column (b, j): sum_L t[(j,L)] g_b[L]
             ke[2 * bb + j] += wq * (t[2 * j] * G[2 * bb] + t[2 * j + 1] * G[2 * bb + 1]);
       }
-      for (int k = 0; k < 8; ++k) out[row * 8 + k] = ok ? ke[k] : 0.0;
-      for (int k = 0; k < 4; ++k) out[EL_F + row * 4 + k] = ok ? fe[k] : 0.0;
-      out[EL_R + row] = ok ? re : 0.0;
-      if (row < 5) {  // qp sums of A (rows 0-3: 4 entries each) and P (row 4)
-        double sv[4] = {};
+      for (int k = 0; k <= row; ++k) st_hint(o + EL_K + pk8(row, k), ok ? ke[k] : 0.0, pol);  // lower part
+      for (int k = 0; k < 4; ++k) st_hint(o + EL_F + row * 4 + k, ok ? fe[k] : 0.0, pol);
+      st_hint(o + EL_R + row, ok ? re : 0.0, pol);
+      if (row < 5 && ok) {  // running qp sums of A (rows 0-3: 4 entries each) and P (row 4) for <A>, <P>
         for (int q = 0; q < nq; ++q) {
           const double wq = sQ[le * 4 + q][28];
-          for (int k = 0; k < 4; ++k) sv[k] += wq * sQ[le * 4 + q][row * 4 + k];
+          for (int k = 0; k < 4; ++k) avg[k] += wq * sQ[le * 4 + q][row * 4 + k];
         }
-        for (int k = 0; k < 4; ++k) out[EL_A + row * 4 + k] = ok ? sv[k] : 0.0;
       }
     }
   }
-  __syncthreads();
-  // ---- coalesced write-back of the block's contiguous element records ----
-  const long nrec = min((long)NH_ELB, n_el - ge0);
-  double* dst = EL + ge0 * EL_STRIDE;
-  for (int k = tid; k < nrec * EL_STRIDE; k += NH_THR) __stcg(dst + k, sOut[k]);
+  __syncthreads();  // sQ reused by the next block
 }
-
-void launch_rve_material_nh(const RveDev& R, int b0, int nb, const double* F, const double* w,
-                            double* EL, double* /*unused*/, int* jflag, cudaStream_t s) {
-  const long n = (long)nb * R.ne;
-  const size_t sm = (size_t)NH_ELB * (4 * 29 + EL_STRIDE) * sizeof(double);
-  cudaFuncSetAttribute(k_rve_element_nh, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  k_rve_element_nh<<<(unsigned)((n + NH_ELB - 1) / NH_ELB), NH_THR, sm, s>>>(R, b0, nb, F, w, EL, jflag);
-}
-
-// ---------------------------------------------------------------------------
-// K1: assembly.  ISO (small strain): element blocks from geometry-only tables,
-// K_e = lam_e Klam_e + mu_e Kmu_e (isotropic closed form K_ab^{ij} = lam g_a^i g_b^j
-// + mu g_a^j g_b^i + mu d_ij g_a.g_b integrated at setup).  Finite strain: the
-// tangent is read per qp from Aq (full-gradient form).
-//
-// Tiles: only the structurally nonzero tiles (per-mesh bitmap) are written,
-// row by row with coalesced 16-byte stores (see the tile writer below).
-// ---------------------------------------------------------------------------
-
 
 template <int DIM, bool ISO>
-__global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double* __restrict__ Kt,
-                                                       double* __restrict__ Y, double* __restrict__ Cavg,
-                                                       double* __restrict__ Pavg, double* __restrict__ rfn,
-                                                       const double* __restrict__ Aq,
-                                                       const double* __restrict__ Pq) {
-  extern __shared__ __align__(128) double smem[];
+__device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const int bl, double* __restrict__ Kt,
+                                             double* __restrict__ Y, double* __restrict__ Cavg,
+                                             double* __restrict__ Pavg, double* __restrict__ rfn,
+                                             const double* __restrict__ EL, double* smem) {
   double* s_row = smem;                      // [8 warps][npw][DIM][64] tile-row buffers
   double* red = s_row + (NTHR / 32) * R.npw * DIM * TILE;  // [NTHR] reduction scratch
   double* s_K = red + NTHR;                  // [ntype][n_phase][ND][ND] element matrices (ISO)
   double* s_F = s_K + (ISO ? R.ntype * R.n_phase * ((1 << DIM) * DIM) * ((1 << DIM) * DIM) : 0);  // [type][phase][ND][m]
   int* s_ep = reinterpret_cast<int*>(s_F + (ISO ? R.ntype * R.n_phase * ((1 << DIM) * DIM) * R.m : 0));
   const int tid = threadIdx.x;
-  const int bl = blockIdx.x;
-  const int b = b0 + bl;
   const int ne = R.ne;
   constexpr int ND = ISO ? (1 << DIM) * DIM : 8;  // nen*dim
 
@@ -230,9 +207,9 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   }
   __syncthreads();
 
-  // ---- volume averages <C> (and <P>) ----
-  {
-    constexpr int NV = ISO ? 2 : 20;
+  // ---- volume average <C> (small strain; finite strain: <A>, <P> come from the element pass) ----
+  if (ISO) {
+    constexpr int NV = 2;
     double acc[NV];
 #pragma unroll
     for (int i = 0; i < NV; ++i) acc[i] = 0.0;
@@ -244,14 +221,6 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
         const double E = mt[2 * p], nu = mt[2 * p + 1], v = R.evol[e];
         acc[0] += v * (E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)));
         acc[1] += v * (E / (2.0 * (1.0 + nu)));
-      }
-    } else {
-      for (int e = tid; e < ne; e += NTHR) {
-        const double* el = Aq + ((long)bl * ne + e) * EL_STRIDE;
-#pragma unroll
-        for (int i = 0; i < 16; ++i) acc[i] += el[EL_A + i];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) acc[16 + i] += el[EL_P + i];
       }
     }
     // one pass: warp shuffles, then NV partial rows in smem
@@ -280,8 +249,6 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
           for (int j = 0; j < DIM; ++j) C[i * m + j] = tot[0] + (i == j ? 2.0 * tot[1] : 0.0);
         for (int i = DIM; i < m; ++i) C[i * m + i] = tot[1];
       } else {
-        for (int i = 0; i < 16; ++i) C[i] = tot[i];
-        for (int i = 0; i < 4; ++i) Pavg[(long)bl * 8 + i] = tot[16 + i];
       }
     }
     __syncthreads();
@@ -305,7 +272,7 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
             for (int k = 0; k < RHSW; ++k)
               if (k < R.m) out[k] += fe[k];
           } else {
-            const double* el = Aq + ((long)bl * ne + e) * EL_STRIDE;
+            const double* el = EL + (long)e * EL_STRIDE;
             const int rw = a * DIM + c;
             for (int k = 0; k < 4; ++k) out[k] += el[EL_F + rw * 4 + k];
             out[4] += el[EL_R + rw];
@@ -388,43 +355,31 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
 #pragma unroll
               for (int jj = 0; jj < DIM; ++jj) blk[i][jj] = 0.0;
             const int nsh = rv[1];
+            // element block (a, b) of the element in `code`: the per-(type, phase) table in shared memory
+            // (small strain) or the CTA's L2-resident element record, K_e packed lower-triangular
+            auto blk_at = [&](int code, int i, int jj) -> double {
+              const int e = code >> 8, r = ((code >> 4) & 15) * DIM + i, c = (code & 15) * DIM + jj;
+              if (ISO) return s_K[(long)s_ep[e] * ND * ND + r * ND + c];
+              return EL[(long)e * EL_STRIDE + EL_K + pk8(r, c)];
+            };
 #pragma unroll
             for (int sidx = 0; sidx < 4 * RS4M - 2 + 1; ++sidx) {
               if (sidx >= nsh) break;
-              int code;
               if (sidx < 4 * RS4M - 2) {
-                code = rv[sidx + 2];
-              } else {  // rare: records longer than RS4M int4s
+                const int code = rv[sidx + 2];
+#pragma unroll
+                for (int i = 0; i < DIM; ++i)
+#pragma unroll
+                  for (int jj = 0; jj < DIM; ++jj) blk[i][jj] += blk_at(code, i, jj);
+              } else {  // rare: records longer than RS4M int4s (tiny periodic meshes)
                 for (int s2 = sidx; s2 < nsh; ++s2) {
                   const int slot = s2 + 2;
-                  const int4 v = __ldg(rec + (slot >> 2));
-                  const int c2 = (slot & 3) == 0 ? v.x : (slot & 3) == 1 ? v.y : (slot & 3) == 2 ? v.z : v.w;
-                  const int e = c2 >> 8, a = (c2 >> 4) & 15, bb = c2 & 15;
-                  if (ISO) {
-                    const double* ke = s_K + (long)s_ep[e] * ND * ND + (a * DIM) * ND + bb * DIM;
-                    for (int i = 0; i < DIM; ++i)
-                      for (int jj = 0; jj < DIM; ++jj) blk[i][jj] += ke[i * ND + jj];
-                  } else {
-                    const double* ke = Aq + ((long)bl * ne + e) * EL_STRIDE + (a * DIM) * 8 + bb * DIM;
-                    for (int i = 0; i < DIM; ++i)
-                      for (int jj = 0; jj < DIM; ++jj) blk[i][jj] += ke[i * 8 + jj];
-                  }
+                  const int4 vv = __ldg(rec + (slot >> 2));
+                  const int c2 = (slot & 3) == 0 ? vv.x : (slot & 3) == 1 ? vv.y : (slot & 3) == 2 ? vv.z : vv.w;
+                  for (int i = 0; i < DIM; ++i)
+                    for (int jj = 0; jj < DIM; ++jj) blk[i][jj] += blk_at(c2, i, jj);
                 }
                 break;
-              }
-              const int e = code >> 8, a = (code >> 4) & 15, bb = code & 15;
-              if (ISO) {
-                const double* ke = s_K + (long)s_ep[e] * ND * ND + (a * DIM) * ND + bb * DIM;
-#pragma unroll
-                for (int i = 0; i < DIM; ++i)
-#pragma unroll
-                  for (int jj = 0; jj < DIM; ++jj) blk[i][jj] += ke[i * ND + jj];
-              } else {
-                const double* ke = Aq + ((long)bl * ne + e) * EL_STRIDE + (a * DIM) * 8 + bb * DIM;
-#pragma unroll
-                for (int i = 0; i < DIM; ++i)
-#pragma unroll
-                  for (int jj = 0; jj < DIM; ++jj) blk[i][jj] += ke[i * 8 + jj];
               }
             }
 #pragma unroll
@@ -452,7 +407,8 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
               v.x = (c0 + 2 * lane == row) ? 1.0 : 0.0;
               v.y = (c0 + 2 * lane + 1 == row) ? 1.0 : 0.0;
             }
-            __stcg(reinterpret_cast<double2*>(gt + rr * TILE + 2 * lane), v);
+            if (ISO) __stcg(reinterpret_cast<double2*>(gt + rr * TILE + 2 * lane), v);
+            else __stcs(reinterpret_cast<double2*>(gt + rr * TILE + 2 * lane), v);  // evict-first: keep records in L2
           }
         }
         __syncwarp();
@@ -466,10 +422,62 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
   }
 }
 
+template <int DIM, bool ISO>
+__global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double* __restrict__ Kt,
+                                                       double* __restrict__ Y, double* __restrict__ Cavg,
+                                                       double* __restrict__ Pavg, double* __restrict__ rfn) {
+  extern __shared__ __align__(128) double smem[];
+  assemble_rve<DIM, ISO>(R, b0 + blockIdx.x, blockIdx.x, Kt, Y, Cavg, Pavg, rfn, nullptr, smem);
+}
+
+// Finite strain, fused: a persistent CTA per slot walks its RVEs; for each it first
+// evaluates every material point and forms the element records into its own scratch slice (one
+// RVE, ne x EL_STRIDE doubles, written and read back by the same CTA while L2-resident), then runs
+// the tile writer from them -- no batch-wide element table round trip through HBM.
+__global__ void __launch_bounds__(NTHR, 4) k_rve_assemble_fs(RveDev R, int b0, int nb, const double* __restrict__ Fbar,
+                                                          const double* __restrict__ w, double* __restrict__ Kt,
+                                                          double* __restrict__ Y, double* __restrict__ Cavg,
+                                                          double* __restrict__ Pavg, double* __restrict__ rfn,
+                                                          double* __restrict__ scratch, int* __restrict__ jflag) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ int sOk[FS_ELB];
+  double* scr = scratch + (long)blockIdx.x * R.ne * EL_STRIDE;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, row = tid & 7;
+  for (int bl = blockIdx.x; bl < nb; bl += gridDim.x) {
+    const int b = b0 + bl;
+    double avg[4] = {0.0, 0.0, 0.0, 0.0};  // this thread's share of sum eta A (row < 4) / sum eta P (row 4)
+    for (int e0 = 0; e0 < R.ne; e0 += FS_ELB)
+      nh_elements(R, b, e0, min(FS_ELB, R.ne - e0), Fbar, w, scr + (long)e0 * EL_STRIDE, jflag, smem, sOk, avg);
+    // <A>, <P>: sum over the elements (lanes with equal row: xor 8, 16; then the 8 warps), / |Omega|
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      avg[k] += __shfl_xor_sync(0xffffffffu, avg[k], 8);
+      avg[k] += __shfl_xor_sync(0xffffffffu, avg[k], 16);
+    }
+    double* red = smem;  // [8 warps][5 rows][4]
+    if (lane < 5)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) red[(warp * 5 + row) * 4 + k] = avg[k];
+    __syncthreads();
+    if (tid < 20) {
+      double t = 0.0;
+      for (int wv = 0; wv < NTHR / 32; ++wv) t += red[wv * 20 + tid];
+      t /= R.vol;
+      if (tid < 16) Cavg[(long)bl * 64 + tid] = t;
+      else Pavg[(long)bl * 8 + tid - 16] = t;
+    }
+    __syncthreads();
+    assemble_rve<2, false>(R, b, bl, Kt, Y, Cavg, Pavg, rfn, scr, smem);
+    __syncthreads();
+  }
+}
+
 size_t rve_assemble_smem(const RveDev& R, int npw) {
   const int dim = R.finite ? 2 : R.dim, nd = (1 << dim) * dim;  // nen*dim
-  return (size_t)((NTHR / 32) * npw * dim * TILE + NTHR) * sizeof(double) +
-         (R.finite ? 0 : (size_t)R.ntype * R.n_phase * nd * (nd + R.m) * sizeof(double) + (size_t)R.ne * sizeof(int));
+  size_t sm = (size_t)((NTHR / 32) * npw * dim * TILE + NTHR) * sizeof(double) +
+              (R.finite ? 0 : (size_t)R.ntype * R.n_phase * nd * (nd + R.m) * sizeof(double) + (size_t)R.ne * sizeof(int));
+  if (R.finite) sm = std::max(sm, (size_t)FS_SMEM_DBL * sizeof(double));  // element staging aliases the row buffers
+  return sm;
 }
 
 int rve_assemble_npw(const RveDev& R) {
@@ -480,26 +488,44 @@ int rve_assemble_npw(const RveDev& R) {
   return npw;
 }
 
-void launch_rve_assemble(const RveDev& R, int b0, int nb, double* Kt, double* Y, double* Cavg,
-                         double* Pavg, double* rfn, const double* Aq, const double* Pq,
-                         cudaStream_t s) {
+int rve_assemble_fs_slots(const RveDev& R) {
+  int dev = 0, sms = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t sm = rve_assemble_smem(R, R.npw);
-  if (R.finite) {
-    auto k = k_rve_assemble<2, false>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, rfn, Aq, Pq);
-  } else if (R.dim == 1) {  // the paper's 1-D benchmark on the device
+  cudaFuncSetAttribute(k_rve_assemble_fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(k_rve_assemble_fs, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_rve_assemble_fs, NTHR, sm);
+  return std::max(1, per) * std::max(1, sms);
+}
+
+void launch_rve_assemble_fs(const RveDev& R, int b0, int nb, const double* F, const double* w, double* Kt,
+                            double* Y, double* Cavg, double* Pavg, double* rfn, double* scratch, int slots,
+                            int* jflag, cudaStream_t s) {
+  const size_t sm = rve_assemble_smem(R, R.npw);
+  cudaFuncSetAttribute(k_rve_assemble_fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(k_rve_assemble_fs, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  k_rve_assemble_fs<<<std::min(nb, slots), NTHR, sm, s>>>(R, b0, nb, F, w, Kt, Y, Cavg, Pavg, rfn, scratch, jflag);
+}
+
+void launch_rve_assemble(const RveDev& R, int b0, int nb, double* Kt, double* Y, double* Cavg, double* Pavg,
+                         double* rfn, cudaStream_t s) {
+  const size_t sm = rve_assemble_smem(R, R.npw);
+  if (R.dim == 1) {  // the paper's 1-D benchmark on the device
     auto k = k_rve_assemble<1, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, rfn, Aq, Pq);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    k<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, rfn);
   } else if (R.dim == 2) {
     auto k = k_rve_assemble<2, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, rfn, Aq, Pq);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    k<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, rfn);
   } else {
     auto k = k_rve_assemble<3, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    k<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, rfn, Aq, Pq);
+    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    k<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, rfn);
   }
 }
 
