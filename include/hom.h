@@ -76,11 +76,12 @@ typedef struct {
 
 /* RVE mesh: an axis-aligned box meshed with Q1/hex8 elements whose opposite
  * faces carry matching nodes; the periodic pairing (eq:Con (iii)) is
- * found in hom_setup by coordinate matching.  Small strain: elements are grouped into
- * geometry types (element matrices equal to 1e-13 relative; a uniform grid has one) and the
- * per-(type, phase) matrices must fit K1's 96 KB shared-memory tables (e.g. <= 69 types x 2
- * phases in 2-D, <= 8 in 3-D); meshes with more distinct element geometries are rejected with
- * HOM_ERR_INVALID_ARG. */
+ * found in hom_setup by coordinate matching.  Any such mesh (graded, distorted interior) is
+ * accepted.  Small strain: elements are grouped into geometry types (element matrices equal to
+ * 1e-13 relative; a uniform grid has one); when the per-(type, phase) matrices fit K1's 96 KB
+ * shared-memory tables (e.g. <= 69 types x 2 phases in 2-D, <= 8 in 3-D) K1 reads them from
+ * shared memory, otherwise it combines the geometry tables (global memory, L2) with the element's
+ * (lambda, mu) on the fly. */
 typedef struct {
   int32_t dim;
   int32_t n_nodes;

@@ -289,16 +289,18 @@ typedef struct {
   double L;
   const double* xc; /* explicit mesh (macro problems on mapped / unstructured meshes) or NULL */
   const int* conn;
+  const double* axes; /* tensor-product grid: node coordinate k along axis d at axes[d*(r+1)+k]; NULL = uniform */
 } grid_t;
 
 static void grid_init(grid_t* g, int dim, int r, double L) {
   g->dim = dim; g->r = r; g->L = L; g->nen = nen_of(dim);
-  g->xc = NULL; g->conn = NULL;
+  g->xc = NULL; g->conn = NULL; g->axes = NULL;
   g->nnode = 1; g->nelem = 1;
   for (int k = 0; k < dim; ++k) { g->nnode *= (r + 1); g->nelem *= r; }
 }
 
 static void mesh_init(grid_t* g, int dim, int nnode, int nelem, const double* xc, const int* conn) {
+  g->axes = NULL;
   g->dim = dim; g->r = -1; g->L = 0.0; g->nen = nen_of(dim);
   g->nnode = nnode; g->nelem = nelem; g->xc = xc; g->conn = conn;
 }
@@ -320,7 +322,7 @@ static void grid_elem(const grid_t* g, int e, int* nodes, double x[][3]) {
       int ik = idx[k] + node_off(g->dim, a, k);
       n += ik * stride;
       stride *= (g->r + 1);
-      x[a][k] = ik * h;
+      x[a][k] = g->axes ? g->axes[k * (g->r + 1) + ik] : ik * h;
     }
     nodes[a] = n;
   }
@@ -428,10 +430,23 @@ static int sky_profile_from_grid(const grid_t* g, const int* eqmap, int neq, sky
  *                (i.e. W[j] = -X e_j in the GPU notation)
  * returns 0, ORC_ERR_NOT_SPD, ORC_ERR_OOM
  */
+static int rve_condense_linear_ax(int dim, int r, double L, const double* axes, int mode, const double* Cq,
+                                  double* C_eff, double* W);
 int orc_rve_condense_linear(int dim, int r, double L, int mode, const double* Cq, double* C_eff,
                             double* W) {
+  return rve_condense_linear_ax(dim, r, L, NULL, mode, Cq, C_eff, W);
+}
+/* the same on a tensor-product RVE grid with arbitrary (graded) node coordinates per axis,
+ * axes [dim][r+1] ascending (axes[d][0] and axes[d][r] are the periodic faces) */
+int orc_rve_condense_linear_axes(int dim, int r, const double* axes, int mode, const double* Cq, double* C_eff,
+                                 double* W) {
+  return rve_condense_linear_ax(dim, r, 1.0, axes, mode, Cq, C_eff, W);
+}
+static int rve_condense_linear_ax(int dim, int r, double L, const double* axes, int mode, const double* Cq,
+                                  double* C_eff, double* W) {
   if (dim < 1 || dim > 3 || r < 1 || mode < 0 || mode > 2) return ORC_ERR_ARG;
   grid_t g; grid_init(&g, dim, r, L);
+  g.axes = axes;
   int m = m_of(dim, 0), nq = 1 << dim, nd = g.nen * dim;
   rvemap_t mp;
   int rc = rvemap_build(&g, mode, &mp);
@@ -708,6 +723,7 @@ typedef struct {
   int kind; /* 0 linear, 1 nh */
   int dim, r, n_rve, phase_per_rve, mat_per_rve, n_phase, mstride;
   double L;
+  const double* axes; /* linear: tensor-product RVE grid coordinates or NULL */
   const uint8_t* phase;
   const double* mat;
   const double* Fbar; const double* w;
@@ -736,8 +752,8 @@ static void* batch_worker(void* arg) {
         orc_linear_C(dim, mt[2 * ph[e]], mt[2 * ph[e] + 1], C);
         for (int q = 0; q < nq; ++q) memcpy(&Cq[((size_t)e * nq + q) * m * m], C, sizeof(double) * m * m);
       }
-      rc = orc_rve_condense_linear(dim, r, 1.0, 0, Cq, &b->C_eff[(size_t)i * m * m],
-                                   b->W ? &b->W[(size_t)i * m * npad] : NULL);
+      rc = rve_condense_linear_ax(dim, r, 1.0, b->axes, 0, Cq, &b->C_eff[(size_t)i * m * m],
+                                  b->W ? &b->W[(size_t)i * m * npad] : NULL);
     } else {
       rc = orc_rve_condense_nh(r, b->L, b->mstride, ph, mt, &b->Fbar[(size_t)i * 4],
                                b->w ? &b->w[(size_t)i * npad] : NULL,
@@ -778,6 +794,19 @@ int orc_condense_batch_linear(int dim, int r, int n_rve, int phase_per_rve, cons
   batch_t b;
   memset(&b, 0, sizeof(b));
   b.kind = 0; b.dim = dim; b.r = r; b.n_rve = n_rve; b.phase_per_rve = phase_per_rve; b.mstride = 2; b.L = 1.0;
+  b.mat_per_rve = mat_per_rve; b.n_phase = n_phase; b.phase = phase; b.mat = mat;
+  b.C_eff = C_eff; b.W = W;
+  return run_batch(&b, nthreads, bad_rve);
+}
+
+/* Linear batch on a tensor-product (graded) RVE grid: axes [dim][r+1]; otherwise as above. */
+int orc_condense_batch_linear_axes(int dim, int r, const double* axes, int n_rve, int phase_per_rve,
+                                   const uint8_t* phase, int mat_per_rve, int n_phase, const double* mat,
+                                   double* C_eff, double* W, int nthreads, int* bad_rve) {
+  batch_t b;
+  memset(&b, 0, sizeof(b));
+  b.kind = 0; b.dim = dim; b.r = r; b.n_rve = n_rve; b.phase_per_rve = phase_per_rve; b.mstride = 2; b.L = 1.0;
+  b.axes = axes;
   b.mat_per_rve = mat_per_rve; b.n_phase = n_phase; b.phase = phase; b.mat = mat;
   b.C_eff = C_eff; b.W = W;
   return run_batch(&b, nthreads, bad_rve);

@@ -51,6 +51,8 @@ def lib():
             L.orc_rve_condense_linear.argtypes = [I, I, D, I, P, P, P]
             L.orc_rve_condense_nh.argtypes = [I, D, I, P, P, P, P, P, P, P, P, P, P]
             L.orc_condense_batch_linear.argtypes = [I, I, I, I, P, I, I, P, P, P, I, P]
+            L.orc_condense_batch_linear_axes.argtypes = [I, I, P, I, I, P, I, I, P, P, P, I, P]
+            L.orc_rve_condense_linear_axes.argtypes = [I, I, P, I, P, P, P]
             L.orc_condense_batch_nh.argtypes = [I, D, I, I, I, P, I, I, P, P, P, P, P, P, P, P, P, I, P]
             L.orc_macro_kin.argtypes = [I, I, D, I, P, P]
             L.orc_macro_residual.argtypes = [I, I, D, I, P, P, P]
@@ -122,8 +124,9 @@ def rve_condense_linear(dim: int, r: int, Cq, mode: int = 0, L: float = 1.0, wan
 
 
 def condense_batch_linear(dim: int, r: int, phase, mat, n_rve: int | None = None,
-                          want_W: bool = False, nthreads: int | None = None):
-    """Batched linear condensation.  phase [n_rve|1][r^dim] u8, mat [n_rve|1][n_phase][2] (E, nu)."""
+                          want_W: bool = False, nthreads: int | None = None, axes=None):
+    """Batched linear condensation.  phase [n_rve|1][r^dim] u8, mat [n_rve|1][n_phase][2] (E, nu);
+    axes [dim][r+1]: node coordinates of a tensor-product (graded) RVE grid (None = uniform [0,1]^dim)."""
     phase = np.ascontiguousarray(phase, dtype=np.uint8)
     mat = _f64(mat)
     nel = r ** dim
@@ -136,9 +139,15 @@ def condense_batch_linear(dim: int, r: int, phase, mat, n_rve: int | None = None
     C = np.zeros((n_rve, m, m))
     W = np.zeros((n_rve, m, dim * nel)) if want_W else None
     bad = ctypes.c_int(-1)
-    rc = lib().orc_condense_batch_linear(dim, r, n_rve, int(phase.shape[0] > 1), _p(phase),
-                                         int(mat.shape[0] > 1), n_phase, _p(mat), _p(C), _p(W),
-                                         nthreads or default_threads(), ctypes.byref(bad))
+    if axes is not None:
+        ax = _f64(np.asarray(axes, dtype=np.float64).reshape(dim, r + 1))
+        rc = lib().orc_condense_batch_linear_axes(dim, r, _p(ax), n_rve, int(phase.shape[0] > 1), _p(phase),
+                                                  int(mat.shape[0] > 1), n_phase, _p(mat), _p(C), _p(W),
+                                                  nthreads or default_threads(), ctypes.byref(bad))
+    else:
+        rc = lib().orc_condense_batch_linear(dim, r, n_rve, int(phase.shape[0] > 1), _p(phase),
+                                             int(mat.shape[0] > 1), n_phase, _p(mat), _p(C), _p(W),
+                                             nthreads or default_threads(), ctypes.byref(bad))
     if rc:
         raise OracleError(rc, "condense_batch_linear", bad.value)
     return (C, W) if want_W else C
@@ -253,16 +262,17 @@ def solve_linear(wl, rve_ids=None, nthreads: int | None = None):
     Returns dict(C_eff [B][m][m], u [n_dof], eps [B][m], W [B or subset][m][N_pad]).
     """
     dim, r = wl.dim, wl.r
+    axes = getattr(wl, "rve_axes", None)
     shared = wl.phase.shape[0] == 1 and wl.mat.shape[0] == 1
     if shared:
-        C1, W1 = condense_batch_linear(dim, r, wl.phase, wl.mat, 1, want_W=True, nthreads=nthreads)
+        C1, W1 = condense_batch_linear(dim, r, wl.phase, wl.mat, 1, want_W=True, nthreads=nthreads, axes=axes)
         C = np.broadcast_to(C1, (wl.n_rve,) + C1.shape[1:]).copy()
         Wsel = W1[0]
     else:
         ids = np.arange(wl.n_rve) if rve_ids is None else np.asarray(rve_ids)
         ph = wl.phase[ids] if wl.phase.shape[0] > 1 else wl.phase
         mt = wl.mat[ids] if wl.mat.shape[0] > 1 else wl.mat
-        Csub, Wsel = condense_batch_linear(dim, r, ph, mt, len(ids), want_W=True, nthreads=nthreads)
+        Csub, Wsel = condense_batch_linear(dim, r, ph, mt, len(ids), want_W=True, nthreads=nthreads, axes=axes)
         if rve_ids is None:
             C = Csub
         else:

@@ -180,9 +180,13 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
                                              const double* __restrict__ EL, double* smem) {
   double* s_row = smem;                      // [8 warps][npw][DIM][64] tile-row buffers
   double* red = s_row + (NTHR / 32) * R.npw * DIM * TILE;  // [NTHR] reduction scratch
-  double* s_K = red + NTHR;                  // [ntype][n_phase][ND][ND] element matrices (ISO)
-  double* s_F = s_K + (ISO ? R.ntype * R.n_phase * ((1 << DIM) * DIM) * ((1 << DIM) * DIM) : 0);  // [type][phase][ND][m]
-  int* s_ep = reinterpret_cast<int*>(s_F + (ISO ? R.ntype * R.n_phase * ((1 << DIM) * DIM) * R.m : 0));
+  // ISO element tables: [ntype][n_phase][ND][ND] (K_e) and [ntype][n_phase][ND][m] (K_fe rows) per RVE in shared
+  // memory, or -- when they do not fit (R.gtab: meshes with many distinct element geometries) -- only the
+  // per-phase (lam, mu) here and the geometry tables Klam/Kmu/FlamT/FmuT read from global memory (L2)
+  const int ntab = ISO ? (R.gtab ? 0 : R.ntype * R.n_phase) : 0;
+  double* s_K = red + NTHR;
+  double* s_F = s_K + (ISO ? (R.gtab ? 2 * R.n_phase : ntab * ((1 << DIM) * DIM) * ((1 << DIM) * DIM)) : 0);
+  int* s_ep = reinterpret_cast<int*>(s_F + (ISO ? ntab * ((1 << DIM) * DIM) * R.m : 0));
   const int tid = threadIdx.x;
   const int ne = R.ne;
   constexpr int ND = ISO ? (1 << DIM) * DIM : 8;  // nen*dim
@@ -190,15 +194,24 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
   if (ISO) {
     const uint8_t* ph = R.phase + (R.phase_per_rve ? (long)b * ne : 0);
     const double* mt = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * R.mat_stride : 0);
-    for (int e = tid; e < ne; e += NTHR) s_ep[e] = R.etype[e] * R.n_phase + ph[e];
+    if (R.gtab) {  // (type << 8 | phase) per element, (lam, mu) per phase
+      for (int e = tid; e < ne; e += NTHR) s_ep[e] = (R.etype[e] << 8) | ph[e];
+      for (int pp = tid; pp < R.n_phase; pp += NTHR) {
+        const double E = mt[2 * pp], nu = mt[2 * pp + 1];
+        s_K[2 * pp] = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu));
+        s_K[2 * pp + 1] = E / (2.0 * (1.0 + nu));
+      }
+    } else {
+      for (int e = tid; e < ne; e += NTHR) s_ep[e] = R.etype[e] * R.n_phase + ph[e];
+    }
     // K_e = lam Klam_t + mu Kmu_t for every (element type t, phase) of this RVE
-    for (int i = tid; i < R.ntype * R.n_phase * ND * ND; i += NTHR) {
+    for (int i = tid; i < ntab * ND * ND; i += NTHR) {
       const int t = i / (R.n_phase * ND * ND), pp = (i / (ND * ND)) % R.n_phase, j = i % (ND * ND);
       const double E = mt[2 * pp], nu = mt[2 * pp + 1];
       const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)), mu = E / (2.0 * (1.0 + nu));
       s_K[i] = lam * R.Klam[(long)t * ND * ND + j] + mu * R.Kmu[(long)t * ND * ND + j];
     }
-    for (int i = tid; i < R.ntype * R.n_phase * ND * R.m; i += NTHR) {  // K_fe element tables
+    for (int i = tid; i < ntab * ND * R.m; i += NTHR) {  // K_fe element tables
       const int t = i / (R.n_phase * ND * R.m), pp = (i / (ND * R.m)) % R.n_phase, j = i % (ND * R.m);
       const double E = mt[2 * pp], nu = mt[2 * pp + 1];
       const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)), mu = E / (2.0 * (1.0 + nu));
@@ -266,7 +279,14 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
       if (i < R.npad && p != R.corner) {
         for (int s = R.inc_ptr[p]; s < R.inc_ptr[p + 1]; ++s) {
           int e = R.inc[s] >> 4, a = R.inc[s] & 15;
-          if (ISO) {
+          if (ISO && R.gtab) {
+            const int tp = s_ep[e], t = tp >> 8, pp = tp & 255;
+            const double lam = s_K[2 * pp], mu = s_K[2 * pp + 1];
+            const long o = ((long)t * ND + a * DIM + c) * R.m;
+#pragma unroll
+            for (int k = 0; k < RHSW; ++k)
+              if (k < R.m) out[k] += lam * __ldg(R.FlamT + o + k) + mu * __ldg(R.FmuT + o + k);
+          } else if (ISO) {
             const double* fe = s_F + ((long)s_ep[e] * ND + a * DIM + c) * R.m;
 #pragma unroll
             for (int k = 0; k < RHSW; ++k)
@@ -359,6 +379,11 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
             // (small strain) or the CTA's L2-resident element record, K_e packed lower-triangular
             auto blk_at = [&](int code, int i, int jj) -> double {
               const int e = code >> 8, r = ((code >> 4) & 15) * DIM + i, c = (code & 15) * DIM + jj;
+              if (ISO && R.gtab) {
+                const int tp = s_ep[e], t = tp >> 8, pp = tp & 255;
+                const long o = (long)t * ND * ND + r * ND + c;
+                return s_K[2 * pp] * __ldg(R.Klam + o) + s_K[2 * pp + 1] * __ldg(R.Kmu + o);
+              }
               if (ISO) return s_K[(long)s_ep[e] * ND * ND + r * ND + c];
               return EL[(long)e * EL_STRIDE + EL_K + pk8(r, c)];
             };
@@ -475,7 +500,9 @@ __global__ void __launch_bounds__(NTHR, 4) k_rve_assemble_fs(RveDev R, int b0, i
 size_t rve_assemble_smem(const RveDev& R, int npw) {
   const int dim = R.finite ? 2 : R.dim, nd = (1 << dim) * dim;  // nen*dim
   size_t sm = (size_t)((NTHR / 32) * npw * dim * TILE + NTHR) * sizeof(double) +
-              (R.finite ? 0 : (size_t)R.ntype * R.n_phase * nd * (nd + R.m) * sizeof(double) + (size_t)R.ne * sizeof(int));
+              (R.finite ? 0
+                   : (R.gtab ? (size_t)2 * R.n_phase : (size_t)R.ntype * R.n_phase * nd * (nd + R.m)) * sizeof(double) +
+                         (size_t)R.ne * sizeof(int));
   if (R.finite) sm = std::max(sm, (size_t)FS_SMEM_DBL * sizeof(double));  // element staging aliases the row buffers
   return sm;
 }

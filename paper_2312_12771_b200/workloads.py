@@ -101,6 +101,7 @@ class Workload:
     nodal_force: np.ndarray | None = None    # [n_dof] external nodal forces (surface tractions)
     rve_size: float = 1.0
     rve_origin: float = 0.0
+    rve_axes: np.ndarray | None = None     # [dim][r+1] node coordinates of a graded tensor-product RVE grid
 
     @property
     def n_qp(self) -> int:
@@ -134,6 +135,10 @@ class Workload:
 
     def rve_mesh(self):
         coords, conn = grid_mesh(self.dim, self.r, self.rve_size)
+        if self.rve_axes is not None:  # graded tensor-product grid: node index -> axis coordinate
+            idx = np.rint(coords * (self.r / self.rve_size)).astype(np.int64)
+            coords = np.stack([self.rve_axes[d][idx[:, d]] for d in range(self.dim)], -1)
+            return np.ascontiguousarray(coords), conn
         return np.ascontiguousarray(coords + self.rve_origin), conn
 
     def flop_per_rve(self) -> float:
@@ -274,6 +279,36 @@ def bench1d(k: int) -> Workload:
     return Workload(f"bench1d_k{k}", 1, n, n, "linear", np.arange(n, dtype=np.uint8)[None], mat,
                     np.array([0, n], np.int32), np.array([0.0, phi1000]), np.array([1.0]),
                     description=f"paper 1-D benchmark, 2^{k} elements per scale", macro_coords=coords)
+
+
+def graded_axes(r: int, dim: int, a: float = 0.6) -> np.ndarray:
+    """Graded node coordinates per axis on [0,1]: x(s) = s - a sin(2 pi s) / (2 pi), s = k / r
+    (monotone for a < 1, element widths from (1 - a)/r at the faces to (1 + a)/r in the middle,
+    symmetric about 1/2; the periodic faces stay at 0 and 1)."""
+    s = np.arange(r + 1) / r
+    x = s - a * np.sin(2 * np.pi * s) / (2 * np.pi)
+    x[0], x[-1] = 0.0, 1.0
+    return np.tile(x, (dim, 1))
+
+
+def graded(dim: int = 2, nel: int = 4, r: int = 16, seed: int = SEED, a: float = 0.6) -> Workload:
+    """A graded periodic RVE (the K1 path for meshes with many distinct element geometries, DESIGN.md
+    §5.3): config 3's inputs (per-RVE random phases and moduli, body force, clamped left edge) in 2-D,
+    config 4's (affine uniaxial strain, all boundary nodes) in 3-D, on a tensor-product RVE grid with
+    the element widths of graded_axes."""
+    wl = config3(nel=nel, r=r, seed=seed) if dim == 2 else config4(nel=nel, r=r)
+    if dim == 3:  # per-RVE random phases / moduli in 3-D as well
+        n = wl.n_rve
+        e = np.arange(r ** 3)
+        b = np.arange(n)[:, None]
+        wl.phase = (uniform(seed, 0, b, e[None, :]) < 0.4).astype(np.uint8)
+        u1 = uniform(seed, 1, b, np.arange(2)[None, :])
+        u2 = uniform(seed, 2, b, np.arange(2)[None, :])
+        wl.mat = np.stack([10.0 ** (2 * u1), 0.2 + 0.2 * u2], -1)
+    wl.rve_axes = graded_axes(r, dim, a)
+    wl.name = f"graded{dim}d"
+    wl.description = f"{dim}-D graded periodic RVE {r}^{dim} (x = s - {a} sin(2 pi s)/(2 pi)), per-RVE random phases"
+    return wl
 
 
 CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}

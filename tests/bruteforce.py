@@ -30,7 +30,9 @@ def _qps(dim):
 
 
 def _grads(dim, h, xi):
-    """Physical gradients of the multilinear shape functions on an axis-aligned cube of size h."""
+    """Physical gradients of the multilinear shape functions on an axis-aligned box with edge
+    lengths h (a scalar: cube)."""
+    h = np.broadcast_to(np.asarray(h, dtype=float), (dim,))
     sn = _ref_nodes(dim)
     out = np.zeros((len(sn), dim))
     for a, s in enumerate(sn):
@@ -39,7 +41,7 @@ def _grads(dim, h, xi):
             for l in range(dim):
                 if l != k:
                     v *= (1 + s[l] * xi[l]) / 2.0
-            out[a, k] = v * 2.0 / h
+            out[a, k] = v * 2.0 / h[k]
     return out
 
 
@@ -126,10 +128,11 @@ class Monolithic:
     basis "constant": one per macro element, shared by its Gauss points (eq:constSolution1/2,
     P:294-315) -- the micro equations are then integrated over the whole element."""
 
-    def __init__(self, dim, nel, r, tangent_of, dir_dof, body=None, basis="dirac"):
+    def __init__(self, dim, nel, r, tangent_of, dir_dof, body=None, basis="dirac", rve_axes=None):
         """tangent_of(b, e) -> full-gradient tangent (dim^2 x dim^2) for linear problems
         (b = fluctuation field index: Gauss point or element)."""
         self.dim, self.nel, self.r = dim, nel, r
+        self.rve_axes = rve_axes  # [dim][r+1] node coordinates of a tensor-product RVE grid (None: uniform)
         self.tangent_of = tangent_of
         self.dir_dof = np.asarray(dir_dof)
         self.body = body
@@ -152,11 +155,15 @@ class Monolithic:
     def _micro_ops(self):
         dim, r = self.dim, self.r
         for e in range(r ** dim):
-            nodes, _ = _elem_nodes(dim, r, e)
+            nodes, idx = _elem_nodes(dim, r, e)
             fd = np.concatenate([self.dofmap[n] for n in nodes])
+            if self.rve_axes is None:
+                h = np.full(dim, 1.0 / r)
+            else:
+                h = np.array([self.rve_axes[k][idx[k] + 1] - self.rve_axes[k][idx[k]] for k in range(dim)])
             for xi in _qps(dim):
-                g = _grads(dim, 1.0 / r, xi)
-                yield e, fd, _grad_op(dim, g), (1.0 / r) ** dim / 2 ** dim * 1.0
+                g = _grads(dim, h, xi)
+                yield e, fd, _grad_op(dim, g), np.prod(h) / 2 ** dim
 
     def assemble(self, u=None, w=None, material=None):
         """Hessian and gradient of the two-scale energy (linear: quadratic energy).
@@ -176,8 +183,7 @@ class Monolithic:
             if self.basis == "constant":
                 b = b // self.nq  # the element's single fluctuation field
             off = self.ndof_M + b * self.nf
-            for e, fd, Bf, wm in self._micro_ops():
-                wm = (0.5 / self.r) ** dim
+            for e, fd, Bf, wm in self._micro_ops():  # wm = det J (unit Gauss weights) of the micro element
                 free = fd >= 0
                 cols = np.concatenate([np.asarray(mdofs), off + fd[free]])
                 Bfull = np.concatenate([Bm, Bf[:, free]], axis=1)

@@ -482,9 +482,13 @@ def test_fluctuations_keep_the_natural_layout(torch_cuda):
 
 
 # ------------------------------------------------------------------ K1 alone (hom_debug_rve_kff)
-@pytest.mark.parametrize("dim,r,ordering,tile_sparse", [(2, 5, "folded", False), (2, 6, "natural", True),
-                                                        (2, 12, "folded", True), (3, 3, "folded", False)])
-def test_k1_kff_equals_bruteforce_micro_block(torch_cuda, dim, r, ordering, tile_sparse):
+@pytest.mark.parametrize("dim,r,ordering,tile_sparse,graded", [(2, 5, "folded", False, False),
+                                                               (2, 6, "natural", True, False),
+                                                               (2, 12, "folded", True, False),
+                                                               (3, 3, "folded", False, False),
+                                                               (2, 12, "folded", False, True),
+                                                               (3, 4, "natural", True, True)])
+def test_k1_kff_equals_bruteforce_micro_block(torch_cuda, dim, r, ordering, tile_sparse, graded):
     """The assembled K_ff of one RVE, entry by entry, against the micro-micro block L of the
     brute-force monolithic assembly (tests/bruteforce.py, own shape functions and periodic map):
     L_b = eta_M K_ff (R2), with random per-element phases and per-RVE moduli."""
@@ -499,6 +503,8 @@ def test_k1_kff_equals_bruteforce_micro_block(torch_cuda, dim, r, ordering, tile
         wl.phase = (rng.random((wl.n_rve, r ** 3)) < 0.4).astype(np.uint8)
         wl.mat = np.stack([np.array([[1.0 + rng.random(), 0.25], [20.0 * rng.random() + 1.0, 0.3]])
                            for _ in range(wl.n_rve)])
+    if graded:  # every element a different box: the K1 global-table path (hom_rve_mesh)
+        wl.rve_axes = W.graded_axes(r, dim, 0.6)
     b = 1
     h = Homogenizer.from_workload(wl, rve_ordering=ordering, tile_sparse=tile_sparse)
     K = h.debug_rve_kff(b).cpu().numpy()
@@ -506,13 +512,26 @@ def test_k1_kff_equals_bruteforce_micro_block(torch_cuda, dim, r, ordering, tile
     mt = wl.mat[b] if wl.mat.ndim == 3 and wl.mat.shape[0] > 1 else (wl.mat[0] if wl.mat.ndim == 3 else wl.mat)
     E = np.array([mt[p, 0] for p in ph]).reshape(1, -1).repeat(wl.n_rve, 0)
     nu = np.array([mt[p, 1] for p in ph]).reshape(1, -1).repeat(wl.n_rve, 0)
-    mono = bf.Monolithic(dim, 1, r, lambda bb, e: bf.iso_tangent_full(dim, E[bb, e], nu[bb, e]), wl.dir_dof)
+    mono = bf.Monolithic(dim, 1, r, lambda bb, e: bf.iso_tangent_full(dim, E[bb, e], nu[bb, e]), wl.dir_dof,
+                         rve_axes=wl.rve_axes)
     Kg, _ = mono.assemble(u=np.zeros(mono.ndof_M))
     off = mono.ndof_M + b * mono.nf
     L = Kg[off:off + mono.nf, off:off + mono.nf] / (0.5 / 1) ** dim  # / eta_M of the 1-element macro mesh
     assert rel(K[dim:, dim:], L) <= 1e-13
     assert np.array_equal(K[:dim, :dim], np.eye(dim)) and not K[:dim, dim:].any() and not K[dim:, :dim].any()
     assert np.array_equal(K, K.T)
+
+
+# ------------------------------------------------------------------ graded (general) RVE meshes
+@pytest.mark.parametrize("dim,nel,r", [(2, 4, 32), (2, 3, 8), (3, 2, 6)])
+def test_graded_rve_matches_oracle(torch_cuda, dim, nel, r):
+    """A graded periodic RVE (W.graded: every element a different box, up to hundreds of element
+    geometries -- the K1 global-table path when the (type, phase) tables overflow shared memory, the
+    shared-memory path otherwise) with per-RVE random phases and moduli: C_eff, u, w against the
+    oracle's graded path (pinned by the graded monolithic brute force and closed forms)."""
+    wl = W.graded(dim, nel=nel, r=r)
+    for ts in (False, True):
+        check_linear_against_oracle(wl, tile_sparse=ts)
 
 
 # ------------------------------------------------------------------ RVE sharding (multi-GPU path, DESIGN.md §7)

@@ -201,10 +201,10 @@ def test_hill_mandel_energy_identity():
 
 
 # ---------------------------------------------------------------- brute force (e)
-def _brute_linear(dim, nel, r, E, nu, dir_dof, dir_val, body):
+def _brute_linear(dim, nel, r, E, nu, dir_dof, dir_val, body, rve_axes=None):
     def tangent(b, e):
         return bf.iso_tangent_full(dim, E[b, e], nu[b, e])
-    mono = bf.Monolithic(dim, nel, r, tangent, dir_dof, body)
+    mono = bf.Monolithic(dim, nel, r, tangent, dir_dof, body, rve_axes=rve_axes)
     u, wfree = mono.solve_linear(dir_val)
     return mono, u, mono.to_indep_layout(wfree)
 
@@ -231,6 +231,50 @@ def test_condensation_equals_monolithic_bruteforce(dim, nel, r):
     w = oracle.recover_linear(Wf, eps)
     np.testing.assert_allclose(u, u_bf, rtol=0, atol=1e-12 * np.abs(u_bf).max())
     np.testing.assert_allclose(w, w_bf, rtol=0, atol=1e-12 * np.abs(w_bf).max())
+
+
+@pytest.mark.parametrize("dim,nel,r", [(2, 2, 4), (3, 1, 3)])
+def test_graded_rve_condensation_equals_monolithic_bruteforce(dim, nel, r):
+    """Check (e) on a graded tensor-product RVE (every element a different box, W.graded_axes): the
+    oracle's graded path (orc_condense_batch_linear_axes) + macro solve + recovery equals the full
+    uncondensed monolithic solve built by tests/bruteforce.py's own box elements."""
+    rng = np.random.default_rng(31 + dim)
+    n_rve = nel ** dim * 2 ** dim
+    phase = (rng.random((n_rve, r ** dim)) < 0.4).astype(np.uint8)
+    mat = np.stack([10 ** (2 * rng.random((n_rve, 2))), 0.2 + 0.2 * rng.random((n_rve, 2))], -1)
+    E = np.take_along_axis(mat[..., 0], phase.astype(int), 1)
+    nu = np.take_along_axis(mat[..., 1], phase.astype(int), 1)
+    axes = W.graded_axes(r, dim, 0.6)
+    nodes = W.face_nodes(dim, nel, 0, 0)
+    dir_dof = np.array([n * dim + c for n in nodes for c in range(dim)], np.int32)
+    dir_val = 1e-3 * rng.standard_normal(len(dir_dof))
+    body = np.array([0.3, -1.0, 0.2][:dim])
+    mono, u_bf, w_bf = _brute_linear(dim, nel, r, E, nu, dir_dof, dir_val, body, rve_axes=axes)
+    C, Wf = oracle.condense_batch_linear(dim, r, phase, mat, n_rve, want_W=True, axes=axes)
+    u = oracle.macro_solve(dim, nel, C, dir_dof, dir_val, body=body)
+    w = oracle.recover_linear(Wf, oracle.macro_kin(dim, nel, u))
+    np.testing.assert_allclose(u, u_bf, rtol=0, atol=1e-12 * np.abs(u_bf).max())
+    np.testing.assert_allclose(w, w_bf, rtol=0, atol=1e-12 * np.abs(w_bf).max())
+    # the grading matters: the same phases on the uniform grid give different tangents
+    assert np.abs(C - oracle.condense_batch_linear(dim, r, phase, mat, n_rve)).max() > 1e-3 * np.abs(C).max()
+
+
+@pytest.mark.parametrize("dim,r", [(2, 8), (3, 4)])
+def test_graded_rve_homogeneous_and_laminate_closed_forms(dim, r):
+    """Graded grids keep the exact results: a homogeneous RVE returns C (any periodic mesh), and the
+    config-1 laminate with its interface on the grid line x = 1/2 (graded_axes is symmetric about
+    1/2) returns the Backus moduli of tests/golden/laminate_cfg1.json (exact for Q1)."""
+    axes = W.graded_axes(r, dim, 0.6)
+    C1 = oracle.linear_C(dim, 3.3, 0.27)
+    Ch = oracle.condense_batch_linear(dim, r, np.zeros((1, r ** dim), np.uint8), np.array([[[3.3, 0.27]]]), 1,
+                                      axes=axes)[0]
+    np.testing.assert_allclose(Ch, C1, rtol=0, atol=1e-13 * np.abs(C1).max())
+    if dim == 2:
+        g = json.load(open(os.path.join(GOLD, "laminate_cfg1.json")))
+        xc = 0.5 * (axes[0][:-1] + axes[0][1:])
+        phase = np.tile((xc >= 0.5).astype(np.uint8), r)[None]  # x fastest
+        C = oracle.condense_batch_linear(2, r, phase, np.array([[[1.0, 0.3], [10.0, 0.3]]]), 1, axes=axes)[0]
+        np.testing.assert_allclose(C, np.array(g["C_eff_voigt"]), rtol=0, atol=1e-12)
 
 
 def test_nh_newton_step_equals_monolithic_bruteforce():
