@@ -12,7 +12,15 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: ranges are no-ops unless a profiler injects itself
+
 #include "hom_internal.cuh"
+
+// NVTX range over one C-ABI call (visible in nsys / ncu --nvtx timelines)
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
 
 using hom::CgState;
 using hom::MacroDev;
@@ -227,6 +235,7 @@ extern "C" {
 
 int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve, const hom_phase_field* ph,
               const hom_materials* mat, const hom_options* options, void* stream) {
+  NvtxScope nvtx_("hom_setup");
   if (!out) return HOM_ERR_INVALID_ARG;
   *out = nullptr;
   hom_ctx* c = new hom_ctx();
@@ -807,6 +816,7 @@ void run(hom_ctx* c, int cls, cudaStream_t s, F&& f) {
 }
 
 int hom_macro_kinematics(hom_ctx* c, const double* d_u, double* d_kin, void* stream) {
+  NvtxScope nvtx_("hom_macro_kinematics");
   if (!c || !d_u || !d_kin) return set_err(c, HOM_ERR_INVALID_ARG, "hom_macro_kinematics: NULL");
   run(c, HOM_PROF_RECOVER, (cudaStream_t)stream,
       [&] { hom::launch_macro_kin(c->M, d_u, d_kin, 1, (cudaStream_t)stream); });
@@ -815,6 +825,7 @@ int hom_macro_kinematics(hom_ctx* c, const double* d_u, double* d_kin, void* str
 
 int hom_condense(hom_ctx* c, const double* d_kin, double* d_C_eff, double* d_P_eff, double* d_P_avg,
                  void* stream) {
+  NvtxScope nvtx_("hom_condense");
   if (!c || !d_C_eff) return set_err(c, HOM_ERR_INVALID_ARG, "hom_condense: NULL");
   if (c->finite && !d_kin) return set_err(c, HOM_ERR_INVALID_ARG, "hom_condense: finite strain needs F");
   cudaStream_t s = (cudaStream_t)stream;
@@ -901,6 +912,7 @@ int hom_debug_rve_kff(hom_ctx* c, int rve, double* d_Kff, void* stream) {
 
 int hom_macro_solve(hom_ctx* c, const double* d_D, const double* d_S, double scale, double* d_x,
                     hom_solve_info* info, void* stream) {
+  NvtxScope nvtx_("hom_macro_solve");
   if (!c || !d_D || !d_x) return set_err(c, HOM_ERR_INVALID_ARG, "hom_macro_solve: NULL");
   cudaStream_t s = (cudaStream_t)stream;
   run(c, HOM_PROF_MACRO_ASSEMBLE, s, [&] { hom::launch_macro_assemble(c->M, d_D, c->val, c->diag, s); });
@@ -938,6 +950,7 @@ int hom_macro_solve(hom_ctx* c, const double* d_D, const double* d_S, double sca
 }
 
 int hom_macro_residual_norm(hom_ctx* c, const double* d_S, double* norm, void* stream) {
+  NvtxScope nvtx_("hom_macro_residual_norm");
   if (!c || !norm) return set_err(c, HOM_ERR_INVALID_ARG, "hom_macro_residual_norm: NULL");
   cudaStream_t s = (cudaStream_t)stream;
   run(c, HOM_PROF_MACRO_ASSEMBLE, s, [&] { hom::launch_macro_rhs(c->M, nullptr, d_S, 0.0, nullptr, c->Rfree, s); });
@@ -947,6 +960,7 @@ int hom_macro_residual_norm(hom_ctx* c, const double* d_S, double* norm, void* s
 }
 
 int hom_recover_fluctuations(hom_ctx* c, const double* d_x, double* d_w, void* stream) {
+  NvtxScope nvtx_("hom_recover_fluctuations");
   if (!c || !d_x) return set_err(c, HOM_ERR_INVALID_ARG, "hom_recover_fluctuations: NULL");
   if (!c->finite && !d_w) return set_err(c, HOM_ERR_INVALID_ARG, "hom_recover_fluctuations: d_w NULL");
   cudaStream_t s = (cudaStream_t)stream;
@@ -963,6 +977,7 @@ int hom_recover_fluctuations(hom_ctx* c, const double* d_x, double* d_w, void* s
 }
 
 int hom_newton_update(hom_ctx* c, double* d_u, const double* d_du, void* stream) {
+  NvtxScope nvtx_("hom_newton_update");
   if (!c || !d_u || !d_du || !c->finite) return set_err(c, HOM_ERR_INVALID_ARG, "hom_newton_update");
   cudaStream_t s = (cudaStream_t)stream;
   run(c, HOM_PROF_RECOVER, s, [&] { hom::launch_macro_kin(c->M, d_du, c->kin, 0, s); });
@@ -1003,6 +1018,7 @@ int hom_macro_update(hom_ctx* c, double* d_u, const double* d_du, void* stream) 
 }
 
 int hom_set_phases(hom_ctx* c, const uint8_t* h_phase, const double* h_params, void* stream) {
+  NvtxScope nvtx_("hom_set_phases");
   if (!c) return HOM_ERR_INVALID_ARG;
   cudaStream_t s = (cudaStream_t)stream;
   if (h_phase) {

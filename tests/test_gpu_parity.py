@@ -335,6 +335,21 @@ def test_cg_not_converged_status(torch_cuda):
     assert e.value.code == 5
 
 
+@pytest.mark.parametrize("nel", [8, 200])
+def test_cg_breakdown_status(torch_cuda, nel):
+    """A negative definite macro operator (the condensed tangents negated) makes p^T K p < 0 in the
+    first PCG iteration: HOM_ERR_CG_BREAKDOWN, not a crash or a silent wrong answer -- on the cluster
+    kernel (nel 8) and on the grid-wide kernels (nel 200: > 32768 DOFs)."""
+    from paper_2312_12771_b200.hom import Homogenizer, HomError
+    wl = W.config2(nel=nel, r=2)
+    h = Homogenizer.from_workload(wl, rve_range=(0, 4) if nel > 8 else None)
+    C = h.condense()
+    C = (-C[:4].mean(0)).expand(wl.n_rve, -1, -1).contiguous() if nel > 8 else -C
+    with pytest.raises(HomError) as e:
+        h.macro_solve(C)
+    assert e.value.code == 6
+
+
 # ------------------------------------------------------------------ tile-sparse factorisation (SURVEY §8(f) 3)
 # Only the tiles of the symbolic tile-level fill are stored and factored; every skipped
 # product is an exact zero, so the results must equal the dense path bit for bit.
