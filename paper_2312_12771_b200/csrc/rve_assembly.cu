@@ -173,7 +173,7 @@ __device__ __forceinline__ void nh_elements(const RveDev& R, int b, int e0, int 
   __syncthreads();  // sQ reused by the next block
 }
 
-template <int DIM, bool ISO>
+template <int DIM, bool ISO, bool GT = false>  // GT: global geometry tables (RveDev::gtab)
 __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const int bl, double* __restrict__ Kt,
                                              double* __restrict__ Y, double* __restrict__ Cavg,
                                              double* __restrict__ Pavg, double* __restrict__ rfn,
@@ -183,9 +183,9 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
   // ISO element tables: [ntype][n_phase][ND][ND] (K_e) and [ntype][n_phase][ND][m] (K_fe rows) per RVE in shared
   // memory, or -- when they do not fit (R.gtab: meshes with many distinct element geometries) -- only the
   // per-phase (lam, mu) here and the geometry tables Klam/Kmu/FlamT/FmuT read from global memory (L2)
-  const int ntab = ISO ? (R.gtab ? 0 : R.ntype * R.n_phase) : 0;
+  const int ntab = ISO ? (GT ? 0 : R.ntype * R.n_phase) : 0;
   double* s_K = red + NTHR;
-  double* s_F = s_K + (ISO ? (R.gtab ? 2 * R.n_phase : ntab * ((1 << DIM) * DIM) * ((1 << DIM) * DIM)) : 0);
+  double* s_F = s_K + (ISO ? (GT ? 2 * R.n_phase : ntab * ((1 << DIM) * DIM) * ((1 << DIM) * DIM)) : 0);
   int* s_ep = reinterpret_cast<int*>(s_F + (ISO ? ntab * ((1 << DIM) * DIM) * R.m : 0));
   const int tid = threadIdx.x;
   const int ne = R.ne;
@@ -194,7 +194,7 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
   if (ISO) {
     const uint8_t* ph = R.phase + (R.phase_per_rve ? (long)b * ne : 0);
     const double* mt = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * R.mat_stride : 0);
-    if (R.gtab) {  // (type << 8 | phase) per element, (lam, mu) per phase
+    if (GT) {  // (type << 8 | phase) per element, (lam, mu) per phase
       for (int e = tid; e < ne; e += NTHR) s_ep[e] = (R.etype[e] << 8) | ph[e];
       for (int pp = tid; pp < R.n_phase; pp += NTHR) {
         const double E = mt[2 * pp], nu = mt[2 * pp + 1];
@@ -279,7 +279,7 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
       if (i < R.npad && p != R.corner) {
         for (int s = R.inc_ptr[p]; s < R.inc_ptr[p + 1]; ++s) {
           int e = R.inc[s] >> 4, a = R.inc[s] & 15;
-          if (ISO && R.gtab) {
+          if (ISO && GT) {
             const int tp = s_ep[e], t = tp >> 8, pp = tp & 255;
             const double lam = s_K[2 * pp], mu = s_K[2 * pp + 1];
             const long o = ((long)t * ND + a * DIM + c) * R.m;
@@ -379,7 +379,7 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
             // (small strain) or the CTA's L2-resident element record, K_e packed lower-triangular
             auto blk_at = [&](int code, int i, int jj) -> double {
               const int e = code >> 8, r = ((code >> 4) & 15) * DIM + i, c = (code & 15) * DIM + jj;
-              if (ISO && R.gtab) {
+              if (ISO && GT) {
                 const int tp = s_ep[e], t = tp >> 8, pp = tp & 255;
                 const long o = (long)t * ND * ND + r * ND + c;
                 return s_K[2 * pp] * __ldg(R.Klam + o) + s_K[2 * pp + 1] * __ldg(R.Kmu + o);
@@ -447,12 +447,12 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
   }
 }
 
-template <int DIM, bool ISO>
+template <int DIM, bool ISO, bool GT>
 __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double* __restrict__ Kt,
                                                        double* __restrict__ Y, double* __restrict__ Cavg,
                                                        double* __restrict__ Pavg, double* __restrict__ rfn) {
   extern __shared__ __align__(128) double smem[];
-  assemble_rve<DIM, ISO>(R, b0 + blockIdx.x, blockIdx.x, Kt, Y, Cavg, Pavg, rfn, nullptr, smem);
+  assemble_rve<DIM, ISO, GT>(R, b0 + blockIdx.x, blockIdx.x, Kt, Y, Cavg, Pavg, rfn, nullptr, smem);
 }
 
 // Finite strain, fused: a persistent CTA per slot walks its RVEs; for each it first
@@ -535,25 +535,27 @@ void launch_rve_assemble_fs(const RveDev& R, int b0, int nb, const double* F, co
   k_rve_assemble_fs<<<std::min(nb, slots), NTHR, sm, s>>>(R, b0, nb, F, w, Kt, Y, Cavg, Pavg, rfn, scratch, jflag);
 }
 
+template <int DIM, bool GT>
+static void launch_k1(const RveDev& R, int b0, int nb, double* Kt, double* Y, double* Cavg, double* Pavg, double* rfn,
+                      size_t sm, cudaStream_t s) {
+  auto k = k_rve_assemble<DIM, true, GT>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  k<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, rfn);
+}
+
 void launch_rve_assemble(const RveDev& R, int b0, int nb, double* Kt, double* Y, double* Cavg, double* Pavg,
                          double* rfn, cudaStream_t s) {
   const size_t sm = rve_assemble_smem(R, R.npw);
-  if (R.dim == 1) {  // the paper's 1-D benchmark on the device
-    auto k = k_rve_assemble<1, true>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    k<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, rfn);
-  } else if (R.dim == 2) {
-    auto k = k_rve_assemble<2, true>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    k<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, rfn);
-  } else {
-    auto k = k_rve_assemble<3, true>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    k<<<nb, NTHR, sm, s>>>(R, b0, Kt, Y, Cavg, Pavg, rfn);
-  }
+  if (R.dim == 1)  // the paper's 1-D benchmark on the device
+    R.gtab ? launch_k1<1, true>(R, b0, nb, Kt, Y, Cavg, Pavg, rfn, sm, s)
+           : launch_k1<1, false>(R, b0, nb, Kt, Y, Cavg, Pavg, rfn, sm, s);
+  else if (R.dim == 2)
+    R.gtab ? launch_k1<2, true>(R, b0, nb, Kt, Y, Cavg, Pavg, rfn, sm, s)
+           : launch_k1<2, false>(R, b0, nb, Kt, Y, Cavg, Pavg, rfn, sm, s);
+  else
+    R.gtab ? launch_k1<3, true>(R, b0, nb, Kt, Y, Cavg, Pavg, rfn, sm, s)
+           : launch_k1<3, false>(R, b0, nb, Kt, Y, Cavg, Pavg, rfn, sm, s);
 }
 
 }  // namespace hom
