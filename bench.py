@@ -371,6 +371,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-companions", action="store_true", help="skip the config-2 / config-5 companion keys")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the RVE-sharded multi-GPU path (NCCL process group, packed all-gather) even at N = 1 "
+                         "(exercises the --gpus N code path on one GPU)")
     ap.add_argument("--spmv-nel", type=int, default=2048, help="scaled macro mesh of the K6 SpMV roofline (0: skip)")
     ap.add_argument("--macro-basis", default="dirac", choices=["dirac", "constant"],
                     help="constant: one RVE per macro element (SURVEY §8(f) 2, small strain)")
@@ -393,7 +396,8 @@ def main():
     config = {"workload": f"{wl.name}: {wl.description}", "config_index": args.config,
               "n_rve": n_rve_run, "rve_dofs": wl.n_pad, "n_f": wl.n_f, "macro_dof": wl.n_dof,
               "flop_per_rve": wl.flop_per_rve(),
-              "parallelism": f"rve-sharded x{world} (C_eff all-gather, replicated macro CG)" if world > 1 else "single",
+              "parallelism": (f"rve-sharded x{world} (packed C_eff all-gather, replicated macro CG)"
+                              if world > 1 or args.sharded else "single"),
               "macro_nel": wl.nel, "rve_per_gpu": n_rve_run / world,
               "factorization": "tile-sparse" if args.tile_sparse else "dense", "macro_basis": args.macro_basis,
               "rve_ordering": args.rve_ordering}
@@ -423,15 +427,25 @@ def main():
 
     import numpy as np
     import torch
-    if world > 1:
+    dist_on = world > 1 or args.sharded  # the sharded path (one rank per GPU, NCCL)
+    if dist_on:
+        import socket
+
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if world > 1:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            with socket.socket() as so:
+                so.bind(("127.0.0.1", 0))
+                port = so.getsockname()[1]
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                    device_id=torch.device("cuda", local))
     else:
         torch.cuda.set_device(0)
     from paper_2312_12771_b200.hom import Homogenizer
 
-    if world > 1:
+    if dist_on:
         from paper_2312_12771_b200.dist import ShardedHomogenizer
         sh = ShardedHomogenizer(wl, tile_sparse=args.tile_sparse, macro_basis=args.macro_basis,
                                 rve_ordering=args.rve_ordering)
@@ -483,7 +497,7 @@ def main():
         cg_iters.append(info.iterations)
 
     def barrier():
-        if world > 1:
+        if dist_on:
             torch.distributed.barrier()
 
     for _ in range(args.warmup):
@@ -510,7 +524,7 @@ def main():
     prof = h.profile_read()
     h.profile(False)
     clocks = sampler.stop()
-    if world > 1:
+    if dist_on:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms = float(t.item())
@@ -579,7 +593,7 @@ def main():
     torch.cuda.synchronize()
     barrier()
     ms_e2e = e0.elapsed_time(e1)
-    if world > 1:
+    if dist_on:
         t = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_e2e = float(t.item())
@@ -587,7 +601,7 @@ def main():
     d2h = C_host.numel() * 8 + u_host.numel() * 8 + (0 if h.finite else w_host.numel() * 8)
 
     if rank != 0:
-        if world > 1:
+        if dist_on:
             torch.distributed.destroy_process_group()
         return
 
@@ -659,7 +673,7 @@ def main():
                                 "per_core_value": detail["per_core_tangents_s"],
                                 "per_core_sample": detail["per_core_sample"]}
     print(json.dumps(line))
-    if world > 1:
+    if dist_on:
         torch.distributed.destroy_process_group()
 
 

@@ -34,6 +34,22 @@ def test_bench_json_line_contract():
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("config", ["1", "5"])
+def test_bench_sharded_path_runs(config):
+    """The --gpus N code path (NCCL process group, ShardedHomogenizer, packed all-gather, max-over-ranks
+    timing) on one GPU via --sharded: linear (config 1) and finite strain (config 5)."""
+    out = subprocess.run([sys.executable, "bench.py", "--config", config, "--steps", "2", "--warmup", "3",
+                          "--no-cpu-baseline", "--spmv-nel", "0", "--no-companions", "--sharded"], cwd=ROOT,
+                         capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["value"] > 0 and d["config"]["parallelism"].startswith("rve-sharded")
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+
+
 def test_reference_arm_json_line_runs_the_oracle():
     """--impl reference (the CPU oracle on the same workload) prints its own contract line."""
     out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--config", "1", "--steps", "1",
