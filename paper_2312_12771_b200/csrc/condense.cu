@@ -1293,358 +1293,15 @@ k_condense_ws(RveDev R, const __grid_constant__ CUtensorMap kmap, const __grid_c
   }
 }
 
-// ====================================================================================
-// k_condense_ws4: k_condense_ws at FOUR CTAs per SM (the occupancy of k_condense): 160 threads at
-// <= 96 registers, <= 53 KB of shared memory -- 8-column k-chunks staged by 16-byte cp.async into an
-// XOR-swizzled [64][8] layout (conflict-free fragment reads), a 2-deep 16-row ring for the streamed
-// TRSM and the backward pass.  The division of work is the one of k_condense_ws.
-// ====================================================================================
-constexpr int KC8 = 8;
-constexpr int W4_STAGE = 2 * 64 * KC8 + KC8 * RHSW;  // A chunk | B chunk | Y rows
-constexpr int W4_STAGES = 2 * W4_STAGE;
-constexpr int W4_SCR = W4_STAGES, W4_SY = W4_SCR + 3 * 320, W4_SY2 = W4_SY + 64 * RHSW, W4_ST = W4_SY2 + 64 * RHSW;
-constexpr int W4_MISC = W4_ST + SD_DBL, W4_SMEM_DBL = W4_MISC + 16;
-constexpr int W4_RC = 16, W4_NCH = 2, W4_CH = W4_RC * TILE;
-static_assert(W4_NCH * W4_CH <= W4_STAGES, "TRSM ring fits the stage area");
-static_assert(2 * (16 * TILE + 16 * RHSW) <= W4_SY, "backward ring fits stages + scratch");
-static_assert(W4_SMEM_DBL * 8 + 1024 <= 56 * 1024, "four CTAs per SM");
-// [64][8] k-chunk, 64-byte rows: element (r, k) at r*8 + (k ^ ((r & 3) << 1)) -- the 16 lanes of a half warp
-// reading rows lr (4 rows) x columns k0 + lc (4) hit 16 distinct banks
-__device__ __forceinline__ int sw8(int r, int k) { return r * KC8 + (k ^ ((r & 3) << 1)); }
-// stage the [64][8] chunk kc (columns 8 kc ..) of a row-major 64x64 global tile: 128 threads x 2 pieces
-__device__ __forceinline__ void stage_chunk8(double* dst, const double* src_tile, int kc, int tid) {
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int idx = tid + NTC * i, r = idx >> 2, c2 = 2 * (idx & 3);
-    cp_async16(dst + sw8(r, c2), src_tile + r * TILE + kc * KC8 + c2);
-  }
-}
-__device__ __forceinline__ void mma_chunk8(double (&acc)[4][4][2], const double* sA, const double* sB, int R0, int C0,
-                                           int lane) {
-  const int lr = lane >> 2, lc = lane & 3;
-#pragma unroll
-  for (int k0 = 0; k0 < KC8; k0 += 4) {
-    double a[4], b[4];
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi) a[mi] = neg(sA[sw8(R0 + 8 * mi + lr, k0 + lc)]);
-#pragma unroll
-    for (int ni = 0; ni < 4; ++ni) b[ni] = sB[sw8(C0 + 8 * ni + lr, k0 + lc)];
-#pragma unroll
-    for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-      for (int ni = 0; ni < 4; ++ni) dmma(acc[mi][ni][0], acc[mi][ni][1], a[mi], b[ni]);
-  }
-}
-template <int W>
-__device__ __forceinline__ void diag_chunk8(double (&acc)[9][2], const double* sA, int lane) {
-  const int lr = lane >> 2, lc = lane & 3;
-#pragma unroll
-  for (int k0 = 0; k0 < KC8; k0 += 4) {
-    double b[8 - W];
-#pragma unroll
-    for (int c = 0; c < 8 - W; ++c) b[c] = sA[sw8(8 * c + lr, k0 + lc)];
-    const double a0 = neg(b[W]), a1 = neg(b[7 - W]);
-    int t = 0;
-#pragma unroll
-    for (int c = 0; c <= W; ++c, ++t) dmma(acc[t][0], acc[t][1], a0, b[c]);
-#pragma unroll
-    for (int c = 0; c <= 7 - W; ++c, ++t) dmma(acc[t][0], acc[t][1], a1, b[c]);
-  }
-}
-
-__global__ void __launch_bounds__(NTC_WS, 4)
-k_condense_ws4(RveDev R, int b0, double* __restrict__ Kt, double* __restrict__ Y, const double* __restrict__ Cavg,
-               const double* __restrict__ Pavg, double* __restrict__ Ceff, double* __restrict__ Peff,
-               double* __restrict__ PavgOut, double* __restrict__ X, int* __restrict__ info) {
-  extern __shared__ __align__(1024) double smem[];
-  double* sStage = smem;
-  double* sScr = smem + W4_SCR;
-  double* sY = smem + W4_SY;
-  double* sY2 = smem + W4_SY2;
-  double* sT = smem + W4_ST;
-  int* sFail = reinterpret_cast<int*>(smem + W4_MISC);
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int lr = lane >> 2, lc = lane & 3;
-  const int bl = blockIdx.x, b = b0 + bl;
-  const int nt = R.nt, NT = R.NT;
-  double* Kb = Kt + (long)bl * R.nslot * TILE_ELEMS;
-  double* Yb = Y + (long)bl * NT * RHSW;
-  double* Xb = X + (long)(b - R.xb0) * NT * RHSW;
-  const TileMask tm{};  // unused (dense structure)
-  if (tid == 0) sFail[0] = 0;
-  __syncthreads();
-
-  if (warp == 4) {
-    // ============================ factor warp (as k_condense_ws) ============================
-    double Sacc0 = 0.0, Sacc1 = 0.0;
-    for (int J = 0; J < nt; ++J) {
-      nbar_sync(BAR_S, NTC_WS);
-      const bool ok = factor_invert_diag<1>(sT, sScr, sFail, J, 0, lane, [] { __syncwarp(); });
-      if (ok) {
-#pragma unroll 1
-        for (int rb = 0; rb < 8; ++rb) {
-          double y0 = 0.0, y1 = 0.0;
-          for (int k0 = 0; k0 < 8 * rb + 8; k0 += 4) dmma(y0, y1, sT[sd(8 * rb + lr, k0 + lc)], sY[swy(k0 + lc, lr)]);
-          const int rr = 8 * rb + lr, cc = 2 * lc;
-          sY2[swy(rr, cc)] = y0;
-          sY2[swy(rr, cc + 1)] = y1;
-          *reinterpret_cast<double2*>(Yb + (long)(J * TILE + rr) * RHSW + cc) = make_double2(y0, y1);
-        }
-        __syncwarp();
-#pragma unroll
-        for (int k0 = 0; k0 < TILE; k0 += 4) dmma(Sacc0, Sacc1, sY2[swy(k0 + lc, lr)], sY2[swy(k0 + lc, lr)]);
-        double* Gjj = tile_ptr<0>(Kb, R, tm, J, J);
-        for (int idx = lane; idx < TILE_ELEMS / 2; idx += 32) {
-          const int r = idx >> 5, cc = 2 * (idx & 31);
-          *reinterpret_cast<double2*>(Gjj + r * TILE + cc) =
-              sd_upper(r, cc) ? make_double2(0.0, 0.0) : make_double2(sT[sd(r, cc)], sT[sd(r, cc + 1)]);
-        }
-      }
-      __syncwarp();
-      nbar_arrive(BAR_G, NTC_WS);
-      if (!ok) return;
-    }
-    double* sSum = sY2;  // the MMA warps' backward ring may already cover the scratch area
-    sSum[lr * 8 + 2 * lc] = Sacc0;
-    sSum[lr * 8 + 2 * lc + 1] = Sacc1;
-    __syncwarp();
-    const int m = R.m;
-    const double* Ca = Cavg + (long)bl * 64;
-    for (int t = lane; t < m * m; t += 32) {
-      const int i = t / m, j = t % m;
-      Ceff[(long)b * m * m + t] = Ca[i * m + j] - sSum[i * 8 + j] / R.vol;
-    }
-    if (R.finite && lane < m) {
-      const double pa = Pavg[(long)bl * 8 + lane];
-      if (Peff) Peff[(long)b * m + lane] = pa - sSum[lane * 8 + m] / R.vol;
-      if (PavgOut) PavgOut[(long)b * m + lane] = pa;
-    }
-    return;
-  }
-
-  // ============================ MMA warps (tid < 128) ============================
-  auto gsync = [] { nbar_sync(BAR_MMA, NTC); };
-  const int R0 = (warp >> 1) * 32, C0 = (warp & 1) * 32;
-  const int cLo = warp, cHi = 7 - warp;
-  constexpr int CPT8 = TILE / KC8;
-  bool failed = false;
-
-  for (int J = 0; J < nt; ++J) {
-    // ---------- S_JJ = A_JJ - sum_K G_JK G_JK^T ; yacc = sum_K G_JK Y_K ----------
-    {
-      double dacc[9][2];
-      double yacc[2][2] = {};
-      DIAG_DISPATCH(diag_load, dacc, tile_ptr<0>(Kb, R, tm, J, J), lane);
-      auto stage_d = [&](int stg, int KK, int kcc) {
-        double* st = sStage + stg * W4_STAGE;
-        stage_chunk8(st, tile_ptr<0>(Kb, R, tm, J, KK), kcc, tid);
-        if (tid < KC8 * RHSW / 2) {  // Y_K rows 8 kcc .., [8][8] plain
-          const int k = tid >> 2, c2 = 2 * (tid & 3);
-          cp_async16(st + 2 * 64 * KC8 + swy(k, c2), Yb + (long)(KK * TILE + kcc * KC8 + k) * RHSW + c2);
-        }
-        cp_async_commit();
-      };
-      int K = 0, kc = 0, par = 0;
-      if (K < J) stage_d(0, 0, 0);
-      while (K < J) {
-        int K2 = K, kc2 = kc + 1;
-        if (kc2 == CPT8) { kc2 = 0; K2 = K + 1; }
-        if (K2 < J) { stage_d(par ^ 1, K2, kc2); cp_async_wait<1>(); }
-        else cp_async_wait<0>();
-        gsync();
-        const double* st = sStage + par * W4_STAGE;
-        switch (warp) {
-          case 0: diag_chunk8<0>(dacc, st, lane); break;
-          case 1: diag_chunk8<1>(dacc, st, lane); break;
-          case 2: diag_chunk8<2>(dacc, st, lane); break;
-          default: diag_chunk8<3>(dacc, st, lane); break;
-        }
-        const double* sYc = st + 2 * 64 * KC8;
-#pragma unroll
-        for (int k0 = 0; k0 < KC8; k0 += 4) {
-          const double bb = sYc[swy(k0 + lc, lr)];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) dmma(yacc[u][0], yacc[u][1], st[sw8(16 * warp + 8 * u + lr, k0 + lc)], bb);
-        }
-        gsync();
-        K = K2; kc = kc2; par ^= 1;
-      }
-      DIAG_DISPATCH(diag_store, dacc, sT, lane);
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int r = 16 * warp + 8 * u + lr, cc = 2 * lc;
-        const double2 y = __ldcg(reinterpret_cast<const double2*>(Yb + (long)(J * TILE + r) * RHSW + cc));
-        sY[swy(r, cc)] = y.x - yacc[u][0];
-        sY[swy(r, cc + 1)] = y.y - yacc[u][1];
-      }
-    }
-    nbar_arrive(BAR_S, NTC_WS);
-    // ---------- off-diagonal accumulation of column J under the chain; park S_IJ in its slot ----------
-    if (J > 0) {
-      for (int I = J + 1; I < nt; ++I) {
-        double acc[4][4][2];
-        double* Aij = tile_ptr<0>(Kb, R, tm, I, J);
-        if (__ldg(R.tile_nz + I * nt + J)) {
-          load_frag(acc, Aij, R0, C0, lane);
-        } else {
-#pragma unroll
-          for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-            for (int ni = 0; ni < 4; ++ni) acc[mi][ni][0] = acc[mi][ni][1] = 0.0;
-        }
-        auto stage_o = [&](int stg, int KK, int kcc) {
-          double* st = sStage + stg * W4_STAGE;
-          stage_chunk8(st, tile_ptr<0>(Kb, R, tm, I, KK), kcc, tid);
-          stage_chunk8(st + 64 * KC8, tile_ptr<0>(Kb, R, tm, J, KK), kcc, tid);
-          cp_async_commit();
-        };
-        int K = 0, kc = 0, par = 0;
-        stage_o(0, 0, 0);
-        while (K < J) {
-          int K2 = K, kc2 = kc + 1;
-          if (kc2 == CPT8) { kc2 = 0; K2 = K + 1; }
-          if (K2 < J) { stage_o(par ^ 1, K2, kc2); cp_async_wait<1>(); }
-          else cp_async_wait<0>();
-          gsync();
-          const double* st = sStage + par * W4_STAGE;
-          mma_chunk8(acc, st, st + 64 * KC8, R0, C0, lane);
-          gsync();
-          K = K2; kc = kc2; par ^= 1;
-        }
-#pragma unroll
-        for (int mi = 0; mi < 4; ++mi)
-#pragma unroll
-          for (int ni = 0; ni < 4; ++ni)
-            *reinterpret_cast<double2*>(Aij + (R0 + 8 * mi + lr) * TILE + C0 + 8 * ni + 2 * lc) =
-                make_double2(acc[mi][ni][0], acc[mi][ni][1]);
-      }
-    } else {  // J = 0: S_I0 = A_I0 in place; fill tiles need explicit zeros
-      for (int I = 1; I < nt; ++I) {
-        if (__ldg(R.tile_nz + I * nt)) continue;
-        double* Ai0 = tile_ptr<0>(Kb, R, tm, I, 0);
-        for (int idx = tid; idx < TILE_ELEMS / 2; idx += NTC)
-          reinterpret_cast<double2*>(Ai0)[idx] = make_double2(0.0, 0.0);
-      }
-    }
-    gsync();
-    nbar_sync(BAR_G, NTC_WS);
-    if (sFail[0]) { failed = true; break; }
-    // ---------- G_IJ = S_IJ (G_JJ^-1)^T, parked tiles streamed in 16-row chunks (2-deep ring) ----------
-    {
-      const int nch = (nt - 1 - J) * (TILE / W4_RC);
-      int nis = 0;
-      auto issue_c = [&]() {
-        const int I = J + 1 + nis / (TILE / W4_RC), rq = nis % (TILE / W4_RC);
-        stage_rows(sStage + (nis % W4_NCH) * W4_CH, tile_ptr<0>(Kb, R, tm, I, J), rq * W4_RC, W4_RC, tid);
-        cp_async_commit();
-        ++nis;
-      };
-      if (nch > 0) issue_c();
-      for (int c = 0; c < nch; ++c) {
-        if (nis < nch) { issue_c(); cp_async_wait<1>(); }
-        else cp_async_wait<0>();
-        gsync();
-        const double* sS = sStage + (c % W4_NCH) * W4_CH;
-        const int I = J + 1 + c / (TILE / W4_RC), rq = c % (TILE / W4_RC);
-        double* Gij = tile_ptr<0>(Kb, R, tm, I, J) + (long)rq * W4_RC * TILE;
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int cb = q ? cHi : cLo;
-          double g[2][2] = {};
-          for (int k0 = 0; k0 < 8 * (cb + 1); k0 += 4) {
-            const double bb = sT[sd(8 * cb + lr, k0 + lc)];
-#pragma unroll
-            for (int mi = 0; mi < 2; ++mi) dmma(g[mi][0], g[mi][1], sS[sw64(8 * mi + lr, k0 + lc)], bb);
-          }
-#pragma unroll
-          for (int mi = 0; mi < 2; ++mi)
-            *reinterpret_cast<double2*>(Gij + (8 * mi + lr) * TILE + 8 * cb + 2 * lc) = make_double2(g[mi][0], g[mi][1]);
-        }
-        gsync();
-      }
-    }
-    gsync();
-  }
-
-  if (failed) {
-    if (tid == 0) info[b] = sFail[0];
-    const double nan = __longlong_as_double(0x7ff8000000000000LL);
-    if (tid < R.m * R.m) Ceff[(long)b * R.m * R.m + tid] = nan;
-    if (Peff && tid < R.m) Peff[(long)b * R.m + tid] = nan;
-    return;
-  }
-
-  // ======================= backward: X = G^-T Y, 2-deep 16-row ring ===================
-  constexpr int RC = 16, RPT = TILE / RC;
-  constexpr int NSTB = 2, BST = RC * TILE + RC * RHSW;
-  for (int J = nt - 1; J >= 0; --J) {
-    double xacc[2][2] = {};
-    int I = J + 1, rq = 0;
-    int nis = 0, ncon = 0;
-    auto issue_b = [&]() {
-      double* nb = smem + (nis % NSTB) * BST;
-      stage_rows(nb, tile_ptr<0>(Kb, R, tm, I, J), rq * RC, RC, tid);
-      stage_rhs(nb + RC * TILE, Xb + (long)(I * TILE + rq * RC) * RHSW, RC, tid);
-      cp_async_commit();
-      ++nis;
-      if (++rq == RPT) { rq = 0; ++I; }
-    };
-    {
-      const double* src = tile_ptr<0>(Kb, R, tm, J, J);
-      for (int idx = tid; idx < TILE * 32; idx += NTC) {
-        const int r = idx >> 5, c2 = 2 * (idx & 31);
-        if (!sd_upper(r, c2)) cp_async16(sT + sd(r, c2), src + r * TILE + c2);
-      }
-      cp_async_commit();
-    }
-    if (I < nt) issue_b();
-    while (ncon < nis) {
-      if (I < nt) { issue_b(); cp_async_wait<1>(); }
-      else cp_async_wait<0>();
-      gsync();
-      const double* tl = smem + (ncon % NSTB) * BST;
-      const double* xi = tl + RC * TILE;
-#pragma unroll
-      for (int k0 = 0; k0 < RC; k0 += 4) {
-        const double bb = xi[swy(k0 + lc, lr)];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) dmma(xacc[u][0], xacc[u][1], tl[sw64(k0 + lc, 16 * warp + 8 * u + lr)], bb);
-      }
-      gsync();
-      ++ncon;
-    }
-    cp_async_wait<0>();
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int r = 16 * warp + 8 * u + lr, cc = 2 * lc;
-      const double2 y = __ldcg(reinterpret_cast<const double2*>(Yb + (long)(J * TILE + r) * RHSW + cc));
-      sY[swy(r, cc)] = y.x - xacc[u][0];
-      sY[swy(r, cc + 1)] = y.y - xacc[u][1];
-    }
-    gsync();
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int r = 16 * warp + 8 * u;
-      double x0 = 0.0, x1 = 0.0;
-      for (int k0 = r; k0 < TILE; k0 += 4) dmma(x0, x1, sT[sd(k0 + lc, r + lr)], sY[swy(k0 + lc, lr)]);
-      const int rr = r + lr, cc = 2 * lc;
-      *reinterpret_cast<double2*>(Xb + (long)(J * TILE + rr) * RHSW + cc) = make_double2(x0, x1);
-    }
-    gsync();
-  }
-}
-
 __global__ void k_first_fail(const int* __restrict__ f, int n, int sentinel, int* out);
 
 // Dense-structure kernel: 0 = k_condense (default), 1 = k_condense_ws (factor warp + 4 MMA warps, 3 CTAs/SM;
-// HOM_CONDENSE=ws), 2 = k_condense_ws4 (the same at 4 CTAs/SM; HOM_CONDENSE=ws4) -- for A/B measurements.
+// HOM_CONDENSE=ws, for A/B measurements; its 4-CTA/SM version with 8-wide cp.async chunks was measured
+// slower still and lives in git history, commit e0bd4eb -- DESIGN.md §5.1).
 static int condense_variant() {
   static const int v = [] {
     const char* e = getenv("HOM_CONDENSE");
-    if (!e) return 0;
-    if (e[0] == 'w' && e[1] == 's' && e[2] == '4') return 2;
-    return e[0] == 'w' ? 1 : 0;
+    return (e && e[0] == 'w') ? 1 : 0;
   }();
   return v;
 }
@@ -1680,13 +1337,6 @@ void launch_condense(const RveDev& R, int b0, int nb, double* Kt, double* Y, con
     const cuuint32_t ybox[2] = {(cuuint32_t)RHSW, (cuuint32_t)KC};
     encode(&ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, Y, ydim, ystr, ybox, one, CU_TENSOR_MAP_INTERLEAVE_NONE,
            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  }
-  if (R.dense_tiles && condense_variant() == 2) {
-    const size_t smw = (size_t)W4_SMEM_DBL * sizeof(double);
-    cudaFuncSetAttribute(k_condense_ws4, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
-    cudaFuncSetAttribute(k_condense_ws4, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    k_condense_ws4<<<nb, NTC_WS, smw, s>>>(R, b0, Kt, Y, Cavg, Pavg, Ceff, Peff, PavgOut, X, info);
-    return;
   }
   if (R.dense_tiles && condense_variant() == 1) {
     const size_t smw = (size_t)WS_SMEM_DBL * sizeof(double);
