@@ -5,6 +5,7 @@
 // step of the method runs on the GPU.
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -670,7 +671,14 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
         if (tile_nz[(size_t)I * nt_ + J]) alist.push_back((I << 16) | J);
     R.n_a = (int)alist.size();
     R.a_list = upload(c, alist, s, &rc);
+    // finite strain: keep the RVE's packed K_e (36 doubles per element) in K1's shared memory when it fits
+    // beside the row buffers at 2 CTAs/SM (HOM_FS_KS=0 forces the all-L2 variant, for A/B)
+    {
+      const char* e = getenv("HOM_FS_KS");
+      R.fs_ks = c->finite && (size_t)R.ne * 36 * sizeof(double) <= 76 * 1024 && !(e && e[0] == '0');
+    }
     R.npw = hom::rve_assemble_npw(R);
+    if (R.fs_ks) R.fs_ke_off = (int)((hom::rve_assemble_smem(R, R.npw) - (size_t)R.ne * 36 * sizeof(double)) / 8);
     // K1 warp work items: the row nodes of each nonzero tile packed greedily into items of
     // <= npw consecutive nodes and <= 32 in-tile neighbour records (one per lane), dealt
     // round-robin over the warps

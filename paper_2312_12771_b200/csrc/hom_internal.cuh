@@ -43,6 +43,7 @@ struct RveDev {
   const double* FlamT;            // [ntype][nen*dim][m] K_fe tables per element type
   const double* FmuT;
   int ntype;
+  int fs_ks, fs_ke_off;            // finite strain: K_e of the RVE kept in K1's shared memory (2 CTAs/SM), its offset
   int gtab;                       // 1: the (type, phase) tables exceed shared memory; K1 reads Klam/Kmu/FlamT/FmuT
                                   // from global memory and combines them with (lam, mu) per phase on the fly
   int npw;                        // K1: row-buffer capacity in RVE nodes per warp (12 / dim)

@@ -102,7 +102,8 @@ __device__ __forceinline__ void st_hint(double* a, double v, uint64_t pol) {
 }
 __device__ __forceinline__ void nh_elements(const RveDev& R, int b, int e0, int cnt, const double* __restrict__ Fbar,
                                             const double* __restrict__ w, double* __restrict__ out,
-                                            int* __restrict__ jflag, double* sm, int* sOk, double (&avg)[4]) {
+                                            int* __restrict__ jflag, double* sm, int* sOk, double (&avg)[4],
+                                            double* ske) {  // ske: K_e of elements e0.. in shared memory, or null
   double (*sQ)[FS_QW] = reinterpret_cast<double (*)[FS_QW]>(sm);  // [FS_ELB * 4][FS_QW]
   const int ne = R.ne, nq = R.nq, tid = threadIdx.x;
   if (tid < FS_ELB) sOk[tid] = 1;
@@ -159,7 +160,11 @@ __device__ __forceinline__ void nh_elements(const RveDev& R, int b, int e0, int 
           for (int j = 0; j < 2; ++j)  // column (b, j): sum_L t[(j,L)] g_b[L]
             ke[2 * bb + j] += wq * (t[2 * j] * G[2 * bb] + t[2 * j + 1] * G[2 * bb + 1]);
       }
-      for (int k = 0; k <= row; ++k) st_hint(o + EL_K + pk8(row, k), ok ? ke[k] : 0.0, pol);  // lower part
+      if (ske) {
+        for (int k = 0; k <= row; ++k) ske[le * 36 + pk8(row, k)] = ok ? ke[k] : 0.0;  // lower part
+      } else {
+        for (int k = 0; k <= row; ++k) st_hint(o + EL_K + pk8(row, k), ok ? ke[k] : 0.0, pol);
+      }
       for (int k = 0; k < 4; ++k) st_hint(o + EL_F + row * 4 + k, ok ? fe[k] : 0.0, pol);
       st_hint(o + EL_R + row, ok ? re : 0.0, pol);
       if (row < 5 && ok) {  // running qp sums of A (rows 0-3: 4 entries each) and P (row 4) for <A>, <P>
@@ -177,7 +182,8 @@ template <int DIM, bool ISO, bool GT = false>  // GT: global geometry tables (Rv
 __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const int bl, double* __restrict__ Kt,
                                              double* __restrict__ Y, double* __restrict__ Cavg,
                                              double* __restrict__ Pavg, double* __restrict__ rfn,
-                                             const double* __restrict__ EL, double* smem) {
+                                             const double* __restrict__ EL, double* smem,
+                                             const double* KE = nullptr, int kes = 0) {  // finite strain: K_e, stride
   double* s_row = smem;                      // [8 warps][npw][DIM][64] tile-row buffers
   double* red = s_row + (NTHR / 32) * R.npw * DIM * TILE;  // [NTHR] reduction scratch
   // ISO element tables: [ntype][n_phase][ND][ND] (K_e) and [ntype][n_phase][ND][m] (K_fe rows) per RVE in shared
@@ -385,7 +391,7 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
                 return s_K[2 * pp] * __ldg(R.Klam + o) + s_K[2 * pp + 1] * __ldg(R.Kmu + o);
               }
               if (ISO) return s_K[(long)s_ep[e] * ND * ND + r * ND + c];
-              return EL[(long)e * EL_STRIDE + EL_K + pk8(r, c)];
+              return KE[(long)e * kes + pk8(r, c)];
             };
 #pragma unroll
             for (int sidx = 0; sidx < 4 * RS4M - 2 + 1; ++sidx) {
@@ -459,7 +465,10 @@ __global__ void __launch_bounds__(NTHR) k_rve_assemble(RveDev R, int b0, double*
 // evaluates every material point and forms the element records into its own scratch slice (one
 // RVE, ne x EL_STRIDE doubles, written and read back by the same CTA while L2-resident), then runs
 // the tile writer from them -- no batch-wide element table round trip through HBM.
-__global__ void __launch_bounds__(NTHR, 4) k_rve_assemble_fs(RveDev R, int b0, int nb, const double* __restrict__ Fbar,
+// KS: the RVE's K_e (36 doubles per element) stays in shared memory for the tile writer (2 CTAs per SM);
+// otherwise every record lives in the L2 scratch (4 CTAs per SM)
+template <bool KS>
+__global__ void __launch_bounds__(NTHR, KS ? 2 : 4) k_rve_assemble_fs(RveDev R, int b0, int nb, const double* __restrict__ Fbar,
                                                           const double* __restrict__ w, double* __restrict__ Kt,
                                                           double* __restrict__ Y, double* __restrict__ Cavg,
                                                           double* __restrict__ Pavg, double* __restrict__ rfn,
@@ -467,12 +476,14 @@ __global__ void __launch_bounds__(NTHR, 4) k_rve_assemble_fs(RveDev R, int b0, i
   extern __shared__ __align__(128) double smem[];
   __shared__ int sOk[FS_ELB];
   double* scr = scratch + (long)blockIdx.x * R.ne * EL_STRIDE;
+  double* sKe = KS ? smem + R.fs_ke_off : nullptr;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, row = tid & 7;
   for (int bl = blockIdx.x; bl < nb; bl += gridDim.x) {
     const int b = b0 + bl;
     double avg[4] = {0.0, 0.0, 0.0, 0.0};  // this thread's share of sum eta A (row < 4) / sum eta P (row 4)
     for (int e0 = 0; e0 < R.ne; e0 += FS_ELB)
-      nh_elements(R, b, e0, min(FS_ELB, R.ne - e0), Fbar, w, scr + (long)e0 * EL_STRIDE, jflag, smem, sOk, avg);
+      nh_elements(R, b, e0, min(FS_ELB, R.ne - e0), Fbar, w, scr + (long)e0 * EL_STRIDE, jflag, smem, sOk, avg,
+                  KS ? sKe + (long)e0 * 36 : nullptr);
     // <A>, <P>: sum over the elements (lanes with equal row: xor 8, 16; then the 8 warps), / |Omega|
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -492,7 +503,8 @@ __global__ void __launch_bounds__(NTHR, 4) k_rve_assemble_fs(RveDev R, int b0, i
       else Pavg[(long)bl * 8 + tid - 16] = t;
     }
     __syncthreads();
-    assemble_rve<2, false>(R, b, bl, Kt, Y, Cavg, Pavg, rfn, scr, smem);
+    if (KS) assemble_rve<2, false>(R, b, bl, Kt, Y, Cavg, Pavg, rfn, scr, smem, sKe, 36);
+    else assemble_rve<2, false>(R, b, bl, Kt, Y, Cavg, Pavg, rfn, scr, smem, scr + EL_K, EL_STRIDE);
     __syncthreads();
   }
 }
@@ -504,14 +516,17 @@ size_t rve_assemble_smem(const RveDev& R, int npw) {
                    : (R.gtab ? (size_t)2 * R.n_phase : (size_t)R.ntype * R.n_phase * nd * (nd + R.m)) * sizeof(double) +
                          (size_t)R.ne * sizeof(int));
   if (R.finite) sm = std::max(sm, (size_t)FS_SMEM_DBL * sizeof(double));  // element staging aliases the row buffers
+  if (R.finite && R.fs_ks) sm = ((sm + 127) / 128) * 128 + (size_t)R.ne * 36 * sizeof(double);  // + K_e of the RVE
   return sm;
 }
 
 int rve_assemble_npw(const RveDev& R) {
-  // largest row buffer (<= 16 rows per warp) that keeps 4 CTAs per SM (<= 56 KB each)
+  // largest row buffer (<= 16 rows per warp) that keeps 4 CTAs per SM (<= 56 KB each), or 2 CTAs per SM
+  // (<= 112 KB) for the finite-strain kernel with K_e in shared memory
   const int dim = R.finite ? 2 : R.dim;
+  const size_t budget = (R.finite && R.fs_ks) ? 112 * 1024 : 56 * 1024;
   int npw = 16 / dim;
-  while (npw > 1 && rve_assemble_smem(R, npw) > 56 * 1024) --npw;
+  while (npw > 1 && rve_assemble_smem(R, npw) > budget) --npw;
   return npw;
 }
 
@@ -520,9 +535,10 @@ int rve_assemble_fs_slots(const RveDev& R) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const size_t sm = rve_assemble_smem(R, R.npw);
-  cudaFuncSetAttribute(k_rve_assemble_fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  cudaFuncSetAttribute(k_rve_assemble_fs, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_rve_assemble_fs, NTHR, sm);
+  auto k = R.fs_ks ? k_rve_assemble_fs<true> : k_rve_assemble_fs<false>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, NTHR, sm);
   return std::max(1, per) * std::max(1, sms);
 }
 
@@ -530,9 +546,10 @@ void launch_rve_assemble_fs(const RveDev& R, int b0, int nb, const double* F, co
                             double* Y, double* Cavg, double* Pavg, double* rfn, double* scratch, int slots,
                             int* jflag, cudaStream_t s) {
   const size_t sm = rve_assemble_smem(R, R.npw);
-  cudaFuncSetAttribute(k_rve_assemble_fs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  cudaFuncSetAttribute(k_rve_assemble_fs, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  k_rve_assemble_fs<<<std::min(nb, slots), NTHR, sm, s>>>(R, b0, nb, F, w, Kt, Y, Cavg, Pavg, rfn, scratch, jflag);
+  auto k = R.fs_ks ? k_rve_assemble_fs<true> : k_rve_assemble_fs<false>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  k<<<std::min(nb, slots), NTHR, sm, s>>>(R, b0, nb, F, w, Kt, Y, Cavg, Pavg, rfn, scratch, jflag);
 }
 
 template <int DIM, bool GT>
