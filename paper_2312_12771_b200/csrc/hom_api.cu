@@ -633,7 +633,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
     }
     R.ntype = c->finite ? 0 : (int)(KlamT.size() / ((size_t)ND * ND));
     // per-(type, phase) tables in K1's shared memory when they fit; else the global-table path
-    R.gtab = (size_t)R.ntype * mat->n_phases * ND * (ND + m) * sizeof(double) > 96 * 1024 ? 1 : 0;
+    R.gtab = (size_t)R.ntype * mat->n_phases * (nen * nen * ((dim * dim + 1) / 2 * 2) + ND * m) * sizeof(double) > 96 * 1024 ? 1 : 0;
     if (R.gtab && mat->n_phases > 256) return fail(HOM_ERR_INVALID_ARG, "more than 256 phases");
     int max_deg = 1;
     for (int pp = 0; pp < R.n_indep; ++pp) max_deg = std::max(max_deg, RP.nbr_ptr[pp + 1] - RP.nbr_ptr[pp]);

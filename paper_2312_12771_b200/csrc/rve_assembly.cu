@@ -189,9 +189,12 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
   // ISO element tables: [ntype][n_phase][ND][ND] (K_e) and [ntype][n_phase][ND][m] (K_fe rows) per RVE in shared
   // memory, or -- when they do not fit (R.gtab: meshes with many distinct element geometries) -- only the
   // per-phase (lam, mu) here and the geometry tables Klam/Kmu/FlamT/FmuT read from global memory (L2)
+  // K_e tables block-major: [tab][a][b][BS] with the DIM x DIM block (a, b) contiguous, padded to BS doubles
+  // (16-byte multiple) so a gather is BS/2 128-bit shared-memory loads instead of DIM^2 64-bit ones
+  constexpr int NEN = 1 << DIM, BS = ((DIM * DIM + 1) / 2) * 2;
   const int ntab = ISO ? (GT ? 0 : R.ntype * R.n_phase) : 0;
   double* s_K = red + NTHR;
-  double* s_F = s_K + (ISO ? (GT ? 2 * R.n_phase : ntab * ((1 << DIM) * DIM) * ((1 << DIM) * DIM)) : 0);
+  double* s_F = s_K + (ISO ? (GT ? 2 * R.n_phase : ntab * NEN * NEN * BS) : 0);
   int* s_ep = reinterpret_cast<int*>(s_F + (ISO ? ntab * ((1 << DIM) * DIM) * R.m : 0));
   const int tid = threadIdx.x;
   const int ne = R.ne;
@@ -215,7 +218,9 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
       const int t = i / (R.n_phase * ND * ND), pp = (i / (ND * ND)) % R.n_phase, j = i % (ND * ND);
       const double E = mt[2 * pp], nu = mt[2 * pp + 1];
       const double lam = E * nu / ((1.0 + nu) * (1.0 - 2.0 * nu)), mu = E / (2.0 * (1.0 + nu));
-      s_K[i] = lam * R.Klam[(long)t * ND * ND + j] + mu * R.Kmu[(long)t * ND * ND + j];
+      const int r = j / ND, c = j % ND;
+      s_K[(((long)(i / (ND * ND)) * NEN + r / DIM) * NEN + c / DIM) * BS + (r % DIM) * DIM + c % DIM] =
+          lam * R.Klam[(long)t * ND * ND + j] + mu * R.Kmu[(long)t * ND * ND + j];
     }
     for (int i = tid; i < ntab * ND * R.m; i += NTHR) {  // K_fe element tables
       const int t = i / (R.n_phase * ND * R.m), pp = (i / (ND * R.m)) % R.n_phase, j = i % (ND * R.m);
@@ -390,7 +395,10 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
                 const long o = (long)t * ND * ND + r * ND + c;
                 return s_K[2 * pp] * __ldg(R.Klam + o) + s_K[2 * pp + 1] * __ldg(R.Kmu + o);
               }
-              if (ISO) return s_K[(long)s_ep[e] * ND * ND + r * ND + c];
+              if (ISO) {
+                const int a = (code >> 4) & 15, bb = code & 15;
+                return s_K[(((long)s_ep[e] * NEN + a) * NEN + bb) * BS + i * DIM + jj];
+              }
               return KE[(long)e * kes + pk8(r, c)];
             };
 #pragma unroll
@@ -398,10 +406,26 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
               if (sidx >= nsh) break;
               if (sidx < 4 * RS4M - 2) {
                 const int code = rv[sidx + 2];
+                if (ISO && !GT) {  // the whole block with BS/2 128-bit loads
+                  const int e = code >> 8, a = (code >> 4) & 15, bb = code & 15;
+                  const double2* kb = reinterpret_cast<const double2*>(s_K + (((long)s_ep[e] * NEN + a) * NEN + bb) * BS);
+                  double v[BS];
 #pragma unroll
-                for (int i = 0; i < DIM; ++i)
+                  for (int q = 0; q < BS / 2; ++q) {
+                    const double2 t2 = kb[q];
+                    v[2 * q] = t2.x;
+                    v[2 * q + 1] = t2.y;
+                  }
 #pragma unroll
-                  for (int jj = 0; jj < DIM; ++jj) blk[i][jj] += blk_at(code, i, jj);
+                  for (int i = 0; i < DIM; ++i)
+#pragma unroll
+                    for (int jj = 0; jj < DIM; ++jj) blk[i][jj] += v[i * DIM + jj];
+                } else {
+#pragma unroll
+                  for (int i = 0; i < DIM; ++i)
+#pragma unroll
+                    for (int jj = 0; jj < DIM; ++jj) blk[i][jj] += blk_at(code, i, jj);
+                }
               } else {  // rare: records longer than RS4M int4s (tiny periodic meshes)
                 for (int s2 = sidx; s2 < nsh; ++s2) {
                   const int slot = s2 + 2;
@@ -513,7 +537,9 @@ size_t rve_assemble_smem(const RveDev& R, int npw) {
   const int dim = R.finite ? 2 : R.dim, nd = (1 << dim) * dim;  // nen*dim
   size_t sm = (size_t)((NTHR / 32) * npw * dim * TILE + NTHR) * sizeof(double) +
               (R.finite ? 0
-                   : (R.gtab ? (size_t)2 * R.n_phase : (size_t)R.ntype * R.n_phase * nd * (nd + R.m)) * sizeof(double) +
+                   : (R.gtab ? (size_t)2 * R.n_phase
+                             : (size_t)R.ntype * R.n_phase * ((size_t)(1 << dim) * (1 << dim) * ((dim * dim + 1) / 2 * 2) + nd * R.m)) *
+                                 sizeof(double) +
                          (size_t)R.ne * sizeof(int));
   if (R.finite) sm = std::max(sm, (size_t)FS_SMEM_DBL * sizeof(double));  // element staging aliases the row buffers
   if (R.finite && R.fs_ks) sm = ((sm + 127) / 128) * 128 + (size_t)R.ne * 36 * sizeof(double);  // + K_e of the RVE
