@@ -779,6 +779,20 @@ def test_cook_table1_classical_iteration_counts(torch_cuda):
             assert inner[-1] < 1e-13 and len(inner) <= 8, inner
 
 
+def test_cook_classical_without_predictor_uses_macro_update(torch_cuda):
+    """The classical scheme's no-predictor variant (q += dq only, hom_macro_update in the C-ABI) converges
+    to the same state as the variant with the eq:reduction predictor."""
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = W.cook(nel=3, r=6, n_steps=2)
+    out = []
+    for pred in (True, False):
+        h = Homogenizer.from_workload(wl, tile_sparse=True)
+        u, hist, ok = h.newton_classical(2, tol=1e-9, micro_tol=1e-13, predictor=pred)
+        assert ok
+        out.append(u.cpu().numpy())
+    assert rel(out[1], out[0]) <= 1e-8
+
+
 def test_cook_classical_and_generalized_reach_the_same_state(torch_cuda):
     """Both schemes solve the same discrete two-scale problem: equal converged u (n_l = 22)."""
     from paper_2312_12771_b200.hom import Homogenizer
