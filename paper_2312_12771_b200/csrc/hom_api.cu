@@ -586,6 +586,14 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   int chunk = c->opt.rve_chunk > 0 ? c->opt.rve_chunk
                                    : (int)std::min<double>(nloc, std::floor(c->opt.mem_budget_gb * 1e9 / per_rve));
   chunk = std::max(1, std::min(chunk, nloc));
+  if (c->opt.rve_chunk <= 0 && chunk < nloc) {
+    // automatic chunks that do not hold the whole range: a whole number of k_condense waves (4 resident
+    // CTAs per SM), so that only the last chunk ends on a partial wave
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    const int wave = 4 * std::max(1, sms);
+    if (chunk >= 2 * wave) chunk = (chunk / wave) * wave;
+  }
   c->chunk = chunk;
 
   R.elem_indep = upload(c, eind, s, &rc);
