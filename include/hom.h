@@ -116,7 +116,8 @@ typedef struct {
   int32_t cg_max_iter;      /* default 20000 if <= 0 */
   int32_t rve_chunk;        /* RVEs condensed per pass; <= 0: automatic (memory budget) */
   int32_t check_info;       /* 1: hom_condense synchronises once to report NOT_SPD / JACOBIAN */
-  double mem_budget_gb;     /* K_ff pool budget for automatic chunking; <= 0: 48 GB */
+  double mem_budget_gb;     /* K_ff pool budget for automatic chunking; <= 0: 96 GB (chunks are then a whole
+                               number of condensation waves, as few launches as the budget allows) */
   int32_t tile_sparse;      /* 0: dense blocked factorisation of every lower 64x64 tile of K_ff
                                (BASELINE north_star).  1: tile-sparse -- only the tiles of the
                                symbolic tile-level fill of K_ff's structural pattern are stored

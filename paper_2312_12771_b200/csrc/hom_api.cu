@@ -255,7 +255,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   c->opt = *options;
   if (c->opt.cg_rtol <= 0) c->opt.cg_rtol = 1e-13;
   if (c->opt.cg_max_iter <= 0) c->opt.cg_max_iter = 20000;
-  if (c->opt.mem_budget_gb <= 0) c->opt.mem_budget_gb = 48.0;
+  if (c->opt.mem_budget_gb <= 0) c->opt.mem_budget_gb = 96.0;
   cudaGetDevice(&c->device);
   const int dim = mac->dim;
   *out = c;
@@ -587,12 +587,21 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
                                    : (int)std::min<double>(nloc, std::floor(c->opt.mem_budget_gb * 1e9 / per_rve));
   chunk = std::max(1, std::min(chunk, nloc));
   if (c->opt.rve_chunk <= 0 && chunk < nloc) {
-    // automatic chunks that do not hold the whole range: a whole number of k_condense waves (4 resident
-    // CTAs per SM), so that only the last chunk ends on a partial wave
+    // automatic chunks that do not hold the whole range: the fewest launches the budget allows, each a
+    // whole number of k_condense waves (4 resident CTAs per SM) -- every launch ends with a drain, and
+    // only the last chunk may end on a partial wave
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-    const int wave = 4 * std::max(1, sms);
-    if (chunk >= 2 * wave) chunk = (chunk / wave) * wave;
+    const int wave = 4 * std::max(1, sms), maxc = chunk;
+    if (maxc >= 2 * wave) {
+      for (int L = (nloc + maxc - 1) / maxc;; ++L) {
+        const int cl = ((nloc + L - 1) / L + wave - 1) / wave * wave;
+        if (cl <= maxc) {
+          chunk = cl;
+          break;
+        }
+      }
+    }
   }
   c->chunk = chunk;
 
