@@ -10,7 +10,7 @@ iteration (kinematics, condensation, residual norms, macro solve, update).
 Default workload: BASELINE.json configs[2] (config 3: 64x64 macro Q1, 16384 RVEs of
 32x32 Q1 with per-RVE random phases and moduli) -- the largest configuration that fits one
 GPU, which is the headline when BASELINE's metric names no configuration; dense blocked
-factorisation through the chunked path (six passes of <= 2774 RVEs over a 48 GB K_ff pool).
+factorisation through the chunked path (four wave-aligned passes of 4144 RVEs over a 96 GB K_ff pool).
 Companion keys: config 2 and config 5 (the configs whose k_condense sits furthest below
 the FP64 roofline), the tile-sparse factorisation of the same workload, and the K6 SpMV
 roofline on a scaled macro mesh.  Prints ONE JSON line on rank 0.
@@ -655,7 +655,7 @@ def main():
     if world == 1 and not args.tile_sparse and not h.finite and args.macro_basis == "dirac":
         line["tile_sparse"] = tile_sparse_line(wl, C, args.steps, args.warmup, args.rve_ordering)
     if world == 1 and not args.no_companions and args.config == 3 and not args.tile_sparse:
-        h.close()  # free the 48 GB K_ff pool before the companion contexts
+        h.close()  # free the K_ff pool (up to 96 GB) before the companion contexts
         torch.cuda.empty_cache()
         line["companions"] = {f"cfg{c}": companion_line(c, max(args.steps, 20), args.warmup) for c in (2, 5)}
     if world == 1 and args.spmv_nel > 0:
