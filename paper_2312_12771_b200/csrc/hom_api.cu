@@ -766,6 +766,37 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   M.dmask = upload(c, dmask, s, &rc);
   M.dval = upload(c, dval, s, &rc);
   M.fbody = upload(c, fbody, s, &rc);
+  M.cg_prof = nullptr;
+  if (getenv("HOM_CG_PROF")) {  // experiment knob: phase timing of the cluster PCG (stderr)
+    M.cg_prof = dalloc<unsigned long long>(c, 256, &rc);
+    if (M.cg_prof) cudaMemsetAsync(M.cg_prof, 0, 256 * 8, s);
+  }
+  {  // coarse space of the two-level macro preconditioner (coarse.cu)
+    hom::CoarseHost H = hom::coarse_build(dim, M.n_nodes, mac->coords, rowptr.data(), col.data(), dmask.data());
+    hom::CoarseDev& C = M.cc;
+    C = hom::CoarseDev{};
+    if (H.nc > 0) {
+      C.nc = H.nc; C.nm = H.nm; C.nagg = H.nagg; C.nbmax = H.nbmax;
+      C.agg = upload(c, H.agg, s, &rc);
+      C.rel = upload(c, H.rel, s, &rc);
+      C.aptr = upload(c, H.aptr, s, &rc);
+      C.anode = upload(c, H.anode, s, &rc);
+      C.nbr = upload(c, H.nbr, s, &rc);
+      C.Ac = dalloc<double>(c, (size_t)H.nc * H.nc, &rc);
+      C.Ainv = dalloc<double>(c, (size_t)H.nc * H.nc, &rc);
+      for (int gi = 0; gi < 2; ++gi) {
+        const auto& L = H.loc[gi];
+        C.nla_max[gi] = L.nla_max;
+        C.kmax[gi] = L.kmax;
+        C.lptr[gi] = upload(c, L.lptr, s, &rc);
+        C.lagg[gi] = upload(c, L.lagg, s, &rc);
+        C.tch[gi] = upload(c, L.tch, s, &rc);
+        C.lnptr[gi] = upload(c, L.lnptr, s, &rc);
+        C.lnode[gi] = upload(c, L.lnode, s, &rc);
+        C.ntch[gi] = upload(c, L.ntch, s, &rc);
+      }
+    }
+  }
 
   c->Kt = dalloc<double>(c, tiles * hom::TILE_ELEMS * chunk, &rc);
   c->Y = dalloc<double>(c, (size_t)R.NT * hom::RHSW * chunk, &rc);
@@ -968,6 +999,16 @@ int hom_macro_solve(hom_ctx* c, const double* d_D, const double* d_S, double sca
     info->iterations = st.iterations;
     info->rel_residual = st.rel_residual;
     info->rhs_norm = st.rhs_norm;
+  }
+  if (c->M.cg_prof) {
+    unsigned long long pr[256];
+    cudaMemcpy(pr, c->M.cg_prof, sizeof(pr), cudaMemcpyDeviceToHost);
+    cudaMemset(c->M.cg_prof, 0, sizeof(pr));
+    for (int g = 0; g < 16; ++g) {
+      fprintf(stderr, "cgprof cta %2d it %d:", g, st.iterations);
+      for (int k = 0; k < 12; ++k) fprintf(stderr, " %7.0f", (double)pr[g * 16 + k] / std::max(st.iterations, 1));
+      fprintf(stderr, "\n");
+    }
   }
   if (st.status == 5) return set_err(c, HOM_ERR_CG_NOT_CONVERGED, "macro CG did not converge");
   if (st.status == 6) return set_err(c, HOM_ERR_CG_BREAKDOWN, "macro CG breakdown (p^T K p <= 0)");

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "../../include/hom.h"
 
 namespace hom {
@@ -74,6 +76,52 @@ struct RveDev {
   const int* int_of;              // [n_indep] natural node -> internal node; nullptr = identity
 };
 
+// Two-level additive macro preconditioner (coarse.cu): aggregates of macro
+// nodes with their rigid-body modes, nc = nagg * nm coarse DOFs (nc = 0: one-level only).
+constexpr int CC_MIN_DOF = 1024, CC_NA2 = 8, CC_NA3 = 3, CC_NC_MAX = 192, CC_NB_MAX = 27,
+              CC_ROWMAX = 96,  // longest CSR row the coarse assembly stages (3-D: 81)
+              CC_NCH = 8;      // chunks per aggregate node list in the PCG's restriction
+struct CoarseDev {
+  int nc, nm, nagg, nbmax;
+  const int* agg;      // [n_nodes] aggregate of each node
+  const double* rel;   // [n_nodes][dim] (x - centroid of its aggregate) / h
+  const int* aptr;     // [nagg+1] nodes of each aggregate: anode[aptr[a] .. aptr[a+1])
+  const int* anode;
+  const int* nbr;      // [nagg][nbmax] aggregates coupled through K_M (-1 padded)
+  double* Ac;          // [nc][nc] P^T K_M P (per solve)
+  double* Ainv;        // [nc][nc] its inverse (dropped modes: zero rows / columns)
+  // per cluster size of k_macro_cg_cluster2 (index 0: G = 16, 1: G = 8)
+  int nla_max[2], kmax[2];
+  const int* lptr[2];   // [G+1] CTA g's aggregates: lagg[lptr[g] .. lptr[g+1])
+  const int* lagg[2];
+  const int* tch[2];    // [nagg][kmax] the CTAs touching each aggregate: g << 16 | its local index there
+  const int* lnptr[2];  // node list of each local aggregate: lnode[lnptr[q] .. lnptr[q+1]) (CTA-local node ids)
+  const int* lnode[2];
+  const int* ntch[2];   // [nagg] number of CTAs touching each aggregate
+};
+struct CoarseHost {
+  int nc = 0, nm = 0, nagg = 0, nbmax = 0;
+  std::vector<int> agg, aptr, anode, nbr;
+  std::vector<double> rel;
+  struct Loc {
+    int nla_max = 0, kmax = 0;
+    std::vector<int> lptr, lagg, tch, lnptr, lnode, ntch;
+  } loc[2];
+};
+CoarseHost coarse_build(int dim, int n_nodes, const double* coords, const int* rowptr, const int* col,
+                        const uint8_t* dmask);
+// coefficient of coarse mode m (0..dim-1: translations, then the rotations) in DOF component
+// c of a node at scaled position d relative to its aggregate centroid: the column of P
+__host__ __device__ __forceinline__ double cc_coef(int dim, int c, int m, const double* d) {
+  if (m < dim) return c == m ? 1.0 : 0.0;
+  if (dim == 2) return c == 0 ? -d[1] : d[0];  // u = w e_z x d
+  switch (m - 3) {                              // 3-D: rotations about x, y, z
+    case 0: return c == 1 ? -d[2] : (c == 2 ? d[1] : 0.0);
+    case 1: return c == 0 ? d[2] : (c == 2 ? -d[0] : 0.0);
+    default: return c == 0 ? -d[1] : (c == 1 ? d[0] : 0.0);
+  }
+}
+
 struct MacroDev {
   int dim, nen, nq, ne, n_nodes, ndof, m, finite, nnz;
   const int* conn;                // [ne][nen]
@@ -104,6 +152,8 @@ struct MacroDev {
   int cg_ellw;  // k_macro_cg_cluster2: ELL width (longest CSR row)
   double* cg_gval;  // [cg_ellw][ndof] ELL slots that do not fit shared memory (L2-resident spill)
   int* cg_gcol;
+  CoarseDev cc;
+  unsigned long long* cg_prof;  // HOM_CG_PROF=1: clock64 phase sums of k_macro_cg_cluster2, [16 CTAs][16]
 };
 constexpr int CG_WDEST = 4;
 
@@ -165,6 +215,8 @@ void cg2_windows(const MacroDev& M, const int* host_rowptr, const int* host_col,
 void cg2_slice_sizes(const MacroDev& M, const int* host_rowptr, int G, int* max_nr, int* max_nnz);
 bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const double* val, const double* rhs,
                               double scale, double rtol, int max_iter, double* x, CgState* st, cudaStream_t s);
+// A_c = P^T K_M P and its inverse for the current values (enqueued before the cluster PCG)
+bool launch_coarse_setup(const MacroDev& M, const double* val, cudaStream_t s);
 void launch_axpy(double* y, const double* x, double a, int n, cudaStream_t s);
 // w between the natural (API) and the internal node order (to_api: internal -> natural)
 void launch_permute_w(const RveDev& R, int B, const double* src, double* dst, int to_api, cudaStream_t s);

@@ -9,6 +9,7 @@
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -566,7 +567,14 @@ __device__ __forceinline__ double cg2_sum(const double* slots, int j, int G) {
   return (t[0] + t[1]) + (t[2] + t[3]);
 }
 
-template <bool WIN, int CG2_THR>  // CG2_THR: 256, or 512 for long slices (more rows in flight)
+// CC: two-level additive preconditioner z = B^-1 r + P A_c^-1 P^T r (coarse.cu).
+// The restriction P^T r of the new residual r_{k+1} = r_k - alpha s_{k+1} is assembled from the
+// partials of P^T r_k and P^T s_{k+1}, which every CTA publishes (one double2 per coarse DOF per
+// destination) together with its (z.w) partial -- alpha is known only after that exchange, so
+// no extra cluster barrier is needed.  Each CTA then forms A_c^-1 r_c on the coarse DOFs of
+// the aggregates its rows touch (fp32 rows of the symmetric A_c^-1: a fixed SPD operator) and
+// adds P z_c in the preconditioner pass.
+template <bool WIN, int CG2_THR, bool CC>  // CG2_THR: 256, or 512 for long slices (more rows in flight)
 __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const double* __restrict__ val,
                                                                const double* __restrict__ b, double scale,
                                                                double rtol, int max_iter, double* __restrict__ xout,
@@ -580,12 +588,18 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
   double* slotsA = sm;                       // [3][CGC_MAXG]: (r.z, r.r)
   double* slotsB = slotsA + 3 * CGC_MAXG;    // [3][CGC_MAXG]: (z.w)
   double* wred = slotsB + 3 * CGC_MAXG;      // [3][32]
+  // CC: this CTA's (P^T r, P^T s) partials on its local aggregates, [nla_max][NM] (same offset
+  // in every CTA: the other CTAs read them through DSMEM)
+  const int gi = G == 16 ? 0 : 1;
+  const int NM = CC ? M.cc.nm : 1, nc = CC ? M.cc.nc : 1, KC = CC ? M.cc.kmax[gi] : 0;
+  const int la0 = CC ? M.cc.lptr[gi][g] : 0, nla = CC ? M.cc.lptr[gi][g + 1] - la0 : 0;
+  double2* lpart = reinterpret_cast<double2*>(wred + 96);
   // z: a full copy (WIN = false) or this CTA's column window [wlo, whi) (WIN = true; indices into zf
   // are then offset by wlo, the CSR columns in shared memory pre-offset)
   const int* wtab = M.cg_win + (G == 16 ? 0 : 2 * CGC_MAXG);
   const int wlo = WIN ? __ldg(wtab + 2 * g) : 0;
   const int zlen = WIN ? M.cg_wmax[G == 16 ? 0 : 1] : n;
-  double* zf = wred + 96;                    // [zlen]
+  double* zf = reinterpret_cast<double*>(lpart + (CC ? M.cc.nla_max[gi] * NM : 0));  // [zlen]
   double* x = zf + zlen;
   double* r = x + nr;
   double* p = r + nr;
@@ -600,6 +614,23 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
   double* sval = mi + nr * dim;
   int* scol = reinterpret_cast<int*>(sval + nell);
   int* srow = scol + nell;
+  // CC, this CTA only: zc [nla * NM], rc [nc], srel [nr] (coordinate i % dim of local node
+  // i / dim, scaled, relative to its aggregate), sainv [nc][nlp] fp32 columns of A_c^-1 on this
+  // CTA's coarse DOFs (nlp = 8 mod 16: conflict-free), sq [nr] local aggregate of each row (-1:
+  // Dirichlet row, zero row of P), the local aggregates' node lists and ids, ntch [nagg]
+  const int nl = nla * NM, nlp = CC ? (nl + 7) / 16 * 16 + 8 : 0;
+  double* zc = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(srow + nr + 1) + 15) & ~uintptr_t(15));
+  float* rcf = reinterpret_cast<float*>(zc + nl);  // [nc] (fp32 coarse solve)
+  double* cpart = zc + nl + (CC ? (nc + 1) / 2 : 0);  // [2 nl][CC_NCH] restriction chunk sums
+  double* srel = cpart + (CC ? 2 * nl * CC_NCH : 0);
+  float* sainv = reinterpret_cast<float*>(srel + (CC ? nr : 0));
+  int* sq = reinterpret_cast<int*>(sainv + (size_t)nlp * nc);
+  int* slnp = sq + (CC ? nr : 0);   // [nla + 1]
+  int* sln = slnp + nla + 1;        // [nr / dim]
+  int* sntch = sln + (CC ? nr / dim : 0);  // [nagg]
+  int* stch = sntch + (CC ? M.cc.nagg : 0);  // [nagg][KC]
+  constexpr int NWARP = CG2_THR / 32;
+  const int lane = tid & 31, warp = tid >> 5;
   double* gval = M.cg_gval + r0;
   int* gcol = M.cg_gcol + r0;
   for (int i = tid; i <= nr; i += CG2_THR) srow[i] = M.rowptr[r0 + i] - nz0;
@@ -697,7 +728,125 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
         else gval[(size_t)j * n + i] = 0.0;
       }
   }
+  if (CC) {
+    const int e00 = M.cc.lnptr[gi][la0];
+    for (int i = tid; i < nr; i += CG2_THR) {
+      srel[i] = M.cc.rel[(size_t)r0 + i];
+      sv[i] = 0.0;
+    }
+    for (int q = tid; q <= nla; q += CG2_THR) slnp[q] = M.cc.lnptr[gi][la0 + q] - e00;
+    for (int a = tid; a < M.cc.nagg; a += CG2_THR) sntch[a] = M.cc.ntch[gi][a];
+    for (int t = tid; t < M.cc.nagg * KC; t += CG2_THR) stch[t] = M.cc.tch[gi][t];
+    for (int q = warp; q < nla; q += NWARP)
+      for (int e = M.cc.lnptr[gi][la0 + q] + lane; e < M.cc.lnptr[gi][la0 + q + 1]; e += 32) {
+        const int l = M.cc.lnode[gi][e];
+        sln[e - e00] = l;
+        for (int c = 0; c < dim; ++c) sq[l * dim + c] = M.dmask[r0 + l * dim + c] ? -1 : q;
+      }
+    for (int t = tid; t < nl * nc; t += CG2_THR) {
+      const int cc = t / nl, rw = t - cc * nl, q = rw / NM, m = rw - q * NM;
+      sainv[cc * nlp + rw] = (float)M.cc.Ainv[(size_t)(M.cc.lagg[gi][la0 + q] * NM + m) * nc + cc];
+    }
+  }
   cl.sync();  // every CTA of the cluster is running before the first DSMEM store
+  // CC: (P^T r, P^T s) over this CTA's rows of each local aggregate -> lpart
+  auto cc_restrict = [&](bool with_s) {
+    // thread per (local coarse DOF t = q * NM + m, vector, chunk of the aggregate's local node
+    // list): serial sums in list order, then the CC_NCH chunk sums in chunk order (fixed order)
+    for (int u = tid; u < 2 * nl * CC_NCH; u += CG2_THR) {
+      const int ch = u % CC_NCH, tv = u / CC_NCH, t = tv >> 1, q = t / NM, m = t - q * NM;
+      const double* vec = (tv & 1) ? sv : r;
+      const int e0 = slnp[q], L = slnp[q + 1] - e0;
+      double acc = 0.0;
+      if (!(tv & 1) || with_s)
+        for (int e = e0 + L * ch / CC_NCH; e < e0 + L * (ch + 1) / CC_NCH; ++e) {
+          const int l = sln[e];
+          if (m < dim) {
+            acc += vec[l * dim + m];
+          } else {
+            const double* d = srel + l * dim;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              if (c < dim) acc += cc_coef(dim, c, m, d) * vec[l * dim + c];
+          }
+        }
+      cpart[u] = acc;
+    }
+    __syncthreads();
+    for (int tv = tid; tv < 2 * nl; tv += CG2_THR) {
+      double acc = 0.0;
+#pragma unroll
+      for (int ch = 0; ch < CC_NCH; ++ch) acc += cpart[tv * CC_NCH + ch];
+      reinterpret_cast<double*>(lpart)[tv] = acc;
+    }
+  };
+  // CC: r_c = sum_k (P^T r)_k - alpha sum_k (P^T s)_k (thread per coarse DOF), then
+  // zc = A_c^-1 r_c on this CTA's coarse DOFs: lane = (row t0 + lane % 8, column group lane / 8),
+  // columns c = group + 4 u, two butterfly steps (fixed order)
+  auto cc_rc = [&](double alpha) {
+    for (int c = tid; c < nc; c += CG2_THR) {
+      const int a = c / NM, m = c - a * NM, nt = sntch[a];
+      double sr = 0.0, ss = 0.0;
+      double2 t4[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)  // DSMEM loads from the CTAs touching aggregate a, in flight together
+        if (k < nt) {
+          const int tk = stch[a * KC + k];
+          t4[k] = cl.map_shared_rank(lpart, tk >> 16)[(tk & 0xffff) * NM + m];
+        }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k < nt) {
+          sr += t4[k].x;
+          ss += t4[k].y;
+        }
+      for (int k = 4; k < nt; ++k) {
+        const int tk = stch[a * KC + k];
+        const double2 t = cl.map_shared_rank(lpart, tk >> 16)[(tk & 0xffff) * NM + m];
+        sr += t.x;
+        ss += t.y;
+      }
+      rcf[c] = (float)(sr - alpha * ss);
+    }
+    __syncthreads();
+  };
+  auto cc_mv = [&]() {
+    for (int t0 = warp * 8; t0 < nl; t0 += NWARP * 8) {
+      const int t = t0 + (lane & 7), cg = lane >> 3;
+      float a0 = 0.0f, a1 = 0.0f;
+      if (t < nl) {
+        int c = cg;
+#pragma unroll 4
+        for (; c + 4 < nc; c += 8) {
+          a0 = fmaf(sainv[c * nlp + t], rcf[c], a0);
+          a1 = fmaf(sainv[(c + 4) * nlp + t], rcf[c + 4], a1);
+        }
+        if (c < nc) a0 = fmaf(sainv[c * nlp + t], rcf[c], a0);
+      }
+      float a = a0 + a1;
+      a += __shfl_xor_sync(0xffffffffu, a, 8);
+      a += __shfl_xor_sync(0xffffffffu, a, 16);
+      if (cg == 0 && t < nl) zc[t] = (double)a;
+    }
+    __syncthreads();
+  };
+  // CC: (P z_c)_i for local row i
+  auto cc_prolong = [&](int i) {
+    const int q = sq[i];
+    if (q < 0) return 0.0;
+    const int l = i / dim, c = i - l * dim;
+    double z = 0.0;
+#pragma unroll
+    for (int m = 0; m < 6; ++m)
+      if (m < NM) z += cc_coef(dim, c, m, srel + l * dim) * zc[q * NM + m];
+    return z;
+  };
+  if (CC) {  // r_c of r_0 = b: one extra exchange before the first preconditioner application
+    cc_restrict(false);
+    cl.sync();
+    cc_rc(0.0);
+    cc_mv();
+  }
 
   // z = M^-1 r on the local rows, scattered into every CTA's copy; returns (r.z, r.r) partials
   auto precond_publish = [&](double* part) {
@@ -706,6 +855,7 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
       const int nl = i / dim, ci = i % dim;
       double z = 0.0;
       for (int cj = 0; cj < dim; ++cj) z += mi[i * dim + cj] * r[nl * dim + cj];
+      if (CC) z += cc_prolong(i);
       rz += r[i] * z;
       rr += r[i] * r[i];
       put_z(i, z);
@@ -715,7 +865,7 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
     part[1] = rr;
   };
   // w = A z (local rows, free DOFs only); returns the (z.w) partial
-  auto spmv = [&]() {
+  auto spmv = [&](double beta_s) {  // CC: also s = w + beta_s s (needed before the exchange)
     double zw = 0.0;
     for (int i = tid; i < nr; i += CG2_THR) {
       double s0 = 0.0, s1 = 0.0;
@@ -743,6 +893,7 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
       }
       const double wi = s0 + s1;
       w[i] = wi;
+      if (CC) sv[i] = wi + beta_s * sv[i];
       zw += zf[zown + i] * wi;
     }
     return zw;
@@ -756,8 +907,9 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
   const double bnorm = sqrt(rr);
   int it = 0, status = 0;
   if (bnorm > 0.0) {
-    v[0] = spmv();
-    cg2_publish<CG2_THR>(cl, slotsB, 1, v, wred);
+    v[0] = spmv(0.0);
+    cg2_publish<CG2_THR>(cl, slotsB, 1, v, wred);  // its CTA barrier also completes r and s
+    if (CC) cc_restrict(true);
     cl.sync();
     double del = cg2_sum(slotsB, 0, G);
     if (!(del > 0.0)) status = 6;
@@ -781,9 +933,11 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
           double pi = p[i], si = sv[i];
           if (!OVL && !first) {
             pi = zf[zown + i] + beta * pi;
-            si = w[i] + beta * si;
             p[i] = pi;
-            sv[i] = si;
+            if (!CC) {
+              si = w[i] + beta * si;
+              sv[i] = si;
+            }
           }
           x[i] += alpha * pi;
           ri = r[i] - alpha * si;
@@ -795,6 +949,13 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
           double z = 0.0;
           z += mi[i * 2] * re;
           z += mi[i * 2 + 1] * ro;
+          if (CC) {
+            const int q = sq[i];
+            if (q >= 0) {
+              const int c = i & 1;
+              z += zc[q * 3 + c] + (c == 0 ? -srel[i + 1] : srel[i - 1]) * zc[q * 3 + 2];
+            }
+          }
           rz += ri * z;
           rr2 += ri * ri;
           put_z(i, z);
@@ -803,7 +964,22 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
       part[0] = rz;
       part[1] = rr2;
     };
+    long long tprev = clock64();
+    auto mark = [&](int k) {  // HOM_CG_PROF phase timing (thread 0 of every CTA)
+      if (M.cg_prof && tid == 0) {
+        const long long t = clock64();
+        M.cg_prof[g * 16 + k] += (unsigned long long)(t - tprev);
+        tprev = t;
+      }
+    };
     for (it = 1; it <= max_iter && status == 0; ++it) {
+      mark(0);
+      if (CC) {
+        cc_rc(alpha);
+        mark(11);
+        cc_mv();
+      }
+      mark(1);
       if (dim == 2) {
         fused2(it == 1, v);
       } else {
@@ -814,23 +990,33 @@ __global__ void __launch_bounds__(CG2_THR) k_macro_cg_cluster2(MacroDev M, const
         __syncthreads();  // r complete before the block preconditioner mixes components
         precond_publish(v);
       }
+      mark(2);
       cg2_publish<CG2_THR>(cl, slotsA, 2, v, wred);
+      mark(3);
       cl.sync();
+      mark(4);
       const double gn = cg2_sum(slotsA, 0, G);
       rr = cg2_sum(slotsA, 1, G);
       if (sqrt(rr) <= rtol * bnorm) break;
-      v[0] = spmv();
       beta = gn / gam;
-      cg2_publish<CG2_THR>(cl, slotsB, 1, v, wred);
+      v[0] = spmv(beta);
+      mark(5);
+      cg2_publish<CG2_THR>(cl, slotsB, 1, v, wred);  // its CTA barrier also completes r and s
+      mark(6);
+      if (CC) cc_restrict(true);
+      mark(7);
       cl.barrier_arrive();
+      mark(8);
       // the direction updates need beta (known) and local rows only: they run while the cluster
       // barrier of the (z.w) exchange completes
       if (OVL || dim != 2)
         for (int i = tid; i < nr; i += CG2_THR) {
           p[i] = zf[zown + i] + beta * p[i];
-          sv[i] = w[i] + beta * sv[i];
+          if (!CC) sv[i] = w[i] + beta * sv[i];
         }
+      mark(9);
       cl.barrier_wait();
+      mark(10);
       del = cg2_sum(slotsB, 0, G);
       const double den = del - beta * gn / alpha;
       if (!(den > 0.0)) { status = 6; break; }
@@ -895,29 +1081,43 @@ bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const do
     const char* e = getenv("HOM_CG_FULLZ");  // experiment knob: 1 = try the full z copy first
     return e ? atoi(e) : 0;
   }();
-  // preference: the whole ELL slice in shared memory, z windows (fewer DSMEM stores), 16 CTAs
-  for (int c = 0; c < 8; ++c) {
-      const int spill = c >> 2, gi = c & 1, win = ((c >> 1) & 1) ^ (prefer_full ? 0 : 1);
+  // preference: the two-level preconditioner, the whole ELL slice in shared memory, z windows
+  // (fewer DSMEM stores), 16 CTAs
+  bool cc_ready = false;
+  for (int c = 0; c < 16; ++c) {
+      const int use_cc = !(c >> 3), spill = (c >> 2) & 1, gi = c & 1, win = ((c >> 1) & 1) ^ (prefer_full ? 0 : 1);
       const int G = gi == 0 ? 16 : 8;
+      if (use_cc && M.cc.nc <= 0) continue;
       if (force_G && G != force_G) continue;
       if (win && !M.cg_wok[gi]) continue;
       const int max_nr = slice[gi][0];
       const int zlen = win ? M.cg_wmax[gi] : M.ndof;
-      const size_t base = (size_t)(6 * CGC_MAXG + 96 + zlen + 5 * max_nr + max_nr * M.dim) * 8 +
-                          (size_t)(max_nr + 1) * 4 + 64;
-      const size_t cap = 220 * 1024;
+      size_t base = (size_t)(6 * CGC_MAXG + 96 + zlen + 5 * max_nr + max_nr * M.dim) * 8 +
+                    (size_t)(max_nr + 1) * 4 + 64;
+      if (use_cc) {  // k_macro_cg_cluster2's CC arrays
+        const int nla = M.cc.nla_max[gi], nl = nla * M.cc.nm, nlp = (nl + 7) / 16 * 16 + 8;
+        base += (size_t)nl * 16 + 16 + (size_t)(nl + M.cc.nc + max_nr + 2 * nl * CC_NCH) * 8 + (size_t)nlp * M.cc.nc * 4 +
+                (size_t)(max_nr + 1 + nla + max_nr / M.dim + M.cc.nagg * (1 + M.cc.kmax[gi])) * 4;
+      }
+      const size_t cap = 227 * 1024;  // the sm_100 per-CTA opt-in maximum
       if (base > cap) continue;
       int js = (int)std::min<size_t>(M.cg_ellw, (cap - base) / ((size_t)max_nr * 12));
       if (js < M.cg_ellw) {
         if (!spill) continue;
         js &= ~1;
+        if (js < 2) continue;
       } else if (spill) {
         continue;  // already tried without
       }
       const size_t sm = base + (size_t)max_nr * js * 12;
       const bool wide = max_nr > 768;
-      auto k = win ? (wide ? k_macro_cg_cluster2<true, 512> : k_macro_cg_cluster2<true, 256>)
-                   : (wide ? k_macro_cg_cluster2<false, 512> : k_macro_cg_cluster2<false, 256>);
+      decltype(&k_macro_cg_cluster2<true, 256, true>) k;
+      if (use_cc)
+        k = win ? (wide ? k_macro_cg_cluster2<true, 512, true> : k_macro_cg_cluster2<true, 256, true>)
+                : (wide ? k_macro_cg_cluster2<false, 512, true> : k_macro_cg_cluster2<false, 256, true>);
+      else
+        k = win ? (wide ? k_macro_cg_cluster2<true, 512, false> : k_macro_cg_cluster2<true, 256, false>)
+                : (wide ? k_macro_cg_cluster2<false, 512, false> : k_macro_cg_cluster2<false, 256, false>);
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
       if (G > 8) cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
       cudaLaunchConfig_t cfg = {};
@@ -937,6 +1137,15 @@ bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const do
         cudaGetLastError();
         continue;
       }
+      if (use_cc && !cc_ready) {  // A_c and its inverse for these values, same stream
+        if (!launch_coarse_setup(M, val, s)) {
+          cudaGetLastError();
+          continue;
+        }
+        cc_ready = true;
+      }
+      if (getenv("HOM_CG_VERBOSE"))
+        fprintf(stderr, "cg2: cc %d G %d win %d wide %d js %d/%d smem %zu\n", use_cc, G, win, (int)wide, js, M.cg_ellw, sm);
       cudaError_t e = cudaLaunchKernelEx(&cfg, k, M, val, rhs, scale, rtol, max_iter, x, st, js);
       if (e == cudaSuccess) return true;
       cudaGetLastError();
