@@ -975,9 +975,10 @@ int hom_macro_solve(hom_ctx* c, const double* d_D, const double* d_S, double sca
   run(c, HOM_PROF_MACRO_ASSEMBLE, s, [&] { hom::launch_macro_rhs(c->M, c->val, d_S, scale, c->rhs, nullptr, s); });
   // macro PCG: one cluster with the matrix in shared memory when it fits (config sizes),
   // else grid-wide kernels (scaled meshes); the cluster kernel with a global CSR as the last resort
+  int extra = 0;  // the two-level preconditioner's setup kernels (coarse.cu)
   run(c, HOM_PROF_CG, s, [&] {
     if (hom::launch_macro_cg_cluster2(c->M, c->cg2_slice, c->val, c->rhs, scale, c->opt.cg_rtol,
-                                      c->opt.cg_max_iter, d_x, c->cgst, s))
+                                      c->opt.cg_max_iter, d_x, c->cgst, s, &extra))
       return;
     if (c->M.ndof >= 32768) {
       hom::launch_macro_cg_large(c->M, c->val, c->diag, c->rhs, scale, c->opt.cg_rtol, c->opt.cg_max_iter, d_x,
@@ -989,6 +990,7 @@ int hom_macro_solve(hom_ctx* c, const double* d_D, const double* d_S, double sca
       hom::launch_macro_cg(c->M, c->val, c->diag, c->rhs, scale, c->opt.cg_rtol, c->opt.cg_max_iter, d_x,
                            c->cgwork, c->cgst, s);
   });
+  c->launches += extra;
   int rc = check_cuda(c, cudaGetLastError(), "hom_macro_solve");
   if (rc) return rc;
   CgState st{};

@@ -214,7 +214,8 @@ void cg2_windows(const MacroDev& M, const int* host_rowptr, const int* host_col,
                  int* wok);
 void cg2_slice_sizes(const MacroDev& M, const int* host_rowptr, int G, int* max_nr, int* max_nnz);
 bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const double* val, const double* rhs,
-                              double scale, double rtol, int max_iter, double* x, CgState* st, cudaStream_t s);
+                              double scale, double rtol, int max_iter, double* x, CgState* st, cudaStream_t s,
+                              int* extra_launches = nullptr);
 // A_c = P^T K_M P and its inverse for the current values (enqueued before the cluster PCG)
 bool launch_coarse_setup(const MacroDev& M, const double* val, cudaStream_t s);
 void launch_axpy(double* y, const double* x, double a, int n, cudaStream_t s);

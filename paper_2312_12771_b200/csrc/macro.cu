@@ -1072,7 +1072,9 @@ void cg2_slice_sizes(const MacroDev& M, const int* host_rowptr, int G, int* max_
 }
 
 bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const double* val, const double* rhs,
-                              double scale, double rtol, int max_iter, double* x, CgState* st, cudaStream_t s) {
+                              double scale, double rtol, int max_iter, double* x, CgState* st, cudaStream_t s,
+                              int* extra_launches) {
+  if (extra_launches) *extra_launches = 0;
   static const int force_G = [] {
     const char* e = getenv("HOM_CG_CLUSTER");  // experiment knob: 8 or 16
     return e ? atoi(e) : 0;
@@ -1143,6 +1145,7 @@ bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const do
           continue;
         }
         cc_ready = true;
+        if (extra_launches) *extra_launches = 2;  // k_coarse_assemble, k_coarse_invert
       }
       if (getenv("HOM_CG_VERBOSE"))
         fprintf(stderr, "cg2: cc %d G %d win %d wide %d js %d/%d smem %zu\n", use_cc, G, win, (int)wide, js, M.cg_ellw, sm);
