@@ -1106,8 +1106,7 @@ bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const do
       int js = (int)std::min<size_t>(M.cg_ellw, (cap - base) / ((size_t)max_nr * 12));
       if (js < M.cg_ellw) {
         if (!spill) continue;
-        js &= ~1;
-        if (js < 2) continue;
+        js &= ~1;  // may be 0: the whole ELL slice from L2
       } else if (spill) {
         continue;  // already tried without
       }
