@@ -145,6 +145,12 @@ typedef struct {
                                (first appearance in the mesh).  The layout of w at the API (d_w of
                                hom_recover_fluctuations / hom_set_fluctuations / hom_get_fluctuations)
                                is always the natural one. */
+  int32_t macro_precond;    /* preconditioner of the macro PCG (a6): 0 = two-level (default): node-block
+                               Jacobi + an additive coarse space of node aggregates with their rigid-body
+                               modes, A_c = P^T K_M P formed and inverted on the device every solve
+                               (meshes with >= 1024 DOFs in 2-D / 3-D, otherwise 1);
+                               1 = node-block Jacobi only.  The solution is the same (rtol), only the
+                               iteration count differs. */
 } hom_options;
 
 typedef struct {

@@ -29,12 +29,12 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 CoarseHost coarse_build(int dim, int n_nodes, const double* coords, const int* rowptr, const int* col,
-                        const uint8_t* dmask) {
+                        const uint8_t* dmask, int one_level) {
   CoarseHost H;
   H.nc = 0;
   const int ndof = n_nodes * dim;
   const char* e = getenv("HOM_CG_COARSE");  // experiment knob: 0 = one-level block Jacobi only
-  if ((e && atoi(e) == 0) || dim < 2 || ndof < CC_MIN_DOF) return H;
+  if (one_level || (e && atoi(e) == 0) || dim < 2 || ndof < CC_MIN_DOF) return H;
   const char* ena = getenv("HOM_CG_COARSE_NA");  // experiment knob: aggregates per axis
   const int nm = dim == 2 ? 3 : 6, na = ena ? atoi(ena) : (dim == 2 ? CC_NA2 : CC_NA3);
   if (na < 1) return H;

@@ -268,6 +268,8 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   c->dim = dim;
   c->finite = mat->kind >= 1;
   c->m = c->finite ? 4 : (dim == 1 ? 1 : (dim == 2 ? 3 : 6));
+  if (options->macro_precond < 0 || options->macro_precond > 1)
+    return fail(HOM_ERR_INVALID_ARG, "macro_precond must be 0 (two-level) or 1 (node-block Jacobi)");
   if (options->macro_basis < 0 || options->macro_basis > 1 || (options->macro_basis == 1 && c->finite))
     return fail(HOM_ERR_INVALID_ARG, "macro_basis must be 0 (Dirac) or 1 (constant, small strain only)");
   c->B = mac->n_elems * (options->macro_basis == 1 ? 1 : nq);
@@ -772,7 +774,8 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
     if (M.cg_prof) cudaMemsetAsync(M.cg_prof, 0, 256 * 8, s);
   }
   {  // coarse space of the two-level macro preconditioner (coarse.cu)
-    hom::CoarseHost H = hom::coarse_build(dim, M.n_nodes, mac->coords, rowptr.data(), col.data(), dmask.data());
+    hom::CoarseHost H =
+        hom::coarse_build(dim, M.n_nodes, mac->coords, rowptr.data(), col.data(), dmask.data(), c->opt.macro_precond);
     hom::CoarseDev& C = M.cc;
     C = hom::CoarseDev{};
     if (H.nc > 0) {

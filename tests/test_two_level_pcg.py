@@ -7,8 +7,6 @@ to the numpy model's range (tools/cg_coarse_model.py), and the result is
 bitwise reproducible run to run (fixed summation order in A_c, its inverse and
 the per-iteration restriction).
 """
-import os
-
 import numpy as np
 import pytest
 
@@ -34,15 +32,7 @@ def torch_cuda():
 
 def solve(wl, coarse=True):
     from paper_2312_12771_b200.hom import Homogenizer
-    old = os.environ.get("HOM_CG_COARSE")
-    os.environ["HOM_CG_COARSE"] = "1" if coarse else "0"
-    try:
-        h = Homogenizer.from_workload(wl)
-    finally:
-        if old is None:
-            del os.environ["HOM_CG_COARSE"]
-        else:
-            os.environ["HOM_CG_COARSE"] = old
+    h = Homogenizer.from_workload(wl, macro_precond="two_level" if coarse else "jacobi")
     C, u, w, info = h.solve_linear()
     out = (C.cpu().numpy(), u.cpu().numpy(), info)
     h.close()
