@@ -29,7 +29,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 CoarseHost coarse_build(int dim, int n_nodes, const double* coords, const int* rowptr, const int* col,
-                        const uint8_t* dmask, int one_level) {
+                        int one_level) {
   CoarseHost H;
   H.nc = 0;
   const int ndof = n_nodes * dim;
@@ -140,7 +140,6 @@ CoarseHost coarse_build(int dim, int n_nodes, const double* coords, const int* r
     for (int a = 0; a < nagg; ++a)
       for (size_t k = 0; k < who[a].size(); ++k) L.tch[(size_t)a * L.kmax + k] = who[a][k];
   }
-  (void)dmask;
   H.nm = nm;
   H.nagg = nagg;
   H.nc = nagg * nm;

@@ -775,7 +775,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   }
   {  // coarse space of the two-level macro preconditioner (coarse.cu)
     hom::CoarseHost H =
-        hom::coarse_build(dim, M.n_nodes, mac->coords, rowptr.data(), col.data(), dmask.data(), c->opt.macro_precond);
+        hom::coarse_build(dim, M.n_nodes, mac->coords, rowptr.data(), col.data(), c->opt.macro_precond);
     hom::CoarseDev& C = M.cc;
     C = hom::CoarseDev{};
     if (H.nc > 0) {

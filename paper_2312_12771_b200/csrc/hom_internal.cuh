@@ -108,8 +108,9 @@ struct CoarseHost {
     std::vector<int> lptr, lagg, tch, lnptr, lnode, ntch;
   } loc[2];
 };
+// host side, once per macro mesh (Dirichlet rows of P are zeroed on the device through dmask)
 CoarseHost coarse_build(int dim, int n_nodes, const double* coords, const int* rowptr, const int* col,
-                        const uint8_t* dmask, int one_level);
+                        int one_level);
 // coefficient of coarse mode m (0..dim-1: translations, then the rotations) in DOF component
 // c of a node at scaled position d relative to its aggregate centroid: the column of P
 __host__ __device__ __forceinline__ double cc_coef(int dim, int c, int m, const double* d) {
