@@ -88,3 +88,24 @@ def test_mapped_mesh_two_level_parity(torch_cuda):
     o = oracle.macro_solve(2, 24, C2, wl.dir_dof, wl.dir_val, body=wl.body, mesh=(mc, conn))
     assert rel(u1, o) <= TOL_U and rel(u2, o) <= TOL_U, (rel(u1, o), rel(u2, o))
     assert i2.iterations < i1.iterations, (i1.iterations, i2.iterations)
+
+
+def test_fully_constrained_aggregates_drop_their_modes(torch_cuda):
+    """The leftmost node columns (both components) are prescribed: the aggregates of that strip have
+    no free DOF, their rows of A_c are zero and the sweep drops those modes (pivot <= 1e-10 of the
+    original diagonal); a roller strip (x components only) leaves a rank-deficient mode pattern in
+    the next aggregates.  u must still match the direct solve and the coarse space must still pay."""
+    wl = W.config2(nel=32, r=8)
+    nn = wl.nel + 1
+    nodes = np.arange(nn * nn)
+    ix = nodes % nn
+    clamp = nodes[ix <= 5]
+    roll = nodes[(ix >= 6) & (ix <= 9)]
+    dof = np.concatenate([2 * clamp, 2 * clamp + 1, 2 * roll]).astype(np.int32)
+    wl.dir_dof = np.sort(dof)
+    wl.dir_val = np.zeros(len(dof))
+    C1, u1, i1 = solve(wl, coarse=False)
+    C2, u2, i2 = solve(wl, coarse=True)
+    o = oracle.macro_solve(2, wl.nel, C2, wl.dir_dof, wl.dir_val, body=wl.body)
+    assert rel(u1, o) <= TOL_U and rel(u2, o) <= TOL_U, (rel(u1, o), rel(u2, o))
+    assert i2.iterations < i1.iterations, (i1.iterations, i2.iterations)
