@@ -29,7 +29,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 }
 
 CoarseHost coarse_build(int dim, int n_nodes, const double* coords, const int* rowptr, const int* col,
-                        int one_level) {
+                        int one_level, int ggrid) {
   CoarseHost H;
   H.nc = 0;
   const int ndof = n_nodes * dim;
@@ -110,8 +110,9 @@ CoarseHost coarse_build(int dim, int n_nodes, const double* coords, const int* r
     for (size_t q = 0; q < nb[a].size(); ++q) H.nbr[(size_t)a * H.nbmax + q] = nb[a][q];
   // per cluster size: the aggregates each CTA's node range touches, its position among the
   // CTAs touching each aggregate, and its node list per local aggregate
-  for (int gi = 0; gi < 2; ++gi) {
-    const int G = gi == 0 ? 16 : 8;
+  H.ggrid = ggrid;
+  for (int gi = 0; gi < 3; ++gi) {
+    const int G = gi == 0 ? 16 : (gi == 1 ? 8 : ggrid);
     auto& L = H.loc[gi];
     L.ntch.assign(nagg, 0);
     L.lptr.assign(G + 1, 0);

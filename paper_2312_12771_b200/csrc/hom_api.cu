@@ -774,8 +774,11 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
     if (M.cg_prof) cudaMemsetAsync(M.cg_prof, 0, 256 * 8, s);
   }
   {  // coarse space of the two-level macro preconditioner (coarse.cu)
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    sms = std::max(sms, 1);
     hom::CoarseHost H =
-        hom::coarse_build(dim, M.n_nodes, mac->coords, rowptr.data(), col.data(), c->opt.macro_precond);
+        hom::coarse_build(dim, M.n_nodes, mac->coords, rowptr.data(), col.data(), c->opt.macro_precond, sms);
     hom::CoarseDev& C = M.cc;
     C = hom::CoarseDev{};
     if (H.nc > 0) {
@@ -787,17 +790,26 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
       C.nbr = upload(c, H.nbr, s, &rc);
       C.Ac = dalloc<double>(c, (size_t)H.nc * H.nc, &rc);
       C.Ainv = dalloc<double>(c, (size_t)H.nc * H.nc, &rc);
-      for (int gi = 0; gi < 2; ++gi) {
+      C.ggrid = H.ggrid;
+      for (int gi = 0; gi < 3; ++gi) {
         const auto& L = H.loc[gi];
-        C.nla_max[gi] = L.nla_max;
-        C.kmax[gi] = L.kmax;
-        C.lptr[gi] = upload(c, L.lptr, s, &rc);
-        C.lagg[gi] = upload(c, L.lagg, s, &rc);
-        C.tch[gi] = upload(c, L.tch, s, &rc);
-        C.lnptr[gi] = upload(c, L.lnptr, s, &rc);
-        C.lnode[gi] = upload(c, L.lnode, s, &rc);
-        C.ntch[gi] = upload(c, L.ntch, s, &rc);
+        const int* d_lptr = upload(c, L.lptr, s, &rc);
+        const int* d_lagg = upload(c, L.lagg, s, &rc);
+        const int* d_tch = upload(c, L.tch, s, &rc);
+        const int* d_lnptr = upload(c, L.lnptr, s, &rc);
+        const int* d_lnode = upload(c, L.lnode, s, &rc);
+        const int* d_ntch = upload(c, L.ntch, s, &rc);
+        if (gi < 2) {
+          C.nla_max[gi] = L.nla_max; C.kmax[gi] = L.kmax;
+          C.lptr[gi] = d_lptr; C.lagg[gi] = d_lagg; C.tch[gi] = d_tch;
+          C.lnptr[gi] = d_lnptr; C.lnode[gi] = d_lnode; C.ntch[gi] = d_ntch;
+        } else {
+          C.nla_max_g = L.nla_max; C.kmax_g = L.kmax;
+          C.lptr_g = d_lptr; C.lagg_g = d_lagg; C.tch_g = d_tch;
+          C.lnptr_g = d_lnptr; C.lnode_g = d_lnode; C.ntch_g = d_ntch;
+        }
       }
+      C.gpart = dalloc<double2>(c, (size_t)std::max(H.ggrid, 1) * std::max(H.loc[2].nla_max, 1) * H.nm, &rc);
     }
   }
 
@@ -979,11 +991,16 @@ int hom_macro_solve(hom_ctx* c, const double* d_D, const double* d_S, double sca
   // macro PCG: one cluster with the matrix in shared memory when it fits (config sizes),
   // else grid-wide kernels (scaled meshes); the cluster kernel with a global CSR as the last resort
   int extra = 0;  // the two-level preconditioner's setup kernels (coarse.cu)
+  const char* fge = getenv("HOM_CG_FORCE_GRID");  // test / experiment knob: the persistent grid-wide PCG
+  const int force_grid = fge ? atoi(fge) : 0;
   run(c, HOM_PROF_CG, s, [&] {
-    if (hom::launch_macro_cg_cluster2(c->M, c->cg2_slice, c->val, c->rhs, scale, c->opt.cg_rtol,
-                                      c->opt.cg_max_iter, d_x, c->cgst, s, &extra))
+    if (!force_grid && hom::launch_macro_cg_cluster2(c->M, c->cg2_slice, c->val, c->rhs, scale, c->opt.cg_rtol,
+                                                     c->opt.cg_max_iter, d_x, c->cgst, s, &extra))
       return;
-    if (c->M.ndof >= 32768) {
+    if (c->M.ndof >= 32768 || force_grid) {
+      if (hom::launch_macro_cg_grid(c->M, c->val, c->rhs, scale, c->opt.cg_rtol, c->opt.cg_max_iter, d_x, c->cgwork,
+                                    c->cgl_part, c->cgst, s, &extra))
+        return;
       hom::launch_macro_cg_large(c->M, c->val, c->diag, c->rhs, scale, c->opt.cg_rtol, c->opt.cg_max_iter, d_x,
                                  c->cgwork, c->cgl_sc, c->cgl_part, c->cgst, s);
       return;

@@ -98,6 +98,10 @@ struct CoarseDev {
   const int* lnptr[2];  // node list of each local aggregate: lnode[lnptr[q] .. lnptr[q+1]) (CTA-local node ids)
   const int* lnode[2];
   const int* ntch[2];   // [nagg] number of CTAs touching each aggregate
+  // the same for k_macro_cg_grid's partition (G = ggrid CTAs, one per SM)
+  int ggrid, nla_max_g, kmax_g;
+  const int *lptr_g, *lagg_g, *tch_g, *lnptr_g, *lnode_g, *ntch_g;
+  double2* gpart;       // [ggrid][nla_max[2] * nm] k_macro_cg_grid's restriction partials
 };
 struct CoarseHost {
   int nc = 0, nm = 0, nagg = 0, nbmax = 0;
@@ -106,11 +110,12 @@ struct CoarseHost {
   struct Loc {
     int nla_max = 0, kmax = 0;
     std::vector<int> lptr, lagg, tch, lnptr, lnode, ntch;
-  } loc[2];
+  } loc[3];
+  int ggrid = 0;
 };
 // host side, once per macro mesh (Dirichlet rows of P are zeroed on the device through dmask)
 CoarseHost coarse_build(int dim, int n_nodes, const double* coords, const int* rowptr, const int* col,
-                        int one_level);
+                        int one_level, int ggrid);
 // coefficient of coarse mode m (0..dim-1: translations, then the rotations) in DOF component
 // c of a node at scaled position d relative to its aggregate centroid: the column of P
 __host__ __device__ __forceinline__ double cc_coef(int dim, int c, int m, const double* d) {
@@ -207,6 +212,10 @@ bool launch_macro_cg_cluster(const MacroDev& M, int max_slice_nnz, const double*
                              CgState* st, cudaStream_t s);
 void launch_norm(const double* v, int n, double* out, cudaStream_t s);
 void launch_spmv(const MacroDev& M, const double* val, const double* x, double* y, cudaStream_t s);
+// persistent cooperative PCG for meshes beyond one cluster (one CTA per SM); false if it does not fit
+bool launch_macro_cg_grid(const MacroDev& M, const double* val, const double* rhs, double scale, double rtol,
+                          int max_iter, double* x, double* zg, double* part, CgState* st, cudaStream_t s,
+                          int* extra_launches = nullptr);
 void launch_macro_cg_large(const MacroDev& M, const double* val, const double* diag, const double* rhs,
                            double scale, double rtol, int max_iter, double* xout, double* work, double* sc,
                            double* part, CgState* st, cudaStream_t s);

@@ -1155,6 +1155,378 @@ bool launch_macro_cg_cluster2(const MacroDev& M, const int (*slice)[2], const do
   return false;
 }
 
+// ---------------------------------------------------------------- persistent grid-wide PCG
+// Meshes beyond one cluster (e.g. the config-3 macro mesh at N = 8, nel 181, 66k DOFs): one
+// cooperative launch, one CTA per SM, the same Chronopoulos-Gear iteration and node-block Jacobi
+// preconditioner as k_macro_cg_cluster2.  Each CTA owns a node range: its CSR slice as column-major
+// ELL (shared memory, trailing slots in the global [slot][ndof] spill) and its x, r, p, s, w and
+// block inverses in shared memory; z goes to a global array (L2) that the SpMV gathers read with
+// ld.global.cg after the grid barrier.  Two grid barriers per iteration; the dot products are
+// per-CTA partials in global memory summed by every CTA in CTA order (bitwise deterministic).
+constexpr int CGG_THR = 512;
+__device__ __forceinline__ double cgg_sum(const double* part, int G, int j, double* sred) {
+  // every thread returns sum_g part[g * 4 + j] in g order (warp 0 sums, broadcast through sred)
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) {
+    double a = 0.0;
+    for (int g = lane; g < G; g += 32) a += __ldcg(part + g * 4 + j);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    if (lane == 0) sred[j] = a;
+  }
+  __syncthreads();
+  const double v = sred[j];
+  return v;
+}
+template <bool CC>  // CC: the two-level preconditioner of k_macro_cg_cluster2, partials through L2
+__global__ void __launch_bounds__(CGG_THR) k_macro_cg_grid(MacroDev M, const double* __restrict__ val,
+                                                           const double* __restrict__ b, double scale, double rtol,
+                                                           int max_iter, double* __restrict__ xout, CgState* st,
+                                                           double* __restrict__ zg, double* __restrict__ part, int js) {
+  cgx::grid_group grid = cgx::this_grid();
+  const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int n = M.ndof, dim = M.dim;
+  const int nd0 = (int)((long)M.n_nodes * g / G), nd1 = (int)((long)M.n_nodes * (g + 1) / G);
+  const int r0 = nd0 * dim, nr = (nd1 - nd0) * dim;
+  extern __shared__ __align__(16) double sm[];
+  double* sred = sm;              // [8]
+  double* wred = sred + 8;        // [3][32]
+  double* x = wred + 96;
+  double* r = x + nr;
+  double* p = r + nr;
+  double* sv = p + nr;
+  double* w = sv + nr;
+  double* zl = w + nr;
+  double* mi = zl + nr;           // [nr][dim]
+  const int nz0 = M.rowptr[r0], ew = M.cg_ellw, nell = js * nr;
+  double* sval = mi + nr * dim;
+  int* scol = reinterpret_cast<int*>(sval + nell);
+  int* srow = scol + nell;
+  double* gval = M.cg_gval + r0;
+  int* gcol = M.cg_gcol + r0;
+  // CC: zc [nl], rcf [nc] fp32, cpart [2 nl][CC_NCH], srel [nr], sainv [nc][nlp] fp32,
+  // sq [nr], slnp [nla + 1], sln [nr / dim], sntch [nagg], stch [nagg][KC]
+  constexpr int NWARP = CGG_THR / 32;
+  const int NM = CC ? M.cc.nm : 1, nc = CC ? M.cc.nc : 1, KC = CC ? M.cc.kmax_g : 0;
+  const int la0 = CC ? M.cc.lptr_g[g] : 0, nla = CC ? M.cc.lptr_g[g + 1] - la0 : 0;
+  const int nl = nla * NM, nlp = CC ? (nl + 7) / 16 * 16 + 8 : 0, nlm = CC ? M.cc.nla_max_g * NM : 0;
+  double* zc = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(srow + nr + 1) + 15) & ~uintptr_t(15));
+  float* rcf = reinterpret_cast<float*>(zc + nl);
+  double* cpart = zc + nl + (CC ? (nc + 1) / 2 : 0);
+  double* srel = cpart + (CC ? 2 * nl * CC_NCH : 0);
+  float* sainv = reinterpret_cast<float*>(srel + (CC ? nr : 0));
+  int* sq = reinterpret_cast<int*>(sainv + (size_t)nlp * nc);
+  int* slnp = sq + (CC ? nr : 0);
+  int* sln = slnp + (CC ? nla + 1 : 0);
+  int* sntch = sln + (CC ? nr / dim : 0);
+  int* stch = sntch + (CC ? M.cc.nagg : 0);
+  double2* gpart = CC ? M.cc.gpart : nullptr;
+  for (int i = tid; i <= nr; i += CGG_THR) srow[i] = M.rowptr[r0 + i] - nz0;
+  __syncthreads();
+  for (int e = tid; e < ew * nr; e += CGG_THR) {
+    const int j = e / nr, i = e - j * nr, k = srow[i] + j;
+    const bool in = k < srow[i + 1];
+    const double vv = in ? val[nz0 + k] : 0.0;
+    const int cc = in ? M.col[nz0 + k] : r0 + i;  // padding points at the row's own z
+    if (j < js) {
+      sval[e] = vv;
+      scol[e] = cc;
+    } else {
+      gval[(size_t)j * n + i] = vv;
+      gcol[(size_t)j * n + i] = cc;
+    }
+  }
+  __syncthreads();
+  // node-block Jacobi (as k_macro_cg_cluster2)
+  for (int nd = nd0 + tid; nd < nd1; nd += CGG_THR) {
+    double a[3][3] = {}, inv[3][3] = {};
+    bool fr[3] = {false, false, false};
+    for (int ci = 0; ci < dim; ++ci) {
+      const int row = nd * dim + ci;
+      fr[ci] = !M.dmask[row];
+      const int li = row - r0, len = srow[li + 1] - srow[li];
+      for (int j = 0; j < len; ++j) {
+        const int cc = (j < js ? scol[j * nr + li] : gcol[(size_t)j * n + li]) - nd * dim;
+        if (cc >= 0 && cc < dim) a[ci][cc] = j < js ? sval[j * nr + li] : gval[(size_t)j * n + li];
+      }
+    }
+    for (int ci = 0; ci < 3; ++ci)
+      for (int cj = 0; cj < 3; ++cj)
+        if (ci >= dim || cj >= dim || !fr[ci] || !fr[cj]) a[ci][cj] = (ci == cj) ? 1.0 : 0.0;
+    const double det = a[0][0] * (a[1][1] * a[2][2] - a[1][2] * a[2][1]) -
+                       a[0][1] * (a[1][0] * a[2][2] - a[1][2] * a[2][0]) +
+                       a[0][2] * (a[1][0] * a[2][1] - a[1][1] * a[2][0]);
+    inv[0][0] = (a[1][1] * a[2][2] - a[1][2] * a[2][1]) / det;
+    inv[0][1] = (a[0][2] * a[2][1] - a[0][1] * a[2][2]) / det;
+    inv[0][2] = (a[0][1] * a[1][2] - a[0][2] * a[1][1]) / det;
+    inv[1][0] = (a[1][2] * a[2][0] - a[1][0] * a[2][2]) / det;
+    inv[1][1] = (a[0][0] * a[2][2] - a[0][2] * a[2][0]) / det;
+    inv[1][2] = (a[0][2] * a[1][0] - a[0][0] * a[1][2]) / det;
+    inv[2][0] = (a[1][0] * a[2][1] - a[1][1] * a[2][0]) / det;
+    inv[2][1] = (a[0][1] * a[2][0] - a[0][0] * a[2][1]) / det;
+    inv[2][2] = (a[0][0] * a[1][1] - a[0][1] * a[1][0]) / det;
+    for (int ci = 0; ci < dim; ++ci)
+      for (int cj = 0; cj < dim; ++cj)
+        mi[((nd - nd0) * dim + ci) * dim + cj] = (fr[ci] && fr[cj]) ? inv[ci][cj] : 0.0;
+  }
+  __syncthreads();
+  for (int i = tid; i < nr; i += CGG_THR) {
+    const int gi = r0 + i;
+    x[i] = 0.0;
+    r[i] = M.dmask[gi] ? 0.0 : b[gi];
+    sv[i] = 0.0;
+    if (M.dmask[gi])
+      for (int j = 0; j < ew; ++j) {
+        if (j < js) sval[j * nr + i] = 0.0;
+        else gval[(size_t)j * n + i] = 0.0;
+      }
+  }
+  if (CC) {
+    const int e00 = M.cc.lnptr_g[la0];
+    for (int i = tid; i < nr; i += CGG_THR) srel[i] = M.cc.rel[(size_t)r0 + i];
+    for (int q = tid; q <= nla; q += CGG_THR) slnp[q] = M.cc.lnptr_g[la0 + q] - e00;
+    for (int a = tid; a < M.cc.nagg; a += CGG_THR) sntch[a] = M.cc.ntch_g[a];
+    for (int t = tid; t < M.cc.nagg * KC; t += CGG_THR) stch[t] = M.cc.tch_g[t];
+    for (int q = warp; q < nla; q += NWARP)
+      for (int e = M.cc.lnptr_g[la0 + q] + lane; e < M.cc.lnptr_g[la0 + q + 1]; e += 32) {
+        const int l = M.cc.lnode_g[e];
+        sln[e - e00] = l;
+        for (int c = 0; c < dim; ++c) sq[l * dim + c] = M.dmask[r0 + l * dim + c] ? -1 : q;
+      }
+    for (int t = tid; t < nl * nc; t += CGG_THR) {
+      const int cc = t / nl, rw = t - cc * nl, q = rw / NM, m = rw - q * NM;
+      sainv[cc * nlp + rw] = (float)M.cc.Ainv[(size_t)(M.cc.lagg_g[la0 + q] * NM + m) * nc + cc];
+    }
+  }
+  __syncthreads();
+  // CC: (P^T r, P^T s) partials of this CTA's aggregates -> gpart (global, read after the grid barrier)
+  auto cc_restrict = [&](bool with_s) {
+    for (int u = tid; u < 2 * nl * CC_NCH; u += CGG_THR) {
+      const int ch = u % CC_NCH, tv = u / CC_NCH, t = tv >> 1, q = t / NM, m = t - q * NM;
+      const double* vec = (tv & 1) ? sv : r;
+      const int e0 = slnp[q], L = slnp[q + 1] - e0;
+      double acc = 0.0;
+      if (!(tv & 1) || with_s)
+        for (int e = e0 + L * ch / CC_NCH; e < e0 + L * (ch + 1) / CC_NCH; ++e) {
+          const int l = sln[e];
+          if (m < dim) {
+            acc += vec[l * dim + m];
+          } else {
+            const double* d = srel + l * dim;
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+              if (c < dim) acc += cc_coef(dim, c, m, d) * vec[l * dim + c];
+          }
+        }
+      cpart[u] = acc;
+    }
+    __syncthreads();
+    double* gp = reinterpret_cast<double*>(gpart + (size_t)g * nlm);
+    for (int tv = tid; tv < 2 * nl; tv += CGG_THR) {
+      double acc = 0.0;
+#pragma unroll
+      for (int ch = 0; ch < CC_NCH; ++ch) acc += cpart[tv * CC_NCH + ch];
+      gp[tv] = acc;
+    }
+  };
+  // CC: r_c from the partials of the CTAs touching each aggregate, then zc = A_c^-1 r_c (fp32)
+  auto cc_solve = [&](double alpha) {
+    for (int c = tid; c < nc; c += CGG_THR) {
+      const int a = c / NM, m = c - a * NM, nt = sntch[a];
+      double sr = 0.0, ss = 0.0;
+      for (int k = 0; k < nt; ++k) {
+        const int tk = stch[a * KC + k];
+        const double2 t = __ldcg(gpart + (size_t)(tk >> 16) * nlm + (tk & 0xffff) * NM + m);
+        sr += t.x;
+        ss += t.y;
+      }
+      rcf[c] = (float)(sr - alpha * ss);
+    }
+    __syncthreads();
+    for (int t0 = warp * 8; t0 < nl; t0 += NWARP * 8) {
+      const int t = t0 + (lane & 7), cg = lane >> 3;
+      float a0 = 0.0f, a1 = 0.0f;
+      if (t < nl) {
+        int c = cg;
+        for (; c + 4 < nc; c += 8) {
+          a0 = fmaf(sainv[c * nlp + t], rcf[c], a0);
+          a1 = fmaf(sainv[(c + 4) * nlp + t], rcf[c + 4], a1);
+        }
+        if (c < nc) a0 = fmaf(sainv[c * nlp + t], rcf[c], a0);
+      }
+      float a = a0 + a1;
+      a += __shfl_xor_sync(0xffffffffu, a, 8);
+      a += __shfl_xor_sync(0xffffffffu, a, 16);
+      if (cg == 0 && t < nl) zc[t] = (double)a;
+    }
+    __syncthreads();
+  };
+  if (CC) {
+    cc_restrict(false);
+    grid.sync();
+    cc_solve(0.0);
+  }
+  // block reduction of up to 2 partials into part[g * 4 + j0 .. j0 + nv)
+  auto publish = [&](double v0, double v1, int j0, int nv) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+      v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+    }
+    if (lane == 0) { wred[warp] = v0; wred[32 + warp] = v1; }
+    __syncthreads();
+    if (tid < nv) {
+      double a = 0.0;
+      for (int k = 0; k < CGG_THR / 32; ++k) a += wred[32 * tid + k];
+      part[g * 4 + j0 + tid] = a;
+    }
+  };
+  // z = M^-1 r (local rows) -> zl, zg; (r.z, r.r) partials
+  auto precond = [&]() {
+    double rz = 0.0, rr = 0.0;
+    for (int i = tid; i < nr; i += CGG_THR) {
+      const int nd = i / dim;
+      double z = 0.0;
+      for (int cj = 0; cj < dim; ++cj) z += mi[i * dim + cj] * r[nd * dim + cj];
+      if (CC) {
+        const int q = sq[i];
+        if (q >= 0)
+#pragma unroll
+          for (int m = 0; m < 6; ++m)
+            if (m < NM) z += cc_coef(dim, i - nd * dim, m, srel + nd * dim) * zc[q * NM + m];
+      }
+      zl[i] = z;
+      zg[r0 + i] = z;
+      rz += r[i] * z;
+      rr += r[i] * r[i];
+    }
+    publish(rz, rr, 0, 2);
+  };
+  // w = A z (gathers from zg through L2); (z.w) partial
+  auto spmv = [&](double beta_s) {  // CC: also s = w + beta_s s
+    double zw = 0.0;
+    for (int i = tid; i < nr; i += CGG_THR) {
+      double s0 = 0.0, s1 = 0.0;
+      int j = 0;
+      for (; j + 1 < js; j += 2) {
+        s0 += sval[j * nr + i] * __ldcg(zg + scol[j * nr + i]);
+        s1 += sval[(j + 1) * nr + i] * __ldcg(zg + scol[(j + 1) * nr + i]);
+      }
+      if (j < js) {
+        s0 += sval[j * nr + i] * __ldcg(zg + scol[j * nr + i]);
+        ++j;
+      }
+      for (; j < ew; ++j) s0 += __ldcg(gval + (size_t)j * n + i) * __ldcg(zg + __ldcg(gcol + (size_t)j * n + i));
+      const double wi = s0 + s1;
+      w[i] = wi;
+      if (CC) sv[i] = wi + beta_s * sv[i];
+      zw += zl[i] * wi;
+    }
+    publish(zw, 0.0, 2, 1);
+    if (CC) cc_restrict(true);  // publish's CTA barrier also completes w and s
+  };
+  precond();
+  grid.sync();
+  double gam = cgg_sum(part, G, 0, sred), rr = cgg_sum(part, G, 1, sred);
+  const double bnorm = sqrt(rr);
+  int it = 0, status = 0;
+  if (bnorm > 0.0) {
+    spmv(0.0);
+    grid.sync();
+    double del = cgg_sum(part, G, 2, sred);
+    if (!(del > 0.0)) status = 6;
+    double alpha = gam / del;
+    for (int i = tid; i < nr; i += CGG_THR) { p[i] = zl[i]; sv[i] = w[i]; }
+    for (it = 1; it <= max_iter && status == 0; ++it) {
+      if (CC) cc_solve(alpha);
+      for (int i = tid; i < nr; i += CGG_THR) {
+        x[i] += alpha * p[i];
+        r[i] -= alpha * sv[i];
+      }
+      __syncthreads();  // r complete before the block preconditioner mixes components
+      precond();
+      grid.sync();
+      const double gn = cgg_sum(part, G, 0, sred);
+      rr = cgg_sum(part, G, 1, sred);
+      if (sqrt(rr) <= rtol * bnorm) break;
+      const double beta = gn / gam;
+      spmv(beta);
+      for (int i = tid; i < nr; i += CGG_THR) {
+        p[i] = zl[i] + beta * p[i];
+        if (!CC) sv[i] = w[i] + beta * sv[i];
+      }
+      grid.sync();
+      del = cgg_sum(part, G, 2, sred);
+      const double den = del - beta * gn / alpha;
+      if (!(den > 0.0)) { status = 6; break; }
+      alpha = gn / den;
+      gam = gn;
+    }
+    if (status == 0 && it > max_iter) { status = 5; it = max_iter; }
+  }
+  for (int i = tid; i < nr; i += CGG_THR) {
+    const int gi = r0 + i;
+    xout[gi] = M.dmask[gi] ? scale * M.dval[gi] : x[i];
+  }
+  if (g == 0 && tid == 0) {
+    st->iterations = it;
+    st->status = status;
+    st->rel_residual = bnorm > 0.0 ? sqrt(rr) / bnorm : 0.0;
+    st->rhs_norm = bnorm;
+  }
+}
+
+bool launch_macro_cg_grid(const MacroDev& M, const double* val, const double* rhs, double scale, double rtol,
+                          int max_iter, double* x, double* zg, double* part, CgState* st, cudaStream_t s,
+                          int* extra_launches) {
+  if (extra_launches) *extra_launches = 0;
+  int dev = 0, sms = 0, coop = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop || sms <= 0 || sms > 2 * 592) return false;
+  const int G = sms;
+  int max_nr = 0;
+  for (int g = 0; g < G; ++g) {
+    const int nd0 = (int)((long)M.n_nodes * g / G), nd1 = (int)((long)M.n_nodes * (g + 1) / G);
+    max_nr = std::max(max_nr, (nd1 - nd0) * M.dim);
+  }
+  const size_t cap = 227 * 1024;
+  for (int use_cc = (M.cc.nc > 0 && M.cc.ggrid == G) ? 1 : 0; use_cc >= 0; --use_cc) {
+    size_t base = (size_t)(8 + 96 + 6 * max_nr + max_nr * M.dim) * 8 + (size_t)(max_nr + 1) * 4 + 64;
+    if (use_cc) {
+      const int nla = M.cc.nla_max_g, nl = nla * M.cc.nm, nlp = (nl + 7) / 16 * 16 + 8;
+      base += 16 + (size_t)(nl + (M.cc.nc + 1) / 2 + nl * CC_NCH * 2 + max_nr) * 8 + (size_t)nlp * M.cc.nc * 4 +
+              (size_t)(max_nr + nla + 1 + max_nr / M.dim + M.cc.nagg * (1 + M.cc.kmax_g)) * 4;
+    }
+    if (base > cap) continue;
+    int js = (int)std::min<size_t>(M.cg_ellw, (cap - base) / ((size_t)max_nr * 12));
+    if (js < M.cg_ellw) js &= ~1;
+    const size_t sm = base + (size_t)max_nr * js * 12;
+    auto k = use_cc ? k_macro_cg_grid<true> : k_macro_cg_grid<false>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, CGG_THR, sm) != cudaSuccess || per < 1) {
+      cudaGetLastError();
+      continue;
+    }
+    if (use_cc) {
+      if (!launch_coarse_setup(M, val, s)) {
+        cudaGetLastError();
+        continue;
+      }
+      if (extra_launches) *extra_launches = 2;
+    }
+    if (getenv("HOM_CG_VERBOSE")) fprintf(stderr, "cgg: cc %d G %d js %d/%d smem %zu\n", use_cc, G, js, M.cg_ellw, sm);
+    MacroDev Mc = M;
+    void* args[] = {&Mc, (void*)&val, (void*)&rhs, &scale, &rtol, &max_iter, &x, &st, &zg, &part, &js};
+    cudaError_t e = cudaLaunchCooperativeKernel((void*)k, dim3(G), dim3(CGG_THR), args, sm, s);
+    if (e == cudaSuccess) return true;
+    cudaGetLastError();
+  }
+  return false;
+}
+
 // ---------------------------------------------------------------- K6 SpMV + large-problem PCG
 // For macro problems too large for one cluster's shared memory (scaled meshes, multi-GPU
 // weak scaling): grid-wide kernels.  K6 (k_spmv) streams the CSR matrix once per call --

@@ -109,3 +109,25 @@ def test_fully_constrained_aggregates_drop_their_modes(torch_cuda):
     o = oracle.macro_solve(2, wl.nel, C2, wl.dir_dof, wl.dir_val, body=wl.body)
     assert rel(u1, o) <= TOL_U and rel(u2, o) <= TOL_U, (rel(u1, o), rel(u2, o))
     assert i2.iterations < i1.iterations, (i1.iterations, i2.iterations)
+
+
+@pytest.mark.parametrize("precond", ["two_level", "jacobi"])
+def test_persistent_grid_pcg_matches_direct_solve(torch_cuda, precond, monkeypatch):
+    """The cooperative one-CTA-per-SM PCG (meshes beyond one cluster; forced here on the config-2 mesh)
+    gives the direct solve's u and the cluster kernel's iteration count with the two-level form."""
+    from paper_2312_12771_b200.hom import Homogenizer
+    wl = W.config2(nel=32, r=8)
+    h = Homogenizer.from_workload(wl, macro_precond=precond)
+    C = h.condense()
+    u_c, i_c = h.macro_solve(C)
+    u_c = u_c.cpu().numpy()
+    monkeypatch.setenv("HOM_CG_FORCE_GRID", "1")
+    u_g, i_g = h.macro_solve(C)
+    u_g = u_g.cpu().numpy()
+    monkeypatch.delenv("HOM_CG_FORCE_GRID")
+    o = oracle.macro_solve(2, wl.nel, C.cpu().numpy(), wl.dir_dof, wl.dir_val, body=wl.body)
+    h.close()
+    assert rel(u_g, o) <= TOL_U and rel(u_c, o) <= TOL_U, (rel(u_g, o), rel(u_c, o))
+    assert i_g.rel_residual <= 1e-13
+    if precond == "two_level":
+        assert abs(i_g.iterations - i_c.iterations) <= 3, (i_g.iterations, i_c.iterations)
