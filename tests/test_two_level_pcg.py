@@ -112,11 +112,13 @@ def test_fully_constrained_aggregates_drop_their_modes(torch_cuda):
 
 
 @pytest.mark.parametrize("precond", ["two_level", "jacobi"])
-def test_persistent_grid_pcg_matches_direct_solve(torch_cuda, precond, monkeypatch):
-    """The cooperative one-CTA-per-SM PCG (meshes beyond one cluster; forced here on the config-2 mesh)
-    gives the direct solve's u and the cluster kernel's iteration count with the two-level form."""
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_persistent_grid_pcg_matches_direct_solve(torch_cuda, precond, cfg, monkeypatch):
+    """The cooperative one-CTA-per-SM PCG (meshes beyond one cluster; forced here on the config-2 and the
+    3-D config-4 meshes) gives the direct solve's u and the cluster kernel's iteration count with the
+    two-level form."""
     from paper_2312_12771_b200.hom import Homogenizer
-    wl = W.config2(nel=32, r=8)
+    wl = W.config2(nel=32, r=8) if cfg == 2 else W.config4(r=4)
     h = Homogenizer.from_workload(wl, macro_precond=precond)
     C = h.condense()
     u_c, i_c = h.macro_solve(C)
@@ -125,7 +127,7 @@ def test_persistent_grid_pcg_matches_direct_solve(torch_cuda, precond, monkeypat
     u_g, i_g = h.macro_solve(C)
     u_g = u_g.cpu().numpy()
     monkeypatch.delenv("HOM_CG_FORCE_GRID")
-    o = oracle.macro_solve(2, wl.nel, C.cpu().numpy(), wl.dir_dof, wl.dir_val, body=wl.body)
+    o = oracle.macro_solve(wl.dim, wl.nel, C.cpu().numpy(), wl.dir_dof, wl.dir_val, body=wl.body)
     h.close()
     assert rel(u_g, o) <= TOL_U and rel(u_c, o) <= TOL_U, (rel(u_g, o), rel(u_c, o))
     assert i_g.rel_residual <= 1e-13
