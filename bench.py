@@ -379,6 +379,8 @@ def main():
                     help="constant: one RVE per macro element (SURVEY §8(f) 2, small strain)")
     ap.add_argument("--tile-sparse", action="store_true",
                     help="factor only the symbolic tile fill of K_ff (SURVEY §8(f) 3) instead of every lower tile")
+    ap.add_argument("--macro-precond", default="two_level", choices=["two_level", "jacobi"],
+                    help="macro PCG preconditioner (hom_options.macro_precond)")
     ap.add_argument("--rve-ordering", default="folded", choices=["folded", "natural"],
                     help="internal order of the RVE nodes (rows of K_ff); w at the API is natural either way")
     args = ap.parse_args()
@@ -400,7 +402,7 @@ def main():
                               if world > 1 or args.sharded else "single"),
               "macro_nel": wl.nel, "rve_per_gpu": n_rve_run / world,
               "factorization": "tile-sparse" if args.tile_sparse else "dense", "macro_basis": args.macro_basis,
-              "rve_ordering": args.rve_ordering}
+              "rve_ordering": args.rve_ordering, "macro_precond": args.macro_precond}
 
     if args.impl == "reference":
         if rank != 0:
@@ -448,12 +450,12 @@ def main():
     if dist_on:
         from paper_2312_12771_b200.dist import ShardedHomogenizer
         sh = ShardedHomogenizer(wl, tile_sparse=args.tile_sparse, macro_basis=args.macro_basis,
-                                rve_ordering=args.rve_ordering)
+                                rve_ordering=args.rve_ordering, macro_precond=args.macro_precond)
         h = sh.h
     else:
         sh = None
         h = Homogenizer.from_workload(wl, tile_sparse=args.tile_sparse, macro_basis=args.macro_basis,
-                                      rve_ordering=args.rve_ordering)
+                                      rve_ordering=args.rve_ordering, macro_precond=args.macro_precond)
     work = h.work
     config["l2"] = (f"no flush: each step writes and re-reads the K_ff tile pool ({h.sizes.rve_count * work.g_tiles * 32768 / 1e9:.2f} GB, "
                     f"{work.g_tiles} 64x64 tiles per RVE), larger than the 126 MB L2")
