@@ -119,19 +119,22 @@ CoarseHost coarse_build(int dim, int n_nodes, const double* coords, const int* r
     L.lagg.clear(); L.lnptr.assign(1, 0); L.lnode.clear();
     std::vector<std::vector<int>> who(nagg);
     L.nla_max = 0;
+    std::vector<std::vector<int>> bucket(nagg);  // this CTA's nodes of each aggregate (one pass)
     for (int g = 0; g < G; ++g) {
       const int nd0 = (int)((long)n_nodes * g / G), nd1 = (int)((long)n_nodes * (g + 1) / G);
       std::vector<int> la;
-      for (int n = nd0; n < nd1; ++n) la.push_back(H.agg[n]);
+      for (int n = nd0; n < nd1; ++n) {
+        if (bucket[H.agg[n]].empty()) la.push_back(H.agg[n]);
+        bucket[H.agg[n]].push_back(n - nd0);
+      }
       std::sort(la.begin(), la.end());
-      la.erase(std::unique(la.begin(), la.end()), la.end());
       for (int a : la) {
         who[a].push_back(g << 16 | (int)(L.lagg.size() - L.lptr[g]));
         L.lagg.push_back(a);
         L.ntch[a]++;
-        for (int n = nd0; n < nd1; ++n)
-          if (H.agg[n] == a) L.lnode.push_back(n - nd0);
+        L.lnode.insert(L.lnode.end(), bucket[a].begin(), bucket[a].end());  // increasing node order
         L.lnptr.push_back((int)L.lnode.size());
+        bucket[a].clear();
       }
       L.lptr[g + 1] = (int)L.lagg.size();
       L.nla_max = std::max(L.nla_max, (int)la.size());
