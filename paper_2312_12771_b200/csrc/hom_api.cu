@@ -991,14 +991,14 @@ int hom_macro_solve(hom_ctx* c, const double* d_D, const double* d_S, double sca
   // macro PCG: one cluster with the matrix in shared memory when it fits (config sizes),
   // else grid-wide kernels (scaled meshes); the cluster kernel with a global CSR as the last resort
   int extra = 0;  // the two-level preconditioner's setup kernels (coarse.cu)
-  const char* fge = getenv("HOM_CG_FORCE_GRID");  // test / experiment knob: the persistent grid-wide PCG
-  const int force_grid = fge ? atoi(fge) : 0;
+  const char* fge = getenv("HOM_CG_FORCE_GRID");  // test / experiment knobs: 1 = the persistent grid-wide
+  const int force_grid = fge ? atoi(fge) : 0;      // PCG, 2 = the multi-kernel one (k_spmv + k_cgl_*)
   run(c, HOM_PROF_CG, s, [&] {
     if (!force_grid && hom::launch_macro_cg_cluster2(c->M, c->cg2_slice, c->val, c->rhs, scale, c->opt.cg_rtol,
                                                      c->opt.cg_max_iter, d_x, c->cgst, s, &extra))
       return;
     if (c->M.ndof >= 32768 || force_grid) {
-      if (hom::launch_macro_cg_grid(c->M, c->val, c->rhs, scale, c->opt.cg_rtol, c->opt.cg_max_iter, d_x, c->cgwork,
+      if (force_grid != 2 && hom::launch_macro_cg_grid(c->M, c->val, c->rhs, scale, c->opt.cg_rtol, c->opt.cg_max_iter, d_x, c->cgwork,
                                     c->cgl_part, c->cgst, s, &extra))
         return;
       hom::launch_macro_cg_large(c->M, c->val, c->diag, c->rhs, scale, c->opt.cg_rtol, c->opt.cg_max_iter, d_x,

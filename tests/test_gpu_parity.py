@@ -639,13 +639,18 @@ def test_macro_spmv_matches_oracle_operator(torch_cuda):
     assert np.all(y[~free] == 0.0)
 
 
-def test_large_macro_grid_pcg_matches_direct_solve(torch_cuda):
-    """ndof >= 32768 selects the grid-wide PCG (k_spmv + deterministic block reductions)."""
+@pytest.mark.parametrize("path", ["default", "multi_kernel"])
+def test_large_macro_grid_pcg_matches_direct_solve(torch_cuda, path, monkeypatch):
+    """ndof >= 32768: the default path (cluster PCG with every ELL slot in L2, or the persistent
+    grid-wide PCG) and the multi-kernel grid-wide PCG (k_spmv + deterministic block reductions,
+    HOM_CG_FORCE_GRID=2) both reproduce the direct solve, bitwise run to run."""
     from paper_2312_12771_b200.hom import Homogenizer
     wl = W.config2(nel=128, r=2)
     h = Homogenizer.from_workload(wl)
     assert wl.n_dof >= 32768
     C = h.condense()
+    if path == "multi_kernel":
+        monkeypatch.setenv("HOM_CG_FORCE_GRID", "2")
     u, info = h.macro_solve(C)
     assert info.rel_residual <= 1e-13
     u_direct = oracle.macro_solve(2, wl.nel, C.cpu().numpy(), wl.dir_dof, wl.dir_val, body=wl.body)
