@@ -610,6 +610,41 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   R.elem_indep = upload(c, eind, s, &rc);
   R.grad = upload(c, rgrad, s, &rc);
   R.wdet = upload(c, rw, s, &rc);
+  R.fs_ntype = 0;
+  if (c->finite) {  // qp geometry types of the material pass (a uniform grid has one)
+    const int gq = nen * dim + 1;
+    std::vector<double> tgeo;
+    std::vector<int> fet(R.ne, 0);
+    int nt_ = 0;
+    for (int e = 0; e < R.ne && nt_ <= 16; ++e) {
+      double scale = 0.0;
+      for (size_t i = 0; i < (size_t)nq * nen * dim; ++i) scale = std::max(scale, std::fabs(rgrad[(size_t)e * nq * nen * dim + i]));
+      int found = -1;
+      for (int t = 0; t < nt_ && found < 0; ++t) {
+        bool same = true;
+        for (int q = 0; q < nq && same; ++q) {
+          for (int i = 0; i < nen * dim && same; ++i)
+            same = std::fabs(rgrad[((size_t)e * nq + q) * nen * dim + i] - tgeo[((size_t)t * nq + q) * gq + i]) <= 1e-13 * scale;
+          same = same && std::fabs(rw[(size_t)e * nq + q] - tgeo[((size_t)t * nq + q) * gq + nen * dim]) <=
+                             1e-13 * std::fabs(rw[(size_t)e * nq + q]);
+        }
+        if (same) found = t;
+      }
+      if (found < 0) {
+        found = nt_++;
+        for (int q = 0; q < nq; ++q) {
+          for (int i = 0; i < nen * dim; ++i) tgeo.push_back(rgrad[((size_t)e * nq + q) * nen * dim + i]);
+          tgeo.push_back(rw[(size_t)e * nq + q]);
+        }
+      }
+      fet[e] = found;
+    }
+    if (nt_ <= 16) {
+      R.fs_ntype = nt_;
+      R.fs_tgeo = upload(c, tgeo, s, &rc);
+      R.fs_etype = upload(c, fet, s, &rc);
+    }
+  }
   R.inc_ptr = upload(c, RP.inc_ptr, s, &rc);
   R.inc = upload(c, RP.inc, s, &rc);
   R.nbr_ptr = upload(c, RP.nbr_ptr, s, &rc);

@@ -46,6 +46,11 @@ struct RveDev {
   const double* FmuT;
   int ntype;
   int fs_ks, fs_ke_off;            // finite strain: K_e of the RVE kept in K1's shared memory (2 CTAs/SM), its offset
+  // finite strain, K_e in shared memory: qp geometry per element type (identical grad / wdet), staged
+  // with the RVE's w, phases and connectivity in the material pass (fs_ntype = 0: not staged)
+  int fs_ntype;
+  const double* fs_tgeo;          // [fs_ntype][nq][nen * dim + 1] (dN/dx at the qp, then Gauss weight * det J)
+  const int* fs_etype;            // [ne]
   int gtab;                       // 1: the (type, phase) tables exceed shared memory; K1 reads Klam/Kmu/FlamT/FmuT
                                   // from global memory and combines them with (lam, mu) per phase on the fly
   int npw;                        // K1: row-buffer capacity in RVE nodes per warp (12 / dim)

@@ -178,6 +178,115 @@ __device__ __forceinline__ void nh_elements(const RveDev& R, int b, int e0, int 
   __syncthreads();  // sQ reused by the next block
 }
 
+// Staged variant (K_e in shared memory and few element geometry types, R.fs_ntype > 0): the RVE's w,
+// phases, connectivity and the per-type qp geometry are copied into shared memory once per RVE
+// (fs_stage), so the material points read no global memory except the material constants; the
+// symmetric tangent A is staged as its 10 distinct entries.  Same arithmetic order as nh_elements.
+constexpr int FS_QW2 = 14;  // per qp: A (10, upper triangle packed), P (4)
+__device__ __forceinline__ int sym4(int i, int j) {
+  const int lo = i < j ? i : j, hi = i < j ? j : i;
+  return lo * 4 - (lo * (lo - 1)) / 2 + (hi - lo);
+}
+struct FsStage {
+  double* w;        // [npad]
+  double* geo;      // [fs_ntype][nq][9]
+  int* ei;          // [ne][4]
+  int* et;          // [ne]
+  uint8_t* ph;      // [ne]
+};
+__device__ __forceinline__ FsStage fs_stage_layout(const RveDev& R, double* sm) {
+  FsStage S;
+  S.w = sm + FS_ELB * 4 * FS_QW2;
+  S.geo = S.w + R.npad;
+  S.ei = reinterpret_cast<int*>(S.geo + R.fs_ntype * R.nq * 9);
+  S.et = S.ei + R.ne * 4;
+  S.ph = reinterpret_cast<uint8_t*>(S.et + R.ne);
+  return S;
+}
+__device__ __forceinline__ void fs_stage(const RveDev& R, int b, const double* __restrict__ w, const FsStage& S) {
+  const int tid = threadIdx.x;
+  const double* wb = w + (long)b * R.npad;
+  for (int i = tid; i < R.npad; i += NTHR) S.w[i] = wb[i];
+  for (int i = tid; i < R.fs_ntype * R.nq * 9; i += NTHR) S.geo[i] = R.fs_tgeo[i];
+  for (int i = tid; i < R.ne * 4; i += NTHR) S.ei[i] = R.elem_indep[i];
+  for (int i = tid; i < R.ne; i += NTHR) {
+    S.et[i] = R.fs_etype[i];
+    S.ph[i] = R.phase[(R.phase_per_rve ? (long)b * R.ne : 0) + i];
+  }
+  __syncthreads();
+}
+__device__ __forceinline__ void nh_elements_st(const RveDev& R, int b, int e0, int cnt, const double* __restrict__ Fbar,
+                                               int* __restrict__ jflag, double* sm, int* sOk, double (&avg)[4],
+                                               double* ske, const FsStage& S, double* __restrict__ out) {
+  double (*sQ)[FS_QW2] = reinterpret_cast<double (*)[FS_QW2]>(sm);  // [FS_ELB * 4][FS_QW2]
+  const int nq = R.nq, tid = threadIdx.x;
+  if (tid < FS_ELB) sOk[tid] = 1;
+  __syncthreads();
+  if (tid < FS_ELB * 4) {  // ---- phase 1: material point per (element, qp) ----
+    const int le = tid >> 2, q = tid & 3;
+    if (le < cnt && q < nq) {
+      const int e = e0 + le;
+      const double* Fb = Fbar + (long)b * 4;
+      const int np = R.mat_stride;
+      const double* mp = R.mat + (R.mat_per_rve ? (long)b * R.n_phase * np : 0) + np * S.ph[e];
+      const double alpha = mp[0], beta = np == 3 ? mp[1] : 0.0, kappa = mp[np - 1];
+      const double* G = S.geo + (S.et[e] * nq + q) * 9;
+      double F[4] = {Fb[0], Fb[1], Fb[2], Fb[3]};
+      for (int aa = 0; aa < 4; ++aa) {  // F~ = F + grad w (eq:microGrad)
+        const int p = S.ei[e * 4 + aa];
+        const double w0 = S.w[2 * p], w1 = S.w[2 * p + 1];
+        F[0] += w0 * G[2 * aa]; F[1] += w0 * G[2 * aa + 1];
+        F[2] += w1 * G[2 * aa]; F[3] += w1 * G[2 * aa + 1];
+      }
+      double A[16];
+      double* Q = sQ[tid];
+      if (!cook_material(F, alpha, beta, kappa, Q + 10, A)) {
+        atomicMin(&jflag[b], e * nq + q);  // first failing qp of this RVE (init INT_MAX)
+        sOk[le] = 0;
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = i; j < 4; ++j) Q[sym4(i, j)] = A[i * 4 + j];
+    }
+  }
+  __syncthreads();
+  {  // ---- phase 2: element rows (a, i) ----
+    const int le = tid >> 3, row = tid & 7, a = row >> 1, i = row & 1;
+    double* o = out + (long)le * EL_STRIDE;
+    const uint64_t pol = l2_policy_evict_last();
+    if (le < cnt) {
+      const int e = e0 + le;
+      const bool ok = sOk[le];
+      double ke[8] = {}, fe[4] = {}, re = 0.0;
+      for (int q = 0; q < nq; ++q) {
+        const double* A = sQ[le * 4 + q];
+        const double* P = A + 10;
+        const double* G = S.geo + (S.et[e] * nq + q) * 9;
+        const double wq = G[8];
+        const double ga0 = G[2 * a], ga1 = G[2 * a + 1];
+        double t[4];  // row (a, i): t[k] = sum_J g_a[J] A[(i,J), k]
+        for (int k = 0; k < 4; ++k) t[k] = ga0 * A[sym4(2 * i, k)] + ga1 * A[sym4(2 * i + 1, k)];
+        for (int k = 0; k < 4; ++k) fe[k] += wq * t[k];
+        re += wq * (ga0 * P[2 * i] + ga1 * P[2 * i + 1]);
+        for (int bb = 0; bb < 4; ++bb)
+          for (int j = 0; j < 2; ++j)  // column (b, j): sum_L t[(j,L)] g_b[L]
+            ke[2 * bb + j] += wq * (t[2 * j] * G[2 * bb] + t[2 * j + 1] * G[2 * bb + 1]);
+      }
+      for (int k = 0; k <= row; ++k) ske[le * 36 + pk8(row, k)] = ok ? ke[k] : 0.0;  // lower part
+      for (int k = 0; k < 4; ++k) st_hint(o + EL_F + row * 4 + k, ok ? fe[k] : 0.0, pol);
+      st_hint(o + EL_R + row, ok ? re : 0.0, pol);
+      if (row < 5 && ok)  // running qp sums of A (rows 0-3: 4 entries each) and P (row 4) for <A>, <P>
+        for (int q = 0; q < nq; ++q) {
+          const double wq = S.geo[(S.et[e] * nq + q) * 9 + 8];
+          const double* A = sQ[le * 4 + q];
+          for (int k = 0; k < 4; ++k) avg[k] += wq * (row < 4 ? A[sym4(row, k)] : A[10 + k]);
+        }
+    }
+  }
+  __syncthreads();  // sQ reused by the next block
+}
+
 template <int DIM, bool ISO, bool GT = false>  // GT: global geometry tables (RveDev::gtab)
 __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const int bl, double* __restrict__ Kt,
                                              double* __restrict__ Y, double* __restrict__ Cavg,
@@ -505,9 +614,17 @@ __global__ void __launch_bounds__(NTHR, KS ? 2 : 4) k_rve_assemble_fs(RveDev R, 
   for (int bl = blockIdx.x; bl < nb; bl += gridDim.x) {
     const int b = b0 + bl;
     double avg[4] = {0.0, 0.0, 0.0, 0.0};  // this thread's share of sum eta A (row < 4) / sum eta P (row 4)
-    for (int e0 = 0; e0 < R.ne; e0 += FS_ELB)
-      nh_elements(R, b, e0, min(FS_ELB, R.ne - e0), Fbar, w, scr + (long)e0 * EL_STRIDE, jflag, smem, sOk, avg,
-                  KS ? sKe + (long)e0 * 36 : nullptr);
+    if (KS && R.fs_ntype > 0) {  // staged material pass
+      const FsStage S = fs_stage_layout(R, smem);
+      fs_stage(R, b, w, S);
+      for (int e0 = 0; e0 < R.ne; e0 += FS_ELB)
+        nh_elements_st(R, b, e0, min(FS_ELB, R.ne - e0), Fbar, jflag, smem, sOk, avg, sKe + (long)e0 * 36, S,
+                       scr + (long)e0 * EL_STRIDE);
+    } else {
+      for (int e0 = 0; e0 < R.ne; e0 += FS_ELB)
+        nh_elements(R, b, e0, min(FS_ELB, R.ne - e0), Fbar, w, scr + (long)e0 * EL_STRIDE, jflag, smem, sOk, avg,
+                    KS ? sKe + (long)e0 * 36 : nullptr);
+    }
     // <A>, <P>: sum over the elements (lanes with equal row: xor 8, 16; then the 8 warps), / |Omega|
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
@@ -542,6 +659,8 @@ size_t rve_assemble_smem(const RveDev& R, int npw) {
                                  sizeof(double) +
                          (size_t)R.ne * sizeof(int));
   if (R.finite) sm = std::max(sm, (size_t)FS_SMEM_DBL * sizeof(double));  // element staging aliases the row buffers
+  if (R.finite && R.fs_ks && R.fs_ntype > 0)  // staged material pass (w, phases, connectivity, qp geometry)
+    sm = std::max(sm, (size_t)(FS_ELB * 4 * FS_QW2 + R.npad + R.fs_ntype * R.nq * 9) * 8 + (size_t)R.ne * 5 * 4 + R.ne);
   if (R.finite && R.fs_ks) sm = ((sm + 127) / 128) * 128 + (size_t)R.ne * 36 * sizeof(double);  // + K_e of the RVE
   return sm;
 }
