@@ -182,7 +182,7 @@ __device__ __forceinline__ void nh_elements(const RveDev& R, int b, int e0, int 
 // phases, connectivity and the per-type qp geometry are copied into shared memory once per RVE
 // (fs_stage), so the material points read no global memory except the material constants; the
 // symmetric tangent A is staged as its 10 distinct entries.  Same arithmetic order as nh_elements.
-constexpr int FS_QW2 = 14;  // per qp: A (10, upper triangle packed), P (4)
+constexpr int FS_QW2 = 14, FS_ELB2 = 64;  // per qp: A (10, upper triangle packed), P (4); elements per pass
 __device__ __forceinline__ int sym4(int i, int j) {
   const int lo = i < j ? i : j, hi = i < j ? j : i;
   return lo * 4 - (lo * (lo - 1)) / 2 + (hi - lo);
@@ -196,7 +196,7 @@ struct FsStage {
 };
 __device__ __forceinline__ FsStage fs_stage_layout(const RveDev& R, double* sm) {
   FsStage S;
-  S.w = sm + FS_ELB * 4 * FS_QW2;
+  S.w = sm + FS_ELB2 * 4 * FS_QW2;
   S.geo = S.w + R.npad;
   S.ei = reinterpret_cast<int*>(S.geo + R.fs_ntype * R.nq * 9);
   S.et = S.ei + R.ne * 4;
@@ -218,11 +218,11 @@ __device__ __forceinline__ void fs_stage(const RveDev& R, int b, const double* _
 __device__ __forceinline__ void nh_elements_st(const RveDev& R, int b, int e0, int cnt, const double* __restrict__ Fbar,
                                                int* __restrict__ jflag, double* sm, int* sOk, double (&avg)[4],
                                                double* ske, const FsStage& S, double* __restrict__ out) {
-  double (*sQ)[FS_QW2] = reinterpret_cast<double (*)[FS_QW2]>(sm);  // [FS_ELB * 4][FS_QW2]
+  double (*sQ)[FS_QW2] = reinterpret_cast<double (*)[FS_QW2]>(sm);  // [FS_ELB2 * 4][FS_QW2]
   const int nq = R.nq, tid = threadIdx.x;
-  if (tid < FS_ELB) sOk[tid] = 1;
+  if (tid < FS_ELB2) sOk[tid] = 1;
   __syncthreads();
-  if (tid < FS_ELB * 4) {  // ---- phase 1: material point per (element, qp) ----
+  if (tid < FS_ELB2 * 4) {  // ---- phase 1: material point per (element, qp) ----
     const int le = tid >> 2, q = tid & 3;
     if (le < cnt && q < nq) {
       const int e = e0 + le;
@@ -251,11 +251,11 @@ __device__ __forceinline__ void nh_elements_st(const RveDev& R, int b, int e0, i
     }
   }
   __syncthreads();
-  {  // ---- phase 2: element rows (a, i) ----
-    const int le = tid >> 3, row = tid & 7, a = row >> 1, i = row & 1;
+  const uint64_t pol = l2_policy_evict_last();
+  for (int le = tid >> 3; le < cnt; le += NTHR / 8) {  // ---- phase 2: element rows (a, i) ----
+    const int row = tid & 7, a = row >> 1, i = row & 1;
     double* o = out + (long)le * EL_STRIDE;
-    const uint64_t pol = l2_policy_evict_last();
-    if (le < cnt) {
+    {
       const int e = e0 + le;
       const bool ok = sOk[le];
       double ke[8] = {}, fe[4] = {}, re = 0.0;
@@ -607,7 +607,7 @@ __global__ void __launch_bounds__(NTHR, KS ? 2 : 4) k_rve_assemble_fs(RveDev R, 
                                                           double* __restrict__ Pavg, double* __restrict__ rfn,
                                                           double* __restrict__ scratch, int* __restrict__ jflag) {
   extern __shared__ __align__(128) double smem[];
-  __shared__ int sOk[FS_ELB];
+  __shared__ int sOk[FS_ELB2];
   double* scr = scratch + (long)blockIdx.x * R.ne * EL_STRIDE;
   double* sKe = KS ? smem + R.fs_ke_off : nullptr;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, row = tid & 7;
@@ -617,8 +617,8 @@ __global__ void __launch_bounds__(NTHR, KS ? 2 : 4) k_rve_assemble_fs(RveDev R, 
     if (KS && R.fs_ntype > 0) {  // staged material pass
       const FsStage S = fs_stage_layout(R, smem);
       fs_stage(R, b, w, S);
-      for (int e0 = 0; e0 < R.ne; e0 += FS_ELB)
-        nh_elements_st(R, b, e0, min(FS_ELB, R.ne - e0), Fbar, jflag, smem, sOk, avg, sKe + (long)e0 * 36, S,
+      for (int e0 = 0; e0 < R.ne; e0 += FS_ELB2)
+        nh_elements_st(R, b, e0, min(FS_ELB2, R.ne - e0), Fbar, jflag, smem, sOk, avg, sKe + (long)e0 * 36, S,
                        scr + (long)e0 * EL_STRIDE);
     } else {
       for (int e0 = 0; e0 < R.ne; e0 += FS_ELB)
@@ -660,7 +660,7 @@ size_t rve_assemble_smem(const RveDev& R, int npw) {
                          (size_t)R.ne * sizeof(int));
   if (R.finite) sm = std::max(sm, (size_t)FS_SMEM_DBL * sizeof(double));  // element staging aliases the row buffers
   if (R.finite && R.fs_ks && R.fs_ntype > 0)  // staged material pass (w, phases, connectivity, qp geometry)
-    sm = std::max(sm, (size_t)(FS_ELB * 4 * FS_QW2 + R.npad + R.fs_ntype * R.nq * 9) * 8 + (size_t)R.ne * 5 * 4 + R.ne);
+    sm = std::max(sm, (size_t)(FS_ELB2 * 4 * FS_QW2 + R.npad + R.fs_ntype * R.nq * 9) * 8 + (size_t)R.ne * 5 * 4 + R.ne);
   if (R.finite && R.fs_ks) sm = ((sm + 127) / 128) * 128 + (size_t)R.ne * 36 * sizeof(double);  // + K_e of the RVE
   return sm;
 }
