@@ -272,16 +272,12 @@ __device__ __forceinline__ void nh_elements_st(const RveDev& R, int b, int e0, i
         for (int bb = 0; bb < 4; ++bb)
           for (int j = 0; j < 2; ++j)  // column (b, j): sum_L t[(j,L)] g_b[L]
             ke[2 * bb + j] += wq * (t[2 * j] * G[2 * bb] + t[2 * j + 1] * G[2 * bb + 1]);
+        if (row < 5 && ok)  // running qp sums of A (rows 0-3: 4 entries each) and P (row 4) for <A>, <P>
+          for (int k = 0; k < 4; ++k) avg[k] += wq * (row < 4 ? A[sym4(row, k)] : P[k]);
       }
       for (int k = 0; k <= row; ++k) ske[le * 36 + pk8(row, k)] = ok ? ke[k] : 0.0;  // lower part
       for (int k = 0; k < 4; ++k) st_hint(o + EL_F + row * 4 + k, ok ? fe[k] : 0.0, pol);
       st_hint(o + EL_R + row, ok ? re : 0.0, pol);
-      if (row < 5 && ok)  // running qp sums of A (rows 0-3: 4 entries each) and P (row 4) for <A>, <P>
-        for (int q = 0; q < nq; ++q) {
-          const double wq = S.geo[(S.et[e] * nq + q) * 9 + 8];
-          const double* A = sQ[le * 4 + q];
-          for (int k = 0; k < 4; ++k) avg[k] += wq * (row < 4 ? A[sym4(row, k)] : A[10 + k]);
-        }
     }
   }
   __syncthreads();  // sQ reused by the next block
