@@ -697,14 +697,49 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
       for (size_t k = 0; k + 1 < RP.sh_ptr.size(); ++k) max_sh = std::max(max_sh, RP.sh_ptr[k + 1] - RP.sh_ptr[k]);
       R.maxdeg = max_deg;
       R.rs4 = (2 + max_sh + 3) / 4;
+      // stencil classes (small strain, shared-memory tables): the sorted list of element-local node
+      // pairs (a, b) of a record; when every shared element of a record has the same (type, phase)
+      // table t, K_pq = sum_(a,b) K_t[a][b] is one precomputed block of the class (per RVE, K1)
+      std::map<std::vector<int>, int> cls_of;
+      std::vector<int> cls_ptr{0}, cls_ab;
+      bool use_cls = !c->finite && !R.gtab;
+      {  // HOM_K1_CLS=0: plain records (A/B)
+        const char* e = getenv("HOM_K1_CLS");
+        if (e && e[0] == '0') use_cls = false;
+      }
       std::vector<int> rec((size_t)R.n_indep * max_deg * R.rs4 * 4, -1);
       for (int pp = 0; pp < R.n_indep; ++pp)
         for (int k = RP.nbr_ptr[pp]; k < RP.nbr_ptr[pp + 1]; ++k) {
           int* r = rec.data() + ((size_t)pp * max_deg + (k - RP.nbr_ptr[pp])) * R.rs4 * 4;
           r[0] = RP.nbr[k] == R.corner ? -1 : RP.nbr[k];
-          r[1] = RP.sh_ptr[k + 1] - RP.sh_ptr[k];
+          const int nsh = RP.sh_ptr[k + 1] - RP.sh_ptr[k];
+          r[1] = nsh;
           for (int sidx = RP.sh_ptr[k]; sidx < RP.sh_ptr[k + 1]; ++sidx) r[2 + sidx - RP.sh_ptr[k]] = RP.sh[sidx];
+          if (use_cls && nsh > 1) {
+            std::vector<int> key;
+            for (int sidx = RP.sh_ptr[k]; sidx < RP.sh_ptr[k + 1]; ++sidx) key.push_back(RP.sh[sidx] & 0xff);
+            std::sort(key.begin(), key.end());
+            auto it = cls_of.find(key);
+            if (it == cls_of.end()) {
+              if ((int)cls_of.size() == hom::MAX_K1_CLASSES) { use_cls = false; continue; }
+              it = cls_of.emplace(key, (int)cls_of.size()).first;
+              cls_ab.insert(cls_ab.end(), key.begin(), key.end());
+              cls_ptr.push_back((int)cls_ab.size());
+            }
+            r[1] = nsh | ((it->second + 1) << 16);
+          }
         }
+      if ((size_t)R.ntype * mat->n_phases * cls_of.size() * ((dim * dim + 1) / 2 * 2) * sizeof(double) > 8192)
+        use_cls = false;  // class blocks limited to 8 KB of K1's shared memory
+      if (!use_cls) {  // too many classes: plain records
+        for (size_t i = 0; i < rec.size(); i += (size_t)R.rs4 * 4)
+          if (rec[i + 1] >= 0) rec[i + 1] &= 0xffff;
+        cls_ptr.assign(1, 0);
+        cls_ab.clear();
+      }
+      R.ncls = (int)cls_ptr.size() - 1;
+      R.cls_ptr = upload(c, cls_ptr, s, &rc);
+      R.cls_ab = upload(c, cls_ab.empty() ? std::vector<int>{0} : cls_ab, s, &rc);
       R.nrec = reinterpret_cast<const int4*>(upload(c, rec, s, &rc));
     }
     R.etype = upload(c, etype, s, &rc);
@@ -737,39 +772,58 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
     // <= npw consecutive nodes and <= 32 in-tile neighbour records (one per lane), dealt
     // round-robin over the warps
     const int dK = c->finite ? 2 : R.dim;
-    std::vector<int> witem, wlist;
+    // Per item and lane a coverage word (wcov): bit 2n + b = column 2 lane + b of node n's rows is covered by
+    // a neighbour block -- the writer stores zeros elsewhere instead of clearing its row buffer first
+    std::vector<int> witem, wlist, wcov;
     for (int t = 0; t < R.n_a; ++t) {
       const int r0 = (alist[t] >> 16) * 64, c0 = (alist[t] & 0xffff) * 64;
       const int p_lo = r0 / dK, p_hi = (r0 + 63) / dK;
       int p0 = p_lo, nn = 0;
       std::vector<int> lanes;
+      std::vector<unsigned long long> nmask;  // covered columns of each node of the item
       auto flush = [&]() {
         if (nn == 0) return;
         witem.insert(witem.end(), {alist[t], p0, nn, tslot[(size_t)(alist[t] >> 16) * nt_ + (alist[t] & 0xffff)]});
         lanes.resize(32, -1);
         wlist.insert(wlist.end(), lanes.begin(), lanes.end());
+        for (int L = 0; L < 32; ++L) {
+          int w = 0;
+          for (int n = 0; n < nn; ++n)
+            for (int b = 0; b < 2; ++b)
+              if ((nmask[n] >> (2 * L + b)) & 1ull) w |= 1 << (2 * n + b);
+          wcov.push_back(w);
+        }
         lanes.clear();
+        nmask.clear();
         p0 += nn;
         nn = 0;
       };
       for (int pp = p_lo; pp <= p_hi; ++pp) {
         std::vector<int> mine;
+        unsigned long long msk = 0;
         if (pp < R.n_indep && pp != R.corner)
           for (int k = RP.nbr_ptr[pp]; k < RP.nbr_ptr[pp + 1]; ++k) {
             const int q = RP.nbr[k], cq = q * dK - c0;
-            if (q != R.corner && cq + dK > 0 && cq < 64) mine.push_back(pp * R.maxdeg + (k - RP.nbr_ptr[pp]));
+            if (q != R.corner && cq + dK > 0 && cq < 64) {
+              mine.push_back(pp * R.maxdeg + (k - RP.nbr_ptr[pp]));
+              for (int jj = 0; jj < dK; ++jj)
+                if (cq + jj >= 0 && cq + jj < 64) msk |= 1ull << (cq + jj);
+            }
           }
         if ((int)mine.size() > 32) return fail(HOM_ERR_INVALID_ARG, "K1: more than 32 neighbour blocks of one node in one tile");
         if (nn == R.npw || lanes.size() + mine.size() > 32) flush();
         for (int ridx : mine) lanes.push_back((nn << 24) | ridx);
+        nmask.push_back(msk);
         ++nn;
       }
       flush();
     }
+    if (2 * R.npw > 31) return fail(HOM_ERR_INVALID_ARG, "K1: row-buffer nodes exceed the coverage word");
     if ((long)R.n_indep * R.maxdeg >= (1L << 24)) return fail(HOM_ERR_INVALID_ARG, "K1: RVE too large for 24-bit record indices");
     R.n_witem = (int)(witem.size() / 4);
     R.witem = reinterpret_cast<const int4*>(upload(c, witem, s, &rc));
     R.wlist = upload(c, wlist, s, &rc);
+    R.wcov = upload(c, wcov, s, &rc);
   }
   R.tslot = upload(c, tslot, s, &rc);
   R.phase = upload(c, phase, s, &rc);

@@ -15,6 +15,7 @@ constexpr int TILE_ELEMS = TILE * TILE;
 constexpr int KC = 16;            // k-chunk staged per pipeline stage (condense.cu)
 constexpr int RHSW = 8;           // right-hand-side columns kept per RVE (m <= 6, +1 for r_f)
 constexpr int NTHR = 256;         // threads per CTA of the RVE kernels
+constexpr int MAX_K1_CLASSES = 64;  // K1 stencil classes (RveDev::ncls) kept in shared memory
 
 // Geometry + topology of the (shared) RVE mesh and the per-RVE phase/material tables.
 struct RveDev {
@@ -71,10 +72,16 @@ struct RveDev {
   // {q (-1: none / corner), n_sh, code_0 .. code_{n_sh-1}, -1 ...}, code = e<<8 | a<<4 | b
   const int4* nrec;
   int maxdeg, rs4;
+  // K1 stencil classes (small strain, shared-memory tables): record word 1 = n_sh | (class + 1) << 16; a
+  // class is the sorted list of element-local pairs (a << 4 | b) cls_ab[cls_ptr[c] .. cls_ptr[c + 1])
+  int ncls;
+  const int* cls_ptr;
+  const int* cls_ab;
   // K1 warp work items: {tile code I<<16|J, first row node p0, node count nn, pool slot}, and per item one record
   // per lane: (g << 24 | record index) for node p0 + g, -1 = idle lane (<= 32 records, <= npw nodes)
   const int4* witem;
   const int* wlist;
+  const int* wcov;                // [n_witem][32]: bit 2n + b = column 2 lane + b of item node n covered
   int n_witem;
   int xb0;                        // first RVE of the influence store X (the context's local range)
   const int* nat_of;              // [n_indep] internal node -> natural (API) node; nullptr = identity

@@ -89,6 +89,7 @@ __device__ __forceinline__ bool cook_material(const double* F, double alpha, dou
 // the records are staged in shared memory and written as one contiguous, coalesced range to
 // `out` (the CTA's L2-resident scratch, read back by the tile writer of the same CTA).
 constexpr int FS_ELB = 32, FS_QW = 29;
+constexpr int RB_SKEW = 0;  // K1 row-buffer node stride padding (doubles)
 constexpr int FS_SMEM_DBL = FS_ELB * 4 * FS_QW;
 // L2 residency hints: the element records are re-read by the same CTA moments later (evict_last),
 // the K_ff tiles stream out once (evict_first) so they do not push the records out of L2
@@ -289,8 +290,11 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
                                              double* __restrict__ Pavg, double* __restrict__ rfn,
                                              const double* __restrict__ EL, double* smem,
                                              const double* KE = nullptr, int kes = 0) {  // finite strain: K_e, stride
-  double* s_row = smem;                      // [8 warps][npw][DIM][64] tile-row buffers
-  double* red = s_row + (NTHR / 32) * R.npw * DIM * TILE;  // [NTHR] reduction scratch
+  // [8 warps][npw][DIM][64] tile-row buffers, node stride DIM * 64 + RB_SKEW: the block stores of lanes on
+  // different nodes of an item with equal columns fall in different banks (6 g mod 16 distinct for g < 8)
+  constexpr int NSTR = DIM * TILE + RB_SKEW;
+  double* s_row = smem;
+  double* red = s_row + (NTHR / 32) * R.npw * NSTR;  // [NTHR] reduction scratch
   // ISO element tables: [ntype][n_phase][ND][ND] (K_e) and [ntype][n_phase][ND][m] (K_fe rows) per RVE in shared
   // memory, or -- when they do not fit (R.gtab: meshes with many distinct element geometries) -- only the
   // per-phase (lam, mu) here and the geometry tables Klam/Kmu/FlamT/FmuT read from global memory (L2)
@@ -300,7 +304,9 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
   const int ntab = ISO ? (GT ? 0 : R.ntype * R.n_phase) : 0;
   double* s_K = red + NTHR;
   double* s_F = s_K + (ISO ? (GT ? 2 * R.n_phase : ntab * NEN * NEN * BS) : 0);
-  int* s_ep = reinterpret_cast<int*>(s_F + (ISO ? ntab * ((1 << DIM) * DIM) * R.m : 0));
+  double* s_C = s_F + (ISO ? ntab * ((1 << DIM) * DIM) * R.m : 0);  // stencil-class blocks [ncls][ntab][BS]
+  const int ncls = (ISO && !GT) ? R.ncls : 0;
+  int* s_ep = reinterpret_cast<int*>(s_C + ncls * ntab * BS);
   const int tid = threadIdx.x;
   const int ne = R.ne;
   constexpr int ND = ISO ? (1 << DIM) * DIM : 8;  // nen*dim
@@ -335,6 +341,19 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
     }
   }
   __syncthreads();
+  // stencil-class blocks: C_c,t = sum over the class's element-local pairs (a, b) of the table t block
+  // (read by records whose shared elements all use table t; ordered before the gathers by the
+  // barriers of the <C> reduction below)
+  for (int i = tid; i < ncls * ntab * BS; i += NTHR) {
+    const int cl = i / (ntab * BS), t = (i / BS) % ntab, j = i % BS;
+    double v = 0.0;
+    if (j < DIM * DIM)
+      for (int u = __ldg(R.cls_ptr + cl); u < __ldg(R.cls_ptr + cl + 1); ++u) {
+        const int ab = __ldg(R.cls_ab + u);
+        v += s_K[(((long)t * NEN + (ab >> 4)) * NEN + (ab & 15)) * BS + j];
+      }
+    s_C[i] = v;
+  }
 
   // ---- volume average <C> (small strain; finite strain: <A>, <P> come from the element pass) ----
   if (ISO) {
@@ -441,7 +460,7 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
   // Structurally zero tiles are never touched (k_condense starts their accumulators at zero).
   double* Kb = Kt + (long)bl * R.nslot * TILE_ELEMS;
   const int lane = tid & 31, warp = tid >> 5;
-  double* rowbuf = s_row + warp * R.npw * DIM * TILE;
+  double* rowbuf = s_row + warp * R.npw * NSTR;
   // work items {tile, first row node p0, nn nodes} with one in-tile neighbour record per lane,
   // software-pipelined: the next item's header and gather record and the lane word of the item
   // after it are in flight while the current item is formed and stored
@@ -460,10 +479,12 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
   int lw = warp < nw ? __ldg(R.wlist + (long)warp * 32 + lane) : -1;
   int rv[4 * RS4M];
   load_rec(rv, lw);
+  int cw = warp < nw ? __ldg(R.wcov + (long)warp * 32 + lane) : 0;
   int lw1 = warp + WSTRIDE < nw ? __ldg(R.wlist + (long)(warp + WSTRIDE) * 32 + lane) : -1;
   for (int it = warp; it < nw; it += WSTRIDE) {
     const int itn = it + WSTRIDE;
     const int4 wi_n = itn < nw ? __ldg(R.witem + itn) : wi;
+    const int cw_n = itn < nw ? __ldg(R.wcov + (long)itn * 32 + lane) : 0;
     int rv_n[4 * RS4M];
     load_rec(rv_n, lw1);
     const int lw2 = itn + WSTRIDE < nw ? __ldg(R.wlist + (long)(itn + WSTRIDE) * 32 + lane) : -1;
@@ -474,11 +495,9 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
       double* gt = Kb + (long)wi.w * TILE_ELEMS;
       const int c0 = J * TILE;
       {
-        for (int i = lane; i < nn * DIM * TILE / 2; i += 32)
-          reinterpret_cast<double2*>(rowbuf)[i] = make_double2(0.0, 0.0);
-        __syncwarp();
+        // (no clearing of the row buffer: columns no neighbour block covers are stored as zeros, cw)
         if (lw >= 0) {
-          double* rb = rowbuf + (lw >> 24) * DIM * TILE;
+          double* rb = rowbuf + (lw >> 24) * NSTR;
           {
             const int4* rec = R.nrec + (long)(lw & 0xffffff) * R.rs4;
             // the record was loaded a round earlier (rv); records longer than RS4M int4s (tiny
@@ -490,7 +509,7 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
             for (int i = 0; i < DIM; ++i)
 #pragma unroll
               for (int jj = 0; jj < DIM; ++jj) blk[i][jj] = 0.0;
-            const int nsh = rv[1];
+            const int nsh = rv[1] & 0xffff, cls = (rv[1] >> 16) - 1;
             // element block (a, b) of the element in `code`: the per-(type, phase) table in shared memory
             // (small strain) or the CTA's L2-resident element record, K_e packed lower-triangular
             auto blk_at = [&](int code, int i, int jj) -> double {
@@ -506,9 +525,27 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
               }
               return KE[(long)e * kes + pk8(r, c)];
             };
+            // a record whose shared elements all use one (type, phase) table: the class block, one gather
+            bool uni = false;
+            if (ISO && !GT && cls >= 0 && nsh <= 4 * RS4M - 2) {
+              const int t0 = s_ep[rv[2] >> 8];
+              uni = true;
+#pragma unroll
+              for (int sidx = 1; sidx < 4 * RS4M - 2; ++sidx)
+                if (sidx < nsh && s_ep[rv[2 + sidx] >> 8] != t0) uni = false;
+              if (uni) {
+                const double2* kb = reinterpret_cast<const double2*>(s_C + ((long)cls * ntab + t0) * BS);
+#pragma unroll
+                for (int q = 0; q < BS / 2; ++q) {
+                  const double2 t2 = kb[q];
+                  if (2 * q < DIM * DIM) blk[(2 * q) / DIM][(2 * q) % DIM] = t2.x;
+                  if (2 * q + 1 < DIM * DIM) blk[(2 * q + 1) / DIM][(2 * q + 1) % DIM] = t2.y;
+                }
+              }
+            }
 #pragma unroll
             for (int sidx = 0; sidx < 4 * RS4M - 2 + 1; ++sidx) {
-              if (sidx >= nsh) break;
+              if (uni || sidx >= nsh) break;
               if (sidx < 4 * RS4M - 2) {
                 const int code = rv[sidx + 2];
                 if (ISO && !GT) {  // the whole block with BS/2 128-bit loads
@@ -557,12 +594,14 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
           const bool pad = pn >= R.n_indep || pn == R.corner;  // identity rows (corner class, tail)
           double2 vr[DIM];  // all rows of the node loaded before the first store
 #pragma unroll
-          for (int ci = 0; ci < DIM; ++ci) vr[ci] = *reinterpret_cast<const double2*>(rowbuf + (n * DIM + ci) * TILE + 2 * lane);
+          for (int ci = 0; ci < DIM; ++ci) vr[ci] = *reinterpret_cast<const double2*>(rowbuf + n * NSTR + ci * TILE + 2 * lane);
 #pragma unroll
           for (int ci = 0; ci < DIM; ++ci) {
             const int row = pn * DIM + ci, rr = row - r0;
             if (rr < 0 || rr >= TILE) continue;
             double2 v = vr[ci];
+            if (!((cw >> (2 * n)) & 1)) v.x = 0.0;
+            if (!((cw >> (2 * n + 1)) & 1)) v.y = 0.0;
             if (pad || row >= R.npad) {
               v.x = (c0 + 2 * lane == row) ? 1.0 : 0.0;
               v.y = (c0 + 2 * lane + 1 == row) ? 1.0 : 0.0;
@@ -575,6 +614,7 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
       }
     }
     wi = wi_n;
+    cw = cw_n;
     lw = lw1;
 #pragma unroll
     for (int u = 0; u < 4 * RS4M; ++u) rv[u] = rv_n[u];
@@ -648,10 +688,10 @@ __global__ void __launch_bounds__(NTHR, KS ? 2 : 4) k_rve_assemble_fs(RveDev R, 
 
 size_t rve_assemble_smem(const RveDev& R, int npw) {
   const int dim = R.finite ? 2 : R.dim, nd = (1 << dim) * dim;  // nen*dim
-  size_t sm = (size_t)((NTHR / 32) * npw * dim * TILE + NTHR) * sizeof(double) +
+  size_t sm = (size_t)((NTHR / 32) * npw * (dim * TILE + RB_SKEW) + NTHR) * sizeof(double) +
               (R.finite ? 0
                    : (R.gtab ? (size_t)2 * R.n_phase
-                             : (size_t)R.ntype * R.n_phase * ((size_t)(1 << dim) * (1 << dim) * ((dim * dim + 1) / 2 * 2) + nd * R.m)) *
+                             : (size_t)R.ntype * R.n_phase * ((size_t)(R.ncls + (1 << dim) * (1 << dim)) * ((dim * dim + 1) / 2 * 2) + nd * R.m)) *
                                  sizeof(double) +
                          (size_t)R.ne * sizeof(int));
   if (R.finite) sm = std::max(sm, (size_t)FS_SMEM_DBL * sizeof(double));  // element staging aliases the row buffers
