@@ -28,7 +28,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         t = os.path.getmtime(LIB)
         if all(os.path.getmtime(d) <= t for d in deps()):
             return LIB
-    cmd = [NVCC, *FLAGS, "-shared", "-o", LIB, *sources()]
+    extra = os.environ.get("HOM_NVCC_EXTRA", "").split()  # A/B builds only (e.g. -DK1_MINB=3)
+    cmd = [NVCC, *FLAGS, *extra, "-shared", "-o", LIB, *sources()]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.check_call(cmd)

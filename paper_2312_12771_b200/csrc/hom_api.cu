@@ -715,7 +715,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
           const int nsh = RP.sh_ptr[k + 1] - RP.sh_ptr[k];
           r[1] = nsh;
           for (int sidx = RP.sh_ptr[k]; sidx < RP.sh_ptr[k + 1]; ++sidx) r[2 + sidx - RP.sh_ptr[k]] = RP.sh[sidx];
-          if (use_cls && nsh > 1) {
+          if (use_cls && nsh >= 1) {
             std::vector<int> key;
             for (int sidx = RP.sh_ptr[k]; sidx < RP.sh_ptr[k + 1]; ++sidx) key.push_back(RP.sh[sidx] & 0xff);
             std::sort(key.begin(), key.end());
@@ -783,7 +783,9 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
       std::vector<unsigned long long> nmask;  // covered columns of each node of the item
       auto flush = [&]() {
         if (nn == 0) return;
-        witem.insert(witem.end(), {alist[t], p0, nn, tslot[(size_t)(alist[t] >> 16) * nt_ + (alist[t] & 0xffff)]});
+        bool pad = false;  // identity rows (corner class, tail) in the item
+        for (int n = 0; n < nn; ++n) pad = pad || p0 + n >= R.n_indep || p0 + n == R.corner;
+        witem.insert(witem.end(), {alist[t], p0, nn | (pad ? 1 << 8 : 0), tslot[(size_t)(alist[t] >> 16) * nt_ + (alist[t] & 0xffff)]});
         lanes.resize(32, -1);
         wlist.insert(wlist.end(), lanes.begin(), lanes.end());
         for (int L = 0; L < 32; ++L) {
@@ -818,7 +820,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
       }
       flush();
     }
-    if (2 * R.npw > 31) return fail(HOM_ERR_INVALID_ARG, "K1: row-buffer nodes exceed the coverage word");
+    if (R.npw > 8) return fail(HOM_ERR_INVALID_ARG, "K1: row-buffer nodes exceed the coverage word");
     if ((long)R.n_indep * R.maxdeg >= (1L << 24)) return fail(HOM_ERR_INVALID_ARG, "K1: RVE too large for 24-bit record indices");
     R.n_witem = (int)(witem.size() / 4);
     R.witem = reinterpret_cast<const int4*>(upload(c, witem, s, &rc));

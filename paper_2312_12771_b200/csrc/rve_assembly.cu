@@ -63,13 +63,13 @@ __device__ __forceinline__ bool cook_material(const double* F, double alpha, dou
   const double J = 1.0 + Jm1;
   if (!(J > 0.0)) return false;
   const double H[4] = {F[3], -F[2], -F[1], F[0]};  // cof F (2-D specialisation of 1/2 F xx F)
-  const double ab = alpha + 2.0 * beta;
-  const double dPsidJ = 2.0 * beta * J + kappa * Jm1 - 2.0 * ab / J;
-  const double d2 = 2.0 * beta + kappa + 2.0 * ab / (J * J);
+  const double ab = alpha + 2.0 * beta, iJ = 1.0 / J, abJ = 2.0 * ab * iJ;  // one division per material point
+  const double dPsidJ = 2.0 * beta * J + kappa * Jm1 - abJ;
+  const double d2 = 2.0 * beta + kappa + abJ * iJ;
   // P = 2 (alpha + beta) F + g H written as 2 (alpha + beta)(F - H) + (g + 2 (alpha + beta)) H with
   // g + 2 (alpha + beta) = (J - 1)(2 beta + kappa + 2 (alpha + 2 beta) / J): both terms vanish at F = I
   // (the stress-free reference) instead of cancelling
-  const double c0 = 2.0 * (alpha + beta), c1 = Jm1 * (2.0 * beta + kappa + 2.0 * ab / J);
+  const double c0 = 2.0 * (alpha + beta), c1 = Jm1 * (2.0 * beta + kappa + abJ);
   const double FmH[4] = {F[0] - F[3], F[1] + F[2], F[2] + F[1], F[3] - F[0]};
   for (int i = 0; i < 4; ++i) P[i] = c0 * FmH[i] + c1 * H[i];
   // dH/dF is the constant anti-diagonal [0 0 0 1; 0 0 -1 0; 0 -1 0 0; 1 0 0 0]
@@ -89,7 +89,6 @@ __device__ __forceinline__ bool cook_material(const double* F, double alpha, dou
 // the records are staged in shared memory and written as one contiguous, coalesced range to
 // `out` (the CTA's L2-resident scratch, read back by the tile writer of the same CTA).
 constexpr int FS_ELB = 32, FS_QW = 29;
-constexpr int RB_SKEW = 0;  // K1 row-buffer node stride padding (doubles)
 constexpr int FS_SMEM_DBL = FS_ELB * 4 * FS_QW;
 // L2 residency hints: the element records are re-read by the same CTA moments later (evict_last),
 // the K_ff tiles stream out once (evict_first) so they do not push the records out of L2
@@ -290,9 +289,7 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
                                              double* __restrict__ Pavg, double* __restrict__ rfn,
                                              const double* __restrict__ EL, double* smem,
                                              const double* KE = nullptr, int kes = 0) {  // finite strain: K_e, stride
-  // [8 warps][npw][DIM][64] tile-row buffers, node stride DIM * 64 + RB_SKEW: the block stores of lanes on
-  // different nodes of an item with equal columns fall in different banks (6 g mod 16 distinct for g < 8)
-  constexpr int NSTR = DIM * TILE + RB_SKEW;
+  constexpr int NSTR = DIM * TILE;  // [8 warps][npw][DIM][64] tile-row buffers
   double* s_row = smem;
   double* red = s_row + (NTHR / 32) * R.npw * NSTR;  // [NTHR] reduction scratch
   // ISO element tables: [ntype][n_phase][ND][ND] (K_e) and [ntype][n_phase][ND][m] (K_fe rows) per RVE in shared
@@ -307,6 +304,8 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
   double* s_C = s_F + (ISO ? ntab * ((1 << DIM) * DIM) * R.m : 0);  // stencil-class blocks [ncls][ntab][BS]
   const int ncls = (ISO && !GT) ? R.ncls : 0;
   int* s_ep = reinterpret_cast<int*>(s_C + ncls * ntab * BS);
+  // per independent node: the one (type, phase) table of all its incident elements, 255 = several (class path)
+  uint8_t* s_nt = reinterpret_cast<uint8_t*>(s_ep + R.ne);
   const int tid = threadIdx.x;
   const int ne = R.ne;
   constexpr int ND = ISO ? (1 << DIM) * DIM : 8;  // nen*dim
@@ -341,6 +340,14 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
     }
   }
   __syncthreads();
+  if (ncls)
+    for (int p = tid; p < R.n_indep; p += NTHR) {
+      const int s0 = R.inc_ptr[p], s1 = R.inc_ptr[p + 1];
+      int t = s1 > s0 ? s_ep[R.inc[s0] >> 4] : 255;
+      for (int u = s0 + 1; u < s1; ++u)
+        if (s_ep[R.inc[u] >> 4] != t) t = 255;
+      s_nt[p] = (uint8_t)(t < 255 ? t : 255);
+    }
   // stencil-class blocks: C_c,t = sum over the class's element-local pairs (a, b) of the table t block
   // (read by records whose shared elements all use table t; ordered before the gathers by the
   // barriers of the <C> reduction below)
@@ -440,14 +447,15 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
       for (int k = 0; k < RHSW / 2; ++k) dst[k] = make_double2(out[2 * k], out[2 * k + 1]);
     }
     if (!ISO) {  // ||r_f|| over the free DOFs (R_micro)
-      red[tid] = rr;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rr += __shfl_xor_sync(0xffffffffu, rr, o);  // fixed-order tree
+      if ((tid & 31) == 0) red[tid >> 5] = rr;
       __syncthreads();
-      for (int s = NTHR / 2; s > 0; s >>= 1) {
-        if (tid < s) red[tid] += red[tid + s];
-        __syncthreads();
+      if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < NTHR / 32; ++w) t += red[w];
+        rfn[b] = sqrt(t);
       }
-      if (tid == 0) rfn[b] = sqrt(red[0]);
-      __syncthreads();
     }
   }
 
@@ -490,10 +498,13 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
     const int lw2 = itn + WSTRIDE < nw ? __ldg(R.wlist + (long)(itn + WSTRIDE) * 32 + lane) : -1;
     const int I = wi.x >> 16, J = wi.x & 0xffff;
     const int r0 = I * TILE;
-    const int p0 = wi.y, nn = wi.z;
+    const int p0 = wi.y, nn = wi.z & 0xff;
+    const bool ipad = (wi.z >> 8) & 1;  // the item has identity rows
+    double* gt = Kb + (long)wi.w * TILE_ELEMS;
+    const int c0 = J * TILE;
+    // the item's rows inside the tile are contiguous: local rows j (node j / DIM, row j % DIM of it)
+    const int jb = p0 * DIM - r0, j0 = max(0, -jb), j1 = min(nn * DIM, TILE - jb);
     {
-      double* gt = Kb + (long)wi.w * TILE_ELEMS;
-      const int c0 = J * TILE;
       {
         // (no clearing of the row buffer: columns no neighbour block covers are stored as zeros, cw)
         if (lw >= 0) {
@@ -525,14 +536,12 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
               }
               return KE[(long)e * kes + pk8(r, c)];
             };
-            // a record whose shared elements all use one (type, phase) table: the class block, one gather
+            // a record of a node whose incident elements all use one (type, phase) table: the class block
+            // of that table, one gather
             bool uni = false;
-            if (ISO && !GT && cls >= 0 && nsh <= 4 * RS4M - 2) {
-              const int t0 = s_ep[rv[2] >> 8];
-              uni = true;
-#pragma unroll
-              for (int sidx = 1; sidx < 4 * RS4M - 2; ++sidx)
-                if (sidx < nsh && s_ep[rv[2 + sidx] >> 8] != t0) uni = false;
+            if (ISO && !GT && cls >= 0) {
+              const int t0 = s_nt[p0 + (lw >> 24)];
+              uni = t0 != 255;
               if (uni) {
                 const double2* kb = reinterpret_cast<const double2*>(s_C + ((long)cls * ntab + t0) * BS);
 #pragma unroll
@@ -589,25 +598,31 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
           }
         }
         __syncwarp();
-        for (int n = 0; n < nn; ++n) {
-          const int pn = p0 + n;
-          const bool pad = pn >= R.n_indep || pn == R.corner;  // identity rows (corner class, tail)
-          double2 vr[DIM];  // all rows of the node loaded before the first store
-#pragma unroll
-          for (int ci = 0; ci < DIM; ++ci) vr[ci] = *reinterpret_cast<const double2*>(rowbuf + n * NSTR + ci * TILE + 2 * lane);
-#pragma unroll
-          for (int ci = 0; ci < DIM; ++ci) {
-            const int row = pn * DIM + ci, rr = row - r0;
-            if (rr < 0 || rr >= TILE) continue;
-            double2 v = vr[ci];
-            if (!((cw >> (2 * n)) & 1)) v.x = 0.0;
-            if (!((cw >> (2 * n + 1)) & 1)) v.y = 0.0;
-            if (pad || row >= R.npad) {
+        auto row_store = [&](int j, double2 v) {
+          if (ISO) __stcg(reinterpret_cast<double2*>(gt + (jb + j) * TILE + 2 * lane), v);
+          else __stcs(reinterpret_cast<double2*>(gt + (jb + j) * TILE + 2 * lane), v);  // evict-first: keep records in L2
+        };
+        if (!ipad) {
+#pragma unroll 3
+          for (int j = j0; j < j1; ++j) {
+            double2 v = *reinterpret_cast<const double2*>(rowbuf + j * TILE + 2 * lane);
+            const int cb = cw >> (2 * (j / DIM));
+            if (!(cb & 1)) v.x = 0.0;
+            if (!(cb & 2)) v.y = 0.0;
+            row_store(j, v);
+          }
+        } else {
+          for (int j = j0; j < j1; ++j) {
+            double2 v = *reinterpret_cast<const double2*>(rowbuf + j * TILE + 2 * lane);
+            const int n = j / DIM, cb = cw >> (2 * n);
+            if (!(cb & 1)) v.x = 0.0;
+            if (!(cb & 2)) v.y = 0.0;
+            const int pn = p0 + n, row = jb + r0 + j;
+            if (pn >= R.n_indep || pn == R.corner) {  // identity rows (corner class, tail)
               v.x = (c0 + 2 * lane == row) ? 1.0 : 0.0;
               v.y = (c0 + 2 * lane + 1 == row) ? 1.0 : 0.0;
             }
-            if (ISO) __stcg(reinterpret_cast<double2*>(gt + rr * TILE + 2 * lane), v);
-            else __stcs(reinterpret_cast<double2*>(gt + rr * TILE + 2 * lane), v);  // evict-first: keep records in L2
+            row_store(j, v);
           }
         }
         __syncwarp();
@@ -688,12 +703,12 @@ __global__ void __launch_bounds__(NTHR, KS ? 2 : 4) k_rve_assemble_fs(RveDev R, 
 
 size_t rve_assemble_smem(const RveDev& R, int npw) {
   const int dim = R.finite ? 2 : R.dim, nd = (1 << dim) * dim;  // nen*dim
-  size_t sm = (size_t)((NTHR / 32) * npw * (dim * TILE + RB_SKEW) + NTHR) * sizeof(double) +
+  size_t sm = (size_t)((NTHR / 32) * npw * dim * TILE + NTHR) * sizeof(double) +
               (R.finite ? 0
                    : (R.gtab ? (size_t)2 * R.n_phase
                              : (size_t)R.ntype * R.n_phase * ((size_t)(R.ncls + (1 << dim) * (1 << dim)) * ((dim * dim + 1) / 2 * 2) + nd * R.m)) *
                                  sizeof(double) +
-                         (size_t)R.ne * sizeof(int));
+                         (size_t)R.ne * sizeof(int) + (R.ncls ? (size_t)R.n_indep : 0));
   if (R.finite) sm = std::max(sm, (size_t)FS_SMEM_DBL * sizeof(double));  // element staging aliases the row buffers
   if (R.finite && R.fs_ks && R.fs_ntype > 0)  // staged material pass (w, phases, connectivity, qp geometry)
     sm = std::max(sm, (size_t)(FS_ELB2 * 4 * FS_QW2 + R.npad + R.fs_ntype * R.nq * 9) * 8 + (size_t)R.ne * 5 * 4 + R.ne);
@@ -706,7 +721,7 @@ int rve_assemble_npw(const RveDev& R) {
   // (<= 112 KB) for the finite-strain kernel with K_e in shared memory
   const int dim = R.finite ? 2 : R.dim;
   const size_t budget = (R.finite && R.fs_ks) ? 112 * 1024 : 56 * 1024;
-  int npw = 16 / dim;
+  int npw = std::min(8, 16 / dim);
   while (npw > 1 && rve_assemble_smem(R, npw) > budget) --npw;
   return npw;
 }

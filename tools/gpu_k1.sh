@@ -13,6 +13,5 @@ for c in 2 4 5 3; do
   st=10; [ $c = 3 ] && st=3
   timeout 300 python bench.py --config $c --steps $st --warmup 3 --no-cpu-baseline --spmv-nel 0 --no-companions > gpurun_out/${TAG}_c$c.json 2>/dev/null; line gpurun_out/${TAG}_c$c.json "c$c"
 done
-for c in 4 5; do
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_rve_assemble -c 1 -o gpurun_out/${TAG}_k1_c$c -f python tools/profile_step.py --config $c --steps 1 > gpurun_out/${TAG}_ncu_k1_c$c.log 2>&1; echo "ncu c$c rc=$?"
-done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_rve_assemble -c 1 -o gpurun_out/${TAG}_k1_c4 -f python tools/profile_step.py --config 4 --steps 1 > gpurun_out/${TAG}_ncu_k1_c4.log 2>&1; echo "ncu c4 rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_rve_assemble_fs -s 1 -c 1 -o gpurun_out/${TAG}_k1_c5 -f python tools/profile_cfg5.py > gpurun_out/${TAG}_ncu_k1_c5.log 2>&1; echo "ncu c5 rc=$?"

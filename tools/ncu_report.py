@@ -18,7 +18,9 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
         "sm__warps_active.avg.pct_of_peak_sustained_active",
         "launch__registers_per_thread", "launch__occupancy_limit_shared_mem", "launch__occupancy_limit_registers",
         "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
-        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__inst_executed.sum"]
+        "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smsp__inst_executed.sum",
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_st.sum",
+        "l1tex__throughput.avg.pct_of_peak_sustained_active"]
 
 
 def launches(path):
@@ -66,6 +68,8 @@ if __name__ == "__main__":
     ap.add_argument("--full", nargs="*", default=[])
     ap.add_argument("--source", nargs="*", default=[])
     a = ap.parse_args()
+    if a.out.endswith(".ncu-rep"):
+        raise SystemExit("first argument is the OUTPUT .md, not a report")
     lines = [f"# {a.title}", ""]
     if a.launches:
         lines += ["## Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none`, cold-cache, serialised)",
