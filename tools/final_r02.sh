@@ -9,3 +9,5 @@ python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/final_referen
 python tools/parity_report.py > gpurun_out/final_parity.txt 2> gpurun_out/final_parity.err; echo "parity rc=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/final_launches_c3.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --spmv-nel 0 --no-companions > gpurun_out/final_ncu_bench.log 2>&1; echo "launches rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_rve_assemble -c 1 -o gpurun_out/final_k1_c3 -f python tools/profile_step.py --config 3 --steps 1 > gpurun_out/final_ncu_k1_c3.log 2>&1; echo "ncu k1 c3 rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_rve_assemble -c 1 -o gpurun_out/final_k1_c4 -f python tools/profile_step.py --config 4 --steps 1 > gpurun_out/final_ncu_k1_c4.log 2>&1; echo "ncu k1 c4 rc=$?"
