@@ -497,17 +497,25 @@ def test_fluctuations_keep_the_natural_layout(torch_cuda):
 
 
 # ------------------------------------------------------------------ K1 alone (hom_debug_rve_kff)
-@pytest.mark.parametrize("dim,r,ordering,tile_sparse,graded", [(2, 5, "folded", False, False),
-                                                               (2, 6, "natural", True, False),
-                                                               (2, 12, "folded", True, False),
-                                                               (3, 3, "folded", False, False),
-                                                               (2, 12, "folded", False, True),
-                                                               (3, 4, "natural", True, True)])
-def test_k1_kff_equals_bruteforce_micro_block(torch_cuda, dim, r, ordering, tile_sparse, graded):
+@pytest.mark.parametrize("dim,r,ordering,tile_sparse,graded,classes", [(2, 5, "folded", False, False, True),
+                                                                       (2, 6, "natural", True, False, True),
+                                                                       (2, 12, "folded", True, False, True),
+                                                                       (3, 3, "folded", False, False, True),
+                                                                       (3, 5, "folded", False, False, True),
+                                                                       (3, 5, "folded", False, False, False),
+                                                                       (2, 12, "folded", False, False, False),
+                                                                       (2, 12, "folded", False, True, True),
+                                                                       (3, 4, "natural", True, True, True)])
+def test_k1_kff_equals_bruteforce_micro_block(torch_cuda, monkeypatch, dim, r, ordering, tile_sparse, graded,
+                                              classes):
     """The assembled K_ff of one RVE, entry by entry, against the micro-micro block L of the
     brute-force monolithic assembly (tests/bruteforce.py, own shape functions and periodic map):
-    L_b = eta_M K_ff (R2), with random per-element phases and per-RVE moduli."""
+    L_b = eta_M K_ff (R2), with random per-element phases and per-RVE moduli.
+    classes=False: K1's plain per-element gathers (HOM_K1_CLS=0) instead of the stencil-class blocks of
+    uniform nodes; the random phases leave both uniform and interface nodes."""
     from paper_2312_12771_b200.hom import Homogenizer
+    if not classes:
+        monkeypatch.setenv("HOM_K1_CLS", "0")
 
     from . import bruteforce as bf
     rng = np.random.default_rng(40 + r)
