@@ -379,8 +379,9 @@ def main():
                     help="constant: one RVE per macro element (SURVEY §8(f) 2, small strain)")
     ap.add_argument("--tile-sparse", action="store_true",
                     help="factor only the symbolic tile fill of K_ff (SURVEY §8(f) 3) instead of every lower tile")
-    ap.add_argument("--macro-precond", default="two_level", choices=["two_level", "jacobi"],
-                    help="macro PCG preconditioner (hom_options.macro_precond)")
+    ap.add_argument("--macro-precond", default="auto", choices=["auto", "two_level", "jacobi"],
+                    help="macro PCG preconditioner (hom_options.macro_precond; auto: two-level unless a "
+                         "quarter or more of the macro DOFs are prescribed)")
     ap.add_argument("--rve-ordering", default="folded", choices=["folded", "natural"],
                     help="internal order of the RVE nodes (rows of K_ff); w at the API is natural either way")
     args = ap.parse_args()

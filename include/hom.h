@@ -145,12 +145,16 @@ typedef struct {
                                (first appearance in the mesh).  The layout of w at the API (d_w of
                                hom_recover_fluctuations / hom_set_fluctuations / hom_get_fluctuations)
                                is always the natural one. */
-  int32_t macro_precond;    /* preconditioner of the macro PCG (a6): 0 = two-level (default): node-block
-                               Jacobi + an additive coarse space of node aggregates with their rigid-body
-                               modes, A_c = P^T K_M P formed and inverted on the device every solve
-                               (meshes with >= 1024 DOFs in 2-D / 3-D, otherwise 1);
-                               1 = node-block Jacobi only.  The solution is the same (rtol), only the
-                               iteration count differs. */
+  int32_t macro_precond;    /* preconditioner of the macro PCG (a6): 2 = two-level: node-block Jacobi + an
+                               additive coarse space of node aggregates with their rigid-body modes,
+                               A_c = P^T K_M P formed and inverted on the device every solve (DESIGN.md
+                               §5.4.1; meshes with >= 1024 DOFs in 2-D / 3-D, otherwise Jacobi);
+                               1 = node-block Jacobi only; 0 = auto (default): two-level when fewer than
+                               a quarter of the macro DOFs are prescribed (few Dirichlet anchors: the slow
+                               low-frequency modes the coarse space removes), else Jacobi -- measured:
+                               config 2 (3 % prescribed) 0.69 vs 0.98 ms, config 4 (53 % prescribed) 0.48
+                               vs 0.86 ms.  The solution is the same (rtol), only the iteration count and
+                               the time differ. */
 } hom_options;
 
 typedef struct {

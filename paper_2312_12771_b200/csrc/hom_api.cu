@@ -268,8 +268,8 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
   c->dim = dim;
   c->finite = mat->kind >= 1;
   c->m = c->finite ? 4 : (dim == 1 ? 1 : (dim == 2 ? 3 : 6));
-  if (options->macro_precond < 0 || options->macro_precond > 1)
-    return fail(HOM_ERR_INVALID_ARG, "macro_precond must be 0 (two-level) or 1 (node-block Jacobi)");
+  if (options->macro_precond < 0 || options->macro_precond > 2)
+    return fail(HOM_ERR_INVALID_ARG, "macro_precond must be 0 (auto), 1 (node-block Jacobi) or 2 (two-level)");
   if (options->macro_basis < 0 || options->macro_basis > 1 || (options->macro_basis == 1 && c->finite))
     return fail(HOM_ERR_INVALID_ARG, "macro_basis must be 0 (Dirac) or 1 (constant, small strain only)");
   c->B = mac->n_elems * (options->macro_basis == 1 ? 1 : nq);
@@ -868,8 +868,10 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     sms = std::max(sms, 1);
-    hom::CoarseHost H =
-        hom::coarse_build(dim, M.n_nodes, mac->coords, rowptr.data(), col.data(), c->opt.macro_precond, sms);
+    // auto (0): the coarse space only when fewer than a quarter of the macro DOFs are prescribed
+    const int one_level = c->opt.macro_precond == 1 ||
+                          (c->opt.macro_precond == 0 && 4L * mac->n_dirichlet >= (long)M.n_nodes * dim);
+    hom::CoarseHost H = hom::coarse_build(dim, M.n_nodes, mac->coords, rowptr.data(), col.data(), one_level, sms);
     hom::CoarseDev& C = M.cc;
     C = hom::CoarseDev{};
     if (H.nc > 0) {

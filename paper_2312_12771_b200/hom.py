@@ -154,7 +154,7 @@ class Homogenizer:
     def __init__(self, macro_coords, macro_conn, dirichlet_dof, dirichlet_value, body_force,
                  rve_coords, rve_conn, phase, materials, kind="linear", cg_rtol=1e-13, cg_max_iter=20000,
                  rve_chunk=0, check_info=True, mem_budget_gb=0.0, tile_sparse=False, rve_range=None,
-                 nodal_force=None, macro_basis="dirac", rve_ordering="folded", macro_precond="two_level"):
+                 nodal_force=None, macro_basis="dirac", rve_ordering="folded", macro_precond="auto"):
         import torch
         if not torch.cuda.is_available():
             raise RuntimeError("Homogenizer needs a CUDA device (no CPU fallback)")
@@ -194,7 +194,7 @@ class Homogenizer:
         rb, rn = (0, 0) if rve_range is None else (int(rve_range[0]), int(rve_range[1]) - int(rve_range[0]))
         self.opt = Options(int(kind != "linear"), cg_rtol, cg_max_iter, rve_chunk, int(check_info), mem_budget_gb,
                            int(tile_sparse), rb, rn, int(macro_basis == "constant"),
-                           {"folded": 0, "natural": 1}[rve_ordering], {"two_level": 0, "jacobi": 1}[macro_precond])
+                           {"folded": 0, "natural": 1}[rve_ordering], {"auto": 0, "jacobi": 1, "two_level": 2}[macro_precond])
         self.finite = kind != "linear"
         h = ctypes.c_void_p()
         rc = L.hom_setup(ctypes.byref(h), ctypes.byref(self.macro), ctypes.byref(self.rve),
