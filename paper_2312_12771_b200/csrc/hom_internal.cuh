@@ -8,6 +8,23 @@
 
 #include "../../include/hom.h"
 
+// Device-side bounds checks of the shared-memory tables and pool slots, compiled in only for debug builds
+// (HOM_NVCC_EXTRA=-DHOM_DEBUG_BOUNDS; compute-sanitizer is not available on the B200 pool): a failed check
+// prints its location and traps, so the launch fails with an error the caller reports.
+#ifdef HOM_DEBUG_BOUNDS
+#include <cstdio>
+#define HOM_DCHECK(c)                                                                      \
+  do {                                                                                     \
+    if (!(c)) {                                                                            \
+      printf("HOM_DCHECK %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x, #c);                                                        \
+      __trap();                                                                            \
+    }                                                                                      \
+  } while (0)
+#else
+#define HOM_DCHECK(c) ((void)0)
+#endif
+
 namespace hom {
 
 constexpr int TILE = 64;          // K_ff tile edge (rows and columns)
@@ -72,20 +89,20 @@ struct RveDev {
   // {q (-1: none / corner), n_sh, code_0 .. code_{n_sh-1}, -1 ...}, code = e<<8 | a<<4 | b
   const int4* nrec;
   int maxdeg, rs4;
+  // K1 warp work items: {tile code I<<16|J, first row node p0, node count nn, pool slot}, and per item one record
+  // per lane: (g << 24 | record index) for node p0 + g, -1 = idle lane (<= 32 records, <= npw nodes)
+  const int4* witem;
+  const int* wlist;
+  int n_witem;
+  int xb0;                        // first RVE of the influence store X (the context's local range)
+  const int* nat_of;              // [n_indep] internal node -> natural (API) node; nullptr = identity
+  const int* int_of;              // [n_indep] natural node -> internal node; nullptr = identity
   // K1 stencil classes (small strain, shared-memory tables): record word 1 = n_sh | (class + 1) << 16; a
   // class is the sorted list of element-local pairs (a << 4 | b) cls_ab[cls_ptr[c] .. cls_ptr[c + 1])
   int ncls;
   const int* cls_ptr;
   const int* cls_ab;
-  // K1 warp work items: {tile code I<<16|J, first row node p0, node count nn, pool slot}, and per item one record
-  // per lane: (g << 24 | record index) for node p0 + g, -1 = idle lane (<= 32 records, <= npw nodes)
-  const int4* witem;
-  const int* wlist;
   const int* wcov;                // [n_witem][32]: bit 2n + b = column 2 lane + b of item node n covered
-  int n_witem;
-  int xb0;                        // first RVE of the influence store X (the context's local range)
-  const int* nat_of;              // [n_indep] internal node -> natural (API) node; nullptr = identity
-  const int* int_of;              // [n_indep] natural node -> internal node; nullptr = identity
 };
 
 // Two-level additive macro preconditioner (coarse.cu): aggregates of macro

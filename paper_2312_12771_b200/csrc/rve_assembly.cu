@@ -351,8 +351,9 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
   // stencil-class blocks: C_c,t = sum over the class's element-local pairs (a, b) of the table t block
   // (read by records whose shared elements all use table t; ordered before the gathers by the
   // barriers of the <C> reduction below)
+  if (ISO && !GT)
   for (int i = tid; i < ncls * ntab * BS; i += NTHR) {
-    const int cl = i / (ntab * BS), t = (i / BS) % ntab, j = i % BS;
+    const int cl = i / max(ntab * BS, 1), t = (i / BS) % max(ntab, 1), j = i % BS;
     double v = 0.0;
     if (j < DIM * DIM)
       for (int u = __ldg(R.cls_ptr + cl); u < __ldg(R.cls_ptr + cl + 1); ++u) {
@@ -502,6 +503,7 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
     const int r0 = I * TILE;
     const int p0 = wi.y, nn = wi.z & 0xff;
     const bool ipad = (wi.z >> 8) & 1;  // the item has identity rows
+    HOM_DCHECK(wi.w >= 0 && wi.w < R.nslot && nn <= R.npw);
     double* gt = Kb + (long)wi.w * TILE_ELEMS;
     const int c0 = J * TILE;
     // the item's rows inside the tile are contiguous: local rows j (node j / DIM, row j % DIM of it)
@@ -510,6 +512,7 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
       {
         // (no clearing of the row buffer: columns no neighbour block covers are stored as zeros, cw)
         if (lw >= 0) {
+          HOM_DCHECK((lw >> 24) < nn && p0 + (lw >> 24) < R.n_indep);
           double* rb = rowbuf + (lw >> 24) * NSTR;
           {
             const int4* rec = R.nrec + (long)(lw & 0xffffff) * R.rs4;
@@ -536,6 +539,7 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
                 const int a = (code >> 4) & 15, bb = code & 15;
                 return s_K[(((long)s_ep[e] * NEN + a) * NEN + bb) * BS + i * DIM + jj];
               }
+              HOM_DCHECK(e < ne && r < 8 && c < 8);
               return KE[(long)e * kes + pk8(r, c)];
             };
             // a record of a node whose incident elements all use one (type, phase) table: the class block
@@ -544,6 +548,7 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
             if (ISO && !GT && cls >= 0) {
               const int t0 = s_nt[p0 + (lw >> 24)];
               uni = t0 != 255;
+              HOM_DCHECK(cls < ncls && (!uni || t0 < ntab));
               if (uni) {
                 const double2* kb = reinterpret_cast<const double2*>(s_C + ((long)cls * ntab + t0) * BS);
 #pragma unroll
@@ -561,6 +566,7 @@ __device__ __forceinline__ void assemble_rve(const RveDev& R, const int b, const
                 const int code = rv[sidx + 2];
                 if (ISO && !GT) {  // the whole block with BS/2 128-bit loads
                   const int e = code >> 8, a = (code >> 4) & 15, bb = code & 15;
+                  HOM_DCHECK(e < ne && a < NEN && bb < NEN && s_ep[e] < ntab);
                   const double2* kb = reinterpret_cast<const double2*>(s_K + (((long)s_ep[e] * NEN + a) * NEN + bb) * BS);
                   double v[BS];
 #pragma unroll

@@ -92,12 +92,6 @@ __device__ __forceinline__ int swy(int k, int n) { return k * RHSW + (n ^ (((k >
 // space (TileMask).  MODE 2: tile-sparse, any nt, tables in global memory (g_nz, tslot).
 template <int MODE>
 __device__ __forceinline__ double* tile_ptr(double* Kb, const RveDev& R, const TileMask& tm, int I, int J) {
-#ifdef HOM_DEBUG_BOUNDS
-  HOM_DCHECK(I >= J && J >= 0 && I < R.nt);
-  if (MODE == 2) HOM_DCHECK(__ldg(R.tslot + I * R.nt + J) >= 0 && __ldg(R.tslot + I * R.nt + J) < R.nslot);
-  if (MODE == 1) HOM_DCHECK(((tm.row[I] >> J) & 1ull) && tm.rowstart[I] + __popcll(tm.row[I] & ((1ull << J) - 1ull)) < R.nslot);
-  if (MODE == 0) HOM_DCHECK(((I * (I + 1)) >> 1) + J < R.nslot);
-#endif
   if (MODE == 2) return Kb + (long)__ldg(R.tslot + I * R.nt + J) * TILE_ELEMS;
   if (MODE == 1) return Kb + (long)(tm.rowstart[I] + __popcll(tm.row[I] & ((1ull << J) - 1ull))) * TILE_ELEMS;
   return Kb + (long)(((I * (I + 1)) >> 1) + J) * TILE_ELEMS;
@@ -1466,10 +1460,6 @@ __global__ void k_first_fail(const int* __restrict__ f, int n, int sentinel, int
 // Dense-structure kernel: 0 = k_condense (default), 1 = k_condense_ws (factor warp + 4 MMA warps, 3 CTAs/SM;
 // HOM_CONDENSE=ws, for A/B measurements; its 4-CTA/SM version with 8-wide cp.async chunks was measured
 // slower still and lives in git history, commit e0bd4eb -- DESIGN.md §5.1).
-// Off by default: measured slower (profiles/r02/condense_variants.md).  Its code is kept
-// compiled into the tile-sparse instantiations: with it ptxas allocates k_condense<1> without the 96 B of
-// spills the factor's panel phase had otherwise (tile-sparse configs 2 / 3 5 % faster in a same-box A/B,
-// dense unchanged).
 constexpr int LA_Q_DEFAULT = 0;
 static int condense_variant() {
   static const int v = [] {
