@@ -1519,10 +1519,8 @@ void launch_condense(const RveDev& R, int b0, int nb, double* Kt, double* Y, con
   }
   auto k = R.dense_tiles ? k_condense<0> : (tm ? k_condense<1> : k_condense<2>);
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  static const int la_q = [] {  // tile-sparse diagonal lookahead: chunks per pivot-chain window (HOM_LA; 0 = off)
-    const char* e = getenv("HOM_LA");
-    return e ? atoi(e) : LA_Q_DEFAULT;
-  }();
+  const char* la_env = getenv("HOM_LA");  // tile-sparse diagonal lookahead: chunks per pivot-chain window (0 = off)
+  const int la_q = la_env ? atoi(la_env) : LA_Q_DEFAULT;
   k<<<nb, NTC, sm, s>>>(R, tm ? *tm : none, kmap, ymap, b0, Kt, Y, Cavg, Pavg, Ceff, Peff, PavgOut, X, info, la_q);
 }
 

@@ -370,6 +370,20 @@ def test_tile_sparse_matches_oracle_and_dense_bitwise(torch_cuda, make):
     assert wk.flop_executed <= wd.flop_executed
 
 
+@pytest.mark.parametrize("make", [lambda: W.config3(nel=2, r=32, seed=7), lambda: W.config2(nel=4)],
+                         ids=["cfg3-rve", "cfg2-rve"])
+def test_tile_sparse_lookahead_is_bitwise_neutral(torch_cuda, monkeypatch, make):
+    """The tile-sparse diagonal lookahead (HOM_LA > 0, off by default) accumulates the next
+    column's first chunks in the pivot-chain windows and parks them in place: the same DMMAs in the same
+    order, so C_eff, u and w are bitwise those of the default path."""
+    wl = make()
+    base = gpu_linear(wl, tile_sparse=True)
+    monkeypatch.setenv("HOM_LA", "4")
+    la = gpu_linear(wl, tile_sparse=True)
+    assert np.array_equal(la["C"], base["C"]) and np.array_equal(la["u"], base["u"])
+    assert np.array_equal(la["w"], base["w"])
+
+
 def test_tile_sparse_config3_full_rve_fewer_tiles(torch_cuda):
     """Config 3's 32x32 RVE: the tile fill is the band + the periodic wrap row, far below dense."""
     wl = W.config3(nel=4)
