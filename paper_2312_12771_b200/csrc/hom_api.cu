@@ -774,6 +774,7 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
     const int dK = c->finite ? 2 : R.dim;
     // Per item and lane a coverage word (wcov): bit 2n + b = column 2 lane + b of node n's rows is covered by
     // a neighbour block -- the writer stores zeros elsewhere instead of clearing its row buffer first
+    if (R.npw > 8) return fail(HOM_ERR_INVALID_ARG, "K1: row-buffer nodes exceed the coverage word");
     std::vector<int> witem, wlist, wcov;
     for (int t = 0; t < R.n_a; ++t) {
       const int r0 = (alist[t] >> 16) * 64, c0 = (alist[t] & 0xffff) * 64;
@@ -820,7 +821,6 @@ int hom_setup(hom_ctx** out, const hom_macro_mesh* mac, const hom_rve_mesh* rve,
       }
       flush();
     }
-    if (R.npw > 8) return fail(HOM_ERR_INVALID_ARG, "K1: row-buffer nodes exceed the coverage word");
     if ((long)R.n_indep * R.maxdeg >= (1L << 24)) return fail(HOM_ERR_INVALID_ARG, "K1: RVE too large for 24-bit record indices");
     R.n_witem = (int)(witem.size() / 4);
     R.witem = reinterpret_cast<const int4*>(upload(c, witem, s, &rc));
